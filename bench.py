@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark of the DyMoE mixed-precision MoE layer on B200 (BASELINE.json metric:
+"MoE-layer tokens/s (prefill, decode) + achieved HBM GB/s / tensor-pipe %").
+
+One step = one pass of the whole hot path (route -> score -> assign -> permute -> fused-
+dequant expert FFN -> combine) of one Mixtral-8x7B-shaped MoE layer over one batch, through the
+C ABI (dymoe_moe_forward), with the packed Int8/Int4/Int2 expert weights resident in HBM
+(quantized by dymoe_quantize when the layer is loaded; the quantize kernel is measured in its
+own sub-object).
+
+Workloads:
+  decode  (default, BASELINE.json configs[1]): B tokens per step (default 8), the depth schedule
+          l = step mod 32 of a 32-layer stack, 4 rotating copies of the layer's weights so that
+          no step re-reads weights another step left in L2 (each copy >= 5 GB > 126 MB L2).
+  prefill (configs[2]): 2048 tokens per step, same rotation.
+
+N > 1 (torchrun): every rank runs an independent replica (weak scaling; the decode layer
+does not shard across GPUs in this round).  Timing: W warm-up steps, then K steps bracketed by
+barrier + cuda synchronize, CUDA events on the launching stream, max over ranks.
+
+--impl reference: the CPU oracle (oracle/) timed on this host on a bounded sample of the
+same workload (the reference arm; rank 0 only).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synthetic  # noqa: E402
+
+LADDER_BITS, LADDER_LAMBDAS = (8, 4, 2), (0.25, 0.5)
+NUM_LAYERS = 32
+METRIC = "MoE-layer tokens/s (prefill, decode) + achieved HBM GB/s / tensor-pipe %"
+
+
+def bytes_per_weight(b):
+    return 2.0 if b == 16 else (0.0 if b == 0 else b / 8.0 + 5.0 / 128.0)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j.get("bf16_tflops_sustained"),
+                    src="measured (MEASURED_PEAKS.json)")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# =============================================================================================
+def build_layer_copies(d, cfg, copies, device):
+    """`copies` independent random-init layers: bf16 masters + Int8/Int4/Int2 packed weights."""
+    layers = []
+    for c in range(copies):
+        ex = [{n: t.to(device) for n, t in e.items()} for e in synthetic.expert_weights(cfg, 100 + c, device)]
+        d.quantize_experts(ex, (8, 4, 2))
+        layers.append((d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn), ex))
+    torch.cuda.synchronize()
+    return layers
+
+
+def step_inputs(cfg, n, device):
+    out = []
+    for i in range(n):
+        x, lg, a = synthetic.layer_inputs(cfg, 1000 + i, device)
+        out.append((x.contiguous(), lg.contiguous(), a.contiguous()))
+    return out
+
+
+def algorithmic_bytes(cfg, bits, off):
+    """Per-step algorithmic HBM bytes of the FFN: (W13 kernel, W2 kernel)."""
+    Hd, F = cfg.hidden, cfg.ffn
+    b13 = b2 = 0.0
+    for e in range(cfg.M):
+        n = int(off[e + 1] - off[e])
+        if n == 0 or bits[e] == 0:
+            continue
+        bpw = bytes_per_weight(int(bits[e]))
+        b13 += 2 * F * Hd * bpw + n * Hd * 2 + n * F * 2
+        b2 += Hd * F * bpw + n * F * 2 + n * Hd * 4
+    return b13, b2
+
+
+def algorithmic_flops(cfg, off, bits):
+    n = sum(int(off[e + 1] - off[e]) for e in range(cfg.M) if bits[e] != 0)
+    return 6.0 * cfg.hidden * cfg.ffn * n
+
+
+def run_ours(args, rank, world, device):
+    import paper_2603_19172_b200.dymoe as d
+    d.lib()
+    torch.cuda.set_device(device)
+    peaks = load_peaks()
+    base = synthetic.CONFIGS["mixtral_decode" if args.workload == "decode" else "mixtral_prefill"]
+    T = args.batch if args.workload == "decode" else args.tokens
+    cfg = base.with_tokens(T)
+    phase = d.DYMOE_DECODE if args.workload == "decode" else d.DYMOE_PREFILL
+    layers = build_layer_copies(d, cfg, args.copies, device)
+    n_inputs = 8
+    inputs = step_inputs(cfg, n_inputs, device)
+    ladder = d.make_ladder(LADDER_BITS, LADDER_LAMBDAS)
+    ws = [L.workspace(T, device) for L, _ in layers]
+    out = torch.empty(T, cfg.hidden, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream()
+
+    def plan(i):
+        return i % len(layers), i % NUM_LAYERS, i % n_inputs
+
+    events = None
+
+    def one_step(i, ev=None):
+        c, l, j = plan(i)
+        L = layers[c][0]
+        x, lg, a = inputs[j]
+        L.forward(x, lg, ladder, l, NUM_LAYERS, phase=phase, attn_mass=a, ws=ws[c], out=out,
+                  prof_events=ev)
+
+    # census: algorithmic bytes / flops of every distinct step (bits are data-dependent)
+    census = {}
+    period = math.lcm(len(layers), NUM_LAYERS, n_inputs)
+    for i in range(period):
+        one_step(i)
+        c = plan(i)[0]
+        v = layers[c][0].views(T, ws[c])
+        bits = v["bits"].cpu().numpy()
+        off = v["expert_off"].cpu().numpy()
+        census[plan(i)] = (algorithmic_bytes(cfg, bits, off), algorithmic_flops(cfg, off, bits),
+                           int((np.diff(off) > 0).sum()))
+        rc, word = layers[c][0].check_status(T, ws[c])
+        assert rc == 0, "device status word %x" % word
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device events, max over ranks)
+    K = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    for row in ev:
+        for e_ in row:
+            e_.record(stream)   # creates the CUDA event so its handle can be passed down
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record(stream)
+        for i in range(K):
+            one_step(args.warmup + i, ev[i])
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], device=device)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_per_step = ms / K
+    tokens = T * K * world
+    value = tokens / (ms / 1e3)
+
+    w13_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(K)]
+    w2_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
+    b13 = sum(census[plan(args.warmup + i)][0][0] for i in range(K))
+    b2 = sum(census[plan(args.warmup + i)][0][1] for i in range(K))
+    fl = sum(census[plan(args.warmup + i)][1] for i in range(K))
+    ffn_ms = sum(w13_ms) + sum(w2_ms)
+    achieved_w13 = b13 / (sum(w13_ms) / 1e3) / 1e9
+    achieved_ffn = (b13 + b2) / (ffn_ms / 1e3) / 1e9
+    traffic = load_traffic("k_decode_gemv" if phase == d.DYMOE_DECODE else "k_prefill")
+
+    # ---------------- end-to-end through the public API with host buffers
+    e2e = None
+    if rank == 0 or world > 1:
+        hx = [inp[0].cpu().pin_memory() for inp in inputs]
+        hl = [inp[1].cpu().pin_memory() for inp in inputs]
+        ha = [inp[2].cpu().pin_memory() for inp in inputs]
+        dx = torch.empty_like(inputs[0][0])
+        dl = torch.empty_like(inputs[0][1])
+        da = torch.empty_like(inputs[0][2])
+        hy = torch.empty(T, cfg.hidden, dtype=torch.float32).pin_memory()
+        h2d = hx[0].numel() * 2 + hl[0].numel() * 4 + (ha[0].numel() * 4 if phase == d.DYMOE_PREFILL else 0)
+        d2h = hy.numel() * 4
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(K):
+            c, l, j = plan(args.warmup + i)
+            dx.copy_(hx[j], non_blocking=True)
+            dl.copy_(hl[j], non_blocking=True)
+            if phase == d.DYMOE_PREFILL:
+                da.copy_(ha[j], non_blocking=True)
+            layers[c][0].forward(dx, dl, ladder, l, NUM_LAYERS, phase=phase, attn_mass=da,
+                                 ws=ws[c], out=out)
+            hy.copy_(out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            tt = torch.tensor([e_ms], device=device)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(tt.item())
+        e2e = {"value": T * K * world / (e_ms / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---------------- quantize kernel (row a4), alone: one Mixtral expert per width
+    quant = measure_quantize(d, layers[0][1], cfg, peaks)
+
+    res = None
+    if rank == 0:
+        launches_per_step = 7
+        res = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
+            "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
+            "config": {"workload": "mixtral_%s" % args.workload, "hidden": cfg.hidden, "ffn": cfg.ffn,
+                       "experts": cfg.M, "top_k": cfg.k, "tokens_per_step": T,
+                       "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
+                       "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
+                       "weight_copies": args.copies,
+                       "l2": "inputs larger than L2: %d rotating weight copies, each >= 5 GB" % args.copies,
+                       "parallelism": "replicas" if world > 1 else "single GPU"},
+            "roofline": {"bound": "hbm", "kernel": "k_decode_gemv<W13> (fused-dequant SwiGLU GEMV)"
+                         if phase == d.DYMOE_DECODE else "prefill FFN",
+                         "achieved": achieved_w13, "peak": peaks["hbm"], "unit": "GB/s",
+                         "frac": achieved_w13 / peaks["hbm"], "traffic": traffic,
+                         "peak_src": peaks["src"], "frac_of_8TBs": achieved_w13 / 8000.0,
+                         "ffn_w13_plus_w2_GBs": achieved_ffn,
+                         "ffn_share_of_step": ffn_ms / ms if world == 1 else None,
+                         "algorithmic_bytes_per_step": (b13 + b2) / K},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * K,
+            "quantize": quant,
+            "tensor_tflops_ffn": fl / (ffn_ms / 1e3) / 1e12,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            res["cpu_baseline"] = cpu_baseline(cfg, args, phase == d.DYMOE_PREFILL)
+    return res
+
+
+def load_traffic(kernel_prefix):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        j = json.load(f)
+    for k, v in j.items():
+        if k.startswith(kernel_prefix):
+            return v
+    return None
+
+
+def measure_quantize(d, experts, cfg, peaks, reps=5):
+    out = {}
+    ex = experts[0]
+    for b in (8, 4, 2):
+        jobs = [(ex[n], b, ex["q%d" % b][n]) for n in ("w1", "w3", "w2")]
+        d.dymoe_quantize_batched(jobs)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            d.dymoe_quantize_batched(jobs)
+        e1.record()
+        torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) / reps / 1e3
+        nbytes = 3 * cfg.hidden * cfg.ffn * (2 + bytes_per_weight(b))
+        gbs = nbytes / s / 1e9
+        out["int%d" % b] = {"GB/s": gbs, "frac": gbs / peaks["hbm"], "us": s * 1e6,
+                            "bytes": nbytes}
+    out["note"] = "one Mixtral expert (W1, W3, W2) per launch; 352 MB bf16 read, > L2 per rep"
+    return out
+
+
+# =============================================================================================
+def cpu_baseline(cfg, args, prefill, frac=8):
+    """The oracle as it stands, on this host's cores, on a bounded sample of one step."""
+    from oracle import moe as o_moe, route as o_route, importance as o_imp, schedule as o_sched
+    cores = len(os.sched_getaffinity(0))
+    x, lg, a = synthetic.layer_inputs(cfg, 1000)
+    ex = synthetic.expert_weights(cfg.with_tokens(cfg.T), 100, experts=[0])
+    t0 = time.perf_counter()
+    idx, w, p = o_route.route(lg.numpy(), cfg.k)
+    if prefill:
+        I, _, _ = o_imp.score_prefill(a.numpy(), idx, cfg.M)
+    else:
+        I = o_imp.decode_importance(lg.numpy(), p)
+    bits, _ = o_sched.assign_bits(I, 16, NUM_LAYERS, o_sched.Ladder(LADDER_BITS, LADDER_LAMBDAS), cfg.k)
+    perm = o_moe.permute(idx, bits, cfg.M)
+    t_ctrl = time.perf_counter() - t0
+    # FFN sample: 1/frac of expert 0's rows (W1/W3 rows and the matching W2 columns) at its width
+    e0 = ex[0]
+    Fs = cfg.ffn // frac
+    sub = {"w1": e0["w1"][:Fs].float().numpy(), "w3": e0["w3"][:Fs].float().numpy(),
+           "w2": e0["w2"][:, :Fs].contiguous().float().numpy()}
+    b = int(bits[0]) or 4
+    n_rows = max(int(perm["expert_off"][1] - perm["expert_off"][0]), 1)
+    t1 = time.perf_counter()
+    W1, W3, W2 = o_moe.expert_weights(sub, b)
+    xr = x.float().numpy()[:n_rows].astype(np.float64)
+    o_moe.ffn(xr, W1, W3, W2)
+    t_ffn = (time.perf_counter() - t1) * frac
+    n_active = int((np.diff(perm["expert_off"]) > 0).sum())
+    step_s = t_ctrl + t_ffn * n_active
+    return {"value": cfg.T / step_s, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": "route+score+assign+permute for all %d tokens; FFN of 1/%d of one expert "
+                      "(Int%d, %d rows) scaled x%d and x%d active experts" % (cfg.T, frac, b, n_rows, frac, n_active),
+            "blas_threads": torch.get_num_threads()}
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle on the same workload, bounded sample per step."""
+    base = synthetic.CONFIGS["mixtral_decode" if args.workload == "decode" else "mixtral_prefill"]
+    T = args.batch if args.workload == "decode" else args.tokens
+    cfg = base.with_tokens(T)
+    prefill = args.workload == "prefill"
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, args, prefill, frac=64)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(cpu_baseline(cfg, args, prefill, frac=64))
+    wall = time.perf_counter() - t0
+    v = statistics.median(x["value"] for x in vals)
+    cb = dict(vals[0])
+    cb["value"] = v
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
+            "data": "synthetic", "config": {"workload": "mixtral_%s" % args.workload, "tokens_per_step": T},
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--tokens", type=int, default=2048)
+    ap.add_argument("--copies", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args)))
+        return
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    res = run_ours(args, rank, world, torch.device("cuda", local))
+    if rank == 0:
+        print(json.dumps(res))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

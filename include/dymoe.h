@@ -1,0 +1,261 @@
+/*
+ * dymoe.h — C ABI of the B200 (sm_100a) DyMoE mixed-precision MoE layer.
+ *
+ * Method: "DyMoE: Dynamic Expert Orchestration with Mixed-Precision Quantization for Efficient
+ * MoE Inference on Edge" (arxiv 2603.19172).  Citations "P:n" are lines of the paper text
+ * (PAPER.md); "Rn"/"Dn" are the readings listed in DESIGN.md §3.
+ *
+ * Conventions for every entry point
+ *  - Tensor arguments are DEVICE pointers owned by the caller (the library never frees them and
+ *    keeps none after the call returns), row-major, densely packed, with the shapes stated.
+ *    bf16 tensors are passed as uint16_t (IEEE bfloat16 bit patterns).
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream) and
+ *    never synchronises the device.  Results are valid once the stream reaches the call.
+ *  - Return value: DYMOE_OK or an error code.  On error nothing is launched, and
+ *    dymoe_last_error() returns a thread-local message that names the offending argument.
+ *  - Inputs must be finite; behaviour on NaN/Inf inputs is undefined.
+ *  - Device-side faults that can only be detected while running (e.g. an expert assigned a width
+ *    whose packed weights are not resident) set a status word in the workspace, read back by
+ *    dymoe_check_status (the only call that synchronises, and only on `stream`).
+ */
+#ifndef DYMOE_H
+#define DYMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dymoe_stream_t; /* identical to cudaStream_t */
+
+enum {
+  DYMOE_OK = 0,
+  DYMOE_ERR_INVALID = 1,     /* argument validation failed; message names the field */
+  DYMOE_ERR_CUDA = 2,        /* a CUDA runtime call or launch failed */
+  DYMOE_ERR_NCCL = 3,        /* reserved for collective failures */
+  DYMOE_ERR_WORKSPACE = 4,   /* workspace too small or misaligned */
+  DYMOE_ERR_UNSUPPORTED = 5, /* shape or width outside what the kernels implement */
+  DYMOE_ERR_DEVICE = 6       /* dymoe_check_status: a device-side fault was recorded */
+};
+
+enum { DYMOE_PREFILL = 0, DYMOE_DECODE = 1 };
+enum { DYMOE_M_TOTAL = 0, DYMOE_M_ACTIVE = 1 };  /* reading D5: meaning of M in Eq. 5 */
+enum { DYMOE_OUT_F32 = 0, DYMOE_OUT_BF16 = 1 };
+
+/* device status word bits (dymoe_check_status) */
+enum { DYMOE_STATUS_WIDTH_NOT_RESIDENT = 1 };
+
+#define DYMOE_MAX_TIERS 5
+#define DYMOE_MAX_EXPERTS 256
+#define DYMOE_GROUP 128          /* quantization group along K (reading D15) */
+
+/* ------------------------------------------------------------------------------------------ */
+/* Routing ("the router selects a small subset of experts per token"; gate = Softmax(hW_g),
+ * Eq. 6; g_j "the routing weight assigned to expert E_j", Eq. 3).
+ *   logits   [T][M] f32  (the gate GEMM is outside the path, reading R19)
+ *   topk_idx [T][k] i32  out: experts ordered by (logit desc, index asc); -0.0 == +0.0
+ *   topk_w   [T][k] f32  out: softmax over the k selected logits (sums to 1)
+ *   probs    [T][M] f32  out, nullable: softmax over all M logits
+ * Constraints: T >= 0, 1 <= M <= 256, 1 <= k <= min(M, 8).                                      */
+int dymoe_route(const float* logits, int T, int M, int k, int32_t* topk_idx, float* topk_w,
+                float* probs, dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Expert importance (PAPER §4.2).
+ * PREFILL, token-guided (Eq. 1, Eq. 2):
+ *   S_i = sum_{h=0..H-1} attn_mass[h][i] (fp32, head order; R1b), T_imp = the k_tokens tokens
+ *   with the largest S (ties: lower index, R11), importance[j] = |{i in T_imp : j in topk_idx[i]}|
+ *   stored as exact integers in f32.
+ *   attn_mass [H][T] f32; topk_idx [T][k]; k_tokens = 0 means ceil(0.2 T) (R3);
+ *   heavy [k_tokens] i32 out, nullable: the members of T_imp in ascending token order;
+ *   scratch: device buffer of dymoe_score_scratch_bytes(T) bytes (prefill only, else nullable).
+ * DECODE, gate-guided (Eq. 3): logits [B=T][M] f32.
+ *   B == 1: importance = the logit row (order-equivalent to g = softmax, exact; D10).
+ *   B >  1: importance[j] = sum_b softmax(logits[b])[j], f32, b ascending.
+ * importance [M] f32 out.                                                                        */
+size_t dymoe_score_scratch_bytes(int T);
+int dymoe_score(int phase, const float* attn_mass, int H, const int32_t* topk_idx,
+                const float* logits, int T, int M, int k, int k_tokens, float* importance,
+                int32_t* heavy, void* scratch, dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Depth-aware precision scheduling (PAPER §4.3): retention r(l) = (1-λ)(cos(π l/(L-1))+1)/2 + λ
+ * (Eq. 4; L = 1 gives 1), t = ceil(r(l)·M_eff - 1e-9) (Eq. 5, reading D7),
+ * evaluated in fp64.  Tier ladder (reading D9): widths bits[0] > bits[1] > ... > bits[n-1]
+ * (each in {16,8,4,2,0}; 0 = skip, "4/0"), thresholds lambdas[0] <= ... <= lambdas[n-2]
+ * in [0,1].  Experts ranked by (importance desc, index asc); rank < t_1 -> bits[0],
+ * rank < t_2 -> bits[1], ..., else bits[n-1].  clamp_to_k: t_1 >= min(k_route, M_eff) (D8).
+ * m_mode TOTAL: M_eff = M; ACTIVE: M_eff = #experts with active_mask != 0, inactive experts
+ * get bits[n-1] (D5).  The paper's "4/2" is {bits = {4,2}, lambdas = {λ}}.                    */
+typedef struct dymoe_ladder {
+  int n_tiers;                         /* 1..5 */
+  int bits[DYMOE_MAX_TIERS];
+  double lambdas[DYMOE_MAX_TIERS - 1];
+  int clamp_to_k;                      /* D8 (default 1) */
+  int m_mode;                          /* D5: DYMOE_M_TOTAL or DYMOE_M_ACTIVE */
+  int renorm_on_skip;                  /* D12 (used by combine / moe_forward; default 1) */
+} dymoe_ladder;
+
+/* importance [M] f32 device; active_mask [M] u8 device (required in ACTIVE mode, else
+ * nullable); bits [M] u8 device out; tier_counts [n_tiers-1] host out, nullable — filled
+ * only in TOTAL mode (in ACTIVE mode the counts depend on device data).                        */
+int dymoe_assign_bits(const float* importance, int M, int layer, int num_layers,
+                      const dymoe_ladder* ladder, int k_route, const uint8_t* active_mask,
+                      uint8_t* bits, int32_t* tier_counts, dymoe_stream_t stream);
+
+/* Host helper: r(l) of Eq. 4 and the TOTAL-mode tier counts (no device work). */
+double dymoe_retention_ratio(int layer, int num_layers, double lambda);
+int dymoe_tier_counts(int layer, int num_layers, const dymoe_ladder* ladder, int M_eff,
+                      int k_route, int32_t* counts /* [n_tiers-1] */);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Group-wise quantization + packing (GPTQ's asymmetric min-max grid as round-to-nearest,
+ * readings D14-D16), fp32, exactly in this order per row n and group g of 128 weights along K:
+ *   mn = min(0, min w), mx = max(0, max w), s = (mx-mn)/maxq; if s < 2^-126: mn,mx = -1,+1 and
+ *   s recomputed (D14b); inv = 1/s; z = rint(-mn*inv); q = clamp(rint(w*inv) + z, 0, maxq)
+ *   (rint = half to even, maxq = 2^bits - 1).
+ *   W      [N][K] bf16
+ *   codes  [N][K*bits/32] u32 out: code k at bits (k % (32/bits))*bits of word k/(32/bits)
+ *   scales [N][K/128] f32 out;  zeros [N][K/128] u8 out
+ * Constraints: bits in {2,4,8}, group == 128, K % 128 == 0, N >= 0.                           */
+int dymoe_quantize(const uint16_t* W, int N, int K, int bits, int group, uint32_t* codes,
+                   float* scales, uint8_t* zeros, dymoe_stream_t stream);
+
+typedef struct dymoe_quant_job {
+  const uint16_t* W; int N; int K; int bits;
+  uint32_t* codes; float* scales; uint8_t* zeros;
+} dymoe_quant_job;
+/* Many matrices in one launch (e.g. W1/W3/W2 of every expert of a layer). jobs: host array. */
+int dymoe_quantize_batched(const dymoe_quant_job* jobs, int n_jobs, int group,
+                           dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Expert tables.  A quantized matrix [N][K] at width b (layout of dymoe_quantize): */
+typedef struct dymoe_qmat {
+  const uint32_t* codes;  /* NULL = this width is not resident */
+  const float* scales;
+  const uint8_t* zeros;
+} dymoe_qmat;
+
+/* One SwiGLU expert (reading D18): W1 (gate) and W3 (up) are [F][Hd], W2 (down) is [Hd][F].
+ * w1/w3/w2 are the bf16 masters (needed for the BF16 tier, nullable otherwise);
+ * q[wi][m]: width index wi (0 = Int8, 1 = Int4, 2 = Int2), matrix m (0 = W1, 1 = W3, 2 = W2).  */
+typedef struct dymoe_expert_desc {
+  const uint16_t* w1;
+  const uint16_t* w3;
+  const uint16_t* w2;
+  dymoe_qmat q[3][3];
+} dymoe_expert_desc;
+
+typedef struct dymoe_layer_desc {
+  int M;         /* experts, 1..256 */
+  int k_route;   /* routing top-k, 1..min(M,8) */
+  int hidden;    /* Hd, multiple of 128 */
+  int ffn;       /* F, multiple of 128 */
+  const dymoe_expert_desc* experts;  /* HOST array [M] (its pointers are device pointers) */
+} dymoe_layer_desc;
+
+/* Opaque handle holding a device copy of the expert table (created once per layer; the weights
+ * themselves stay caller-owned and must outlive the handle).  create synchronises once.       */
+typedef struct dymoe_layer dymoe_layer;
+int dymoe_layer_create(const dymoe_layer_desc* desc, dymoe_layer** out);
+int dymoe_layer_destroy(dymoe_layer* layer);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Token permutation (P:203 step 3, BASELINE.json "(c)"): the (token, slot) pairs are stably
+ * sorted by expert id (ties keep token-major order); pairs routed to an expert with bits == 0
+ * (skip, "4/0") are dropped.
+ *   topk_idx [T][k] i32; bits [M] u8 device
+ *   expert_off [M+1] i32 out: rows of expert e are [expert_off[e], expert_off[e+1])
+ *   perm_token, perm_slot [T*k] i32 out (first expert_off[M] valid)
+ *   inv_row [T][k] i32 out: row of pair (t, slot) or -1 if dropped                           */
+int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
+                  int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot, int32_t* inv_row,
+                  dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Expert FFN on the permuted rows (P:203 step 4 "the Model Executor operates on a unified
+ * mixed-precision weight set").  For each expert e with bits[e] > 0 and rows r in
+ * [expert_off[e], expert_off[e+1]):  A = x[perm_token[r]]·deq(W1_e)^T, B = x[..]·deq(W3_e)^T
+ * (fp32 accumulation), h = RNE_bf16(silu(A)*B) (O6), y_perm[r] = h·deq(W2_e)^T (fp32), with
+ * deq = RNE_bf16((q - z)·RNE_bf16(s)) (D17) or the bf16 master for bits == 16.
+ *   x [T][Hd] bf16; h_ws [T*k][F] bf16 scratch (intermediate); y_perm [T*k][Hd] f32 out.
+ * mode: DYMOE_DECODE = fused-dequant GEMV kernels (intended for <= 8 rows per expert),
+ *       DYMOE_PREFILL = fused-dequant tcgen05 grouped GEMM.  Both compute the same function.
+ * status: device u32 word (nullable) receiving DYMOE_STATUS_* bits.                           */
+int dymoe_expert_ffn(const dymoe_layer* layer, int mode, const uint16_t* x, int T,
+                     const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,
+                     uint16_t* h_ws, float* y_perm, uint32_t* status, dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Combine ("0-bit" experts; reading D12): E_t = {slots with inv_row >= 0};
+ * w' = topk_w / sum_{E_t} topk_w if renorm else topk_w; y[t] = sum over slots in order of
+ * w'·y_perm[inv_row[t][slot]]; E_t empty -> y[t] = 0.  y [T][Hd] f32 or bf16 (out_dtype).     */
+int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w, int T,
+                  int k, int Hd, int renorm, int out_dtype, void* y, dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* The whole layer, one step: route -> score -> assign -> permute -> FFN
+ * -> combine, all on `stream` with no host synchronisation (graph-capturable).               */
+typedef struct dymoe_fwd_opts {
+  int phase;                 /* DYMOE_PREFILL (Eq. 1-2) or DYMOE_DECODE (Eq. 3) */
+  int layer, num_layers;     /* l and L of Eq. 4 */
+  dymoe_ladder ladder;
+  const float* attn_mass;    /* prefill: [heads][T] f32 (R1) */
+  int heads;
+  int k_tokens;              /* prefill: 0 => ceil(0.2 T) */
+  int ffn_mode;              /* -1 = choose (DECODE kernels when phase == DECODE), else as in
+                                dymoe_expert_ffn */
+  int out_dtype;             /* DYMOE_OUT_F32 (parity) or DYMOE_OUT_BF16 */
+  const uint8_t* forced_bits;/* device [M], nullable: bypass score/assign (uniform sweeps) */
+  void* prof_events[3];      /* nullable cudaEvent_t's recorded on `stream` before the gate/up
+                                (W1/W3) FFN kernel, between it and the down (W2) kernel, and
+                                after the down kernel (live per-kernel timing for benchmarks) */
+} dymoe_fwd_opts;
+
+/* Workspace: one device buffer of dymoe_workspace_size(...) bytes (256-byte aligned); it holds
+ * every intermediate.  dymoe_workspace_views returns pointers into it (valid after the step
+ * completes on the stream) for inspection: */
+typedef struct dymoe_ws_views {
+  int32_t* topk_idx;   /* [T][k] */
+  float* topk_w;       /* [T][k] */
+  float* probs;        /* [T][M] */
+  float* importance;   /* [M] */
+  int32_t* heavy;      /* [k_tokens] (prefill) */
+  uint8_t* bits;       /* [M] */
+  uint8_t* active;     /* [M] */
+  int32_t* expert_off; /* [M+1] */
+  int32_t* perm_token; /* [T*k] */
+  int32_t* perm_slot;  /* [T*k] */
+  int32_t* inv_row;    /* [T][k] */
+  uint16_t* h;         /* [T*k][F] */
+  float* y_perm;       /* [T*k][Hd] */
+  uint32_t* status;    /* [1] */
+  void* score_scratch;
+} dymoe_ws_views;
+
+size_t dymoe_workspace_size(const dymoe_layer* layer, int T);
+int dymoe_workspace_views(const dymoe_layer* layer, int T, void* workspace,
+                          dymoe_ws_views* views);
+
+/* x [T][Hd] bf16, logits [T][M] f32, y [T][Hd] (out_dtype).  T = 0 is a no-op. */
+int dymoe_moe_forward(const dymoe_layer* layer, const uint16_t* x, const float* logits, int T,
+                      const dymoe_fwd_opts* opts, void* y, void* workspace, size_t ws_bytes,
+                      dymoe_stream_t stream);
+
+/* Synchronises `stream`, returns DYMOE_OK or DYMOE_ERR_DEVICE if a status bit is set in the
+ * workspace's status word (*bits_out receives the word, nullable); clears the word.           */
+int dymoe_check_status(const dymoe_layer* layer, int T, void* workspace, uint32_t* bits_out,
+                       dymoe_stream_t stream);
+
+/* Last error message of the calling thread ("" if none). */
+const char* dymoe_last_error(void);
+/* Library version string. */
+const char* dymoe_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYMOE_H */

@@ -1,0 +1,562 @@
+// Host side of the C ABI declared in include/dymoe.h: argument validation (messages name the
+// offending field), the fp64 depth-aware schedule (Eq. 4-5), workspace layout, the expert-table
+// handle, and launch orchestration of the per-step kernels on the caller's stream.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "dymoe_internal.cuh"
+
+using namespace dymoe;
+
+struct dymoe_layer {
+  int M, k, Hd, F;
+  std::vector<DevExpert> host;
+  DevExpert* dev = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int ok() {
+  g_err.clear();
+  return DYMOE_OK;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(DYMOE_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define CHECK_ARG(cond, ...) \
+  do {                       \
+    if (!(cond)) return fail(DYMOE_ERR_INVALID, __VA_ARGS__); \
+  } while (0)
+
+#define CHECK_LAUNCH(expr, where)                    \
+  do {                                               \
+    cudaError_t _e = (expr);                         \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+bool valid_width(int b) { return b == 16 || b == 8 || b == 4 || b == 2 || b == 0; }
+
+int check_ladder(const dymoe_ladder* L) {
+  CHECK_ARG(L != nullptr, "ladder: must not be NULL");
+  CHECK_ARG(L->n_tiers >= 1 && L->n_tiers <= DYMOE_MAX_TIERS, "ladder.n_tiers: must be in [1, %d]",
+            DYMOE_MAX_TIERS);
+  for (int i = 0; i < L->n_tiers; ++i)
+    CHECK_ARG(valid_width(L->bits[i]), "ladder.bits[%d]: %d is not one of 16, 8, 4, 2, 0", i,
+              L->bits[i]);
+  for (int i = 0; i + 1 < L->n_tiers; ++i) {
+    CHECK_ARG(L->bits[i] > L->bits[i + 1], "ladder.bits: widths must be strictly decreasing");
+    CHECK_ARG(L->lambdas[i] >= 0.0 && L->lambdas[i] <= 1.0,
+              "ladder.lambdas[%d]: must lie in [0, 1]", i);
+    if (i > 0)
+      CHECK_ARG(L->lambdas[i] >= L->lambdas[i - 1], "ladder.lambdas: must be non-decreasing");
+  }
+  CHECK_ARG(L->m_mode == DYMOE_M_TOTAL || L->m_mode == DYMOE_M_ACTIVE,
+            "ladder.m_mode: must be DYMOE_M_TOTAL or DYMOE_M_ACTIVE");
+  return DYMOE_OK;
+}
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct WsLayout {
+  size_t topk_idx, topk_w, probs, importance, heavy, bits, active, active_list, expert_off,
+      perm_token, perm_slot, inv_row, h, y_perm, status, score_scratch, total;
+};
+
+WsLayout ws_layout(int M, int k, int Hd, int F, int T) {
+  WsLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes);
+    return at;
+  };
+  const size_t TK = (size_t)T * k;
+  L.topk_idx = take(TK * 4);
+  L.topk_w = take(TK * 4);
+  L.probs = take((size_t)T * M * 4);
+  L.importance = take((size_t)M * 4);
+  L.heavy = take((size_t)T * 4);
+  L.bits = take((size_t)M);
+  L.active = take((size_t)M);
+  L.active_list = take((size_t)(M + 1) * 4);
+  L.expert_off = take((size_t)(M + 1) * 4);
+  L.perm_token = take(TK * 4);
+  L.perm_slot = take(TK * 4);
+  L.inv_row = take(TK * 4);
+  L.h = take(TK * F * 2);
+  L.y_perm = take(TK * Hd * 4);
+  L.status = take(4);
+  L.score_scratch = take((size_t)T * 4);
+  L.total = o;
+  return L;
+}
+
+cudaStream_t S(dymoe_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_ptr_align(const void* p, size_t a, const char* name) {
+  CHECK_ARG(((uintptr_t)p % a) == 0, "%s: must be %zu-byte aligned", name, a);
+  return DYMOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dymoe_last_error(void) { return g_err.c_str(); }
+const char* dymoe_version(void) { return "dymoe-b200 0.1 (sm_100a)"; }
+
+// ------------------------------------------------------------------------------------------
+int dymoe_route(const float* logits, int T, int M, int k, int32_t* topk_idx, float* topk_w,
+                float* probs, dymoe_stream_t stream) {
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(k >= 1 && k <= M && k <= 8, "k: must satisfy 1 <= k <= min(M, 8)");
+  if (T > 0) {
+    CHECK_ARG(logits != nullptr, "logits: must not be NULL");
+    CHECK_ARG(topk_idx != nullptr, "topk_idx: must not be NULL");
+    CHECK_ARG(topk_w != nullptr, "topk_w: must not be NULL");
+  }
+  CHECK_LAUNCH(launch_route(logits, T, M, k, topk_idx, topk_w, probs, S(stream)), "dymoe_route");
+  return ok();
+}
+
+size_t dymoe_score_scratch_bytes(int T) { return (size_t)(T > 0 ? T : 1) * 4; }
+
+int dymoe_score(int phase, const float* attn_mass, int H, const int32_t* topk_idx,
+                const float* logits, int T, int M, int k, int k_tokens, float* importance,
+                int32_t* heavy, void* scratch, dymoe_stream_t stream) {
+  CHECK_ARG(phase == DYMOE_PREFILL || phase == DYMOE_DECODE, "phase: must be DYMOE_PREFILL or DYMOE_DECODE");
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(importance != nullptr, "importance: must not be NULL");
+  if (phase == DYMOE_PREFILL) {
+    CHECK_ARG(k >= 1 && k <= M, "k: must satisfy 1 <= k <= M");
+    CHECK_ARG(H >= 1, "H: must be >= 1");
+    if (k_tokens == 0) k_tokens = (T + 4) / 5;
+    CHECK_ARG(k_tokens >= 0 && k_tokens <= T, "k_tokens: must satisfy 0 <= k_tokens <= T");
+    if (T > 0) {
+      CHECK_ARG(attn_mass != nullptr, "attn_mass: must not be NULL in PREFILL");
+      CHECK_ARG(topk_idx != nullptr, "topk_idx: must not be NULL in PREFILL");
+      CHECK_ARG(scratch != nullptr, "scratch: must not be NULL in PREFILL");
+    }
+    CHECK_LAUNCH(launch_score_prefill(attn_mass, H, topk_idx, T, M, k, k_tokens, importance,
+                                      heavy, reinterpret_cast<float*>(scratch), S(stream)),
+                 "dymoe_score");
+  } else {
+    CHECK_ARG(T >= 1, "T: DECODE needs at least one token");
+    CHECK_ARG(logits != nullptr, "logits: must not be NULL in DECODE");
+    CHECK_LAUNCH(launch_score_decode(logits, T, M, importance, S(stream)), "dymoe_score");
+  }
+  return ok();
+}
+
+// ------------------------------------------------------------------------------------------
+double dymoe_retention_ratio(int layer, int num_layers, double lambda) {
+  if (num_layers <= 1) return 1.0;
+  const double pi = 3.14159265358979323846;
+  return (1.0 - lambda) * (std::cos(pi * (double)layer / (double)(num_layers - 1)) + 1.0) / 2.0 +
+         lambda;
+}
+
+int dymoe_tier_counts(int layer, int num_layers, const dymoe_ladder* ladder, int M_eff,
+                      int k_route, int32_t* counts) {
+  int rc = check_ladder(ladder);
+  if (rc) return rc;
+  CHECK_ARG(num_layers >= 1, "num_layers: must be >= 1");
+  CHECK_ARG(layer >= 0 && layer < num_layers, "layer: must satisfy 0 <= layer < num_layers");
+  CHECK_ARG(M_eff >= 0, "M_eff: must be >= 0");
+  CHECK_ARG(counts != nullptr || ladder->n_tiers == 1, "counts: must not be NULL");
+  int prev = 0;
+  for (int q = 0; q + 1 < ladder->n_tiers; ++q) {
+    const double r = dymoe_retention_ratio(layer, num_layers, ladder->lambdas[q]);
+    int t = (int)std::ceil(r * (double)M_eff - 1e-9);
+    if (q == 0 && ladder->clamp_to_k) t = std::max(t, std::min(k_route, M_eff));
+    t = std::max(t, prev);
+    t = std::min(t, M_eff);
+    prev = t;
+    counts[q] = t;
+  }
+  return ok();
+}
+
+static int fill_assign_params(const dymoe_ladder* ladder, int M, int k_route, int layer,
+                              int num_layers, AssignParams& p) {
+  int rc = check_ladder(ladder);
+  if (rc) return rc;
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(num_layers >= 1, "num_layers: must be >= 1");
+  CHECK_ARG(layer >= 0 && layer < num_layers, "layer: must satisfy 0 <= layer < num_layers");
+  CHECK_ARG(k_route >= 1 && k_route <= M, "k_route: must satisfy 1 <= k_route <= M");
+  p.M = M;
+  p.k_route = k_route;
+  p.n_tiers = ladder->n_tiers;
+  p.clamp_to_k = ladder->clamp_to_k;
+  p.m_active = ladder->m_mode == DYMOE_M_ACTIVE;
+  for (int i = 0; i < DYMOE_MAX_TIERS; ++i) p.bits[i] = i < ladder->n_tiers ? ladder->bits[i] : 0;
+  for (int i = 0; i + 1 < DYMOE_MAX_TIERS; ++i)
+    p.r[i] = i + 1 < ladder->n_tiers ? dymoe_retention_ratio(layer, num_layers, ladder->lambdas[i])
+                                     : 0.0;
+  return DYMOE_OK;
+}
+
+int dymoe_assign_bits(const float* importance, int M, int layer, int num_layers,
+                      const dymoe_ladder* ladder, int k_route, const uint8_t* active_mask,
+                      uint8_t* bits, int32_t* tier_counts, dymoe_stream_t stream) {
+  AssignParams p{};
+  int rc = fill_assign_params(ladder, M, k_route, layer, num_layers, p);
+  if (rc) return rc;
+  CHECK_ARG(importance != nullptr, "importance: must not be NULL");
+  CHECK_ARG(bits != nullptr, "bits: must not be NULL");
+  CHECK_ARG(!p.m_active || active_mask != nullptr, "active_mask: required in DYMOE_M_ACTIVE mode");
+  if (tier_counts != nullptr && !p.m_active) {
+    rc = dymoe_tier_counts(layer, num_layers, ladder, M, k_route, tier_counts);
+    if (rc) return rc;
+  }
+  CHECK_LAUNCH(launch_assign(importance, active_mask, nullptr, 0, p, bits, nullptr, S(stream)),
+               "dymoe_assign_bits");
+  return ok();
+}
+
+// ------------------------------------------------------------------------------------------
+static int check_quant_job(const dymoe_quant_job& j, int idx, int group) {
+  CHECK_ARG(group == DYMOE_GROUP, "group: only %d is supported", DYMOE_GROUP);
+  CHECK_ARG(j.bits == 2 || j.bits == 4 || j.bits == 8, "jobs[%d].bits: must be 2, 4 or 8", idx);
+  CHECK_ARG(j.N >= 0, "jobs[%d].N: must be >= 0", idx);
+  CHECK_ARG(j.K > 0 && j.K % DYMOE_GROUP == 0, "jobs[%d].K: must be a positive multiple of %d", idx,
+            DYMOE_GROUP);
+  if (j.N > 0) {
+    CHECK_ARG(j.W != nullptr, "jobs[%d].W: must not be NULL", idx);
+    CHECK_ARG(j.codes != nullptr, "jobs[%d].codes: must not be NULL", idx);
+    CHECK_ARG(j.scales != nullptr, "jobs[%d].scales: must not be NULL", idx);
+    CHECK_ARG(j.zeros != nullptr, "jobs[%d].zeros: must not be NULL", idx);
+    int rc = check_ptr_align(j.W, 16, "W");
+    if (rc) return rc;
+    rc = check_ptr_align(j.codes, 16, "codes");
+    if (rc) return rc;
+  }
+  return DYMOE_OK;
+}
+
+int dymoe_quantize(const uint16_t* W, int N, int K, int bits, int group, uint32_t* codes,
+                   float* scales, uint8_t* zeros, dymoe_stream_t stream) {
+  dymoe_quant_job j{W, N, K, bits, codes, scales, zeros};
+  int rc = check_quant_job(j, 0, group);
+  if (rc) {
+    // rename "jobs[0]." to the flat argument names
+    std::string m = g_err;
+    const std::string pre = "jobs[0].";
+    if (m.compare(0, pre.size(), pre) == 0) g_err = m.substr(pre.size());
+    return rc;
+  }
+  CHECK_LAUNCH(launch_quantize(&j, 1, S(stream)), "dymoe_quantize");
+  return ok();
+}
+
+int dymoe_quantize_batched(const dymoe_quant_job* jobs, int n_jobs, int group,
+                           dymoe_stream_t stream) {
+  CHECK_ARG(n_jobs >= 0, "n_jobs: must be >= 0");
+  CHECK_ARG(jobs != nullptr || n_jobs == 0, "jobs: must not be NULL");
+  for (int i = 0; i < n_jobs; ++i) {
+    int rc = check_quant_job(jobs[i], i, group);
+    if (rc) return rc;
+  }
+  CHECK_LAUNCH(launch_quantize(jobs, n_jobs, S(stream)), "dymoe_quantize_batched");
+  return ok();
+}
+
+// ------------------------------------------------------------------------------------------
+int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
+  CHECK_ARG(out != nullptr, "out: must not be NULL");
+  *out = nullptr;
+  CHECK_ARG(d != nullptr, "desc: must not be NULL");
+  CHECK_ARG(d->M >= 1 && d->M <= DYMOE_MAX_EXPERTS, "desc.M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(d->k_route >= 1 && d->k_route <= d->M && d->k_route <= 8,
+            "desc.k_route: must satisfy 1 <= k_route <= min(M, 8)");
+  CHECK_ARG(d->hidden > 0 && d->hidden % 128 == 0, "desc.hidden: must be a positive multiple of 128");
+  CHECK_ARG(d->ffn > 0 && d->ffn % 128 == 0, "desc.ffn: must be a positive multiple of 128");
+  CHECK_ARG(d->experts != nullptr, "desc.experts: must not be NULL");
+  dymoe_layer* L = new (std::nothrow) dymoe_layer();
+  if (!L) return fail(DYMOE_ERR_INVALID, "out of host memory");
+  L->M = d->M;
+  L->k = d->k_route;
+  L->Hd = d->hidden;
+  L->F = d->ffn;
+  L->host.resize(d->M);
+  for (int e = 0; e < d->M; ++e) {
+    const dymoe_expert_desc& x = d->experts[e];
+    DevExpert& y = L->host[e];
+    y.w[0] = x.w1;
+    y.w[1] = x.w3;
+    y.w[2] = x.w2;
+    for (int wi = 0; wi < 3; ++wi)
+      for (int m = 0; m < 3; ++m) {
+        y.q[wi][m].codes = x.q[wi][m].codes;
+        y.q[wi][m].scales = x.q[wi][m].scales;
+        y.q[wi][m].zeros = x.q[wi][m].zeros;
+        if (x.q[wi][m].codes != nullptr && (x.q[wi][m].scales == nullptr || x.q[wi][m].zeros == nullptr)) {
+          delete L;
+          return fail(DYMOE_ERR_INVALID, "desc.experts[%d].q[%d][%d]: scales/zeros must be set with codes", e, wi, m);
+        }
+        if (((uintptr_t)x.q[wi][m].codes) % 16) {
+          delete L;
+          return fail(DYMOE_ERR_INVALID, "desc.experts[%d].q[%d][%d].codes: must be 16-byte aligned", e, wi, m);
+        }
+      }
+    for (int m = 0; m < 3; ++m)
+      if (((uintptr_t)y.w[m]) % 16) {
+        delete L;
+        return fail(DYMOE_ERR_INVALID, "desc.experts[%d].w%d: must be 16-byte aligned", e, m == 0 ? 1 : m == 1 ? 3 : 2);
+      }
+  }
+  cudaError_t e = cudaMalloc(&L->dev, sizeof(DevExpert) * d->M);
+  if (e != cudaSuccess) {
+    delete L;
+    return cuda_fail(e, "dymoe_layer_create");
+  }
+  e = cudaMemcpy(L->dev, L->host.data(), sizeof(DevExpert) * d->M, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(L->dev);
+    delete L;
+    return cuda_fail(e, "dymoe_layer_create");
+  }
+  *out = L;
+  return ok();
+}
+
+int dymoe_layer_destroy(dymoe_layer* L) {
+  if (!L) return ok();
+  if (L->dev) cudaFree(L->dev);
+  delete L;
+  return ok();
+}
+
+// ------------------------------------------------------------------------------------------
+int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
+                  int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot, int32_t* inv_row,
+                  dymoe_stream_t stream) {
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(k >= 1 && k <= M, "k: must satisfy 1 <= k <= M");
+  CHECK_ARG(bits != nullptr, "bits: must not be NULL");
+  CHECK_ARG(expert_off != nullptr, "expert_off: must not be NULL");
+  if (T > 0) {
+    CHECK_ARG(topk_idx != nullptr, "topk_idx: must not be NULL");
+    CHECK_ARG(perm_token && perm_slot && inv_row, "perm_token/perm_slot/inv_row: must not be NULL");
+  }
+  // the active list is an internal by-product; use a small temporary
+  int32_t* active = nullptr;
+  cudaError_t e = cudaMallocAsync(&active, (M + 1) * sizeof(int32_t), S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dymoe_permute");
+  e = launch_permute(topk_idx, T, k, M, bits, expert_off, perm_token, perm_slot, inv_row, active,
+                     S(stream));
+  cudaFreeAsync(active, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dymoe_permute");
+  return ok();
+}
+
+int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w, int T, int k,
+                  int Hd, int renorm, int out_dtype, void* y, dymoe_stream_t stream) {
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(k >= 1 && k <= 8, "k: must be in [1, 8]");
+  CHECK_ARG(Hd > 0 && Hd % 4 == 0, "Hd: must be a positive multiple of 4");
+  CHECK_ARG(out_dtype == DYMOE_OUT_F32 || out_dtype == DYMOE_OUT_BF16, "out_dtype: must be DYMOE_OUT_F32 or DYMOE_OUT_BF16");
+  if (T > 0) {
+    CHECK_ARG(y_perm && inv_row && topk_w && y, "y_perm/inv_row/topk_w/y: must not be NULL");
+    int rc = check_ptr_align(y_perm, 16, "y_perm");
+    if (rc) return rc;
+  }
+  CHECK_LAUNCH(launch_combine(y_perm, inv_row, topk_w, T, k, Hd, renorm, out_dtype, y, S(stream)),
+               "dymoe_combine");
+  return ok();
+}
+
+static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, const uint8_t* bits,
+                   const int32_t* expert_off, const int32_t* perm_token, const int32_t* active_list,
+                   uint16_t* h, float* y_perm, uint32_t* status, cudaStream_t s,
+                   void* const* ev = nullptr) {
+  FfnArgs a{};
+  a.experts = L->dev;
+  a.M = L->M;
+  a.k = L->k;
+  a.Hd = L->Hd;
+  a.F = L->F;
+  a.x = x;
+  a.T = T;
+  a.bits = bits;
+  a.expert_off = expert_off;
+  a.perm_token = perm_token;
+  a.active_list = active_list;
+  a.h = h;
+  a.y_perm = y_perm;
+  a.status = status;
+  if (T == 0) return DYMOE_OK;
+  cudaError_t e = mode == DYMOE_PREFILL ? launch_ffn_prefill(a, s, ev) : launch_ffn_decode(a, s, ev);
+  if (e != cudaSuccess) return cuda_fail(e, "expert ffn");
+  return DYMOE_OK;
+}
+
+// Builds the active list (experts with rows) from expert_off on device.
+__global__ void k_active_from_off(const int32_t* __restrict__ off, int M, int32_t* list) {
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int e = 0; e < M; ++e)
+      if (off[e + 1] > off[e]) list[1 + n++] = e;
+    list[0] = n;
+  }
+}
+
+int dymoe_expert_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T,
+                     const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,
+                     uint16_t* h_ws, float* y_perm, uint32_t* status, dymoe_stream_t stream) {
+  CHECK_ARG(L != nullptr, "layer: must not be NULL");
+  CHECK_ARG(mode == DYMOE_PREFILL || mode == DYMOE_DECODE, "mode: must be DYMOE_PREFILL or DYMOE_DECODE");
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  if (T == 0) return ok();
+  CHECK_ARG(x && bits && expert_off && perm_token && h_ws && y_perm,
+            "x/bits/expert_off/perm_token/h_ws/y_perm: must not be NULL");
+  int rc = check_ptr_align(x, 16, "x");
+  if (rc) return rc;
+  int32_t* active = nullptr;
+  cudaError_t e = cudaMallocAsync(&active, (L->M + 1) * sizeof(int32_t), S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dymoe_expert_ffn");
+  k_active_from_off<<<1, 32, 0, S(stream)>>>(expert_off, L->M, active);
+  rc = run_ffn(L, mode, x, T, bits, expert_off, perm_token, active, h_ws, y_perm, status, S(stream));
+  cudaFreeAsync(active, S(stream));
+  if (rc) return rc;
+  return ok();
+}
+
+// ------------------------------------------------------------------------------------------
+size_t dymoe_workspace_size(const dymoe_layer* L, int T) {
+  if (!L || T < 0) return 0;
+  return ws_layout(L->M, L->k, L->Hd, L->F, T).total;
+}
+
+int dymoe_workspace_views(const dymoe_layer* L, int T, void* ws, dymoe_ws_views* v) {
+  CHECK_ARG(L != nullptr, "layer: must not be NULL");
+  CHECK_ARG(v != nullptr, "views: must not be NULL");
+  CHECK_ARG(ws != nullptr, "workspace: must not be NULL");
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  const WsLayout W = ws_layout(L->M, L->k, L->Hd, L->F, T);
+  char* b = reinterpret_cast<char*>(ws);
+  v->topk_idx = reinterpret_cast<int32_t*>(b + W.topk_idx);
+  v->topk_w = reinterpret_cast<float*>(b + W.topk_w);
+  v->probs = reinterpret_cast<float*>(b + W.probs);
+  v->importance = reinterpret_cast<float*>(b + W.importance);
+  v->heavy = reinterpret_cast<int32_t*>(b + W.heavy);
+  v->bits = reinterpret_cast<uint8_t*>(b + W.bits);
+  v->active = reinterpret_cast<uint8_t*>(b + W.active);
+  v->expert_off = reinterpret_cast<int32_t*>(b + W.expert_off);
+  v->perm_token = reinterpret_cast<int32_t*>(b + W.perm_token);
+  v->perm_slot = reinterpret_cast<int32_t*>(b + W.perm_slot);
+  v->inv_row = reinterpret_cast<int32_t*>(b + W.inv_row);
+  v->h = reinterpret_cast<uint16_t*>(b + W.h);
+  v->y_perm = reinterpret_cast<float*>(b + W.y_perm);
+  v->status = reinterpret_cast<uint32_t*>(b + W.status);
+  v->score_scratch = b + W.score_scratch;
+  return ok();
+}
+
+int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logits, int T,
+                      const dymoe_fwd_opts* o, void* y, void* ws, size_t ws_bytes,
+                      dymoe_stream_t stream) {
+  CHECK_ARG(L != nullptr, "layer: must not be NULL");
+  CHECK_ARG(o != nullptr, "opts: must not be NULL");
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(o->phase == DYMOE_PREFILL || o->phase == DYMOE_DECODE, "opts.phase: must be DYMOE_PREFILL or DYMOE_DECODE");
+  CHECK_ARG(o->out_dtype == DYMOE_OUT_F32 || o->out_dtype == DYMOE_OUT_BF16, "opts.out_dtype: must be DYMOE_OUT_F32 or DYMOE_OUT_BF16");
+  CHECK_ARG(o->ffn_mode == -1 || o->ffn_mode == DYMOE_PREFILL || o->ffn_mode == DYMOE_DECODE,
+            "opts.ffn_mode: must be -1, DYMOE_PREFILL or DYMOE_DECODE");
+  AssignParams ap{};
+  int rc = fill_assign_params(&o->ladder, L->M, L->k, o->layer, o->num_layers, ap);
+  if (rc) {
+    g_err = "opts." + g_err;
+    return rc;
+  }
+  if (T == 0) return ok();
+  CHECK_ARG(x != nullptr, "x: must not be NULL");
+  CHECK_ARG(logits != nullptr, "logits: must not be NULL");
+  CHECK_ARG(y != nullptr, "y: must not be NULL");
+  CHECK_ARG(ws != nullptr, "workspace: must not be NULL");
+  rc = check_ptr_align(x, 16, "x");
+  if (rc) return rc;
+  rc = check_ptr_align(ws, 256, "workspace");
+  if (rc) return rc;
+  const WsLayout W = ws_layout(L->M, L->k, L->Hd, L->F, T);
+  if (ws_bytes < W.total)
+    return fail(DYMOE_ERR_WORKSPACE, "ws_bytes: %zu < dymoe_workspace_size() = %zu", ws_bytes, W.total);
+  int k_tokens = o->k_tokens;
+  if (o->phase == DYMOE_PREFILL) {
+    CHECK_ARG(o->attn_mass != nullptr, "opts.attn_mass: must not be NULL in PREFILL");
+    CHECK_ARG(o->heads >= 1, "opts.heads: must be >= 1");
+    if (k_tokens == 0) k_tokens = (T + 4) / 5;
+    CHECK_ARG(k_tokens >= 0 && k_tokens <= T, "opts.k_tokens: must satisfy 0 <= k_tokens <= T");
+  }
+  dymoe_ws_views v{};
+  dymoe_workspace_views(L, T, ws, &v);
+  int32_t* active_list = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + W.active_list);
+  cudaStream_t s = S(stream);
+
+  CHECK_LAUNCH(launch_route(logits, T, L->M, L->k, v.topk_idx, v.topk_w, v.probs, s), "route");
+  const uint8_t* bits = o->forced_bits;
+  if (bits == nullptr) {
+    if (o->phase == DYMOE_PREFILL) {
+      CHECK_LAUNCH(launch_score_prefill(o->attn_mass, o->heads, v.topk_idx, T, L->M, L->k, k_tokens,
+                                        v.importance, v.heavy,
+                                        reinterpret_cast<float*>(v.score_scratch), s),
+                   "score");
+    } else {
+      CHECK_LAUNCH(launch_score_decode(logits, T, L->M, v.importance, s), "score");
+    }
+    CHECK_LAUNCH(launch_assign(v.importance, nullptr, v.topk_idx, T, ap, v.bits, v.active, s), "assign");
+    bits = v.bits;
+  }
+  CHECK_LAUNCH(launch_permute(v.topk_idx, T, L->k, L->M, bits, v.expert_off, v.perm_token,
+                              v.perm_slot, v.inv_row, active_list, s),
+               "permute");
+  const int mode = o->ffn_mode == -1 ? o->phase : o->ffn_mode;
+  rc = run_ffn(L, mode, x, T, bits, v.expert_off, v.perm_token, active_list, v.h, v.y_perm,
+               v.status, s, o->prof_events);
+  if (rc) return rc;
+  CHECK_LAUNCH(launch_combine(v.y_perm, v.inv_row, v.topk_w, T, L->k, L->Hd,
+                              o->ladder.renorm_on_skip, o->out_dtype, y, s),
+               "combine");
+  return ok();
+}
+
+int dymoe_check_status(const dymoe_layer* L, int T, void* ws, uint32_t* bits_out,
+                       dymoe_stream_t stream) {
+  CHECK_ARG(L != nullptr, "layer: must not be NULL");
+  CHECK_ARG(ws != nullptr, "workspace: must not be NULL");
+  const WsLayout W = ws_layout(L->M, L->k, L->Hd, L->F, T);
+  uint32_t word = 0;
+  uint32_t* dptr = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) + W.status);
+  cudaError_t e = cudaMemcpyAsync(&word, dptr, 4, cudaMemcpyDeviceToHost, S(stream));
+  if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+  if (e == cudaSuccess) e = cudaMemsetAsync(dptr, 0, 4, S(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "dymoe_check_status");
+  if (bits_out) *bits_out = word;
+  if (word) return fail(DYMOE_ERR_DEVICE, "device status word 0x%x (bit 1: an assigned width is not resident)", word);
+  return ok();
+}
+
+}  // extern "C"

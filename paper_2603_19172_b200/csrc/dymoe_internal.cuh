@@ -1,0 +1,90 @@
+// Internal declarations shared by the DyMoE sm_100a kernels and the C-ABI host layer.
+// Nothing here is visible through include/dymoe.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#include "../../include/dymoe.h"
+
+namespace dymoe {
+
+// ------------------------------------------------------------------------------------------
+// Device-side expert table (one entry per expert; copied to device by dymoe_layer_create).
+struct DevQMat {
+  const uint32_t* codes;
+  const float* scales;
+  const uint8_t* zeros;
+};
+struct DevExpert {
+  const uint16_t* w[3];   // bf16 masters W1, W3, W2
+  DevQMat q[3][3];        // [width idx: int8, int4, int2][matrix: W1, W3, W2]
+};
+
+__host__ __device__ inline int width_index(int bits) {
+  return bits == 8 ? 0 : bits == 4 ? 1 : bits == 2 ? 2 : -1;
+}
+
+// ------------------------------------------------------------------------------------------
+// Launchers (each returns cudaGetLastError() of its launch).
+cudaError_t launch_route(const float* logits, int T, int M, int k, int32_t* topk_idx,
+                         float* topk_w, float* probs, cudaStream_t s);
+
+cudaError_t launch_score_prefill(const float* attn, int H, const int32_t* topk_idx, int T,
+                                 int M, int k, int k_tokens, float* importance, int32_t* heavy,
+                                 float* S_scratch, cudaStream_t s);
+cudaError_t launch_score_decode(const float* logits, int B, int M, float* importance,
+                                cudaStream_t s);
+
+struct AssignParams {
+  int M, k_route, n_tiers, clamp_to_k, m_active;
+  int bits[DYMOE_MAX_TIERS];
+  double r[DYMOE_MAX_TIERS - 1];   // host-evaluated Eq. 4 per threshold
+};
+// active_mask (nullable) or, when active_mask == nullptr and m_active, the mask is derived
+// from topk_idx [T][k].  active_out (nullable) receives the derived mask.
+cudaError_t launch_assign(const float* importance, const uint8_t* active_mask,
+                          const int32_t* topk_idx, int T, const AssignParams& p, uint8_t* bits,
+                          uint8_t* active_out, cudaStream_t s);
+
+cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaStream_t s);
+
+cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
+                           int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot,
+                           int32_t* inv_row, int32_t* active_list, cudaStream_t s);
+
+struct FfnArgs {
+  const DevExpert* experts;
+  int M, k, Hd, F;
+  const uint16_t* x;           // [T][Hd]
+  int T;
+  const uint8_t* bits;         // [M]
+  const int32_t* expert_off;   // [M+1]
+  const int32_t* perm_token;   // [T*k]
+  const int32_t* active_list;  // [M+1]: [0] = count, then expert ids
+  uint16_t* h;                 // [T*k][F]
+  float* y_perm;               // [T*k][Hd]
+  uint32_t* status;
+};
+// ev (nullable, 3 entries, each nullable): recorded before W13, between W13 and W2, after W2.
+cudaError_t launch_ffn_decode(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
+cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
+
+inline void record_ev(void* const* ev, int i, cudaStream_t s) {
+  if (ev != nullptr && ev[i] != nullptr) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
+}
+
+cudaError_t launch_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w,
+                           int T, int k, int Hd, int renorm, int out_dtype, void* y,
+                           cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// Small device helpers.
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t l;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
+}  // namespace dymoe

@@ -1,0 +1,149 @@
+// Token permutation (row a5) and weighted combine (row a8) for sm_100a.
+//
+// Permute (P:203 step 3; BASELINE.json "(c)"): stable counting sort of the T*k (token, slot)
+// pairs by expert id; pairs routed to a skipped expert (bits == 0, "4/0") are dropped.
+// One CTA of 1024 threads walks the pairs in token-major chunks of 1024; inside a chunk the
+// stable rank of a pair among same-expert pairs is (running offset) + (same-expert pairs in
+// earlier warps, from a per-warp histogram in shared memory) + (same-expert lanes before it,
+// from __match_any_sync).  Integer-only, bit-exact by construction.
+//
+// Combine (reading D12): y[t] = sum_slot w'[t,slot] * y_perm[inv_row[t,slot]], slot order, fp32.
+#include "../dymoe_internal.cuh"
+
+namespace dymoe {
+
+constexpr int kPermThreads = 1024;
+constexpr int kPermWarps = kPermThreads / 32;
+
+__global__ void __launch_bounds__(kPermThreads)
+k_permute(const int32_t* __restrict__ topk_idx, int T, int k, int M,
+          const uint8_t* __restrict__ bits, int32_t* __restrict__ expert_off,
+          int32_t* __restrict__ perm_token, int32_t* __restrict__ perm_slot,
+          int32_t* __restrict__ inv_row, int32_t* __restrict__ active_list) {
+  __shared__ int running[DYMOE_MAX_EXPERTS];
+  __shared__ int warp_cnt[kPermWarps][DYMOE_MAX_EXPERTS];
+  __shared__ uint8_t keep[DYMOE_MAX_EXPERTS];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int P = T * k;
+  for (int e = tid; e < M; e += kPermThreads) {
+    running[e] = 0;
+    keep[e] = bits[e] != 0;
+  }
+  __syncthreads();
+  // pass 1: counts per expert
+  for (int p = tid; p < P; p += kPermThreads) {
+    const int e = topk_idx[p];
+    if (keep[e]) atomicAdd(&running[e], 1);
+  }
+  __syncthreads();
+  // exclusive scan of counts (M <= 256: warp 0 does it serially per lane-chunk)
+  if (tid == 0) {
+    int acc = 0, na = 0;
+    for (int e = 0; e < M; ++e) {
+      const int c = running[e];
+      expert_off[e] = acc;
+      running[e] = acc;
+      if (c > 0) active_list[1 + na++] = e;
+      acc += c;
+    }
+    expert_off[M] = acc;
+    active_list[0] = na;
+  }
+  __syncthreads();
+  // pass 2: stable placement, chunk by chunk in (token, slot) order
+  for (int c0 = 0; c0 < P; c0 += kPermThreads) {
+    for (int q = tid; q < kPermWarps * M; q += kPermThreads) (&warp_cnt[0][0])[
+        (q / M) * DYMOE_MAX_EXPERTS + (q % M)] = 0;
+    __syncthreads();
+    const int p = c0 + tid;
+    int e = -1;
+    if (p < P) {
+      e = topk_idx[p];
+      if (!keep[e]) {
+        inv_row[p] = -1;
+        e = -1;
+      }
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    const int rank_in_warp = __popc(peers & ((1u << lane) - 1u));
+    if (e >= 0 && rank_in_warp == 0) warp_cnt[w][e] = __popc(peers);
+    __syncthreads();
+    if (e >= 0) {
+      int r = running[e] + rank_in_warp;
+      for (int q = 0; q < w; ++q) r += warp_cnt[q][e];
+      perm_token[r] = p / k;
+      perm_slot[r] = p - (p / k) * k;
+      inv_row[p] = r;
+    }
+    __syncthreads();
+    for (int e2 = tid; e2 < M; e2 += kPermThreads) {
+      int add = 0;
+      for (int q = 0; q < kPermWarps; ++q) add += warp_cnt[q][e2];
+      running[e2] += add;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
+                           int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot,
+                           int32_t* inv_row, int32_t* active_list, cudaStream_t s) {
+  k_permute<<<1, kPermThreads, 0, s>>>(topk_idx, T, k, M, bits, expert_off, perm_token,
+                                       perm_slot, inv_row, active_list);
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------------------------
+// Combine: one CTA per token, float4 over Hd.
+__global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_perm,
+                                                 const int32_t* __restrict__ inv_row,
+                                                 const float* __restrict__ topk_w, int k, int Hd,
+                                                 int renorm, int out_bf16, void* __restrict__ y) {
+  const int t = blockIdx.x;
+  int rows[8];
+  float wt[8];
+  float denom = 0.f;
+  int live = 0;
+  for (int s = 0; s < k; ++s) {
+    rows[s] = inv_row[(size_t)t * k + s];
+    wt[s] = topk_w[(size_t)t * k + s];
+    if (rows[s] >= 0) {
+      denom += wt[s];
+      ++live;
+    }
+  }
+  for (int s = 0; s < k; ++s) wt[s] = renorm ? wt[s] / denom : wt[s];
+  for (int c = threadIdx.x * 4; c < Hd; c += blockDim.x * 4) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < k; ++s) {
+      if (rows[s] < 0) continue;
+      const float4 v = *reinterpret_cast<const float4*>(y_perm + (size_t)rows[s] * Hd + c);
+      acc.x = __fadd_rn(acc.x, __fmul_rn(wt[s], v.x));
+      acc.y = __fadd_rn(acc.y, __fmul_rn(wt[s], v.y));
+      acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], v.z));
+      acc.w = __fadd_rn(acc.w, __fmul_rn(wt[s], v.w));
+    }
+    if (out_bf16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y);
+      __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 o;
+      o.x = *reinterpret_cast<uint32_t*>(&lo);
+      o.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(y) + (size_t)t * Hd + c) = o;
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + (size_t)t * Hd + c) = acc;
+    }
+  }
+  (void)live;
+}
+
+cudaError_t launch_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w,
+                           int T, int k, int Hd, int renorm, int out_dtype, void* y,
+                           cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  k_combine<<<T, 256, 0, s>>>(y_perm, inv_row, topk_w, k, Hd, renorm,
+                              out_dtype == DYMOE_OUT_BF16, y);
+  return cudaGetLastError();
+}
+
+}  // namespace dymoe

@@ -1,0 +1,371 @@
+// Router (row a1), importance scoring (a2) and bit assignment (a3) kernels for sm_100a.
+//
+// Paper: PAPER.md P:111 (router), Eq. 6 P:278 (softmax gate), Eq. 1-2 P:216-227 (prefill
+// token-guided importance), Eq. 3 P:236-241 (decode gate-guided importance), Eq. 4-5
+// P:250-259 (depth-aware schedule), P:312 (tiers).  Readings R1b, R3, D5, D7-D11.
+//
+// All three are latency-bound (a few KB of input per layer); they are written for one launch
+// each with no host round trip so that a decode step can be captured in a CUDA graph.
+#include <cfloat>
+#include <math.h>
+
+#include "../dymoe_internal.cuh"
+
+namespace dymoe {
+
+// ===========================================================================================
+// Route: one warp per token.  Each lane holds up to 8 logits (M <= 256).  Top-k is k rounds of
+// a warp arg-max under the total order (value desc, index asc); comparisons are plain float
+// compares, so -0.0 == +0.0 (reading D11).
+// ===========================================================================================
+__device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
+  return va > vb || (va == vb && ia < ib);
+}
+
+__global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits, int T, int M,
+                                               int k, int32_t* __restrict__ topk_idx,
+                                               float* __restrict__ topk_w,
+                                               float* __restrict__ probs) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= T) return;
+  const float* row = logits + (size_t)warp * M;
+  float v[8];
+  uint32_t taken = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int j = lane + 32 * i;
+    v[i] = j < M ? row[j] : -FLT_MAX;
+  }
+  float sel_v[8];
+  int sel_i[8];
+  for (int r = 0; r < k; ++r) {
+    float bv = 0.f;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int j = lane + 32 * i;
+      if (j < M && !(taken >> i & 1u) && (bi == 0x7fffffff || better(v[i], j, bv, bi))) {
+        bv = v[i];
+        bi = j;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    sel_v[r] = bv;
+    sel_i[r] = bi;
+    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+  }
+  // softmax over the selected logits (max = the first selected), fp32, slot order
+  const float vmax = sel_v[0];
+  float e[8];
+  float z = 0.f;
+  for (int r = 0; r < k; ++r) {
+    e[r] = expf(sel_v[r] - vmax);
+    z += e[r];
+  }
+  if (lane < k) {
+    float my_e = 0.f;
+    int my_i = 0;
+    for (int r = 0; r < k; ++r)
+      if (r == lane) { my_e = e[r]; my_i = sel_i[r]; }
+    topk_idx[(size_t)warp * k + lane] = my_i;
+    topk_w[(size_t)warp * k + lane] = my_e / z;
+  }
+  if (probs != nullptr) {
+    float ev[8];
+    float zs = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int j = lane + 32 * i;
+      ev[i] = j < M ? expf(v[i] - vmax) : 0.f;
+      zs += ev[i];
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) zs += __shfl_xor_sync(0xffffffffu, zs, off);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int j = lane + 32 * i;
+      if (j < M) probs[(size_t)warp * M + j] = ev[i] / zs;
+    }
+  }
+}
+
+cudaError_t launch_route(const float* logits, int T, int M, int k, int32_t* topk_idx,
+                         float* topk_w, float* probs, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int warps_per_block = 8;
+  dim3 grid((T + warps_per_block - 1) / warps_per_block);
+  k_route<<<grid, 32 * warps_per_block, 0, s>>>(logits, T, M, k, topk_idx, topk_w, probs);
+  return cudaGetLastError();
+}
+
+// ===========================================================================================
+// Prefill score: one CTA of 1024 threads.
+//   1. S_i = sum_h a[h][i], fp32, heads in order (Eq. 1 without the 1/H factor, R1b).
+//   2. T_imp = top-k_tokens by (S desc, i asc): 4-pass 8-bit radix select on an order-preserving
+//      u32 key (with -0.0 folded onto +0.0), then the lowest-index ties at the threshold.
+//   3. importance[j] = #{i in T_imp : j in topk_idx[i]} (Eq. 2), exact integer counts.
+// ===========================================================================================
+__device__ __forceinline__ uint32_t order_key(float f) {
+  uint32_t u = __float_as_uint(f);
+  if (u == 0x80000000u) u = 0u;                  // -0.0 == +0.0
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+template <int NT>
+__device__ __forceinline__ int block_exclusive_scan(int v, int* sh_warp, int& total) {
+  // returns exclusive prefix of v over threads in index order; total = sum
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) sh_warp[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < NT / 32 ? sh_warp[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, off);
+      if (lane >= off) t += y;
+    }
+    if (lane < NT / 32) sh_warp[lane] = t;  // inclusive warp prefix
+  }
+  __syncthreads();
+  int base = w > 0 ? sh_warp[w - 1] : 0;
+  total = sh_warp[NT / 32 - 1];
+  __syncthreads();
+  return base + x - v;
+}
+
+constexpr int kScoreThreads = 1024;
+
+__global__ void __launch_bounds__(kScoreThreads)
+k_score_prefill(const float* __restrict__ attn, int H, const int32_t* __restrict__ topk_idx,
+                int T, int M, int k, int k_tokens, float* __restrict__ importance,
+                int32_t* __restrict__ heavy, float* __restrict__ S) {
+  __shared__ int hist[256];
+  __shared__ int cnt[DYMOE_MAX_EXPERTS];
+  __shared__ int sh_warp[32];
+  __shared__ uint32_t sh_prefix;
+  __shared__ int sh_krem;
+  const int tid = threadIdx.x;
+
+  // 1. token scores, sequential over heads (coalesced over tokens)
+  for (int i = tid; i < T; i += kScoreThreads) {
+    float acc = attn[i];
+    for (int h = 1; h < H; ++h) acc = __fadd_rn(acc, attn[(size_t)h * T + i]);
+    S[i] = acc;
+  }
+  for (int j = tid; j < M; j += kScoreThreads) cnt[j] = 0;
+  if (tid == 0) {
+    sh_prefix = 0u;
+    sh_krem = k_tokens;
+  }
+  __syncthreads();
+  if (k_tokens <= 0) {
+    for (int j = tid; j < M; j += kScoreThreads) importance[j] = 0.f;
+    return;
+  }
+
+  // 2. radix select of the k_tokens-th largest key (MSB first, 8 bits per pass)
+  uint32_t prefix_mask = 0u;
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    for (int b = tid; b < 256; b += kScoreThreads) hist[b] = 0;
+    __syncthreads();
+    const uint32_t prefix = sh_prefix;
+    for (int i = tid; i < T; i += kScoreThreads) {
+      uint32_t key = order_key(S[i]);
+      if ((key & prefix_mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      // find digit d (from 255 down) where the cumulative count reaches k_rem
+      const int krem = sh_krem;
+      // each lane owns 8 consecutive digits from the top: lane 0 -> 255..248
+      int local[8];
+      int lsum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        local[q] = hist[255 - (tid * 8 + q)];
+        lsum += local[q];
+      }
+      int incl = lsum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (tid >= off) incl += y;
+      }
+      int excl = incl - lsum;
+      bool mine = excl < krem && incl >= krem;
+      if (mine) {
+        int run = excl;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (run < krem && run + local[q] >= krem) {
+            const uint32_t d = 255u - (uint32_t)(tid * 8 + q);
+            sh_prefix = prefix | (d << shift);
+            sh_krem = krem - run;
+          }
+          run += local[q];
+        }
+      }
+    }
+    prefix_mask |= 255u << shift;
+    __syncthreads();
+  }
+  const uint32_t thresh = sh_prefix;
+  const int need_eq = sh_krem;  // how many tokens with key == thresh belong to T_imp
+
+  // 3. membership in token order; count routed experts of heavy tokens; compact `heavy`
+  int eq_base = 0, out_base = 0;
+  for (int c0 = 0; c0 < T; c0 += kScoreThreads) {
+    const int i = c0 + tid;
+    uint32_t key = i < T ? order_key(S[i]) : 0u;
+    const int is_eq = (i < T && key == thresh) ? 1 : 0;
+    int eq_total;
+    const int eq_rank = eq_base + block_exclusive_scan<kScoreThreads>(is_eq, sh_warp, eq_total);
+    const int is_heavy = (i < T && (key > thresh || (is_eq && eq_rank < need_eq))) ? 1 : 0;
+    int h_total;
+    const int h_pos = out_base + block_exclusive_scan<kScoreThreads>(is_heavy, sh_warp, h_total);
+    if (is_heavy) {
+      if (heavy != nullptr) heavy[h_pos] = i;
+      for (int r = 0; r < k; ++r) atomicAdd(&cnt[topk_idx[(size_t)i * k + r]], 1);
+    }
+    eq_base += eq_total;
+    out_base += h_total;
+  }
+  __syncthreads();
+  for (int j = tid; j < M; j += kScoreThreads) importance[j] = (float)cnt[j];
+}
+
+cudaError_t launch_score_prefill(const float* attn, int H, const int32_t* topk_idx, int T,
+                                 int M, int k, int k_tokens, float* importance, int32_t* heavy,
+                                 float* S_scratch, cudaStream_t s) {
+  k_score_prefill<<<1, kScoreThreads, 0, s>>>(attn, H, topk_idx, T, M, k, k_tokens, importance,
+                                              heavy, S_scratch);
+  return cudaGetLastError();
+}
+
+// ===========================================================================================
+// Decode score (Eq. 3, reading D10): B == 1 -> the logit row; B > 1 -> sum_b softmax(l_b)
+// (fp32, b ascending).  One CTA, one thread per expert, block reductions per token.
+// ===========================================================================================
+__global__ void __launch_bounds__(256) k_score_decode(const float* __restrict__ logits, int B,
+                                                      int M, float* __restrict__ importance) {
+  __shared__ float red[8];
+  __shared__ float bc[2];
+  const int j = threadIdx.x;
+  const int lane = j & 31, w = j >> 5;
+  if (B == 1) {
+    if (j < M) importance[j] = logits[j];
+    return;
+  }
+  float acc = 0.f;
+  for (int b = 0; b < B; ++b) {
+    const float l = j < M ? logits[(size_t)b * M + j] : -FLT_MAX;
+    float m = l;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (lane == 0) red[w] = m;
+    __syncthreads();
+    if (j == 0) {
+      float mm = red[0];
+      for (int q = 1; q < 8; ++q) mm = fmaxf(mm, red[q]);
+      bc[0] = mm;
+    }
+    __syncthreads();
+    const float e = j < M ? expf(l - bc[0]) : 0.f;
+    float z = e;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
+    if (lane == 0) red[w] = z;
+    __syncthreads();
+    if (j == 0) {
+      float zz = 0.f;
+      for (int q = 0; q < 8; ++q) zz += red[q];
+      bc[1] = zz;
+    }
+    __syncthreads();
+    acc += e / bc[1];
+    __syncthreads();
+  }
+  if (j < M) importance[j] = acc;
+}
+
+cudaError_t launch_score_decode(const float* logits, int B, int M, float* importance,
+                                cudaStream_t s) {
+  k_score_decode<<<1, 256, 0, s>>>(logits, B, M, importance);
+  return cudaGetLastError();
+}
+
+// ===========================================================================================
+// Assign bits (Eq. 5 + tiers, readings D5, D7-D9, D11): one CTA, thread j = expert j.
+// rank_j = #{i in candidates : I_i > I_j or (I_i == I_j and i < j)}; t_k = ceil(r_k*M_eff - 1e-9)
+// in fp64 (no contraction: explicit _rn intrinsics) from the host-evaluated r_k.
+// ===========================================================================================
+__global__ void __launch_bounds__(256) k_assign(const float* __restrict__ importance,
+                                                const uint8_t* __restrict__ active_mask,
+                                                const int32_t* __restrict__ topk_idx, int T,
+                                                AssignParams p, uint8_t* __restrict__ bits,
+                                                uint8_t* __restrict__ active_out) {
+  __shared__ float I[DYMOE_MAX_EXPERTS];
+  __shared__ int act[DYMOE_MAX_EXPERTS];
+  __shared__ int n_act;
+  const int j = threadIdx.x;
+  if (j < p.M) {
+    I[j] = importance[j];
+    act[j] = p.m_active ? (active_mask != nullptr ? (active_mask[j] != 0) : 0) : 1;
+  }
+  if (j == 0) n_act = 0;
+  __syncthreads();
+  if (p.m_active && active_mask == nullptr) {
+    for (int q = j; q < T * p.k_route; q += blockDim.x) act[topk_idx[q]] = 1;  // benign race
+    __syncthreads();
+  }
+  if (j < p.M && act[j]) atomicAdd(&n_act, 1);
+  __syncthreads();
+  if (j >= p.M) return;
+  if (active_out != nullptr) active_out[j] = (uint8_t)act[j];
+  const int M_eff = n_act;
+  if (!act[j]) {
+    bits[j] = (uint8_t)p.bits[p.n_tiers - 1];
+    return;
+  }
+  const float Ij = I[j];
+  int rank = 0;
+  for (int i = 0; i < p.M; ++i)
+    if (act[i] && (I[i] > Ij || (I[i] == Ij && i < j))) ++rank;
+  int tier = p.n_tiers - 1;
+  int prev = 0;
+  for (int q = 0; q < p.n_tiers - 1; ++q) {
+    double x = __dsub_rn(__dmul_rn(p.r[q], (double)M_eff), 1e-9);
+    int t = (int)ceil(x);
+    if (q == 0 && p.clamp_to_k) t = max(t, min(p.k_route, M_eff));
+    t = max(t, prev);
+    t = min(t, M_eff);
+    prev = t;
+    if (rank < t && tier == p.n_tiers - 1) tier = q;
+  }
+  bits[j] = (uint8_t)p.bits[tier];
+}
+
+cudaError_t launch_assign(const float* importance, const uint8_t* active_mask,
+                          const int32_t* topk_idx, int T, const AssignParams& p, uint8_t* bits,
+                          uint8_t* active_out, cudaStream_t s) {
+  k_assign<<<1, 256, 0, s>>>(importance, active_mask, topk_idx, T, p, bits, active_out);
+  return cudaGetLastError();
+}
+
+}  // namespace dymoe

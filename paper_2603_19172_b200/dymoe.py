@@ -1,0 +1,381 @@
+"""Thin ctypes binding over libdymoe.so (include/dymoe.h).
+
+Argument marshalling only: every step of the path runs in the library's CUDA kernels.  torch
+is used for device memory (output allocation) and streams.  There is no CPU fallback: if the
+library is missing or the tensors are not on a CUDA device the calls raise.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdymoe.so")
+
+DYMOE_OK = 0
+DYMOE_PREFILL, DYMOE_DECODE = 0, 1
+DYMOE_M_TOTAL, DYMOE_M_ACTIVE = 0, 1
+DYMOE_OUT_F32, DYMOE_OUT_BF16 = 0, 1
+MAX_TIERS = 5
+GROUP = 128
+WIDTH_INDEX = {8: 0, 4: 1, 2: 2}
+
+EXPORTED = [
+    "dymoe_route", "dymoe_score", "dymoe_score_scratch_bytes", "dymoe_assign_bits",
+    "dymoe_retention_ratio", "dymoe_tier_counts", "dymoe_quantize", "dymoe_quantize_batched",
+    "dymoe_layer_create", "dymoe_layer_destroy", "dymoe_permute", "dymoe_expert_ffn",
+    "dymoe_combine", "dymoe_workspace_size", "dymoe_workspace_views", "dymoe_moe_forward",
+    "dymoe_check_status", "dymoe_last_error", "dymoe_version",
+]
+
+
+class DymoeError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("dymoe error %d: %s" % (code, msg))
+        self.code = code
+        self.msg = msg
+
+
+class Ladder(ctypes.Structure):
+    _fields_ = [("n_tiers", ctypes.c_int), ("bits", ctypes.c_int * MAX_TIERS),
+                ("lambdas", ctypes.c_double * (MAX_TIERS - 1)), ("clamp_to_k", ctypes.c_int),
+                ("m_mode", ctypes.c_int), ("renorm_on_skip", ctypes.c_int)]
+
+
+class QuantJob(ctypes.Structure):
+    _fields_ = [("W", ctypes.c_void_p), ("N", ctypes.c_int), ("K", ctypes.c_int),
+                ("bits", ctypes.c_int), ("codes", ctypes.c_void_p), ("scales", ctypes.c_void_p),
+                ("zeros", ctypes.c_void_p)]
+
+
+class QMat(ctypes.Structure):
+    _fields_ = [("codes", ctypes.c_void_p), ("scales", ctypes.c_void_p), ("zeros", ctypes.c_void_p)]
+
+
+class ExpertDesc(ctypes.Structure):
+    _fields_ = [("w1", ctypes.c_void_p), ("w3", ctypes.c_void_p), ("w2", ctypes.c_void_p),
+                ("q", (QMat * 3) * 3)]
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int), ("k_route", ctypes.c_int), ("hidden", ctypes.c_int),
+                ("ffn", ctypes.c_int), ("experts", ctypes.POINTER(ExpertDesc))]
+
+
+class FwdOpts(ctypes.Structure):
+    _fields_ = [("phase", ctypes.c_int), ("layer", ctypes.c_int), ("num_layers", ctypes.c_int),
+                ("ladder", Ladder), ("attn_mass", ctypes.c_void_p), ("heads", ctypes.c_int),
+                ("k_tokens", ctypes.c_int), ("ffn_mode", ctypes.c_int), ("out_dtype", ctypes.c_int),
+                ("forced_bits", ctypes.c_void_p), ("prof_events", ctypes.c_void_p * 3)]
+
+
+class WsViews(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in (
+        "topk_idx", "topk_w", "probs", "importance", "heavy", "bits", "active", "expert_off",
+        "perm_token", "perm_slot", "inv_row", "h", "y_perm", "status", "score_scratch")]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdymoe.so once; raise loudly if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libdymoe.so not built at %s (run paper_2603_19172_b200.build)" % LIB_PATH)
+        L = ctypes.CDLL(LIB_PATH)
+        vp, ci, cz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+        sig = {
+            "dymoe_route": [vp, ci, ci, ci, vp, vp, vp, vp],
+            "dymoe_score": [ci, vp, ci, vp, vp, ci, ci, ci, ci, vp, vp, vp, vp],
+            "dymoe_score_scratch_bytes": [ci],
+            "dymoe_assign_bits": [vp, ci, ci, ci, ctypes.POINTER(Ladder), ci, vp, vp, vp, vp],
+            "dymoe_retention_ratio": [ci, ci, ctypes.c_double],
+            "dymoe_tier_counts": [ci, ci, ctypes.POINTER(Ladder), ci, ci, vp],
+            "dymoe_quantize": [vp, ci, ci, ci, ci, vp, vp, vp, vp],
+            "dymoe_quantize_batched": [ctypes.POINTER(QuantJob), ci, ci, vp],
+            "dymoe_layer_create": [ctypes.POINTER(LayerDesc), ctypes.POINTER(vp)],
+            "dymoe_layer_destroy": [vp],
+            "dymoe_permute": [vp, ci, ci, ci, vp, vp, vp, vp, vp, vp],
+            "dymoe_expert_ffn": [vp, ci, vp, ci, vp, vp, vp, vp, vp, vp, vp],
+            "dymoe_combine": [vp, vp, vp, ci, ci, ci, ci, ci, vp, vp],
+            "dymoe_workspace_size": [vp, ci],
+            "dymoe_workspace_views": [vp, ci, vp, ctypes.POINTER(WsViews)],
+            "dymoe_moe_forward": [vp, vp, vp, ci, ctypes.POINTER(FwdOpts), vp, vp, cz, vp],
+            "dymoe_check_status": [vp, ci, vp, vp, vp],
+            "dymoe_last_error": [],
+            "dymoe_version": [],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ci
+        L.dymoe_retention_ratio.restype = ctypes.c_double
+        L.dymoe_score_scratch_bytes.restype = cz
+        L.dymoe_workspace_size.restype = cz
+        L.dymoe_last_error.restype = ctypes.c_char_p
+        L.dymoe_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != DYMOE_OK:
+        raise DymoeError(rc, lib().dymoe_last_error().decode())
+
+
+def _p(t):
+    """Device pointer of a CUDA tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("dymoe: tensors must live on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("dymoe: tensors must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _u16(t):
+    """bf16 tensor viewed as its bit patterns (no copy)."""
+    return t.view(torch.int16) if t.dtype == torch.bfloat16 else t
+
+
+def make_ladder(bits, lambdas, clamp_to_k=True, m_active=False, renorm_on_skip=True):
+    L = Ladder()
+    L.n_tiers = len(bits)
+    for i, b in enumerate(bits):
+        L.bits[i] = int(b)
+    for i, lam in enumerate(lambdas):
+        L.lambdas[i] = float(lam)
+    L.clamp_to_k = int(bool(clamp_to_k))
+    L.m_mode = DYMOE_M_ACTIVE if m_active else DYMOE_M_TOTAL
+    L.renorm_on_skip = int(bool(renorm_on_skip))
+    return L
+
+
+# ---------------------------------------------------------------------------------------------
+def dymoe_route(logits, k, with_probs=True, stream=None):
+    T, M = logits.shape
+    dev = logits.device
+    idx = torch.empty(T, k, dtype=torch.int32, device=dev)
+    w = torch.empty(T, k, dtype=torch.float32, device=dev)
+    p = torch.empty(T, M, dtype=torch.float32, device=dev) if with_probs else None
+    _check(lib().dymoe_route(_p(logits), T, M, k, _p(idx), _p(w), _p(p), _stream(stream)))
+    return idx, w, p
+
+
+def dymoe_score(phase, M, k=0, topk_idx=None, attn_mass=None, logits=None, k_tokens=0,
+                stream=None):
+    if phase == DYMOE_PREFILL:
+        H, T = attn_mass.shape
+        dev = attn_mass.device
+    else:
+        T = logits.shape[0]
+        H = 0
+        dev = logits.device
+    imp = torch.empty(M, dtype=torch.float32, device=dev)
+    kt = k_tokens if k_tokens else (T + 4) // 5
+    heavy = torch.full((max(kt, 1),), -1, dtype=torch.int32, device=dev) if phase == DYMOE_PREFILL else None
+    scratch = torch.empty(lib().dymoe_score_scratch_bytes(T), dtype=torch.uint8, device=dev) \
+        if phase == DYMOE_PREFILL else None
+    _check(lib().dymoe_score(phase, _p(attn_mass), H, _p(topk_idx), _p(logits), T, M, k, k_tokens,
+                             _p(imp), _p(heavy), _p(scratch), _stream(stream)))
+    return imp, (heavy[:kt] if heavy is not None else None)
+
+
+def dymoe_assign_bits(importance, layer, num_layers, ladder, k_route, active_mask=None,
+                      stream=None):
+    M = importance.shape[0]
+    bits = torch.empty(M, dtype=torch.uint8, device=importance.device)
+    counts = (ctypes.c_int32 * MAX_TIERS)()
+    _check(lib().dymoe_assign_bits(_p(importance), M, layer, num_layers, ctypes.byref(ladder),
+                                   k_route, _p(active_mask), _p(bits), ctypes.cast(counts, ctypes.c_void_p),
+                                   _stream(stream)))
+    return bits, [counts[i] for i in range(ladder.n_tiers - 1)]
+
+
+def dymoe_retention_ratio(layer, num_layers, lam):
+    return lib().dymoe_retention_ratio(layer, num_layers, lam)
+
+
+def dymoe_tier_counts(layer, num_layers, ladder, M_eff, k_route):
+    counts = (ctypes.c_int32 * MAX_TIERS)()
+    _check(lib().dymoe_tier_counts(layer, num_layers, ctypes.byref(ladder), M_eff, k_route,
+                                   ctypes.cast(counts, ctypes.c_void_p)))
+    return [counts[i] for i in range(ladder.n_tiers - 1)]
+
+
+def alloc_qmat(N, K, bits, device):
+    codes = torch.empty(N, K * bits // 32, dtype=torch.int32, device=device)
+    scales = torch.empty(N, K // GROUP, dtype=torch.float32, device=device)
+    zeros = torch.empty(N, K // GROUP, dtype=torch.uint8, device=device)
+    return codes, scales, zeros
+
+
+def dymoe_quantize(W, bits, out=None, stream=None):
+    N, K = W.shape
+    codes, scales, zeros = out if out is not None else alloc_qmat(N, K, bits, W.device)
+    _check(lib().dymoe_quantize(_p(_u16(W)), N, K, bits, GROUP, _p(codes), _p(scales), _p(zeros),
+                                _stream(stream)))
+    return codes, scales, zeros
+
+
+def dymoe_quantize_batched(jobs, stream=None):
+    """jobs: list of (W bf16 [N,K], bits, (codes, scales, zeros))."""
+    arr = (QuantJob * max(len(jobs), 1))()
+    for i, (W, bits, (c, s, z)) in enumerate(jobs):
+        arr[i] = QuantJob(_p(_u16(W)), W.shape[0], W.shape[1], bits, _p(c), _p(s), _p(z))
+    _check(lib().dymoe_quantize_batched(arr, len(jobs), GROUP, _stream(stream)))
+
+
+def dymoe_permute(topk_idx, M, bits, stream=None):
+    T, k = topk_idx.shape
+    dev = topk_idx.device
+    off = torch.empty(M + 1, dtype=torch.int32, device=dev)
+    pt = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev)
+    ps = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev)
+    inv = torch.empty(T, k, dtype=torch.int32, device=dev)
+    _check(lib().dymoe_permute(_p(topk_idx), T, k, M, _p(bits), _p(off), _p(pt), _p(ps), _p(inv),
+                               _stream(stream)))
+    return off, pt, ps, inv
+
+
+def dymoe_combine(y_perm, inv_row, topk_w, renorm=True, out_dtype=DYMOE_OUT_F32, stream=None):
+    T, k = inv_row.shape
+    Hd = y_perm.shape[1]
+    y = torch.empty(T, Hd, dtype=torch.float32 if out_dtype == DYMOE_OUT_F32 else torch.bfloat16,
+                    device=y_perm.device)
+    _check(lib().dymoe_combine(_p(y_perm), _p(inv_row), _p(topk_w), T, k, Hd, int(renorm),
+                               out_dtype, _p(y), _stream(stream)))
+    return y
+
+
+# ---------------------------------------------------------------------------------------------
+class MoELayer:
+    """An expert table (dymoe_layer handle).  `experts` is a list of dicts with bf16 masters
+    'w1','w3' [F,Hd], 'w2' [Hd,F] (optional) and per quantized width b a dict 'q{b}' =
+    {'w1': (codes, scales, zeros), 'w3': ..., 'w2': ...}.  Tensors must outlive the layer."""
+
+    def __init__(self, experts, k_route, hidden, ffn):
+        self.M = len(experts)
+        self.k = k_route
+        self.hidden = hidden
+        self.ffn = ffn
+        self._keep = experts
+        arr = (ExpertDesc * self.M)()
+        for e, ex in enumerate(experts):
+            d = arr[e]
+            for n in ("w1", "w3", "w2"):
+                t = ex.get(n)
+                setattr(d, n, _p(_u16(t)) if t is not None else None)
+            for b, wi in WIDTH_INDEX.items():
+                q = ex.get("q%d" % b)
+                if q is None:
+                    continue
+                for mi, n in enumerate(("w1", "w3", "w2")):
+                    c, s, z = q[n]
+                    d.q[wi][mi] = QMat(_p(c), _p(s), _p(z))
+        desc = LayerDesc(self.M, k_route, hidden, ffn, arr)
+        h = ctypes.c_void_p()
+        _check(lib().dymoe_layer_create(ctypes.byref(desc), ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _lib is not None:
+                _lib.dymoe_layer_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def workspace(self, T, device="cuda"):
+        n = lib().dymoe_workspace_size(self.handle, T)
+        return torch.zeros(max(n, 256), dtype=torch.uint8, device=device)
+
+    def views(self, T, ws):
+        v = WsViews()
+        _check(lib().dymoe_workspace_views(self.handle, T, _p(ws), ctypes.byref(v)))
+        base = ws.data_ptr()
+        M, k, Hd, F = self.M, self.k, self.hidden, self.ffn
+
+        def view(name, shape, dtype):
+            off = getattr(v, name) - base
+            n = 1
+            for s in shape:
+                n *= s
+            nbytes = n * torch.empty(0, dtype=dtype).element_size()
+            return ws[off:off + nbytes].view(dtype).view(*shape)
+        return dict(
+            topk_idx=view("topk_idx", (T, k), torch.int32), topk_w=view("topk_w", (T, k), torch.float32),
+            probs=view("probs", (T, M), torch.float32), importance=view("importance", (M,), torch.float32),
+            heavy=view("heavy", (T,), torch.int32), bits=view("bits", (M,), torch.uint8),
+            active=view("active", (M,), torch.uint8), expert_off=view("expert_off", (M + 1,), torch.int32),
+            perm_token=view("perm_token", (T * k,), torch.int32), perm_slot=view("perm_slot", (T * k,), torch.int32),
+            inv_row=view("inv_row", (T, k), torch.int32), h=view("h", (T * k, F), torch.bfloat16),
+            y_perm=view("y_perm", (T * k, Hd), torch.float32), status=view("status", (1,), torch.int32))
+
+    def expert_ffn(self, x, bits, expert_off, perm_token, mode, stream=None):
+        T = x.shape[0]
+        h = torch.empty(max(T * self.k, 1), self.ffn, dtype=torch.bfloat16, device=x.device)
+        y = torch.empty(max(T * self.k, 1), self.hidden, dtype=torch.float32, device=x.device)
+        status = torch.zeros(1, dtype=torch.int32, device=x.device)
+        _check(lib().dymoe_expert_ffn(self.handle, mode, _p(_u16(x)), T, _p(bits), _p(expert_off),
+                                      _p(perm_token), _p(h), _p(y), _p(status), _stream(stream)))
+        return h, y, status
+
+    def forward(self, x, logits, ladder, layer, num_layers, phase=DYMOE_DECODE, attn_mass=None,
+                k_tokens=0, out_dtype=DYMOE_OUT_F32, forced_bits=None, ffn_mode=-1, ws=None,
+                out=None, stream=None, prof_events=None):
+        """dymoe_moe_forward.  Returns (y, ws).  prof_events: optional 3 torch.cuda.Events
+        (already recorded once so that they exist) recorded around the FFN kernels."""
+        T = x.shape[0]
+        if ws is None:
+            ws = self.workspace(T, x.device)
+        if out is None:
+            out = torch.empty(T, self.hidden, device=x.device,
+                              dtype=torch.float32 if out_dtype == DYMOE_OUT_F32 else torch.bfloat16)
+        o = FwdOpts()
+        o.phase = phase
+        o.layer = layer
+        o.num_layers = num_layers
+        o.ladder = ladder
+        o.attn_mass = _p(attn_mass)
+        o.heads = attn_mass.shape[0] if attn_mass is not None else 0
+        o.k_tokens = k_tokens
+        o.ffn_mode = ffn_mode
+        o.out_dtype = out_dtype
+        o.forced_bits = _p(forced_bits)
+        if prof_events is not None:
+            for i, ev in enumerate(prof_events):
+                o.prof_events[i] = ev.cuda_event
+        _check(lib().dymoe_moe_forward(self.handle, _p(_u16(x)), _p(logits), T, ctypes.byref(o),
+                                       _p(out), _p(ws), ws.numel(), _stream(stream)))
+        return out, ws
+
+    def check_status(self, T, ws, stream=None):
+        word = ctypes.c_uint32()
+        rc = lib().dymoe_check_status(self.handle, T, _p(ws), ctypes.byref(word), _stream(stream))
+        return rc, word.value
+
+
+def quantize_experts(experts, widths=(8, 4, 2), stream=None):
+    """Quantize every expert's W1/W3/W2 to each width in one batched launch (in place: adds
+    'q{b}' entries)."""
+    jobs = []
+    for ex in experts:
+        for b in widths:
+            q = {}
+            for n in ("w1", "w3", "w2"):
+                W = ex[n]
+                q[n] = alloc_qmat(W.shape[0], W.shape[1], b, W.device)
+                jobs.append((W, b, q[n]))
+            ex["q%d" % b] = q
+    for i in range(0, len(jobs), 64):
+        dymoe_quantize_batched(jobs[i:i + 64], stream=stream)
+    return experts

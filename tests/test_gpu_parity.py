@@ -1,0 +1,310 @@
+"""GPU parity: every C-ABI entry point against the CPU oracle on the same seeded inputs.
+
+Bars: bit-exact for indices, counts, heavy sets, bits, codes/scales/zeros and
+permutations; routing weights <= 1e-6 relative; FFN / layer outputs max|y - y_ref| / max|y_ref|
+<= 2e-3 (BASELINE.json north_star) against the oracle's fp64 result on its own dequantized
+weights.
+"""
+import numpy as np
+import pytest
+import torch
+
+import synthetic
+from oracle import route as o_route, importance as o_imp, schedule as o_sched, quant as o_quant
+from oracle import moe as o_moe
+
+pytestmark = pytest.mark.gpu
+
+FFN_TOL = 2e-3
+
+
+def D():
+    import paper_2603_19172_b200.dymoe as d
+    d.lib()
+    return d
+
+
+def rel_err(y, ref):
+    y = np.asarray(y, np.float64)
+    ref = np.asarray(ref, np.float64)
+    den = np.abs(ref).max()
+    return float(np.abs(y - ref).max() / (den if den > 0 else 1.0))
+
+
+# ------------------------------------------------------------------------------------ route
+@pytest.mark.parametrize("T,M,k,ties", [(1, 8, 2, False), (37, 8, 2, False), (300, 64, 6, False),
+                                        (129, 256, 8, False), (64, 8, 2, True), (50, 64, 6, True),
+                                        (0, 8, 2, False)])
+def test_route(T, M, k, ties):
+    d = D()
+    lg = synthetic.random_logits(T, M, seed=T + M, ties=ties)
+    idx, w, p = d.dymoe_route(lg.cuda(), k)
+    r_idx, r_w, r_p = o_route.route(lg.numpy(), k) if T else (np.zeros((0, k)),) * 3
+    assert np.array_equal(idx.cpu().numpy(), r_idx)
+    if T:
+        assert np.abs(w.cpu().numpy() - r_w).max() <= 1e-6 * np.abs(r_w).max()
+        assert np.abs(p.cpu().numpy() - r_p).max() <= 1e-6
+
+
+# ------------------------------------------------------------------------------------ score
+@pytest.mark.parametrize("T,H,M,k,k_tokens,seed", [(16, 32, 8, 2, 0, 0), (2048, 32, 8, 2, 0, 1),
+                                                   (3000, 8, 64, 6, 0, 2), (1025, 4, 8, 2, 1, 3),
+                                                   (1500, 4, 8, 2, 1500, 4), (700, 2, 8, 2, 0, 5),
+                                                   (5, 3, 8, 2, 0, 6)])
+def test_score_prefill(T, H, M, k, k_tokens, seed):
+    d = D()
+    cfg = synthetic.MoEConfig("t", M=M, k=k, hidden=128, ffn=128, T=T, heads=H)
+    a = synthetic.attention_mass(cfg, seed)
+    if seed == 5:  # integer-valued masses: many exact ties in S
+        a = torch.floor(a * 2)
+    lg = synthetic.random_logits(T, M, seed)
+    r_idx, _, _ = o_route.route(lg.numpy(), k)
+    idx = torch.from_numpy(r_idx).cuda()
+    imp, heavy = d.dymoe_score(d.DYMOE_PREFILL, M, k, topk_idx=idx, attn_mass=a.cuda(), k_tokens=k_tokens)
+    r_I, r_heavy, _ = o_imp.score_prefill(a.numpy(), r_idx, M, k_tokens or None)
+    assert np.array_equal(imp.cpu().numpy(), r_I.astype(np.float32))
+    assert np.array_equal(np.sort(heavy.cpu().numpy()), np.sort(r_heavy))
+
+
+@pytest.mark.parametrize("B", [1, 2, 5, 8])
+def test_score_decode(B):
+    d = D()
+    lg = synthetic.random_logits(B, 8, seed=B)
+    imp, _ = d.dymoe_score(d.DYMOE_DECODE, 8, logits=lg.cuda())
+    _, _, p = o_route.route(lg.numpy(), 2)
+    ref = o_imp.decode_importance(lg.numpy(), p)
+    if B == 1:
+        assert np.array_equal(imp.cpu().numpy(), lg.numpy()[0])
+    else:
+        assert np.abs(imp.cpu().numpy() - ref).max() <= 1e-6 * B
+
+
+# ------------------------------------------------------------------------------------ assign
+LADDERS = [((8, 4, 2), (0.25, 0.5), True, False), ((4, 2), (0.5,), True, False),
+           ((4, 0), (0.5,), True, False), ((4, 0), (0.0,), False, False),
+           ((16, 8, 4, 2, 0), (0.1, 0.3, 0.6, 0.9), True, False), ((8, 4, 2), (0.25, 0.5), True, True)]
+
+
+@pytest.mark.parametrize("lad", LADDERS)
+@pytest.mark.parametrize("M", [8, 64])
+def test_assign_bits(lad, M):
+    d = D()
+    bits_t, lams, clamp, act = lad
+    rng = np.random.default_rng(M)
+    for trial in range(12):
+        imp = rng.integers(0, 6, size=M).astype(np.float32)          # prefill-like counts, ties
+        active = (rng.random(M) < 0.6).astype(np.uint8)
+        L = 32
+        l = int(rng.integers(0, L))
+        ladder = d.make_ladder(bits_t, lams, clamp_to_k=clamp, m_active=act)
+        bits, counts = d.dymoe_assign_bits(torch.from_numpy(imp).cuda(), l, L, ladder, 2,
+                                           active_mask=torch.from_numpy(active).cuda() if act else None)
+        o_lad = o_sched.Ladder(bits=bits_t, lambdas=lams, clamp_to_k=clamp, m_active=act)
+        ref, r_counts = o_sched.assign_bits(imp.astype(np.float64), l, L, o_lad, 2, active.astype(bool))
+        assert np.array_equal(bits.cpu().numpy(), ref)
+        if not act:
+            assert counts == r_counts
+
+
+def test_tier_counts_host_matches_oracle():
+    d = D()
+    for M in (8, 64):
+        for lam in np.linspace(0, 1, 21):
+            for L in (1, 2, 4, 8, 32):
+                for l in range(L):
+                    c = d.dymoe_tier_counts(l, L, d.make_ladder((4, 2), (float(lam),)), M, 2)
+                    assert c == o_sched.tier_counts(l, L, o_sched.paper_ladder(2, float(lam)), M, 2)
+
+
+# ------------------------------------------------------------------------------------ quantize
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("N,K,kind", [(64, 256, "normal"), (33, 1408, "normal"), (7, 384, "mixed"),
+                                      (16, 128, "zeros"), (16, 512, "tiny"), (9, 256, "positive"),
+                                      (9, 256, "negative"), (1, 128, "normal"), (0, 256, "normal")])
+def test_quantize(bits, N, K, kind):
+    d = D()
+    W = synthetic.random_matrix_bf16(N, K, seed=N + K + bits, kind=kind)
+    codes, scales, zeros = d.dymoe_quantize(W.cuda(), bits)
+    r_codes, r_s, r_z = o_quant.quantize(W.float().numpy(), bits)
+    assert np.array_equal(codes.cpu().numpy().view(np.uint32), r_codes)
+    assert np.array_equal(scales.cpu().numpy(), r_s)
+    assert np.array_equal(zeros.cpu().numpy(), r_z)
+
+
+def test_quantize_batched_mixed_jobs():
+    d = D()
+    jobs, refs = [], []
+    for i, (N, K, b) in enumerate([(3, 128, 2), (50, 640, 4), (17, 256, 8), (1, 1408, 2)]):
+        W = synthetic.random_matrix_bf16(N, K, seed=100 + i).cuda()
+        out = d.alloc_qmat(N, K, b, "cuda")
+        jobs.append((W, b, out))
+        refs.append(o_quant.quantize(W.float().cpu().numpy(), b))
+    d.dymoe_quantize_batched(jobs)
+    for (W, b, (c, s, z)), (rc, rs, rz) in zip(jobs, refs):
+        assert np.array_equal(c.cpu().numpy().view(np.uint32), rc)
+        assert np.array_equal(s.cpu().numpy(), rs) and np.array_equal(z.cpu().numpy(), rz)
+
+
+# ------------------------------------------------------------------------------------ permute / combine
+@pytest.mark.parametrize("T,M,k", [(1, 8, 2), (16, 8, 2), (2048, 8, 2), (1500, 64, 6), (3, 256, 8), (0, 8, 2)])
+def test_permute(T, M, k):
+    d = D()
+    rng = np.random.default_rng(T + M)
+    idx = np.stack([rng.permutation(M)[:k] for _ in range(T)]).astype(np.int32).reshape(T, k)
+    bits = rng.choice([0, 2, 4, 8, 16], size=M).astype(np.uint8)
+    off, pt, ps, inv = d.dymoe_permute(torch.from_numpy(idx).cuda(), M, torch.from_numpy(bits).cuda())
+    ref = o_moe.permute(idx, bits, M)
+    R = int(ref["expert_off"][-1])
+    assert np.array_equal(off.cpu().numpy(), ref["expert_off"])
+    assert np.array_equal(pt.cpu().numpy()[:R], ref["perm_token"])
+    assert np.array_equal(ps.cpu().numpy()[:R], ref["perm_slot"])
+    assert np.array_equal(inv.cpu().numpy(), ref["inv_row"])
+
+
+@pytest.mark.parametrize("renorm", [True, False])
+def test_combine(renorm):
+    d = D()
+    rng = np.random.default_rng(0)
+    T, k, Hd = 40, 3, 256
+    inv = np.full((T, k), -1, np.int32)
+    rows = rng.permutation(T * k)
+    mask = rng.random((T, k)) < 0.7
+    inv[mask] = rows[: mask.sum()]
+    y_perm = rng.standard_normal((T * k, Hd)).astype(np.float32)
+    w = rng.random((T, k)).astype(np.float32)
+    w /= w.sum(1, keepdims=True)
+    y = d.dymoe_combine(torch.from_numpy(y_perm).cuda(), torch.from_numpy(inv).cuda(),
+                        torch.from_numpy(w).cuda(), renorm=renorm)
+    ref = o_moe.combine(y_perm.astype(np.float64), inv, w.astype(np.float64), renorm)
+    assert rel_err(y.cpu().numpy(), ref) <= 1e-6
+    yb = d.dymoe_combine(torch.from_numpy(y_perm).cuda(), torch.from_numpy(inv).cuda(),
+                         torch.from_numpy(w).cuda(), renorm=renorm, out_dtype=d.DYMOE_OUT_BF16)
+    ref_b = torch.from_numpy(ref).float().to(torch.bfloat16).float().numpy()
+    # <= 1 bf16 ulp elementwise
+    assert (np.abs(yb.float().cpu().numpy() - ref_b) <= np.abs(ref_b) * 2.0 ** -7 + 1e-30).all()
+
+
+# ------------------------------------------------------------------------------------ FFN
+def gpu_experts(cfg, seed, widths=(8, 4, 2)):
+    d = D()
+    ex = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, seed)]
+    d.quantize_experts(ex, widths)
+    return ex
+
+
+def np_experts(cfg, seed):
+    return [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, seed)]
+
+
+FFN_CFGS = [synthetic.CONFIGS["tiny"],
+            synthetic.MoEConfig("mid", M=8, k=2, hidden=1024, ffn=1408, T=24),
+            synthetic.MoEConfig("fg", M=16, k=4, hidden=640, ffn=384, T=9)]
+
+
+@pytest.mark.parametrize("cfg", FFN_CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("mode", ["decode", "prefill"])
+def test_expert_ffn_all_widths(cfg, mode):
+    d = D()
+    ex = gpu_experts(cfg, 1)
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    rng = np.random.default_rng(7)
+    bits = np.array([[16, 8, 4, 2][e % 4] for e in range(cfg.M)], np.uint8)
+    bits[rng.integers(0, cfg.M)] = 0
+    x, lg, _ = synthetic.layer_inputs(cfg, 1)
+    r_idx, _, _ = o_route.route(lg.numpy(), cfg.k)
+    perm = o_moe.permute(r_idx, bits, cfg.M)
+    m = d.DYMOE_DECODE if mode == "decode" else d.DYMOE_PREFILL
+    h, y, status = layer.expert_ffn(x.cuda(), torch.from_numpy(bits).cuda(),
+                                    torch.from_numpy(perm["expert_off"]).cuda(),
+                                    torch.from_numpy(perm["perm_token"]).cuda(), m)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    nx = np_experts(cfg, 1)
+    off = perm["expert_off"]
+    for e in range(cfg.M):
+        lo, hi = int(off[e]), int(off[e + 1])
+        if hi == lo:
+            continue
+        W1, W3, W2 = o_moe.expert_weights(nx[e], int(bits[e]))
+        xr = x.float().numpy()[perm["perm_token"][lo:hi]].astype(np.float64)
+        ref = o_moe.ffn(xr, W1, W3, W2)
+        err = rel_err(y[lo:hi].cpu().numpy(), ref)
+        assert err <= FFN_TOL, (e, int(bits[e]), err)
+
+
+def test_ffn_width_not_resident_sets_status():
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"]
+    ex = gpu_experts(cfg, 2, widths=(4,))
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    x, lg, _ = synthetic.layer_inputs(cfg, 2)
+    bits = torch.full((cfg.M,), 2, dtype=torch.uint8, device="cuda")
+    y, ws = layer.forward(x.cuda(), lg.cuda(), d.make_ladder((4, 2), (0.5,)), 0, 32, forced_bits=bits)
+    rc, word = layer.check_status(cfg.T, ws)
+    assert rc == 6 and word == 1
+    rc, word = layer.check_status(cfg.T, ws)
+    assert rc == 0 and word == 0
+
+
+# ------------------------------------------------------------------------------------ whole layer
+LAYER_CASES = [
+    ("tiny", "decode", (8, 4, 2), (0.25, 0.5), 20, 16),
+    ("tiny", "prefill", (8, 4, 2), (0.25, 0.5), 31, 16),
+    ("tiny", "prefill", (4, 0), (0.5,), 31, 16),
+    ("tiny", "decode", (4, 2), (0.5,), 5, 1),
+    ("tiny", "decode", (16, 8, 4, 2), (0.2, 0.5, 0.8), 25, 8),
+    ("tiny", "prefill", (4, 0), (0.0,), 31, 40),
+]
+
+
+@pytest.mark.parametrize("case", LAYER_CASES)
+def test_moe_forward_layer(case):
+    d = D()
+    name, phase, bits_t, lams, l, T = case
+    cfg = synthetic.CONFIGS[name].with_tokens(T)
+    ex = gpu_experts(cfg, 3)
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    x, lg, a = synthetic.layer_inputs(cfg, 3)
+    ph = d.DYMOE_PREFILL if phase == "prefill" else d.DYMOE_DECODE
+    y, ws = layer.forward(x.cuda(), lg.cuda(), d.make_ladder(bits_t, lams), l, 32, phase=ph,
+                          attn_mass=a.cuda() if ph == d.DYMOE_PREFILL else None)
+    torch.cuda.synchronize()
+    v = layer.views(T, ws)
+    o_lad = o_sched.Ladder(bits=bits_t, lambdas=lams)
+    ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), np_experts(cfg, 3), l, 32, o_lad, cfg.k,
+                            phase=phase, attn_mass=a.numpy())
+    assert np.array_equal(v["topk_idx"].cpu().numpy(), ref["topk_idx"])
+    assert np.array_equal(v["bits"].cpu().numpy(), ref["bits"])
+    if phase == "prefill":
+        assert np.array_equal(v["importance"].cpu().numpy(), ref["importance"].astype(np.float32))
+    assert np.array_equal(v["expert_off"].cpu().numpy(), ref["expert_off"])
+    assert np.array_equal(v["inv_row"].cpu().numpy(), ref["inv_row"])
+    assert rel_err(y.cpu().numpy(), ref["y"]) <= FFN_TOL
+    assert layer.check_status(T, ws)[0] == 0
+
+
+def test_moe_forward_bf16_output_and_empty():
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"]
+    ex = gpu_experts(cfg, 4)
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    x, lg, _ = synthetic.layer_inputs(cfg, 4)
+    lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
+    y32, _ = layer.forward(x.cuda(), lg.cuda(), lad, 7, 32)
+    y16, _ = layer.forward(x.cuda(), lg.cuda(), lad, 7, 32, out_dtype=d.DYMOE_OUT_BF16)
+    assert torch.equal(y16, y32.to(torch.bfloat16))
+    y0, _ = layer.forward(x[:0].cuda(), lg[:0].cuda(), lad, 7, 32)
+    assert y0.shape == (0, cfg.hidden)
+
+
+def test_invalid_arguments_name_the_field():
+    d = D()
+    lg = torch.zeros(4, 8, device="cuda")
+    with pytest.raises(d.DymoeError, match="k:"):
+        d.dymoe_route(lg, 9)
+    with pytest.raises(d.DymoeError, match="ladder.lambdas"):
+        d.dymoe_assign_bits(torch.zeros(8, device="cuda"), 0, 32, d.make_ladder((8, 4, 2), (0.6, 0.5)), 2)
+    with pytest.raises(d.DymoeError, match="K:"):
+        d.dymoe_quantize(torch.zeros(4, 100, dtype=torch.bfloat16, device="cuda"), 4)
+    with pytest.raises(d.DymoeError, match="bits:"):
+        d.dymoe_quantize(torch.zeros(4, 128, dtype=torch.bfloat16, device="cuda"), 3)
