@@ -78,7 +78,7 @@ size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
   size_t topk_idx, topk_w, probs, importance, heavy, bits, active, active_list, expert_off,
-      perm_token, perm_slot, inv_row, h, y_perm, status, score_scratch, total;
+      perm_token, perm_slot, inv_row, h, y_perm, y_part, status, score_scratch, total;
 };
 
 WsLayout ws_layout(int M, int k, int Hd, int F, int T) {
@@ -104,6 +104,7 @@ WsLayout ws_layout(int M, int k, int Hd, int F, int T) {
   L.inv_row = take(TK * 4);
   L.h = take(TK * F * 2);
   L.y_perm = take(TK * Hd * 4);
+  L.y_part = take((size_t)decode_w2_slices(F) * TK * Hd * 4);
   L.status = take(4);
   L.score_scratch = take((size_t)T * 4);
   L.total = o;
@@ -384,15 +385,18 @@ int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk
     int rc = check_ptr_align(y_perm, 16, "y_perm");
     if (rc) return rc;
   }
-  CHECK_LAUNCH(launch_combine(y_perm, inv_row, topk_w, T, k, Hd, renorm, out_dtype, y, S(stream)),
+  CHECK_LAUNCH(launch_combine(y_perm, 1, T * k, inv_row, topk_w, T, k, Hd, renorm, out_dtype, y,
+                              S(stream)),
                "dymoe_combine");
   return ok();
 }
 
 static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, const uint8_t* bits,
                    const int32_t* expert_off, const int32_t* perm_token, const int32_t* active_list,
-                   uint16_t* h, float* y_perm, uint32_t* status, cudaStream_t s,
-                   void* const* ev = nullptr) {
+                   uint16_t* h, float* y_perm, float* y_part, int part_rows, int* parts_out,
+                   uint32_t* status, cudaStream_t s, void* const* ev = nullptr) {
+  // On return *parts_out = number of K-slice partials written to y_part ([parts][part_rows][Hd]),
+  // or 0 if the result was written to y_perm directly.
   FfnArgs a{};
   a.experts = L->dev;
   a.M = L->M;
@@ -407,7 +411,10 @@ static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, con
   a.active_list = active_list;
   a.h = h;
   a.y_perm = y_perm;
+  a.y_part = y_part;
+  a.part_rows = part_rows;
   a.status = status;
+  *parts_out = decode_w2_slices(L->F);
   if (T == 0) return DYMOE_OK;
   cudaError_t e = mode == DYMOE_PREFILL ? launch_ffn_prefill(a, s, ev) : launch_ffn_decode(a, s, ev);
   if (e != cudaSuccess) return cuda_fail(e, "expert ffn");
@@ -435,11 +442,23 @@ int dymoe_expert_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T,
             "x/bits/expert_off/perm_token/h_ws/y_perm: must not be NULL");
   int rc = check_ptr_align(x, 16, "x");
   if (rc) return rc;
+  const int rows = T * L->k;
+  const int SK = decode_w2_slices(L->F);
   int32_t* active = nullptr;
+  float* parts = nullptr;
   cudaError_t e = cudaMallocAsync(&active, (L->M + 1) * sizeof(int32_t), S(stream));
+  if (e == cudaSuccess)
+    e = cudaMallocAsync(&parts, (size_t)SK * rows * L->Hd * sizeof(float), S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dymoe_expert_ffn");
   k_active_from_off<<<1, 32, 0, S(stream)>>>(expert_off, L->M, active);
-  rc = run_ffn(L, mode, x, T, bits, expert_off, perm_token, active, h_ws, y_perm, status, S(stream));
+  int n_parts = 0;
+  rc = run_ffn(L, mode, x, T, bits, expert_off, perm_token, active, h_ws, y_perm, parts, rows,
+               &n_parts, status, S(stream));
+  if (rc == DYMOE_OK && n_parts > 0) {
+    e = launch_reduce_parts(parts, n_parts, rows, rows, L->Hd, y_perm, S(stream));
+    if (e != cudaSuccess) rc = cuda_fail(e, "dymoe_expert_ffn");
+  }
+  cudaFreeAsync(parts, S(stream));
   cudaFreeAsync(active, S(stream));
   if (rc) return rc;
   return ok();
@@ -534,11 +553,14 @@ int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logi
                               v.perm_slot, v.inv_row, active_list, s),
                "permute");
   const int mode = o->ffn_mode == -1 ? o->phase : o->ffn_mode;
+  float* y_part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + W.y_part);
+  int n_parts = 0;
   rc = run_ffn(L, mode, x, T, bits, v.expert_off, v.perm_token, active_list, v.h, v.y_perm,
-               v.status, s, o->prof_events);
+               y_part, T * L->k, &n_parts, v.status, s, o->prof_events);
   if (rc) return rc;
-  CHECK_LAUNCH(launch_combine(v.y_perm, v.inv_row, v.topk_w, T, L->k, L->Hd,
-                              o->ladder.renorm_on_skip, o->out_dtype, y, s),
+  CHECK_LAUNCH(launch_combine(n_parts > 0 ? y_part : v.y_perm, n_parts > 0 ? n_parts : 1, T * L->k,
+                              v.inv_row, v.topk_w, T, L->k, L->Hd, o->ladder.renorm_on_skip,
+                              o->out_dtype, y, s),
                "combine");
   return ok();
 }

@@ -64,9 +64,17 @@ struct FfnArgs {
   const int32_t* perm_token;   // [T*k]
   const int32_t* active_list;  // [M+1]: [0] = count, then expert ids
   uint16_t* h;                 // [T*k][F]
-  float* y_perm;               // [T*k][Hd]
+  float* y_perm;               // [T*k][Hd]   (prefill kernels)
+  float* y_part;               // [SK][part_rows][Hd] (decode kernels: W2 K-slice partials)
+  int part_rows;               // row capacity of one partial slice (>= T*k)
   uint32_t* status;
 };
+// Number of K-slices (and slice length) the decode W2 kernel splits F into.
+int decode_w2_slices(int F);
+int decode_w2_slice_k(int F);
+// y_perm[r][n] = sum_s y_part[s][r][n] (slice order)
+cudaError_t launch_reduce_parts(const float* y_part, int n_parts, int part_rows, int rows, int Hd,
+                                float* y_perm, cudaStream_t s);
 // ev (nullable, 3 entries, each nullable): recorded before W13, between W13 and W2, after W2.
 cudaError_t launch_ffn_decode(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
 cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
@@ -75,9 +83,11 @@ inline void record_ev(void* const* ev, int i, cudaStream_t s) {
   if (ev != nullptr && ev[i] != nullptr) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
 }
 
-cudaError_t launch_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w,
-                           int T, int k, int Hd, int renorm, int out_dtype, void* y,
-                           cudaStream_t s);
+// y_perm may hold n_parts partial slices [n_parts][part_rows][Hd]; they are summed in slice order
+// before weighting (n_parts = 1, part_rows ignored for a plain y_perm).
+cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, const int32_t* inv_row,
+                           const float* topk_w, int T, int k, int Hd, int renorm, int out_dtype,
+                           void* y, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------------
 // Small device helpers.

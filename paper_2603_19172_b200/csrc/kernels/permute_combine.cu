@@ -94,11 +94,49 @@ cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const u
 }
 
 // -------------------------------------------------------------------------------------------
-// Combine: one CTA per token, float4 over Hd.
-__global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_perm,
+// Combine: one CTA per token, float4 over Hd.  With n_parts > 1 the expert outputs arrive as
+// K-slice partials (decode W2 kernel) and are summed in slice order first.
+__device__ __forceinline__ float4 load_row(const float* __restrict__ y_perm, int n_parts,
+                                           size_t part_stride, int row, int Hd, int c) {
+  float4 v = *reinterpret_cast<const float4*>(y_perm + (size_t)row * Hd + c);
+  for (int p = 1; p < n_parts; ++p) {
+    const float4 u = *reinterpret_cast<const float4*>(y_perm + p * part_stride + (size_t)row * Hd + c);
+    v.x = __fadd_rn(v.x, u.x);
+    v.y = __fadd_rn(v.y, u.y);
+    v.z = __fadd_rn(v.z, u.z);
+    v.w = __fadd_rn(v.w, u.w);
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ y_part, int n_parts,
+                                                      int part_rows, int rows, int Hd,
+                                                      float* __restrict__ y_perm) {
+  const size_t stride = (size_t)part_rows * Hd;
+  const size_t total4 = (size_t)rows * Hd / 4;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const int row = (int)(i * 4 / Hd), c = (int)(i * 4 - (size_t)row * Hd);
+    *reinterpret_cast<float4*>(y_perm + (size_t)row * Hd + c) =
+        load_row(y_part, n_parts, stride, row, Hd, c);
+  }
+}
+
+cudaError_t launch_reduce_parts(const float* y_part, int n_parts, int part_rows, int rows, int Hd,
+                                float* y_perm, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  const size_t total4 = (size_t)rows * Hd / 4;
+  const int blocks = (int)((total4 + 255) / 256 < 4096 ? (total4 + 255) / 256 : 4096);
+  k_reduce_parts<<<blocks, 256, 0, s>>>(y_part, n_parts, part_rows, rows, Hd, y_perm);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_perm, int n_parts,
+                                                 int part_rows,
                                                  const int32_t* __restrict__ inv_row,
                                                  const float* __restrict__ topk_w, int k, int Hd,
                                                  int renorm, int out_bf16, void* __restrict__ y) {
+  const size_t part_stride = (size_t)part_rows * Hd;
   const int t = blockIdx.x;
   int rows[8];
   float wt[8];
@@ -117,7 +155,7 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < k; ++s) {
       if (rows[s] < 0) continue;
-      const float4 v = *reinterpret_cast<const float4*>(y_perm + (size_t)rows[s] * Hd + c);
+      const float4 v = load_row(y_perm, n_parts, part_stride, rows[s], Hd, c);
       acc.x = __fadd_rn(acc.x, __fmul_rn(wt[s], v.x));
       acc.y = __fadd_rn(acc.y, __fmul_rn(wt[s], v.y));
       acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], v.z));
@@ -137,11 +175,11 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
   (void)live;
 }
 
-cudaError_t launch_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w,
-                           int T, int k, int Hd, int renorm, int out_dtype, void* y,
-                           cudaStream_t s) {
+cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, const int32_t* inv_row,
+                           const float* topk_w, int T, int k, int Hd, int renorm, int out_dtype,
+                           void* y, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  k_combine<<<T, 256, 0, s>>>(y_perm, inv_row, topk_w, k, Hd, renorm,
+  k_combine<<<T, 256, 0, s>>>(y_perm, n_parts, part_rows, inv_row, topk_w, k, Hd, renorm,
                               out_dtype == DYMOE_OUT_BF16, y);
   return cudaGetLastError();
 }

@@ -89,7 +89,7 @@ def test_validation_messages_name_the_field(d):
     rc, msg = _err(d, L.dymoe_score(0, FAKE, 32, FAKE, None, 10, 8, 2, 11, FAKE, None, FAKE, None))
     assert rc == 1 and msg.startswith("k_tokens:")
     rc, msg = _err(d, L.dymoe_combine(FAKE, FAKE, FAKE, 3, 2, 6, 1, 7, FAKE, None))
-    assert rc == 1 and msg.startswith("Hd:") or msg.startswith("out_dtype:")
+    assert rc == 1 and (msg.startswith("Hd:") or msg.startswith("out_dtype:"))
     desc = d.LayerDesc(8, 2, 100, 256, None)
     h = ctypes.c_void_p()
     rc, msg = _err(d, L.dymoe_layer_create(ctypes.byref(desc), ctypes.byref(h)))

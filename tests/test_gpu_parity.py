@@ -150,7 +150,7 @@ def test_quantize_batched_mixed_jobs():
 def test_permute(T, M, k):
     d = D()
     rng = np.random.default_rng(T + M)
-    idx = np.stack([rng.permutation(M)[:k] for _ in range(T)]).astype(np.int32).reshape(T, k)
+    idx = np.array([rng.permutation(M)[:k] for _ in range(T)], dtype=np.int32).reshape(T, k)
     bits = rng.choice([0, 2, 4, 8, 16], size=M).astype(np.uint8)
     off, pt, ps, inv = d.dymoe_permute(torch.from_numpy(idx).cuda(), M, torch.from_numpy(bits).cuda())
     ref = o_moe.permute(idx, bits, M)
