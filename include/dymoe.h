@@ -158,9 +158,14 @@ typedef struct dymoe_layer_desc {
 } dymoe_layer_desc;
 
 /* Opaque handle holding a device copy of the expert table (created once per layer; the weights
- * themselves stay caller-owned and must outlive the handle).  create synchronises once.       */
+ * themselves stay caller-owned and must outlive the handle).  create synchronises once.
+ * The handle also owns a derived per-group word (bf16 bits of RNE_bf16(scale) << 16 | zero) for
+ * every resident quantized matrix — the exact pair dequant (D17) consumes — so the decode
+ * kernels fetch a group's metadata with one 4-byte copy.  If scales/zeros are re-quantized after
+ * create, call dymoe_layer_refresh (asynchronous on `stream`) before the next forward.        */
 typedef struct dymoe_layer dymoe_layer;
 int dymoe_layer_create(const dymoe_layer_desc* desc, dymoe_layer** out);
+int dymoe_layer_refresh(dymoe_layer* layer, dymoe_stream_t stream);
 int dymoe_layer_destroy(dymoe_layer* layer);
 
 /* ------------------------------------------------------------------------------------------ */

@@ -17,6 +17,7 @@ struct dymoe_layer {
   int M, k, Hd, F;
   std::vector<DevExpert> host;
   DevExpert* dev = nullptr;
+  uint32_t* meta_pool = nullptr;   // derived dequant metadata of every resident quantized matrix
 };
 
 namespace {
@@ -328,24 +329,65 @@ int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
         return fail(DYMOE_ERR_INVALID, "desc.experts[%d].w%d: must be 16-byte aligned", e, m == 0 ? 1 : m == 1 ? 3 : 2);
       }
   }
-  cudaError_t e = cudaMalloc(&L->dev, sizeof(DevExpert) * d->M);
+  // derived per-group dequant metadata for every resident quantized matrix (one pool)
+  size_t meta_words = 0;
+  for (int ex = 0; ex < d->M; ++ex)
+    for (int wi = 0; wi < 3; ++wi)
+      for (int m = 0; m < 3; ++m)
+        if (L->host[ex].q[wi][m].codes != nullptr) {
+          const size_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
+          meta_words += N * (K / DYMOE_GROUP);
+        }
+  cudaError_t e = cudaSuccess;
+  if (meta_words > 0) e = cudaMalloc(&L->meta_pool, meta_words * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&L->dev, sizeof(DevExpert) * d->M);
   if (e != cudaSuccess) {
-    delete L;
+    dymoe_layer_destroy(L);
     return cuda_fail(e, "dymoe_layer_create");
   }
-  e = cudaMemcpy(L->dev, L->host.data(), sizeof(DevExpert) * d->M, cudaMemcpyHostToDevice);
+  size_t at = 0;
+  for (int ex = 0; ex < d->M && e == cudaSuccess; ++ex)
+    for (int wi = 0; wi < 3; ++wi)
+      for (int m = 0; m < 3; ++m) {
+        DevQMat& q = L->host[ex].q[wi][m];
+        q.meta = nullptr;
+        if (q.codes == nullptr) continue;
+        const size_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
+        const size_t n = N * (K / DYMOE_GROUP);
+        q.meta = L->meta_pool + at;
+        if (e == cudaSuccess) e = launch_build_meta(q.scales, q.zeros, n, L->meta_pool + at, nullptr);
+        at += n;
+      }
+  if (e == cudaSuccess)
+    e = cudaMemcpy(L->dev, L->host.data(), sizeof(DevExpert) * d->M, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
-    cudaFree(L->dev);
-    delete L;
+    dymoe_layer_destroy(L);
     return cuda_fail(e, "dymoe_layer_create");
   }
   *out = L;
   return ok();
 }
 
+int dymoe_layer_refresh(dymoe_layer* L, dymoe_stream_t stream) {
+  CHECK_ARG(L != nullptr, "layer: must not be NULL");
+  for (int ex = 0; ex < L->M; ++ex)
+    for (int wi = 0; wi < 3; ++wi)
+      for (int m = 0; m < 3; ++m) {
+        const DevQMat& q = L->host[ex].q[wi][m];
+        if (q.codes == nullptr) continue;
+        const size_t N = m == 2 ? L->Hd : L->F, K = m == 2 ? L->F : L->Hd;
+        CHECK_LAUNCH(launch_build_meta(q.scales, q.zeros, N * (K / DYMOE_GROUP),
+                                       const_cast<uint32_t*>(q.meta), S(stream)),
+                     "dymoe_layer_refresh");
+      }
+  return ok();
+}
+
 int dymoe_layer_destroy(dymoe_layer* L) {
   if (!L) return ok();
   if (L->dev) cudaFree(L->dev);
+  if (L->meta_pool) cudaFree(L->meta_pool);
   delete L;
   return ok();
 }

@@ -16,7 +16,13 @@ struct DevQMat {
   const uint32_t* codes;
   const float* scales;
   const uint8_t* zeros;
+  // Derived by the layer handle (dymoe_layer_create / refresh), owned by it: per group
+  // (bf16 bits of RNE_bf16(scale)) << 16 | zero — exactly the two values dequant (D17) consumes,
+  // in one 4-byte word, so the decode kernels fetch a group's metadata with one copy.
+  const uint32_t* meta;
 };
+cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, size_t n, uint32_t* meta,
+                              cudaStream_t s);
 struct DevExpert {
   const uint16_t* w[3];   // bf16 masters W1, W3, W2
   DevQMat q[3][3];        // [width idx: int8, int4, int2][matrix: W1, W3, W2]

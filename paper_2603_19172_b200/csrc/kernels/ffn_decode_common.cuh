@@ -1,0 +1,206 @@
+// Register-level building blocks of the decode fused-dequant GEMV (ffn_decode.cu): traits per
+// width, 128-bit loads, LOP3/PRMT dequant into mma.sync A fragments, matching B fragments, the
+// swizzled x layout, and the cost-proportional allocation of virtual CTAs to experts.
+#pragma once
+#include "../dymoe_internal.cuh"
+
+namespace dymoe {
+namespace dec {
+
+template <int BITS>
+struct WT {
+  static constexpr int CODES = 128 / BITS;   // k values per lane per row per chunk
+  static constexpr int CHUNK_K = 4 * CODES;  // k per chunk (a lane quad covers 64 bytes)
+  static constexpr int STEPS = CODES / 4;    // mma k16 steps per chunk
+  static constexpr int XU4 = CODES / 8;      // uint4 of x per lane per chunk
+  // row padding (in 16-byte granules, mod 8) that makes the 2 token rows of an LDS.128 phase
+  // hit disjoint bank groups (see x_granule)
+  static constexpr int PAD = BITS == 2 ? 4 : BITS == 4 ? 2 : BITS == 8 ? 1 : 4;
+  static constexpr int GPQ = BITS == 2 ? 2 : 1;   // quantization groups a lane quad spans per chunk
+};
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kMaxTok = 8;      // tokens per pass (mma N)
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float ld_f32(const float* p) {
+  float r;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r) : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ uint32_t lop_or_and(uint32_t x, uint32_t mask, uint32_t orv) {
+  uint32_t r;  // (x & mask) | orv in one LOP3
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(x), "r"(mask), "r"(orv));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf2_sub(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&a),
+                             *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t bf2_mul(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmul2(*reinterpret_cast<__nv_bfloat162*>(&a),
+                             *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  __nv_bfloat162 r = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t word(const uint4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+
+struct DQ {
+  uint32_t ss, zz;  // bf16x2 (s, s) and (128+z, 128+z)
+  float sf, zf;     // Int8: bf16(s) as float, 2^23 + z
+};
+__device__ __forceinline__ DQ make_dq(float s, uint32_t z) {
+  DQ d;
+  const __nv_bfloat16 sb = __float2bfloat16_rn(s);
+  const uint32_t sbits = *reinterpret_cast<const uint16_t*>(&sb);
+  d.ss = sbits | (sbits << 16);
+  const uint32_t zb = 0x4300u | z;  // bf16(128 + z), exact for z < 128 (Int2/Int4)
+  d.zz = zb | (zb << 16);
+  d.sf = __bfloat162float(sb);
+  d.zf = __uint_as_float(0x4B000000u | z);
+  return d;
+}
+
+// A-fragment pair (logical k slots lo = {2c, 2c+1}, hi = {2c+8, 2c+9}) for step s of a chunk.
+template <int BITS>
+__device__ __forceinline__ void a_frag(const uint4& w, const DQ& dq, int s, uint32_t& lo,
+                                       uint32_t& hi) {
+  if constexpr (BITS == 16) {
+    lo = word(w, 2 * s);
+    hi = word(w, 2 * s + 1);
+  } else if constexpr (BITS == 4) {
+    const uint32_t x = word(w, s >> 1);
+    const int sh = 8 * (s & 1);
+    lo = bf2_mul(bf2_sub(lop_or_and(x >> sh, 0x000F000Fu, 0x43004300u), dq.zz), dq.ss);
+    hi = bf2_mul(bf2_sub(lop_or_and(x >> (sh + 4), 0x000F000Fu, 0x43004300u), dq.zz), dq.ss);
+  } else if constexpr (BITS == 2) {
+    const uint32_t x = word(w, s >> 2);
+    const int sh = 4 * (s & 3);
+    lo = bf2_mul(bf2_sub(lop_or_and(x >> sh, 0x00030003u, 0x43004300u), dq.zz), dq.ss);
+    hi = bf2_mul(bf2_sub(lop_or_and(x >> (sh + 2), 0x00030003u, 0x43004300u), dq.zz), dq.ss);
+  } else {  // 8
+    // q - z exact in fp32 (2^23 + q minus 2^23 + z), packed to bf16x2 exactly (|q - z| <= 255
+    // has 8 significant bits), then one HMUL2 per pair gives RNE((q - z)·s) (D17)
+    const uint32_t x = word(w, s);
+    const float d0 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7440u)), dq.zf);
+    const float d1 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7441u)), dq.zf);
+    const float d2 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7442u)), dq.zf);
+    const float d3 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7443u)), dq.zf);
+    lo = bf2_mul(pack_bf2(d0, d1), dq.ss);
+    hi = bf2_mul(pack_bf2(d2, d3), dq.ss);
+  }
+}
+
+// B fragment (x permuted to a_frag's k order) for step s, from the chunk's x registers.
+template <int BITS>
+__device__ __forceinline__ void b_frag(const uint4 (&xv)[WT<BITS>::XU4], int s, uint32_t& b0,
+                                       uint32_t& b1) {
+  if constexpr (BITS == 16) {
+    b0 = word(xv[0], 2 * s);
+    b1 = word(xv[0], 2 * s + 1);
+  } else if constexpr (BITS == 8) {
+    b0 = word(xv[s >> 1], 2 * (s & 1));
+    b1 = word(xv[s >> 1], 2 * (s & 1) + 1);
+  } else if constexpr (BITS == 4) {
+    const uint4& u = xv[s >> 1];
+    const int j = s & 1;
+    const uint32_t a = word(u, j), c = word(u, j + 2);
+    b0 = prmt(a, c, 0x5410u);
+    b1 = prmt(a, c, 0x7632u);
+  } else {  // 2
+    const int q = s >> 2, j = s & 3;
+    const uint32_t a = word(xv[2 * q], j), c = word(xv[2 * q + 1], j);
+    b0 = prmt(a, c, 0x5410u);
+    b1 = prmt(a, c, 0x7632u);
+  }
+}
+
+// x slice in shared memory: [8 tokens][row_gran granules of 16 B], granule index XOR-swizzled
+// with (g >> 3) & 7 so that the 4 lanes of a quad (k offsets c*XU4 granules apart) hit distinct
+// bank groups; row_gran = sliceK/8 + PAD puts the second token row of a phase on the other four.
+__device__ __forceinline__ int x_granule(int g) { return g ^ ((g >> 3) & 7); }
+
+struct Alloc {
+  int n_act;
+  int expert[DYMOE_MAX_EXPERTS];
+  int first_unit[DYMOE_MAX_EXPERTS + 1];
+  int units_total;
+  long long cost[DYMOE_MAX_EXPERTS];   // scratch
+  long long rem[DYMOE_MAX_EXPERTS];
+  int u[DYMOE_MAX_EXPERTS];
+};
+
+__device__ __forceinline__ int wcost(int b) { return b == 16 ? 256 : 16 * b + 5; }
+
+// Cost-proportional allocation of `units_total` units to the active experts (largest remainder,
+// ties to the lower list index; every active expert gets >= 1 unit).  Thread 0 only.
+__device__ void compute_alloc(const FfnArgs& a, int units_grid, Alloc& A) {
+  const int n = a.active_list[0];
+  A.n_act = n;
+  long long* cost = A.cost;
+  long long total = 0;
+  for (int i = 0; i < n; ++i) {
+    const int e = a.active_list[1 + i];
+    A.expert[i] = e;
+    const int rows = a.expert_off[e + 1] - a.expert_off[e];
+    const int chunks = (rows + kMaxTok - 1) / kMaxTok;
+    cost[i] = (long long)wcost(a.bits[e]) * chunks;
+    total += cost[i];
+  }
+  const int U = units_grid > n ? units_grid : n;
+  A.units_total = U;
+  int* u = A.u;
+  long long* rem = A.rem;
+  int used = 0;
+  for (int i = 0; i < n; ++i) {
+    const long long num = (long long)(U - n) * cost[i];   // n units reserved (one each)
+    u[i] = 1 + (int)(num / total);
+    rem[i] = num % total;
+    used += u[i];
+  }
+  while (used < U) {  // hand out the rest by largest remainder
+    int best = 0;
+    for (int i = 1; i < n; ++i)
+      if (rem[i] > rem[best]) best = i;
+    u[best] += 1;
+    rem[best] = -1;
+    ++used;
+  }
+  int acc = 0;
+  for (int i = 0; i < n; ++i) {
+    A.first_unit[i] = acc;
+    acc += u[i];
+  }
+  A.first_unit[n] = acc;
+}
+
+
+}  // namespace dec
+}  // namespace dymoe

@@ -147,6 +147,25 @@ __global__ void __launch_bounds__(256) k_quantize(const __grid_constant__ QJobs 
   }
 }
 
+// Derived dequant metadata: meta[i] = bf16bits(RNE_bf16(scales[i])) << 16 | zeros[i].
+__global__ void __launch_bounds__(256) k_build_meta(const float* __restrict__ scales,
+                                                    const uint8_t* __restrict__ zeros, size_t n,
+                                                    uint32_t* __restrict__ meta) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const __nv_bfloat16 sb = __float2bfloat16_rn(scales[i]);
+    meta[i] = ((uint32_t)*reinterpret_cast<const uint16_t*>(&sb) << 16) | (uint32_t)zeros[i];
+  }
+}
+
+cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, size_t n, uint32_t* meta,
+                              cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const size_t blocks = (n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192;
+  k_build_meta<<<(unsigned)blocks, 256, 0, s>>>(scales, zeros, n, meta);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

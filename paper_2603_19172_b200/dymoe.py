@@ -23,7 +23,7 @@ WIDTH_INDEX = {8: 0, 4: 1, 2: 2}
 EXPORTED = [
     "dymoe_route", "dymoe_score", "dymoe_score_scratch_bytes", "dymoe_assign_bits",
     "dymoe_retention_ratio", "dymoe_tier_counts", "dymoe_quantize", "dymoe_quantize_batched",
-    "dymoe_layer_create", "dymoe_layer_destroy", "dymoe_permute", "dymoe_expert_ffn",
+    "dymoe_layer_create", "dymoe_layer_refresh", "dymoe_layer_destroy", "dymoe_permute", "dymoe_expert_ffn",
     "dymoe_combine", "dymoe_workspace_size", "dymoe_workspace_views", "dymoe_moe_forward",
     "dymoe_check_status", "dymoe_last_error", "dymoe_version",
 ]
@@ -97,6 +97,7 @@ def lib():
             "dymoe_quantize_batched": [ctypes.POINTER(QuantJob), ci, ci, vp],
             "dymoe_layer_create": [ctypes.POINTER(LayerDesc), ctypes.POINTER(vp)],
             "dymoe_layer_destroy": [vp],
+            "dymoe_layer_refresh": [vp, vp],
             "dymoe_permute": [vp, ci, ci, ci, vp, vp, vp, vp, vp, vp],
             "dymoe_expert_ffn": [vp, ci, vp, ci, vp, vp, vp, vp, vp, vp, vp],
             "dymoe_combine": [vp, vp, vp, ci, ci, ci, ci, ci, vp, vp],
@@ -293,6 +294,10 @@ class MoELayer:
                 self.handle = None
         except Exception:
             pass
+
+    def refresh(self, stream=None):
+        """dymoe_layer_refresh: rebuild the derived dequant metadata after re-quantizing."""
+        _check(lib().dymoe_layer_refresh(self.handle, _stream(stream)))
 
     def workspace(self, T, device="cuda"):
         n = lib().dymoe_workspace_size(self.handle, T)
