@@ -456,7 +456,8 @@ static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, con
   a.y_part = y_part;
   a.part_rows = part_rows;
   a.status = status;
-  *parts_out = decode_w2_slices(L->F);
+  // decode kernels write K-slice partials of W2; the prefill grouped GEMM writes y_perm directly
+  *parts_out = mode == DYMOE_PREFILL ? 0 : decode_w2_slices(L->F);
   if (T == 0) return DYMOE_OK;
   cudaError_t e = mode == DYMOE_PREFILL ? launch_ffn_prefill(a, s, ev) : launch_ffn_decode(a, s, ev);
   if (e != cudaSuccess) return cuda_fail(e, "expert ffn");

@@ -1,9 +1,524 @@
-// Prefill expert FFN (row a6).  Temporary: routes through the decode GEMV kernels (which loop
-// over 8-token chunks) until the tcgen05 grouped GEMM lands.
+// Prefill expert FFN (row a6): fused-dequant grouped GEMM on the 5th-generation tensor cores
+// (tcgen05 / TMEM) for sm_100a.
+//
+// Paper: P:203 step 4 (executor on a unified mixed-precision weight set), P:312 (Int4/Int2,
+// skip), P:354 (prefill time).  Readings D13, D17, D18, O6: A = xp·deq(W1)^T, B = xp·deq(W3)^T
+// (fp32 accumulation in TMEM), h = RNE_bf16(silu(A)·B), y = h·deq(W2)^T (fp32),
+// deq = RNE_bf16((q - z)·RNE_bf16(s)).
+//
+// Roofline: tensor cores (a dense contraction: 2*3*Hd*F flops per routed (token, expert) pair,
+// arithmetic intensity 512-3500 flop/B).  Design:
+//  * CTA tile = 256 tokens (two M=128 UMMA accumulators) x 128 weight rows per matrix; GEMM 1
+//    stacks the W1 and W3 rows of the same output features into one N=256 B tile, so one
+//    tcgen05.mma produces gate and up side by side and SwiGLU is fused in the epilogue.
+//    TMEM: 2 x 256 fp32 columns (GEMM 1) or 2 x 128 (GEMM 2).
+//  * warp roles (11 warps): warps 0-1 gather the token rows (A, bf16) with cp.async into
+//    128B-swizzled K-major smem tiles (rows of x by perm_token for GEMM 1, rows of h for
+//    GEMM 2; rows past the expert's count are zero-filled); warps 2-9 stream the packed codes
+//    + per-group dequant words from HBM (one stage ahead, in registers), dequantize in natural
+//    k order (LOP3/PRMT magic-number extraction, HSUB2 (128+z), HMUL2 s — bit-identical to D17)
+//    and store bf16 into the swizzled B tile, then fence.proxy.async and arrive; one thread of
+//    warp 10 issues tcgen05.mma (kind::f16, bf16 x bf16 -> f32) and tcgen05.commit frees each
+//    smem stage; after the K loop warps 2-9 drain TMEM (tcgen05.ld 32x32b) for the epilogue.
+//  * 3-stage mbarrier pipeline (64 KB per stage), persistent grid of one CTA per SM walking the
+//    (expert, 256-token tile, 128-row tile) list round-robin.  Each dequantized weight tile
+//    feeds 256 tokens, so dequant costs ~2 ALU ops per 512 MMA flops.
 #include "../dymoe_internal.cuh"
 
 namespace dymoe {
-cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev) {
-  return launch_ffn_decode(a, s, ev);
+namespace pf {
+
+constexpr int BM = 128;           // UMMA M (tokens per accumulator)
+constexpr int MT = 2;             // accumulators per CTA tile -> 256 tokens
+constexpr int TOK = BM * MT;
+constexpr int BN = 128;           // weight rows per matrix per tile
+constexpr int BK = 64;            // k per stage (one 128-byte swizzle atom row)
+constexpr int STAGES = 3;
+constexpr int A_BYTES = TOK * BK * 2;          // 32 KB
+constexpr int B_BYTES_MAX = 2 * BN * BK * 2;   // 32 KB (GEMM 1: W1 + W3 rows)
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
+constexpr int kAWarps = 2, kBWarps = 8;
+constexpr int kMmaWarp = kAWarps + kBWarps;
+constexpr int kThreads = (kMmaWarp + 1) * 32;   // 352
+constexpr int kAThreads = kAWarps * 32, kBThreads = kBWarps * 32;
+constexpr int kSmem = STAGES * STAGE_BYTES + 1024;   // + alignment slack
+
+// ---------------------------------------------------------------------------------------- PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async_zfill(uint32_t saddr, const void* g, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);        // start address
+  d |= (uint64_t)1u << 16;                        // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;              // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1u << 46;                        // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;                        // layout: SWIZZLE_128B
+  return d;
+}
+// Instruction descriptor, kind::f16: bf16 A/B, f32 D, both K-major.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// byte offset of 16-byte chunk j (k = 8j..8j+7) of row r inside a 128B-swizzled K-major tile
+__device__ __forceinline__ uint32_t sw128_off(int r, int j) {
+  return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((j ^ (r & 7)) << 4));
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+__device__ __forceinline__ uint32_t bf2_sub(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t bf2_mul(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmul2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
+  __nv_bfloat162 r = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w));
+}
+
+// ---------------------------------------------------------------------------------------- dequant
+// Natural-order bf16 pairs from packed codes; every pair = RNE_bf16((q - z)·s) (D17).
+struct DQP {
+  uint32_t zz, ss;   // bf16x2 (128 + z, 128 + z) and (s, s)
+  float zf;          // Int8: 2^23 + z
+};
+__device__ __forceinline__ DQP dqp_from_meta(uint32_t m) {
+  DQP d;
+  d.ss = prmt(m, 0u, 0x3232u);
+  const uint32_t zb = 0x4300u | (m & 0xffu);
+  d.zz = zb | (zb << 16);
+  d.zf = __uint_as_float(0x4B000000u | (m & 0xffu));
+  return d;
+}
+__device__ __forceinline__ uint32_t fin(uint32_t magic_pair, const DQP& d) {
+  return bf2_mul(bf2_sub(magic_pair, d.zz), d.ss);
+}
+// Int4: one word = 8 codes (k0..k7) -> 4 bf16 pairs in k order (one 16-byte chunk)
+__device__ __forceinline__ uint4 deq_int4_word(uint32_t w, const DQP& d) {
+  const uint32_t e = w & 0x0F0F0F0Fu;          // bytes: n0 n2 n4 n6
+  const uint32_t o = (w >> 4) & 0x0F0F0F0Fu;   // bytes: n1 n3 n5 n7
+  const uint32_t t0 = prmt(e, o, 0x5140u);     // n0 n1 n2 n3
+  const uint32_t t1 = prmt(e, o, 0x7362u);     // n4 n5 n6 n7
+  const uint32_t M = 0x43434343u;
+  uint4 r;
+  r.x = fin(prmt(t0, M, 0x7170u), d);   // (n0, n1): bytes [n0, 43, n1, 43]
+  r.y = fin(prmt(t0, M, 0x7372u), d);
+  r.z = fin(prmt(t1, M, 0x7170u), d);
+  r.w = fin(prmt(t1, M, 0x7372u), d);
+  return r;
+}
+// Int2: one word = 16 codes (k0..k15) -> two 16-byte chunks
+__device__ __forceinline__ void deq_int2_word(uint32_t w, const DQP& d, uint4& lo, uint4& hi) {
+  const uint32_t b0 = w & 0x03030303u;          // c0 c4 c8  c12
+  const uint32_t b1 = (w >> 2) & 0x03030303u;   // c1 c5 c9  c13
+  const uint32_t b2 = (w >> 4) & 0x03030303u;   // c2 c6 c10 c14
+  const uint32_t b3 = (w >> 6) & 0x03030303u;   // c3 c7 c11 c15
+  const uint32_t t0 = prmt(b0, b1, 0x5140u);    // c0 c1 c4 c5
+  const uint32_t t1 = prmt(b2, b3, 0x5140u);    // c2 c3 c6 c7
+  const uint32_t t2 = prmt(b0, b1, 0x7362u);    // c8 c9 c12 c13
+  const uint32_t t3 = prmt(b2, b3, 0x7362u);    // c10 c11 c14 c15
+  const uint32_t M = 0x43434343u;
+  lo.x = fin(prmt(t0, M, 0x7170u), d);   // c0 c1
+  lo.y = fin(prmt(t1, M, 0x7170u), d);   // c2 c3
+  lo.z = fin(prmt(t0, M, 0x7372u), d);   // c4 c5
+  lo.w = fin(prmt(t1, M, 0x7372u), d);   // c6 c7
+  hi.x = fin(prmt(t2, M, 0x7170u), d);   // c8 c9
+  hi.y = fin(prmt(t3, M, 0x7170u), d);   // c10 c11
+  hi.z = fin(prmt(t2, M, 0x7372u), d);   // c12 c13
+  hi.w = fin(prmt(t3, M, 0x7372u), d);   // c14 c15
+}
+// Int8: two words = 8 codes -> one 16-byte chunk
+__device__ __forceinline__ uint32_t deq_int8_pair(uint32_t w, int i, const DQP& d) {
+  const float d0 = __fsub_rn(__uint_as_float(prmt(w, 0x4B000000u, 0x7440u + i)), d.zf);
+  const float d1 = __fsub_rn(__uint_as_float(prmt(w, 0x4B000000u, 0x7441u + i)), d.zf);
+  return bf2_mul(pack_bf2(d0, d1), d.ss);
+}
+
+// ---------------------------------------------------------------------------------------- tiles
+struct Sched {
+  int n;                                   // active experts
+  int expert[DYMOE_MAX_EXPERTS];
+  int first[DYMOE_MAX_EXPERTS + 1];        // prefix of tiles per expert
+};
+struct Tile {
+  int e, m0, n0, rows;   // expert, first token row (relative), first weight row, valid tokens
+};
+__device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t, int ntiles_n) {
+  int i = 0;
+  while (S.first[i + 1] <= t) ++i;
+  Tile r;
+  r.e = S.expert[i];
+  const int local = t - S.first[i];
+  const int mt = local / ntiles_n, nt = local - mt * ntiles_n;
+  const int n_e = a.expert_off[r.e + 1] - a.expert_off[r.e];
+  r.m0 = mt * TOK;
+  r.n0 = nt * BN;
+  r.rows = min(TOK, n_e - r.m0);
+  return r;
+}
+
+template <bool W13>
+__global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ Sched S;
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ int n_tiles_sh;
+  constexpr int NW = W13 ? 2 * BN : BN;               // weight rows in the B tile
+  constexpr int NCOL = W13 ? 2 * BN : BN;             // TMEM columns per accumulator
+  constexpr uint32_t TMEM_COLS = MT * NCOL <= 256 ? 256 : 512;
+  constexpr uint32_t IDESC = make_idesc(BM, NCOL);
+  const int K = W13 ? a.Hd : a.F;
+  const int NWR = W13 ? a.F : a.Hd;                  // weight rows per matrix
+  const int ntiles_n = NWR / BN;
+  const int nk = K / BK;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sbase = smem_u32(smem);
+  auto sA = [&](int s) { return sbase + s * STAGE_BYTES; };
+  auto sB = [&](int s) { return sbase + s * STAGE_BYTES + A_BYTES; };
+
+  if (threadIdx.x == 0) {
+    const int n = a.active_list[0];
+    int acc = 0, na = 0;
+    for (int i = 0; i < n; ++i) {
+      const int e = a.active_list[1 + i];
+      const int n_e = a.expert_off[e + 1] - a.expert_off[e];
+      if (a.bits[e] == 0 || n_e == 0) continue;
+      S.expert[na] = e;
+      S.first[na] = acc;
+      acc += ((n_e + TOK - 1) / TOK) * ntiles_n;
+      ++na;
+    }
+    S.first[na] = acc;
+    S.n = na;
+    n_tiles_sh = acc;
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), kAThreads + kBThreads);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&tfull_bar), 1);
+    mbar_init(smem_u32(&tempty_bar), kBThreads);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+  const int n_tiles = n_tiles_sh;
+
+  if (warp < kAWarps) {
+    // ------------------------------------------------------------------ A producer (tokens)
+    const int tid = threadIdx.x;   // 0..63
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile T = tile_at(S, a, t, ntiles_n);
+      const int off = a.expert_off[T.e];
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+        const uint32_t dst = sA(stage);
+#pragma unroll 4
+        for (int i = 0; i < (TOK * 8) / kAThreads; ++i) {     // 32 x 16-byte chunks each
+          const int id = i * kAThreads + tid;
+          const int r = id >> 3, j = id & 7;
+          const bool ok = r < T.rows;
+          const uint16_t* src;
+          if (W13) {
+            const int tokrow = ok ? a.perm_token[off + T.m0 + r] : 0;
+            src = a.x + (size_t)tokrow * a.Hd + kb * BK + j * 8;
+          } else {
+            src = a.h + (size_t)(off + T.m0 + (ok ? r : 0)) * a.F + kb * BK + j * 8;
+          }
+          cp_async_zfill(dst + sw128_off(r, j), src, ok ? 16u : 0u);
+        }
+        cp_async_arrive_noinc(smem_u32(&full_bar[stage]));
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp < kMmaWarp) {
+    // ------------------------------------------------------------------ B producer (dequant)
+    const int tb = threadIdx.x - kAThreads;   // 0..255
+    int stage = 0;
+    uint32_t phase = 0, tphase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile T = tile_at(S, a, t, ntiles_n);
+      const int be = a.bits[T.e];
+      const DevExpert& E = a.experts[T.e];
+      // this thread's weight row (GEMM 1: 0-127 W1, 128-255 W3; GEMM 2: two threads per row)
+      const int wr = W13 ? tb : (tb >> 1);
+      const int khalf = W13 ? 0 : (tb & 1);          // GEMM 2: which 32-k half of the stage
+      const int mi = W13 ? (wr >= BN ? 1 : 0) : 2;
+      const int row = T.n0 + (W13 ? (wr & (BN - 1)) : wr);
+      const int kper = W13 ? BK : BK / 2;            // k values per thread per stage
+      const int wi = width_index(be);
+      const uint8_t* codes = be == 16 ? reinterpret_cast<const uint8_t*>(E.w[mi])
+                                      : reinterpret_cast<const uint8_t*>(E.q[wi][mi].codes);
+      const uint32_t* meta = be == 16 ? nullptr : E.q[wi][mi].meta;
+      const size_t row_bytes = (size_t)K * be / 8;
+      const int gpr = K / DYMOE_GROUP;
+      const uint8_t* rowp = codes + (size_t)row * row_bytes;
+      const uint32_t* metap = meta ? meta + (size_t)row * gpr : nullptr;
+      // bytes per thread per stage: kper * be / 8  (<= 128)
+      uint4 cur[8], nxt[8];
+      uint32_t mcur = 0, mnxt = 0;
+      const int nvec = (kper * be / 8 + 15) / 16;    // 16-byte loads per thread per stage
+      const int nbytes = kper * be / 8;               // 8 (GEMM 2 Int2) .. 128 bytes
+      auto load = [&](uint4 (&v)[8], uint32_t& mw, int kb) {
+        const size_t kbyte = ((size_t)kb * BK + khalf * kper) * be / 8;
+        if (nbytes == 8) {
+          const uint2 u = __ldg(reinterpret_cast<const uint2*>(rowp + kbyte));
+          v[0] = make_uint4(u.x, u.y, 0u, 0u);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i < nvec) v[i] = ldg_stream(rowp + kbyte + 16 * i);
+        }
+        if (metap) mw = __ldg(metap + (kb * BK + khalf * kper) / DYMOE_GROUP);
+      };
+      load(cur, mcur, 0);
+      for (int kb = 0; kb < nk; ++kb) {
+        if (kb + 1 < nk) load(nxt, mnxt, kb + 1);
+        mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+        const uint32_t dst = sB(stage);
+        const int j0 = khalf * (kper / 8);          // first 16-byte chunk of this thread
+        const DQP d = dqp_from_meta(mcur);
+        if (be == 4) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i < kper / 32) {
+              const uint4 v = cur[i];
+              uint4 o;
+              o = deq_int4_word(v.x, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 0), o.x, o.y, o.z, o.w);
+              o = deq_int4_word(v.y, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 1), o.x, o.y, o.z, o.w);
+              o = deq_int4_word(v.z, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 2), o.x, o.y, o.z, o.w);
+              o = deq_int4_word(v.w, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 3), o.x, o.y, o.z, o.w);
+            }
+          }
+        } else if (be == 2) {
+          // kper codes = kper/16 words: W13 64 k = 16 B (one uint4), GEMM 2 32 k = 8 B
+          const uint4 v = cur[0];
+          const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q < kper / 16) {
+              uint4 lo, hi;
+              deq_int2_word(wv[q], d, lo, hi);
+              sts128(dst + sw128_off(wr, j0 + 2 * q), lo.x, lo.y, lo.z, lo.w);
+              sts128(dst + sw128_off(wr, j0 + 2 * q + 1), hi.x, hi.y, hi.z, hi.w);
+            }
+          }
+        } else if (be == 8) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (i < kper / 16) {
+              const uint4 v = cur[i];   // 16 codes = two 16-byte output chunks
+              sts128(dst + sw128_off(wr, j0 + 2 * i), deq_int8_pair(v.x, 0, d), deq_int8_pair(v.x, 2, d),
+                     deq_int8_pair(v.y, 0, d), deq_int8_pair(v.y, 2, d));
+              sts128(dst + sw128_off(wr, j0 + 2 * i + 1), deq_int8_pair(v.z, 0, d),
+                     deq_int8_pair(v.z, 2, d), deq_int8_pair(v.w, 0, d), deq_int8_pair(v.w, 2, d));
+            }
+          }
+        } else {  // bf16 master: copy
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (i < kper / 8) sts128(dst + sw128_off(wr, j0 + i), cur[i].x, cur[i].y, cur[i].z, cur[i].w);
+        }
+        fence_proxy_async();
+        mbar_arrive(smem_u32(&full_bar[stage]));
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
+        mcur = mnxt;
+      }
+      // ---- epilogue: TMEM -> registers -> global
+      mbar_wait(smem_u32(&tfull_bar), tphase);
+      tphase ^= 1;
+      tc_fence_after();
+      const int q = warp & 3;                         // TMEM lane quarter this warp may access
+      const int mt = (warp - kAWarps) >> 2;           // accumulator (token half) of this warp
+      const int trow = mt * BM + q * 32 + lane;       // token row within the tile
+      const size_t grow = (size_t)(a.expert_off[T.e] + T.m0 + trow);
+      const bool live = trow < T.rows;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * NCOL);
+#pragma unroll 1
+      for (int cc = 0; cc < BN / 32; ++cc) {
+        if (W13) {
+          uint32_t g[32], u[32];
+          tmem_ld32(tbase + cc * 32, g);
+          tmem_ld32(tbase + BN + cc * 32, u);
+          tmem_ld_wait();
+          if (live) {
+            uint32_t hv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              float h2[2];
+#pragma unroll
+              for (int k2 = 0; k2 < 2; ++k2) {
+                const float A = __uint_as_float(g[2 * i + k2]), B = __uint_as_float(u[2 * i + k2]);
+                h2[k2] = __fmul_rn(__fdiv_rn(A, __fadd_rn(1.f, expf(-A))), B);
+              }
+              hv[i] = pack_bf2(h2[0], h2[1]);
+            }
+            uint4* dstp = reinterpret_cast<uint4*>(a.h + grow * a.F + T.n0 + cc * 32);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dstp[i] = make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
+          }
+        } else {
+          uint32_t v[32];
+          tmem_ld32(tbase + cc * 32, v);
+          tmem_ld_wait();
+          if (live) {
+            uint4* dstp = reinterpret_cast<uint4*>(a.y_perm + grow * a.Hd + T.n0 + cc * 32);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dstp[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(&tempty_bar));
+    }
+  } else {
+    // ------------------------------------------------------------------ MMA issuer (1 thread)
+    int stage = 0;
+    uint32_t phase = 0, tphase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      if (lane == 0) {
+        mbar_wait(smem_u32(&tempty_bar), tphase ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(&full_bar[stage]), phase);
+          fence_proxy_async();   // A arrived through cp.async (generic proxy) -> tensor core reads
+          tc_fence_after();
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad = sw128_desc(sA(stage) + mt * (BM * 128) + kk * 32);
+              const uint64_t bd = sw128_desc(sB(stage) + kk * 32);
+              tc_mma(tmem + mt * NCOL, ad, bd, IDESC, (kb | kk) != 0);
+            }
+          tc_commit(smem_u32(&empty_bar[stage]));
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(smem_u32(&tfull_bar));
+      }
+      __syncwarp();
+      tphase ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+}  // namespace pf
+
+cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev) {
+  using namespace pf;
+  if (a.Hd % BN || a.F % BN || a.Hd % BK || a.F % BK) return cudaErrorInvalidValue;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_prefill_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_prefill_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  }
+  record_ev(ev, 0, s);
+  k_prefill_gemm<true><<<sms, kThreads, kSmem, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  record_ev(ev, 1, s);
+  k_prefill_gemm<false><<<sms, kThreads, kSmem, s>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  record_ev(ev, 2, s);
+  return cudaSuccess;
+}
+
 }  // namespace dymoe
