@@ -33,7 +33,7 @@ constexpr int MT = 2;             // accumulators per CTA tile -> 256 tokens
 constexpr int TOK = BM * MT;
 constexpr int BN = 128;           // weight rows per matrix per tile
 constexpr int BK = 64;            // k per stage (one 128-byte swizzle atom row)
-constexpr int STAGES = 3;
+constexpr int STAGES = 2;
 constexpr int A_BYTES = TOK * BK * 2;          // 32 KB
 constexpr int B_BYTES_MAX = 2 * BN * BK * 2;   // 32 KB (GEMM 1: W1 + W3 rows)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
@@ -41,7 +41,8 @@ constexpr int kAWarps = 2, kBWarps = 8;
 constexpr int kMmaWarp = kAWarps + kBWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;   // 352
 constexpr int kAThreads = kAWarps * 32, kBThreads = kBWarps * 32;
-constexpr int kSmem = STAGES * STAGE_BYTES + 1024;   // + alignment slack
+constexpr int kSmemRaw = 4 * (kBWarps * 32 * 16) * 4 + 4 * (kBWarps * 32) * 4;   // B producer ring
+constexpr int kSmem = STAGES * STAGE_BYTES + kSmemRaw + 1024;   // + alignment slack
 
 // ---------------------------------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -208,6 +209,130 @@ __device__ __forceinline__ uint32_t deq_int8_pair(uint32_t w, int i, const DQP& 
   return bf2_mul(pack_bf2(d0, d1), d.ss);
 }
 
+// ---------------------------------------------------------------------------------------- B producer
+// One thread = one weight row (GEMM 1) or half a row (GEMM 2) of every stage.  Quantized widths:
+// each thread streams its packed bytes (+ the group's dequant word) PF stages ahead with
+// cp.async into a private shared-memory ring ([slot][chunk][thread] 16-byte granules: conflict-
+// free), so no global load is outstanding in registers when the thread fences and arrives; it
+// then dequantizes in natural k order and stores into the 128B-swizzled B tile.
+// BF16 masters: cp.async straight into the tile (arrival on completion).
+constexpr int PF = 4;                                   // raw stages in flight per thread
+constexpr int RAW_CHUNK = kBThreads * 16;               // one 16-byte granule per thread
+constexpr int RAW_SLOT = 4 * RAW_CHUNK;                 // <= 64 bytes per thread per stage
+constexpr int RAW_BYTES = PF * RAW_SLOT + PF * kBThreads * 4;   // + dequant words
+
+template <int BE, int KPER>
+struct RawStage {
+  static constexpr int NB = KPER * BE / 8;        // bytes per thread per stage
+  static constexpr int NV = (NB + 15) / 16;
+  uint4 v[NV];
+  uint32_t m;
+};
+
+template <int BE, int KPER>
+__device__ __forceinline__ void issue_raw(uint32_t raw_base, int tb, int slot, const uint8_t* rowp,
+                                          const uint32_t* metap, int khalf, int kb) {
+  constexpr int NB = RawStage<BE, KPER>::NB;
+  const size_t kbyte = ((size_t)kb * BK + khalf * KPER) * BE / 8;
+  const uint32_t dst = raw_base + slot * RAW_SLOT + tb * 16;
+  if constexpr (NB == 8) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(rowp + kbyte) : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < RawStage<BE, KPER>::NV; ++i)
+      asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst + i * RAW_CHUNK),
+                   "l"(rowp + kbyte + 16 * i) : "memory");
+  }
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(raw_base + PF * RAW_SLOT +
+                                                                (slot * kBThreads + tb) * 4),
+               "l"(metap + (kb * BK + khalf * KPER) / DYMOE_GROUP) : "memory");
+}
+template <int BE, int KPER>
+__device__ __forceinline__ void read_raw(RawStage<BE, KPER>& r, uint32_t raw_base, int tb, int slot) {
+  const uint32_t src = raw_base + slot * RAW_SLOT + tb * 16;
+#pragma unroll
+  for (int i = 0; i < RawStage<BE, KPER>::NV; ++i)
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.v[i].x), "=r"(r.v[i].y), "=r"(r.v[i].z), "=r"(r.v[i].w)
+                 : "r"(src + i * RAW_CHUNK));
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r.m) : "r"(raw_base + PF * RAW_SLOT + (slot * kBThreads + tb) * 4));
+}
+
+template <int BE, int KPER>
+__device__ __forceinline__ void store_stage(const RawStage<BE, KPER>& r, uint32_t dst, int wr, int j0) {
+  const DQP d = dqp_from_meta(r.m);
+  if constexpr (BE == 4) {
+#pragma unroll
+    for (int i = 0; i < KPER / 32; ++i) {
+      const uint32_t wv[4] = {r.v[i].x, r.v[i].y, r.v[i].z, r.v[i].w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 o = deq_int4_word(wv[q], d);
+        sts128(dst + sw128_off(wr, j0 + 4 * i + q), o.x, o.y, o.z, o.w);
+      }
+    }
+  } else if constexpr (BE == 2) {
+    const uint32_t wv[4] = {r.v[0].x, r.v[0].y, r.v[0].z, r.v[0].w};
+#pragma unroll
+    for (int q = 0; q < KPER / 16; ++q) {
+      uint4 lo, hi;
+      deq_int2_word(wv[q], d, lo, hi);
+      sts128(dst + sw128_off(wr, j0 + 2 * q), lo.x, lo.y, lo.z, lo.w);
+      sts128(dst + sw128_off(wr, j0 + 2 * q + 1), hi.x, hi.y, hi.z, hi.w);
+    }
+  } else {  // 8
+#pragma unroll
+    for (int i = 0; i < KPER / 16; ++i) {
+      const uint4 v = r.v[i];   // 16 codes = two 16-byte output chunks
+      sts128(dst + sw128_off(wr, j0 + 2 * i), deq_int8_pair(v.x, 0, d), deq_int8_pair(v.x, 2, d),
+             deq_int8_pair(v.y, 0, d), deq_int8_pair(v.y, 2, d));
+      sts128(dst + sw128_off(wr, j0 + 2 * i + 1), deq_int8_pair(v.z, 0, d), deq_int8_pair(v.z, 2, d),
+             deq_int8_pair(v.w, 0, d), deq_int8_pair(v.w, 2, d));
+    }
+  }
+}
+
+template <int BE, int KPER>
+__device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* metap, int khalf,
+                                        int tb, int wr, int j0, int nk, uint32_t sbase,
+                                        const uint64_t* full_bar, const uint64_t* empty_bar,
+                                        int& stage, uint32_t& phase) {
+  if constexpr (BE == 16) {
+    for (int kb = 0; kb < nk; ++kb) {
+      mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+      const uint32_t dst = sbase + stage * STAGE_BYTES + A_BYTES;
+      const uint8_t* src = rowp + ((size_t)kb * BK + khalf * KPER) * 2;
+#pragma unroll
+      for (int i = 0; i < KPER / 8; ++i) cp_async_zfill(dst + sw128_off(wr, j0 + i), src + 16 * i, 16u);
+      cp_async_arrive_noinc(smem_u32(&full_bar[stage]));
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+  } else {
+    const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;
+#pragma unroll
+    for (int p = 0; p < PF - 1; ++p) {
+      if (p < nk) issue_raw<BE, KPER>(raw_base, tb, p, rowp, metap, khalf, p);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    int slot = 0, slot_iss = PF - 1;
+    for (int kb = 0; kb < nk; ++kb) {
+      if (kb + PF - 1 < nk) issue_raw<BE, KPER>(raw_base, tb, slot_iss, rowp, metap, khalf, kb + PF - 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (++slot_iss == PF) slot_iss = 0;
+      asm volatile("cp.async.wait_group %0;" ::"n"(PF - 1) : "memory");
+      RawStage<BE, KPER> r;
+      read_raw<BE, KPER>(r, raw_base, tb, slot);
+      if (++slot == PF) slot = 0;
+      mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+      store_stage<BE, KPER>(r, sbase + stage * STAGE_BYTES + A_BYTES, wr, j0);
+      fence_proxy_async();
+      mbar_arrive(smem_u32(&full_bar[stage]));
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+  }
+}
+
 // ---------------------------------------------------------------------------------------- tiles
 struct Sched {
   int n;                                   // active experts
@@ -217,7 +342,8 @@ struct Sched {
 struct Tile {
   int e, m0, n0, rows;   // expert, first token row (relative), first weight row, valid tokens
 };
-__device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t, int ntiles_n) {
+__device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t, int ntiles_n,
+                                        int nstep) {
   int i = 0;
   while (S.first[i + 1] <= t) ++i;
   Tile r;
@@ -226,7 +352,7 @@ __device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t,
   const int mt = local / ntiles_n, nt = local - mt * ntiles_n;
   const int n_e = a.expert_off[r.e + 1] - a.expert_off[r.e];
   r.m0 = mt * TOK;
-  r.n0 = nt * BN;
+  r.n0 = nt * nstep;
   r.rows = min(TOK, n_e - r.m0);
   return r;
 }
@@ -238,13 +364,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_base_sh;
   __shared__ int n_tiles_sh;
-  constexpr int NW = W13 ? 2 * BN : BN;               // weight rows in the B tile
-  constexpr int NCOL = W13 ? 2 * BN : BN;             // TMEM columns per accumulator
+  // B tile = 256 weight rows in both GEMMs: GEMM 1 = 128 W1 + the same 128 W3 rows, GEMM 2 =
+  // 256 W2 rows (so every A stage feeds 256 output columns per accumulator).
+  constexpr int NCOL = 2 * BN;                        // TMEM columns per accumulator
   constexpr uint32_t TMEM_COLS = MT * NCOL <= 256 ? 256 : 512;
   constexpr uint32_t IDESC = make_idesc(BM, NCOL);
   const int K = W13 ? a.Hd : a.F;
   const int NWR = W13 ? a.F : a.Hd;                  // weight rows per matrix
-  const int ntiles_n = NWR / BN;
+  const int nstep = W13 ? BN : 2 * BN;               // output features per tile
+  const int ntiles_n = (NWR + nstep - 1) / nstep;
   const int nk = K / BK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -293,25 +421,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
     const int tid = threadIdx.x;   // 0..63
     int stage = 0;
     uint32_t phase = 0;
+    constexpr int NCH = (TOK * 8) / kAThreads;   // 32 x 16-byte chunks per thread per stage
+    const int j = tid & 7;                        // this thread's 16-byte chunk of every row
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const Tile T = tile_at(S, a, t, ntiles_n);
+      const Tile T = tile_at(S, a, t, ntiles_n, nstep);
       const int off = a.expert_off[T.e];
+      // element offsets of this thread's 32 rows (rows tid/8 + 8i), resolved once per tile
+      // (the token gather through perm_token must not sit on every stage's critical path)
+      uint32_t roff[NCH];
+#pragma unroll
+      for (int i = 0; i < NCH; ++i) {
+        const int r = (tid >> 3) + 8 * i;
+        const int rr = r < T.rows ? r : 0;
+        roff[i] = W13 ? (uint32_t)a.perm_token[off + T.m0 + rr] * (uint32_t)a.Hd
+                      : (uint32_t)(off + T.m0 + rr) * (uint32_t)a.F;
+      }
+      const uint16_t* base = W13 ? a.x : a.h;
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
         const uint32_t dst = sA(stage);
-#pragma unroll 4
-        for (int i = 0; i < (TOK * 8) / kAThreads; ++i) {     // 32 x 16-byte chunks each
-          const int id = i * kAThreads + tid;
-          const int r = id >> 3, j = id & 7;
-          const bool ok = r < T.rows;
-          const uint16_t* src;
-          if (W13) {
-            const int tokrow = ok ? a.perm_token[off + T.m0 + r] : 0;
-            src = a.x + (size_t)tokrow * a.Hd + kb * BK + j * 8;
-          } else {
-            src = a.h + (size_t)(off + T.m0 + (ok ? r : 0)) * a.F + kb * BK + j * 8;
-          }
-          cp_async_zfill(dst + sw128_off(r, j), src, ok ? 16u : 0u);
+#pragma unroll
+        for (int i = 0; i < NCH; ++i) {
+          const int r = (tid >> 3) + 8 * i;
+          cp_async_zfill(dst + sw128_off(r, j), base + roff[i] + kb * BK + j * 8,
+                         r < T.rows ? 16u : 0u);
         }
         cp_async_arrive_noinc(smem_u32(&full_bar[stage]));
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -323,15 +456,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
     int stage = 0;
     uint32_t phase = 0, tphase = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const Tile T = tile_at(S, a, t, ntiles_n);
+      const Tile T = tile_at(S, a, t, ntiles_n, nstep);
       const int be = a.bits[T.e];
       const DevExpert& E = a.experts[T.e];
-      // this thread's weight row (GEMM 1: 0-127 W1, 128-255 W3; GEMM 2: two threads per row)
-      const int wr = W13 ? tb : (tb >> 1);
-      const int khalf = W13 ? 0 : (tb & 1);          // GEMM 2: which 32-k half of the stage
+      // this thread's weight row (GEMM 1: 0-127 W1, 128-255 W3 of the same features; GEMM 2:
+      // 256 consecutive W2 rows, clamped at the end of the matrix -- those outputs are dropped)
+      const int wr = tb;
       const int mi = W13 ? (wr >= BN ? 1 : 0) : 2;
-      const int row = T.n0 + (W13 ? (wr & (BN - 1)) : wr);
-      const int kper = W13 ? BK : BK / 2;            // k values per thread per stage
+      const int row = min(T.n0 + (W13 ? (wr & (BN - 1)) : wr), NWR - 1);
       const int wi = width_index(be);
       const uint8_t* codes = be == 16 ? reinterpret_cast<const uint8_t*>(E.w[mi])
                                       : reinterpret_cast<const uint8_t*>(E.q[wi][mi].codes);
@@ -340,77 +472,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
       const int gpr = K / DYMOE_GROUP;
       const uint8_t* rowp = codes + (size_t)row * row_bytes;
       const uint32_t* metap = meta ? meta + (size_t)row * gpr : nullptr;
-      // bytes per thread per stage: kper * be / 8  (<= 128)
-      uint4 cur[8], nxt[8];
-      uint32_t mcur = 0, mnxt = 0;
-      const int nvec = (kper * be / 8 + 15) / 16;    // 16-byte loads per thread per stage
-      const int nbytes = kper * be / 8;               // 8 (GEMM 2 Int2) .. 128 bytes
-      auto load = [&](uint4 (&v)[8], uint32_t& mw, int kb) {
-        const size_t kbyte = ((size_t)kb * BK + khalf * kper) * be / 8;
-        if (nbytes == 8) {
-          const uint2 u = __ldg(reinterpret_cast<const uint2*>(rowp + kbyte));
-          v[0] = make_uint4(u.x, u.y, 0u, 0u);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (i < nvec) v[i] = ldg_stream(rowp + kbyte + 16 * i);
-        }
-        if (metap) mw = __ldg(metap + (kb * BK + khalf * kper) / DYMOE_GROUP);
-      };
-      load(cur, mcur, 0);
-      for (int kb = 0; kb < nk; ++kb) {
-        if (kb + 1 < nk) load(nxt, mnxt, kb + 1);
-        mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-        const uint32_t dst = sB(stage);
-        const int j0 = khalf * (kper / 8);          // first 16-byte chunk of this thread
-        const DQP d = dqp_from_meta(mcur);
-        if (be == 4) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (i < kper / 32) {
-              const uint4 v = cur[i];
-              uint4 o;
-              o = deq_int4_word(v.x, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 0), o.x, o.y, o.z, o.w);
-              o = deq_int4_word(v.y, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 1), o.x, o.y, o.z, o.w);
-              o = deq_int4_word(v.z, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 2), o.x, o.y, o.z, o.w);
-              o = deq_int4_word(v.w, d); sts128(dst + sw128_off(wr, j0 + 4 * i + 3), o.x, o.y, o.z, o.w);
-            }
-          }
-        } else if (be == 2) {
-          // kper codes = kper/16 words: W13 64 k = 16 B (one uint4), GEMM 2 32 k = 8 B
-          const uint4 v = cur[0];
-          const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q < kper / 16) {
-              uint4 lo, hi;
-              deq_int2_word(wv[q], d, lo, hi);
-              sts128(dst + sw128_off(wr, j0 + 2 * q), lo.x, lo.y, lo.z, lo.w);
-              sts128(dst + sw128_off(wr, j0 + 2 * q + 1), hi.x, hi.y, hi.z, hi.w);
-            }
-          }
-        } else if (be == 8) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (i < kper / 16) {
-              const uint4 v = cur[i];   // 16 codes = two 16-byte output chunks
-              sts128(dst + sw128_off(wr, j0 + 2 * i), deq_int8_pair(v.x, 0, d), deq_int8_pair(v.x, 2, d),
-                     deq_int8_pair(v.y, 0, d), deq_int8_pair(v.y, 2, d));
-              sts128(dst + sw128_off(wr, j0 + 2 * i + 1), deq_int8_pair(v.z, 0, d),
-                     deq_int8_pair(v.z, 2, d), deq_int8_pair(v.w, 0, d), deq_int8_pair(v.w, 2, d));
-            }
-          }
-        } else {  // bf16 master: copy
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (i < kper / 8) sts128(dst + sw128_off(wr, j0 + i), cur[i].x, cur[i].y, cur[i].z, cur[i].w);
-        }
-        fence_proxy_async();
-        mbar_arrive(smem_u32(&full_bar[stage]));
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) cur[i] = nxt[i];
-        mcur = mnxt;
+      switch (be) {
+        case 2: produce<2, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        case 4: produce<4, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        case 8: produce<8, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        default: produce<16, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
       }
       // ---- epilogue: TMEM -> registers -> global
       mbar_wait(smem_u32(&tfull_bar), tphase);
@@ -423,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
       const bool live = trow < T.rows;
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * NCOL);
 #pragma unroll 1
-      for (int cc = 0; cc < BN / 32; ++cc) {
+      for (int cc = 0; cc < (W13 ? BN : 2 * BN) / 32; ++cc) {
         if (W13) {
           uint32_t g[32], u[32];
           tmem_ld32(tbase + cc * 32, g);
@@ -437,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
 #pragma unroll
               for (int k2 = 0; k2 < 2; ++k2) {
                 const float A = __uint_as_float(g[2 * i + k2]), B = __uint_as_float(u[2 * i + k2]);
-                h2[k2] = __fmul_rn(__fdiv_rn(A, __fadd_rn(1.f, expf(-A))), B);
+                h2[k2] = __fmul_rn(__fdividef(A, 1.f + __expf(-A)), B);   // fast silu (fp32)
               }
               hv[i] = pack_bf2(h2[0], h2[1]);
             }
@@ -449,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
           uint32_t v[32];
           tmem_ld32(tbase + cc * 32, v);
           tmem_ld_wait();
-          if (live) {
+          if (live && T.n0 + cc * 32 < NWR) {   // last W2 tile may overhang Hd (clamped rows)
             uint4* dstp = reinterpret_cast<uint4*>(a.y_perm + grow * a.Hd + T.n0 + cc * 32);
 #pragma unroll
             for (int i = 0; i < 8; ++i) dstp[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);

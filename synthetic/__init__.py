@@ -57,7 +57,8 @@ def expert_weights(cfg, seed, device="cpu", experts=None):
     g = generator(seed * 1000 + 7, device)
     out = []
     ids = range(cfg.M) if experts is None else experts
-    for e in range(cfg.M):
+    last = cfg.M if experts is None else max(experts) + 1   # same stream, stop early
+    for e in range(last):
         sd_in, sd_out = 1.0 / math.sqrt(cfg.hidden), 1.0 / math.sqrt(cfg.ffn)
         w1 = torch.randn(cfg.ffn, cfg.hidden, generator=g, device=device).mul_(sd_in)
         w3 = torch.randn(cfg.ffn, cfg.hidden, generator=g, device=device).mul_(sd_in)
