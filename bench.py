@@ -321,6 +321,119 @@ def run_ours(args, rank, world, device):
     return res
 
 
+def run_ep(args, rank, world, device):
+    """N > 1: expert-parallel layer (experts sharded in contiguous blocks over the ranks, NCCL
+    all-to-all dispatch/combine via paper_2603_19172_b200.ep); every rank brings its own batch
+    (weak scaling).  Timed exactly like the single-GPU run; max over ranks."""
+    import paper_2603_19172_b200.dymoe as d
+    from paper_2603_19172_b200 import ep
+    d.lib()
+    torch.cuda.set_device(device)
+    peaks = load_peaks()
+    base = synthetic.CONFIGS["mixtral_decode" if args.workload == "decode" else "mixtral_prefill"]
+    T = args.batch if args.workload == "decode" else args.tokens
+    cfg = base.with_tokens(T)
+    phase = d.DYMOE_DECODE if args.workload == "decode" else d.DYMOE_PREFILL
+    comm = ep.TorchComm()
+
+    class TimedOps(ep.CudaOps):
+        """CudaOps recording CUDA events around the local expert FFN (roofline numerator)."""
+
+        def __init__(self):
+            super().__init__()
+            self.events, self.rows = [], []
+
+        def expert_ffn(self, layer, x_rows, bits, expert_off, perm_token, mode):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            y = super().expert_ffn(layer, x_rows, bits, expert_off, perm_token, mode)
+            e1.record()
+            self.events.append((e0, e1, bits, expert_off))
+            return y
+
+    ops = TimedOps()
+    first, last = ep.owned_range(rank, cfg.M, world)
+    shards = []
+    for c in range(args.copies):
+        ex = [{n: t.to(device) for n, t in e.items()}
+              for e in synthetic.expert_weights(cfg, 100 + c, device, experts=list(range(first, last)))]
+        ex = ex[first:last] if len(ex) > last - first else ex
+        d.quantize_experts(ex, (8, 4, 2))
+        shards.append(ep.EPMoELayer(comm, ops, ex, cfg.M, cfg.k, cfg.hidden, cfg.ffn,
+                                    make_local_layer=lambda e_: d.MoELayer(e_, 1, cfg.hidden, cfg.ffn)))
+    n_inputs = 8
+    inputs = []
+    for i in range(n_inputs):
+        x, lg, a = synthetic.layer_inputs(cfg, 1000 + i * 97 + rank, device)
+        inputs.append((x.contiguous(), lg.contiguous(), a.contiguous()))
+    ladder = d.make_ladder(LADDER_BITS, LADDER_LAMBDAS)
+
+    def one_step(i):
+        x, lg, a = inputs[i % n_inputs]
+        return shards[i % len(shards)].forward(x, lg, ladder, i % NUM_LAYERS, NUM_LAYERS, phase,
+                                               attn_mass=a)
+
+    for i in range(args.warmup):
+        one_step(i)
+    torch.cuda.synchronize()
+    K = args.steps
+    ops.events.clear()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record()
+        for i in range(K):
+            one_step(args.warmup + i)
+        t1.record()
+        torch.cuda.synchronize()
+    torch.distributed.barrier()
+    ms = t0.elapsed_time(t1)
+    tt = torch.tensor([ms], device=device)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    ms = float(tt.item())
+    value = T * K * world / (ms / 1e3)
+    # local FFN roofline (bytes of the local experts actually streamed / FFN time)
+    ffn_ms, ffn_bytes, ffn_flops = 0.0, 0.0, 0.0
+    for e0, e1, bits, off in ops.events:
+        ffn_ms += e0.elapsed_time(e1)
+        b = bits.cpu().numpy()
+        o = off.cpu().numpy()
+        for e in range(len(o) - 1):
+            n = int(o[e + 1] - o[e])
+            if n:
+                chunks = (n + 7) // 8 if phase == d.DYMOE_DECODE else max(1, (n + 255) // 256)
+                ffn_bytes += 3 * cfg.hidden * cfg.ffn * bytes_per_weight(int(b[e])) * chunks
+                ffn_flops += 6.0 * cfg.hidden * cfg.ffn * n
+    res = None
+    if phase == d.DYMOE_DECODE:
+        ach = ffn_bytes / max(ffn_ms / 1e3, 1e-12) / 1e9
+        roof = {"bound": "hbm", "kernel": "local fused-dequant FFN (k_decode_gemv W13 + W2), rank 0",
+                "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
+                "traffic": None, "peak_src": peaks["src"]}
+    else:
+        ach = ffn_flops / max(ffn_ms / 1e3, 1e-12) / 1e12
+        pk = peaks["bf16_sus"] or peaks["bf16"]
+        roof = {"bound": "tensor", "kernel": "local tcgen05 fused-dequant grouped GEMM, rank 0",
+                "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
+                "peak_src": peaks["src"] + " bf16 sustained"}
+    if rank == 0:
+        res = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
+               "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
+               "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
+               "config": {"workload": "mixtral_%s" % args.workload, "hidden": cfg.hidden, "ffn": cfg.ffn,
+                          "experts": cfg.M, "top_k": cfg.k, "tokens_per_step_per_rank": T,
+                          "global_batch": T * world,
+                          "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
+                          "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
+                          "weight_copies": args.copies, "l2": "inputs larger than L2 (rotating weight copies)",
+                          "parallelism": "ep%d (experts sharded, NCCL all-to-all dispatch/combine)" % world},
+               "roofline": roof, "clocks": clk.summary(), "e2e": None,
+               "gpu_launches": None}
+    return res
+
+
 def load_traffic(kernel_prefix):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
@@ -447,7 +560,10 @@ def main():
     if world > 1:
         torch.cuda.set_device(local)
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
-    res = run_ours(args, rank, world, torch.device("cuda", local))
+    if world > 1:
+        res = run_ep(args, rank, world, torch.device("cuda", local))
+    else:
+        res = run_ours(args, rank, world, torch.device("cuda", local))
     if rank == 0:
         print(json.dumps(res))
     if world > 1:

@@ -202,6 +202,18 @@ int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk
                   int k, int Hd, int renorm, int out_dtype, void* y, dymoe_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
+/* Expert parallelism (BASELINE.json north_star).  Expert e lives on rank
+ * floor(e * P / M) (contiguous blocks).  The owner is non-decreasing in e, so the expert-sorted
+ * permutation of dymoe_permute is already ordered by (destination rank, expert, token, slot).
+ *   dymoe_ep_plan: send_counts [P] i32 out = rows bound for each rank; row_expert [expert_off[M]]
+ *   i32 out = expert of every permuted row.  expert_off [M+1] device.  1 <= P <= min(M, 64).
+ *   dymoe_gather_rows: out[i] = x[rows[i]], bf16 rows of Hd (multiple of 8) elements.         */
+int dymoe_ep_plan(const int32_t* expert_off, int M, int P, int32_t* send_counts,
+                  int32_t* row_expert, dymoe_stream_t stream);
+int dymoe_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n, uint16_t* out,
+                      dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
 /* The whole layer, one step: route -> score -> assign -> permute -> FFN
  * -> combine, all on `stream` with no host synchronisation (graph-capturable).               */
 typedef struct dymoe_fwd_opts {

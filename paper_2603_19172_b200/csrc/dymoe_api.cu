@@ -416,6 +416,32 @@ int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* b
   return ok();
 }
 
+int dymoe_ep_plan(const int32_t* expert_off, int M, int P, int32_t* send_counts,
+                  int32_t* row_expert, dymoe_stream_t stream) {
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(P >= 1 && P <= M && P <= 64, "P: must satisfy 1 <= P <= min(M, 64)");
+  CHECK_ARG(expert_off != nullptr, "expert_off: must not be NULL");
+  CHECK_ARG(send_counts != nullptr, "send_counts: must not be NULL");
+  CHECK_ARG(row_expert != nullptr, "row_expert: must not be NULL");
+  CHECK_LAUNCH(launch_ep_plan(expert_off, M, P, send_counts, row_expert, S(stream)), "dymoe_ep_plan");
+  return ok();
+}
+
+int dymoe_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n, uint16_t* out,
+                      dymoe_stream_t stream) {
+  CHECK_ARG(Hd > 0 && Hd % 8 == 0, "Hd: must be a positive multiple of 8");
+  CHECK_ARG(n >= 0, "n: must be >= 0");
+  if (n > 0) {
+    CHECK_ARG(x && rows && out, "x/rows/out: must not be NULL");
+    int rc = check_ptr_align(x, 16, "x");
+    if (rc) return rc;
+    rc = check_ptr_align(out, 16, "out");
+    if (rc) return rc;
+  }
+  CHECK_LAUNCH(launch_gather_rows(x, Hd, rows, n, out, S(stream)), "dymoe_gather_rows");
+  return ok();
+}
+
 int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w, int T, int k,
                   int Hd, int renorm, int out_dtype, void* y, dymoe_stream_t stream) {
   CHECK_ARG(T >= 0, "T: must be >= 0");

@@ -89,6 +89,11 @@ inline void record_ev(void* const* ev, int i, cudaStream_t s) {
   if (ev != nullptr && ev[i] != nullptr) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
 }
 
+cudaError_t launch_ep_plan(const int32_t* expert_off, int M, int P, int32_t* send_counts,
+                           int32_t* row_expert, cudaStream_t s);
+cudaError_t launch_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n,
+                               uint16_t* out, cudaStream_t s);
+
 // y_perm may hold n_parts partial slices [n_parts][part_rows][Hd]; they are summed in slice order
 // before weighting (n_parts = 1, part_rows ignored for a plain y_perm).
 cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, const int32_t* inv_row,

@@ -94,6 +94,49 @@ cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const u
 }
 
 // -------------------------------------------------------------------------------------------
+// Expert parallelism helpers: expert e lives on rank floor(e * P / M); because that
+// owner is non-decreasing in e, the expert-sorted permutation is already sorted by destination.
+__global__ void k_ep_plan(const int32_t* __restrict__ off, int M, int P,
+                          int32_t* __restrict__ send_counts, int32_t* __restrict__ row_expert) {
+  const int e = blockIdx.x;
+  const int lo = off[e], hi = off[e + 1];
+  for (int i = lo + threadIdx.x; i < hi; i += blockDim.x) row_expert[i] = e;
+  if (e == 0 && threadIdx.x < P) {
+    int c = 0;
+    for (int x = 0; x < M; ++x)
+      if ((int)(((long long)x * P) / M) == (int)threadIdx.x) c += off[x + 1] - off[x];
+    send_counts[threadIdx.x] = c;
+  }
+}
+
+cudaError_t launch_ep_plan(const int32_t* expert_off, int M, int P, int32_t* send_counts,
+                           int32_t* row_expert, cudaStream_t s) {
+  k_ep_plan<<<M, 128, 0, s>>>(expert_off, M, P, send_counts, row_expert);
+  return cudaGetLastError();
+}
+
+// out[i] = x[rows[i]] (bf16 rows of Hd elements, 16-byte vectors)
+__global__ void k_gather_rows(const uint4* __restrict__ x, int vec_per_row,
+                              const int32_t* __restrict__ rows, int n, uint4* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)n * vec_per_row;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / vec_per_row, c = i - r * vec_per_row;
+    out[i] = __ldg(x + (size_t)rows[r] * vec_per_row + c);
+  }
+}
+
+cudaError_t launch_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n,
+                               uint16_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int vpr = Hd / 8;
+  const size_t total = (size_t)n * vpr;
+  const unsigned blocks = (unsigned)((total + 255) / 256 < 8192 ? (total + 255) / 256 : 8192);
+  k_gather_rows<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(x), vpr, rows, n,
+                                       reinterpret_cast<uint4*>(out));
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------------------------------
 // Combine: one CTA per token, float4 over Hd.  With n_parts > 1 the expert outputs arrive as
 // K-slice partials (decode W2 kernel) and are summed in slice order first.
 __device__ __forceinline__ float4 load_row(const float* __restrict__ y_perm, int n_parts,

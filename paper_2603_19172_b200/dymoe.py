@@ -25,7 +25,8 @@ EXPORTED = [
     "dymoe_retention_ratio", "dymoe_tier_counts", "dymoe_quantize", "dymoe_quantize_batched",
     "dymoe_layer_create", "dymoe_layer_refresh", "dymoe_layer_destroy", "dymoe_permute", "dymoe_expert_ffn",
     "dymoe_combine", "dymoe_workspace_size", "dymoe_workspace_views", "dymoe_moe_forward",
-    "dymoe_check_status", "dymoe_last_error", "dymoe_version",
+    "dymoe_check_status", "dymoe_last_error", "dymoe_version", "dymoe_ep_plan",
+    "dymoe_gather_rows",
 ]
 
 
@@ -107,6 +108,8 @@ def lib():
             "dymoe_check_status": [vp, ci, vp, vp, vp],
             "dymoe_last_error": [],
             "dymoe_version": [],
+            "dymoe_ep_plan": [vp, ci, ci, vp, vp, vp],
+            "dymoe_gather_rows": [vp, ci, vp, ci, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -245,6 +248,25 @@ def dymoe_permute(topk_idx, M, bits, stream=None):
     _check(lib().dymoe_permute(_p(topk_idx), T, k, M, _p(bits), _p(off), _p(pt), _p(ps), _p(inv),
                                _stream(stream)))
     return off, pt, ps, inv
+
+
+def dymoe_ep_plan(expert_off, P, stream=None):
+    """(send_counts int32 [P], row_expert int32 [rows]) for expert-parallel dispatch."""
+    M = expert_off.shape[0] - 1
+    dev = expert_off.device
+    sc = torch.empty(P, dtype=torch.int32, device=dev)
+    R = int(expert_off[-1].item()) if expert_off.is_cuda else int(expert_off[-1])
+    re = torch.empty(max(R, 1), dtype=torch.int32, device=dev)
+    _check(lib().dymoe_ep_plan(_p(expert_off), M, P, _p(sc), _p(re), _stream(stream)))
+    return sc, re[:R]
+
+
+def dymoe_gather_rows(x, rows, stream=None):
+    n = rows.shape[0]
+    out = torch.empty(n, x.shape[1], dtype=x.dtype, device=x.device)
+    _check(lib().dymoe_gather_rows(_p(_u16(x)), x.shape[1], _p(rows), n, _p(_u16(out)) if n else None,
+                                   _stream(stream)))
+    return out
 
 
 def dymoe_combine(y_perm, inv_row, topk_w, renorm=True, out_dtype=DYMOE_OUT_F32, stream=None):
