@@ -233,7 +233,8 @@ def run_ours(args, rank, world, device):
     ffn_ms = sum(w13_ms) + sum(w2_ms)
     achieved_w13 = b13 / (sum(w13_ms) / 1e3) / 1e9
     achieved_ffn = (b13 + b2) / (ffn_ms / 1e3) / 1e9
-    traffic = load_traffic("k_decode_gemv" if phase == d.DYMOE_DECODE else "k_prefill")
+    tr = load_traffic("k_decode_gemv<W13>" if phase == d.DYMOE_DECODE else "k_prefill_gemm<W13>")
+    traffic = tr["traffic"] if tr else None
 
     # ---------------- end-to-end through the public API with host buffers
     e2e = None
@@ -278,7 +279,7 @@ def run_ours(args, rank, world, device):
         roofline = {"bound": "hbm", "kernel": "k_decode_gemv<W13> (fused-dequant SwiGLU GEMV)",
                     "achieved": achieved_w13, "peak": peaks["hbm"], "unit": "GB/s",
                     "frac": achieved_w13 / peaks["hbm"], "traffic": traffic,
-                    "peak_src": peaks["src"], "frac_of_8TBs": achieved_w13 / 8000.0,
+                    "traffic_capture": tr, "peak_src": peaks["src"], "frac_of_8TBs": achieved_w13 / 8000.0,
                     "ffn_w13_plus_w2_GBs": achieved_ffn,
                     "ffn_share_of_step": ffn_ms / ms if world == 1 else None,
                     "algorithmic_bytes_per_step": (b13 + b2) / K}
@@ -290,7 +291,7 @@ def run_ours(args, rank, world, device):
         pk = peaks["bf16_sus"] or peaks["bf16"]
         roofline = {"bound": "tensor", "kernel": "k_prefill_gemm<W13> + <W2> (tcgen05 fused-dequant grouped GEMM)",
                     "achieved": tfl, "peak": pk, "unit": "TFLOP/s", "frac": tfl / pk,
-                    "traffic": traffic, "peak_src": peaks["src"] + " bf16 sustained",
+                    "traffic": traffic, "traffic_capture": tr, "peak_src": peaks["src"] + " bf16 sustained",
                     "frac_of_2250": tfl / 2250.0, "w13_tflops": tfl13,
                     "ffn_share_of_step": ffn_ms / ms if world == 1 else None,
                     "algorithmic_flops_per_step": fl / K, "hbm_GBs_ffn": achieved_ffn}
@@ -434,16 +435,16 @@ def run_ep(args, rank, world, device):
     return res
 
 
-def load_traffic(kernel_prefix):
+def load_traffic(kernel_key):
+    """dram read+write bytes of the dominant kernel from the committed ncu --set full capture
+    (profiles/traffic.json, written from profiles/r01_ncu_*.md), with the algorithmic work of
+    the same captured launch so the two can be compared."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         j = json.load(f)
-    for k, v in j.items():
-        if k.startswith(kernel_prefix):
-            return v
-    return None
+    return j.get(kernel_key)
 
 
 def measure_quantize(d, experts, cfg, peaks, reps=5):
