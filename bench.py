@@ -14,9 +14,10 @@ Workloads:
           no step re-reads weights another step left in L2 (each copy >= 5 GB > 126 MB L2).
   prefill (configs[2]): 2048 tokens per step, same rotation.
 
-N > 1 (torchrun): every rank runs an independent replica (weak scaling; the decode layer
-does not shard across GPUs in this round).  Timing: W warm-up steps, then K steps bracketed by
-barrier + cuda synchronize, CUDA events on the launching stream, max over ranks.
+N > 1 (torchrun): expert parallelism (paper_2603_19172_b200/ep.py): experts sharded in
+contiguous blocks over the ranks, NCCL all-to-all token dispatch/combine, every rank bringing its
+own batch (weak scaling).  Timing: W warm-up steps, then K steps bracketed by barrier + cuda
+synchronize, CUDA events on the launching stream, max over ranks.
 
 --impl reference: the CPU oracle (oracle/) timed on this host on a bounded sample of the
 same workload (the reference arm; rank 0 only).
