@@ -1,4 +1,4 @@
-ncu --set full --clock-control none --import-source on -k regex:"k_decode_gemv" -s 4 -c 2 -o gpurun_out/r01_decode_full python tools/profile_step.py --workload decode --layer 20 --input 4 --warmup 2 > gpurun_out/ncu1.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_prefill_gemm" -s 2 -c 2 -o gpurun_out/r01_prefill_full python tools/profile_step.py --workload prefill --layer 20 --input 4 --warmup 1 > gpurun_out/ncu2.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_quantize" -s 0 -c 1 -o gpurun_out/r01_quant_full python tools/profile_step.py --workload decode --layer 0 --input 0 --warmup 0 > gpurun_out/ncu3.log 2>&1
-tail -2 gpurun_out/ncu*.log
+timeout 900 python -m pytest tests -m gpu -q -rf -x -k "quantize" 2>&1 | tail -3
+timeout 600 python bench.py --steps 16 --warmup 3 --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
+python -c "
+import json; j=json.load(open('gpurun_out/bench.json'));print({k:(round(v['GB/s']),round(v['frac'],3)) for k,v in j['quantize'].items() if isinstance(v,dict)})"

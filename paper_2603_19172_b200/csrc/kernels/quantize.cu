@@ -8,12 +8,14 @@
 //   s < 2^-126 -> (mn, mx) = (-1, +1), s recomputed (D14b);
 //   inv = 1/s; z = rint(-mn * inv); q = clamp(rint(w * inv) + z, 0, maxq)
 //
-// HBM-bound: per weight it reads 2 B and writes b/8 B (+5 B per group).  Mapping: a half-warp
-// (16 lanes x 16 B = 128 bf16) owns one group; lanes min/max-reduce with 4 xor-shuffles inside
-// the half-warp, quantize their 8 weights and write their packed bits contiguously, so a warp
-// reads 512 contiguous bytes and writes 64 (int2) .. 256 (int8) contiguous bytes per group
-// pair.  Each thread keeps UNROLL groups of loads in flight.  Grid: a multiple of the SM
-// count (grid-stride over group pairs), so one launch covers any number of matrices.
+// HBM-bound in bytes (2 B read + b/8 B written per weight) but, at HBM rate, tight in ALU issue
+// slots (~2.6 T weights/s).  So one LANE owns one whole 128-weight group: the per-group scalar
+// work (two IEEE divisions, z) is amortised over 128 weights instead of 8, the min/max runs on
+// packed bf16 pairs (HMNMX2, exact), and rint(w*inv) uses the 1.5*2^23 magic add (exact
+// round-half-even for |x| < 2^22) whose bit pattern is the integer, so one IADD also adds z.
+// A warp owns 32 consecutive groups = 8 KB of contiguous input and writes its packed codes
+// contiguously; every 16-byte load hits a 32-byte sector whose other half the next load uses
+// (L1-allocating).  Jobs are padded to whole warps, so a warp never straddles two matrices.
 #include "../dymoe_internal.cuh"
 
 namespace dymoe {
@@ -23,126 +25,142 @@ struct QJob {
   uint32_t* codes;
   float* scales;
   uint8_t* zeros;
-  long long first_pair;  // global index of this job's first group pair
-  int N, K, bits;
+  long long first_warp;  // global warp index of this job's first 32 groups
+  long long n_groups;
+  int K, bits;
 };
 
 constexpr int kMaxJobs = 64;
 struct QJobs {
   QJob j[kMaxJobs];
   int n;
-  long long total_pairs;
+  long long total_warps;
 };
 
-__device__ __forceinline__ float bf16lo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bf16hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+__device__ __forceinline__ uint32_t hmin2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmin2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t hmax2(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// one code: clamp(rint(w * inv) + z, 0, maxq) with w the bf16 in the high (hi=1) / low half of u
+template <int BITS>
+__device__ __forceinline__ uint32_t qcode(uint32_t u, bool hi, float inv, int zbias) {
+  const float w = __uint_as_float(hi ? (u & 0xffff0000u) : (u << 16));
+  // |w * inv| <= maxq + 1 < 2^22, so adding 1.5 * 2^23 rounds to an integer (half to even) and
+  // the low mantissa bits hold it in two's-complement offset by 0x4B400000
+  const float t = __fadd_rn(__fmul_rn(w, inv), 12582912.0f);
+  int q = (int)__float_as_uint(t) - zbias;   // zbias = 0x4B400000 - z
+  q = max(q, 0);
+  q = min(q, (1 << BITS) - 1);
+  return (uint32_t)q;
+}
 
 template <int BITS>
-__device__ __forceinline__ void quant_group(const uint4 raw, int lane16, long long grp_in_job,
-                                            const QJob& J, bool valid) {
-  // grp_in_job: index of this half-warp's group within the job (row-major over [N][K/128])
-  float w[8] = {bf16lo(raw.x), bf16hi(raw.x), bf16lo(raw.y), bf16hi(raw.y),
-                bf16lo(raw.z), bf16hi(raw.z), bf16lo(raw.w), bf16hi(raw.w)};
-  float mn = 0.f, mx = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    mn = fminf(mn, w[i]);
-    mx = fmaxf(mx, w[i]);
-  }
-#pragma unroll
-  for (int off = 8; off > 0; off >>= 1) {  // xor within the 16-lane half
-    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, off));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-  }
+__device__ __forceinline__ void quant_lane_group(const QJob& J, long long g) {
   constexpr float maxq = (float)((1 << BITS) - 1);
+  const uint4* src = reinterpret_cast<const uint4*>(J.W) + g * 16;   // 128 bf16 = 16 x 16 B
+  uint4 v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __ldg(src + i);
+  // packed min / max over the 64 bf16 pairs (exact), then the two halves, then 0 (GPTQ grid)
+  uint32_t mn2 = v[0].x, mx2 = v[0].x;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t a[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      mn2 = hmin2(mn2, a[j]);
+      mx2 = hmax2(mx2, a[j]);
+    }
+  }
+  float mn = fminf(__uint_as_float(mn2 << 16), __uint_as_float(mn2 & 0xffff0000u));
+  float mx = fmaxf(__uint_as_float(mx2 << 16), __uint_as_float(mx2 & 0xffff0000u));
+  mn = fminf(mn, 0.f);
+  mx = fmaxf(mx, 0.f);
   float s = __fdiv_rn(__fsub_rn(mx, mn), maxq);
   if (!(s >= 1.17549435e-38f)) {  // s < 2^-126 (D14b)
     mn = -1.f;
-    mx = 1.f;
-    s = __fdiv_rn(__fsub_rn(mx, mn), maxq);
+    s = __fdiv_rn(2.f, maxq);
   }
   const float inv = __frcp_rn(s);
-  const float z = rintf(__fmul_rn(-mn, inv));
-  uint32_t q[8];
+  const float zf = rintf(__fmul_rn(-mn, inv));
+  const int z = (int)zf;
+  const int zbias = 0x4B400000 - z;
+  J.scales[g] = s;
+  J.zeros[g] = (uint8_t)z;
+  // codes: group g occupies 128*BITS/8 contiguous bytes of its row (rows are whole groups)
+  uint4* dst = reinterpret_cast<uint4*>(J.codes) + g * (BITS * 128 / 8 / 16);
+  if constexpr (BITS == 8) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    float v = __fadd_rn(rintf(__fmul_rn(w[i], inv)), z);
-    v = fminf(fmaxf(v, 0.f), maxq);
-    q[i] = (uint32_t)v;
-  }
-  const int K = J.K;
-  const long long gpr = K / DYMOE_GROUP;           // groups per row
-  const long long row = grp_in_job / gpr;
-  const long long g = grp_in_job - row * gpr;
-  // packed words of this lane: lane16 covers k = g*128 + lane16*8 .. +8
-  uint32_t* rowp = J.codes + row * ((long long)K * BITS / 32);
-  if (BITS == 8) {
-    uint2 o;
-    o.x = q[0] | q[1] << 8 | q[2] << 16 | q[3] << 24;
-    o.y = q[4] | q[5] << 8 | q[6] << 16 | q[7] << 24;
-    if (valid) reinterpret_cast<uint2*>(rowp)[(g * 128 + lane16 * 8) / 8] = o;
-  } else if (BITS == 4) {
-    uint32_t o = 0;
+    for (int i = 0; i < 16; i += 2) {   // 16 codes per 16-byte store
+      uint32_t o[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o |= q[i] << (4 * i);
-    if (valid) rowp[(g * 128 + lane16 * 8) / 8] = o;
-  } else {  // BITS == 2: 16 bits per lane, pair lanes (even | odd << 16)
-    uint32_t o = 0;
+      for (int h = 0; h < 2; ++h) {
+        const uint4 a = v[i + h];
+        o[2 * h] = qcode<8>(a.x, false, inv, zbias) | qcode<8>(a.x, true, inv, zbias) << 8 |
+                   qcode<8>(a.y, false, inv, zbias) << 16 | qcode<8>(a.y, true, inv, zbias) << 24;
+        o[2 * h + 1] = qcode<8>(a.z, false, inv, zbias) | qcode<8>(a.z, true, inv, zbias) << 8 |
+                       qcode<8>(a.w, false, inv, zbias) << 16 | qcode<8>(a.w, true, inv, zbias) << 24;
+      }
+      dst[i / 2] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  } else if constexpr (BITS == 4) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o |= q[i] << (2 * i);
-    uint32_t other = __shfl_xor_sync(0xffffffffu, o, 1);
-    if (valid && (lane16 & 1) == 0) rowp[(g * 128 + lane16 * 8) / 16] = o | (other << 16);
-  }
-  if (valid && lane16 == 0) {
-    J.scales[grp_in_job] = s;
-    J.zeros[grp_in_job] = (uint8_t)z;
+    for (int i = 0; i < 16; i += 4) {   // 32 codes per 16-byte store
+      uint32_t o[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint4 a = v[i + h];
+        const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+        uint32_t word = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          word |= (qcode<4>(w4[j], false, inv, zbias) | qcode<4>(w4[j], true, inv, zbias) << 4) << (8 * j);
+        o[h] = word;
+      }
+      dst[i / 4] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  } else {   // 2
+#pragma unroll
+    for (int i = 0; i < 16; i += 8) {   // 64 codes per 16-byte store
+      uint32_t o[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        uint32_t word = 0;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint4 a = v[i + 2 * h + hh];
+          const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            word |= (qcode<2>(w4[j], false, inv, zbias) | qcode<2>(w4[j], true, inv, zbias) << 2)
+                    << (16 * hh + 4 * j);
+        }
+        o[h] = word;
+      }
+      dst[i / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
   }
 }
 
-constexpr int kQuantUnroll = 4;
-
 __global__ void __launch_bounds__(256) k_quantize(const __grid_constant__ QJobs jobs) {
   const int lane = threadIdx.x & 31;
-  const int half = lane >> 4, lane16 = lane & 15;
-  const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  // each warp handles kQuantUnroll consecutive pairs per iteration
-  for (long long base = warp * kQuantUnroll; base < jobs.total_pairs;
-       base += nwarps * kQuantUnroll) {
-    uint4 raw[kQuantUnroll];
-    int jid[kQuantUnroll];
-    long long gij[kQuantUnroll];
-    bool ok[kQuantUnroll];
-#pragma unroll
-    for (int u = 0; u < kQuantUnroll; ++u) {
-      const long long pair = base + u;
-      ok[u] = pair < jobs.total_pairs;
-      int jj = 0;
-      if (ok[u]) {
-        while (jj + 1 < jobs.n && jobs.j[jj + 1].first_pair <= pair) ++jj;
-      }
-      jid[u] = jj;
-      const QJob& J = jobs.j[jj];
-      const long long ngroups = (long long)J.N * (J.K / DYMOE_GROUP);
-      gij[u] = (pair - J.first_pair) * 2 + half;
-      ok[u] = ok[u] && gij[u] < ngroups;
-      raw[u] = make_uint4(0, 0, 0, 0);
-      if (ok[u]) {
-        const long long gpr = J.K / DYMOE_GROUP;
-        const long long row = gij[u] / gpr, g = gij[u] - row * gpr;
-        const uint4* src = reinterpret_cast<const uint4*>(J.W + row * J.K + g * DYMOE_GROUP);
-        raw[u] = __ldcs(src + lane16);  // streamed once: evict-first
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kQuantUnroll; ++u) {
-      const QJob& J = jobs.j[jid[u]];
-      // the half-warp shuffles need all 32 lanes: compute even when !ok, store only if ok
-      switch (J.bits) {
-        case 2: quant_group<2>(raw[u], lane16, gij[u], J, ok[u]); break;
-        case 4: quant_group<4>(raw[u], lane16, gij[u], J, ok[u]); break;
-        default: quant_group<8>(raw[u], lane16, gij[u], J, ok[u]); break;
-      }
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < jobs.total_warps;
+       w += nwarps) {
+    int jj = 0;
+    while (jj + 1 < jobs.n && jobs.j[jj + 1].first_warp <= w) ++jj;
+    const QJob& J = jobs.j[jj];
+    const long long g = (w - J.first_warp) * 32 + lane;
+    if (g >= J.n_groups) continue;
+    switch (J.bits) {
+      case 2: quant_lane_group<2>(J, g); break;
+      case 4: quant_lane_group<4>(J, g); break;
+      default: quant_lane_group<8>(J, g); break;
     }
   }
 }
@@ -173,22 +191,22 @@ cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaSt
   for (int start = 0; start < n_jobs; start += kMaxJobs) {
     QJobs J{};
     J.n = 0;
-    long long pairs = 0;
-    for (int i = start; i < n_jobs && J.n < kMaxJobs; ++i) {
+    long long warps = 0;
+    for (int i = start; i < n_jobs && i < start + kMaxJobs; ++i) {
       const dymoe_quant_job& h = jobs_host[i];
       const long long ng = (long long)h.N * (h.K / DYMOE_GROUP);
       if (ng == 0) continue;
       QJob& q = J.j[J.n++];
       q.W = h.W; q.codes = h.codes; q.scales = h.scales; q.zeros = h.zeros;
-      q.N = h.N; q.K = h.K; q.bits = h.bits;
-      q.first_pair = pairs;
-      pairs += (ng + 1) / 2;
+      q.K = h.K; q.bits = h.bits;
+      q.n_groups = ng;
+      q.first_warp = warps;
+      warps += (ng + 31) / 32;
     }
-    J.total_pairs = pairs;
-    if (pairs == 0) continue;
-    const long long warps_needed = (pairs + kQuantUnroll - 1) / kQuantUnroll;
-    long long blocks = (warps_needed + 7) / 8;
-    const long long cap = (long long)sms * 8;   // 8 CTAs of 256 threads per SM resident
+    J.total_warps = warps;
+    if (warps == 0) continue;
+    long long blocks = (warps + 7) / 8;
+    const long long cap = (long long)sms * 8;   // 8 CTAs of 256 threads per SM (grid-stride)
     if (blocks > cap) blocks = cap;
     k_quantize<<<(unsigned)blocks, 256, 0, s>>>(J);
     cudaError_t e = cudaGetLastError();
