@@ -74,6 +74,13 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
   return r;
 }
+// x slice loads: the slice is constant for the whole run_tiles call, so the load is a pure function
+// of its address (non-volatile: the compiler may schedule it freely)
+__device__ __forceinline__ uint4 lds128_const(uint32_t a) {
+  uint4 r;
+  asm("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
+  return r;
+}
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t r;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
@@ -81,69 +88,110 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 }
 
 // Dequant parameters from a metadata word (bf16 scale bits << 16 | zero).
+template <int BITS>
 __device__ __forceinline__ DQ dq_from_meta(uint32_t w) {
   DQ d;
   d.ss = prmt(w, 0u, 0x3232u);                       // (s, s)
-  const uint32_t zb = 0x4300u | (w & 0xffu);         // bf16(128 + z)
-  d.zz = zb | (zb << 16);
+  if constexpr (BITS == 2) {
+    const uint32_t zl2 = prmt(w, 0u, 0x4040u);       // (z, z)
+    d.zz = zl2 + 0x43004300u;                        // bf16(128 + z)
+    d.zz1 = zl2 * 4u + 0x42004200u;                  // bf16(32 + z)
+    d.zz2 = zl2 * 16u + 0x41004100u;                 // bf16(8 + z)
+  } else {
+    d.zz = prmt(w, 0x43u, 0x4040u);                  // (bf16(128 + z), bf16(128 + z))
+  }
   d.sf = __uint_as_float(w & 0xffff0000u);
-  d.zf = __uint_as_float(0x4B000000u | (w & 0xffu));
+  d.zf = __uint_as_float(prmt(w, 0x4B000000u, 0x7440u));   // 2^23 + z
   return d;
 }
 
-// Issue the copies of the item at (tile, chunk ci) into the stage at shared address `st`.
+// Per-lane producer state: the global addresses this lane copies for the current tile at chunk
+// `warp` (j = 0).  Item j of the tile is these + j * 512 bytes (codes) / + j * GADV words (meta):
+// no per-item address arithmetic beyond one 64-bit add per copy.
 template <int BITS, int NM>
-__device__ __forceinline__ void issue_item(uint32_t st, const uint8_t* const (&mat)[NM],
-                                           const uint32_t* const (&meta)[NM], size_t row_bytes,
-                                           int gpr, int tile, int ci, int nck, int kl, int k0,
-                                           int lane) {
-  constexpr int CK = WT<BITS>::CHUNK_K;
-  if (ci >= nck) return;
-  const int gr = lane & 3;
-  const int k_lane = ci * CK + gr * WT<BITS>::CODES;       // first k of this lane's granule
-  if (k_lane < kl) {
-    const size_t kbytes = (size_t)(k0 + k_lane) * BITS / 8;
+struct Producer {
+  static constexpr int RG = Ring<NM>::ROWS / 8;               // row groups of 8 rows
+  static constexpr int CK = WT<BITS>::CHUNK_K;
+  static constexpr int GADV = kWarps * CK / DYMOE_GROUP;      // meta words per item step
+  const uint8_t* src[RG];
+  const uint32_t* msrc;
+  size_t tile_step;      // bytes between this lane's rows of tile t and t + 2
+  int mtile_step;        // meta words between ...
+  int k_lane0;           // k of this lane's granule at j = 0 (relative to the slice)
+  bool meta8;            // Int2: the chunk's two metadata words are one aligned 8-byte copy
+
+  __device__ __forceinline__ void init(const uint8_t* const (&mat)[NM],
+                                       const uint32_t* const (&meta)[NM], size_t row_bytes,
+                                       int gpr, int tile, int k0, int warp, int lane) {
+    const int gr = lane & 3;
+    const size_t kbytes = (size_t)k0 * BITS / 8 + (size_t)warp * 64 + gr * 16;
 #pragma unroll
-    for (int i = 0; i < Ring<NM>::ROWS / 8; ++i) {
-      const int r = i * 8 + (lane >> 2);                    // stage row: m*16 + 8h + g
-      const int m = r >> 4, rr = r & 15;
-      cp_async<16>(st + r * 64 + gr * 16, mat[m] + (size_t)(tile * 16 + rr) * row_bytes + kbytes);
+    for (int i = 0; i < RG; ++i) {
+      const int r = i * 8 + (lane >> 2), m = r >> 4, rr = r & 15;
+      src[i] = mat[m] + (size_t)(tile * 16 + rr) * row_bytes + kbytes;
+    }
+    tile_step = (size_t)32 * row_bytes;
+    k_lane0 = warp * CK + gr * WT<BITS>::CODES;
+    if constexpr (BITS != 16) {
+      const int r = lane < Ring<NM>::ROWS ? lane : 0, m = r >> 4, rr = r & 15;
+      msrc = meta[m] + (size_t)(tile * 16 + rr) * gpr + (k0 + warp * CK) / DYMOE_GROUP;
+      mtile_step = 32 * gpr;
+      meta8 = (((uintptr_t)msrc) & 7) == 0;   // invariant: every step is an even word count
     }
   }
-  if constexpr (BITS != 16) {
-    constexpr int GCH = BITS == 2 ? 2 : 1;                   // groups touched by a chunk
-    if (lane < Ring<NM>::ROWS) {
-      const int r = lane, m = r >> 4, rr = r & 15;
-      const int g0 = (k0 + ci * CK) / DYMOE_GROUP;
-      const uint32_t* src = meta[m] + (size_t)(tile * 16 + rr) * gpr + g0;
-      const uint32_t dst = st + Ring<NM>::W_BYTES + r * 8;
-      const bool both = GCH == 2 && ci * CK + DYMOE_GROUP < kl;
-      if (GCH == 2 && both && ((uintptr_t)src & 7) == 0) {
-        cp_async<8>(dst, src);
-      } else {
-        cp_async<4>(dst, src);
-        if (GCH == 2 && both) cp_async<4>(dst + 4, src + 1);
+  __device__ __forceinline__ void next_tile() {
+#pragma unroll
+    for (int i = 0; i < RG; ++i) src[i] += tile_step;
+    if constexpr (BITS != 16) msrc += mtile_step;
+  }
+  // copy item j (chunk ci = warp + 8 j) into the stage at shared address st
+  __device__ __forceinline__ void issue(uint32_t st, int j, int ci, int nck, int kl, bool ragged,
+                                       int lane) const {
+    if (ci >= nck) return;
+    const int gr = lane & 3;
+    const uint32_t dst = st + (lane >> 2) * 64 + gr * 16;
+    if (!ragged || k_lane0 + j * kWarps * CK < kl) {
+#pragma unroll
+      for (int i = 0; i < RG; ++i) cp_async<16>(dst + i * 512, src[i] + (size_t)j * 512);
+    }
+    if constexpr (BITS != 16) {
+      if (lane < Ring<NM>::ROWS) {
+        const uint32_t* p = msrc + j * GADV;
+        const uint32_t mdst = st + Ring<NM>::W_BYTES + lane * 8;
+        if constexpr (BITS == 2) {
+          const bool both = !ragged || ci * CK + DYMOE_GROUP < kl;
+          if (both && meta8) {
+            cp_async<8>(mdst, p);
+          } else {
+            cp_async<4>(mdst, p);
+            if (both) cp_async<4>(mdst + 4, p + 1);
+          }
+        } else {
+          cp_async<4>(mdst, p);
+        }
       }
     }
   }
-}
+};
 
-// One virtual CTA: expert e, k-slice ks (global k range [k0, k0 + kl)), tiles [t0, t1),
-// tokens [tok0, tok0 + nt).
+// One virtual CTA: expert e, k-slice [k0, k0 + kl), tiles [t0, t1), nt tokens whose x slice is
+// staged at shared address xs (x_pos layout, row_gran granules per token).  Outputs: W13 -> bf16
+// h at out[tok * ostride + n]; W2 -> fp32 partials at out[tok * ostride + n].
 template <bool W13, int BITS>
-__device__ __noinline__ void run_tiles(const FfnArgs& a, int e, int k0, int kl, int t0, int t1,
-                                       int tok0, int nt, int ks, const uint4* xs, int row_gran,
-                                       float* red, uint32_t ring_base, int* sync) {
+__device__ __noinline__ void run_tiles(const DevExpert* __restrict__ experts, int e, int K, int k0,
+                                       int kl, int t0, int t1, int nt, void* out, int ostride,
+                                       uint32_t xs, int row_gran, float* red, uint32_t ring_base,
+                                       int* sync) {
   using Tr = WT<BITS>;
   constexpr int NM = W13 ? 2 : 1;
   constexpr int S = Pipe<W13>::STAGES;
   constexpr int STAGE = Ring<NM>::STAGE;
+  constexpr int CK = Tr::CHUNK_K;
   const int lane = threadIdx.x & 31;
   const int grp = threadIdx.x >> 8;                 // warp group: tiles t0 + grp, +2, ...
   const int warp = (threadIdx.x >> 5) & (kWarps - 1);  // warp within the group
   const int g = lane >> 2, c = lane & 3;
-  const int K = W13 ? a.Hd : a.F;
-  const DevExpert& E = a.experts[e];
+  const DevExpert& E = experts[e];
   const int wi = width_index(BITS);
   const uint8_t* mat[NM];
   const uint32_t* meta[NM];
@@ -158,15 +206,18 @@ __device__ __noinline__ void run_tiles(const FfnArgs& a, int e, int k0, int kl, 
       meta[m] = E.q[wi][mi].meta;
     }
   }
-  const size_t row_bytes = (size_t)K * BITS / 8;
-  const int gpr = K / DYMOE_GROUP;
-  const int nck = (kl + Tr::CHUNK_K - 1) / Tr::CHUNK_K;      // chunks per tile (slice)
-  const int cmax = (nck + kWarps - 1) / kWarps;              // per warp (same for all warps)
+  const int nck = (kl + CK - 1) / CK;            // chunks per tile (slice)
+  const int cmax = (nck + kWarps - 1) / kWarps;  // per warp (same for all warps)
+  const bool ragged = (kl % CK) != 0;
   const int my_tiles = (t1 - t0 - grp + 1) / 2;
   const int n_items = (my_tiles > 0 ? my_tiles : 0) * cmax;
+  if (n_items == 0) return;
   const uint32_t ring = ring_base + (threadIdx.x >> 5) * (S * STAGE);
   red += grp * (2 * kWarps * NM * kRedTile);
   sync += grp * 4;   // [arrivals buf0, arrivals buf1, generation buf0, generation buf1]
+
+  Producer<BITS, NM> pr;
+  pr.init(mat, meta, (size_t)K * BITS / 8, K / DYMOE_GROUP, t0 + grp, k0, warp, lane);
 
   float acc[NM][4];
 #pragma unroll
@@ -174,43 +225,36 @@ __device__ __noinline__ void run_tiles(const FfnArgs& a, int e, int k0, int kl, 
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
 
-  // producer cursor: the next item to issue is at (tile_iss, chunk warp + 8 * j_iss)
-  int tile_iss = t0 + grp, j_iss = 0;
+  // producer cursor: the next item to issue is chunk warp + 8 * j_iss of the producer's tile
+  int j_iss = 0;
 #pragma unroll
   for (int p = 0; p < S - 1; ++p) {
-    if (p < n_items)
-      issue_item<BITS, NM>(ring + p * STAGE, mat, meta, row_bytes, gpr, tile_iss,
-                           warp + kWarps * j_iss, nck, kl, k0, lane);
+    if (p < n_items) pr.issue(ring + p * STAGE, j_iss, warp + kWarps * j_iss, nck, kl, ragged, lane);
     cp_commit();
-    if (++j_iss == cmax) { j_iss = 0; tile_iss += 2; }
+    if (++j_iss == cmax) { j_iss = 0; pr.next_tile(); }
   }
 
+  // this lane's x address at chunk 0: token row g, quad position c (x_pos layout)
+  const uint32_t xlane = xs + (uint32_t)(g * row_gran + c) * 16;
   int tile_seq = 0;
   int tile = t0 + grp, j = 0;      // consumer cursor
   int slot = 0, slot_iss = S - 1;  // ring slots of the consumer / producer
   for (int q = 0; q < n_items; ++q) {
     // refill: item q + S - 1 goes into the slot consumed in the previous iteration
     if (q + S - 1 < n_items)
-      issue_item<BITS, NM>(ring + slot_iss * STAGE, mat, meta, row_bytes, gpr, tile_iss,
-                           warp + kWarps * j_iss, nck, kl, k0, lane);
+      pr.issue(ring + slot_iss * STAGE, j_iss, warp + kWarps * j_iss, nck, kl, ragged, lane);
     cp_commit();
-    if (++j_iss == cmax) { j_iss = 0; tile_iss += 2; }
+    if (++j_iss == cmax) { j_iss = 0; pr.next_tile(); }
     if (++slot_iss == S) slot_iss = 0;
     const int ci = warp + kWarps * j;
-    const int kb = ci * Tr::CHUNK_K + c * Tr::CODES;
-    const bool ok = ci < nck && kb < kl;
-    // x for this chunk from the swizzled smem slice; beyond the slice x is zero, so stale ring
-    // bytes (always finite: the ring is zeroed at kernel start and only ever holds weights)
-    // contribute nothing -- no per-lane masking of the weights
-    uint4 xv[Tr::XU4];
-    const int gbase = kb / 8;
-#pragma unroll
-    for (int i = 0; i < Tr::XU4; ++i)
-      xv[i] = ok ? xs[g * row_gran + x_granule(gbase + i)] : make_uint4(0, 0, 0, 0);
+    const bool live = ci < nck;
+    // x for this chunk: beyond the slice the staged x is zero, so stale ring bytes (always
+    // finite: the ring is zeroed at kernel start and only ever holds weights) contribute nothing
+    const uint32_t xa = xlane + (uint32_t)ci * (2 * CK);
     cp_wait<S - 1>();
     __syncwarp();   // the stage's rows were copied by other lanes
     const uint32_t st = ring + slot * STAGE;
-    if (ci < nck) {
+    if (live) {
       DQ dq[NM][2];
       if constexpr (BITS != 16) {
         const int gi = BITS == 2 ? (c >> 1) : 0;            // group within the chunk
@@ -218,23 +262,31 @@ __device__ __noinline__ void run_tiles(const FfnArgs& a, int e, int k0, int kl, 
         for (int m = 0; m < NM; ++m)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            dq[m][h] = dq_from_meta(lds32(st + Ring<NM>::W_BYTES + (m * 16 + 8 * h + g) * 8 + gi * 4));
+            dq[m][h] = dq_from_meta<BITS>(lds32(st + Ring<NM>::W_BYTES + (m * 16 + 8 * h + g) * 8 + gi * 4));
       }
       uint4 w[NM][2];
 #pragma unroll
       for (int m = 0; m < NM; ++m)
 #pragma unroll
         for (int h = 0; h < 2; ++h) w[m][h] = lds128(st + (m * 16 + 8 * h + g) * 64 + c * 16);
+      using X = XB<BITS>;
 #pragma unroll
-      for (int s = 0; s < Tr::STEPS; ++s) {
-        uint32_t b0, b1;
-        b_frag<BITS>(xv, s, b0, b1);
+      for (int blk = 0; blk < X::NB; ++blk) {
+        uint4 xb[X::GPB];
 #pragma unroll
-        for (int m = 0; m < NM; ++m) {
-          uint32_t glo, ghi, g8lo, g8hi;
-          a_frag<BITS>(w[m][0], dq[m][0], s, glo, ghi);
-          a_frag<BITS>(w[m][1], dq[m][1], s, g8lo, g8hi);
-          mma16816(acc[m], glo, g8lo, ghi, g8hi, b0, b1);
+        for (int i = 0; i < X::GPB; ++i) xb[i] = lds128_const(xa + (blk * X::GPB + i) * 64);
+#pragma unroll
+        for (int ss = 0; ss < X::SPB; ++ss) {
+          const int s = blk * X::SPB + ss;
+          uint32_t b0, b1;
+          b_frag<BITS>(xb, ss, b0, b1);
+#pragma unroll
+          for (int m = 0; m < NM; ++m) {
+            uint32_t glo, ghi, g8lo, g8hi;
+            a_frag<BITS>(w[m][0], dq[m][0], s, glo, ghi);
+            a_frag<BITS>(w[m][1], dq[m][1], s, g8lo, g8hi);
+            mma16816(acc[m], glo, g8lo, ghi, g8hi, b0, b1);
+          }
         }
       }
     }
@@ -279,14 +331,14 @@ __device__ __noinline__ void run_tiles(const FfnArgs& a, int e, int k0, int kl, 
               s0 = __fadd_rn(s0, pp[0]);
               if (NM == 2) s1 = __fadd_rn(s1, pp[kRedTile]);
             }
-            const size_t r = (size_t)(tok0 + tok);
             const int n = tile * 16 + r16;
             if (W13) {
-              const float silu = __fdiv_rn(s0, __fadd_rn(1.f, expf(-s0)));
+              // silu(A) * B, fast exp / divide (well inside the FFN tolerance)
+              const float silu = __fdividef(s0, 1.f + __expf(-s0));
               const __nv_bfloat16 hv = __float2bfloat16_rn(__fmul_rn(silu, s1));
-              a.h[r * a.F + n] = *reinterpret_cast<const uint16_t*>(&hv);
+              reinterpret_cast<__nv_bfloat16*>(out)[(size_t)tok * ostride + n] = hv;
             } else {
-              a.y_part[((size_t)ks * a.part_rows + r) * a.Hd + n] = s0;
+              reinterpret_cast<float*>(out)[(size_t)tok * ostride + n] = s0;
             }
           }
         }
@@ -304,6 +356,18 @@ __device__ __noinline__ void run_tiles(const FfnArgs& a, int e, int k0, int kl, 
   cp_wait<0>();
 }
 
+// x slice layout in shared memory ("x_pos"): [8 tokens][row_gran granules of 16 B].  Within each
+// chunk of CK k values (4 * XU4 granules), the granule lane quad position c reads as its i-th
+// (logical granule c * XU4 + i) is stored at position i * 4 + c, so a lane's XU4 loads are 64 B
+// apart (immediate offsets) and the 4 lanes of a quad hit 4 consecutive bank groups; row_gran = 4
+// (mod 8) puts the other token row of an LDS.128 phase on the other four.
+__device__ __forceinline__ int x_logical(int pos, int xu4) {
+  const int span = 4 * xu4;
+  const int chunk = pos / span, w = pos - chunk * span;
+  return chunk * span + (w & 3) * xu4 + (w >> 2);
+}
+__host__ __device__ inline int x_row_gran(int sliceK) { return (sliceK + 255) / 256 * 32 + 4; }
+
 template <bool W13>
 __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a, int SK, int sliceK) {
   extern __shared__ __align__(16) uint8_t smem[];
@@ -318,7 +382,8 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
   const int K = W13 ? a.Hd : a.F;
   const int N = W13 ? a.F : a.Hd;
   const int NT = N / 16;
-  if (threadIdx.x == 0) compute_alloc(a, gridDim.x / SK, A);
+  const int row_gran = x_row_gran(sliceK);
+  if (threadIdx.x == 0) compute_alloc(a, gridDim.x / SK, W13, A);
   {  // zero the weight ring once: stale stage bytes are then always finite (see run_tiles)
     uint4* rz = reinterpret_cast<uint4*>(smem + red_bytes);
     const int n16 = (int)(ring_bytes / 16);
@@ -358,37 +423,45 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
       continue;
     }
     if (t1 <= t0 || kl <= 0) continue;
+    int xu4;
+    switch (be) {
+      case 2: xu4 = WT<2>::XU4; break;
+      case 4: xu4 = WT<4>::XU4; break;
+      case 8: xu4 = WT<8>::XU4; break;
+      default: xu4 = WT<16>::XU4; break;
+    }
+    const int gran = kl / 8;                        // granules of real x
+    const int npos = (kl + 255) / 256 * 32;         // staged positions (zero beyond gran)
     for (int tok0 = r_lo; tok0 < r_hi; tok0 += kMaxTok) {
       const int nt = min(kMaxTok, r_hi - tok0);
-      int pad;
-      switch (be) {
-        case 2: pad = WT<2>::PAD; break;
-        case 4: pad = WT<4>::PAD; break;
-        case 8: pad = WT<8>::PAD; break;
-        default: pad = WT<16>::PAD; break;
-      }
-      const int row_gran = sliceK / 8 + pad;
-      // stage the x slice of this pass's tokens (zero rows beyond nt), granule-swizzled
+      // stage the x slice of this pass's tokens (zero rows beyond nt), x_pos layout
       __syncthreads();  // the previous pass is done with xs / red / tile_sync
       if (threadIdx.x < 8) tile_sync[threadIdx.x] = 0;
-      const int gran = kl / 8;
-      for (int idx = threadIdx.x; idx < kMaxTok * gran; idx += blockDim.x) {
-        const int t = idx / gran, gi = idx - t * gran;
+      for (int idx = threadIdx.x; idx < kMaxTok * npos; idx += blockDim.x) {
+        const int t = idx / npos, pos = idx - t * npos;
+        const int gl = x_logical(pos, xu4);
         uint4 v4 = make_uint4(0, 0, 0, 0);
-        if (t < nt) {
+        if (t < nt && gl < gran) {
           const int r = tok0 + t;
           const uint16_t* src = W13 ? a.x + (size_t)a.perm_token[r] * a.Hd : a.h + (size_t)r * a.F;
-          v4 = *reinterpret_cast<const uint4*>(src + k0 + gi * 8);
+          v4 = *reinterpret_cast<const uint4*>(src + k0 + gl * 8);
         }
-        xs[t * row_gran + x_granule(gi)] = v4;
+        xs[t * row_gran + pos] = v4;
       }
       __syncthreads();
+      void* out = W13 ? (void*)(a.h + (size_t)tok0 * a.F)
+                      : (void*)(a.y_part + ((size_t)ks * a.part_rows + tok0) * a.Hd);
+      const int ostride = W13 ? a.F : a.Hd;
+      const uint32_t xsa = (uint32_t)__cvta_generic_to_shared(xs);
+#define DYMOE_RUN(B) run_tiles<W13, B>(a.experts, e, K, k0, kl, t0, t1, nt, out, ostride, xsa, \
+                                       row_gran, red, ring_base, tile_sync)
       switch (be) {
-        case 2: run_tiles<W13, 2>(a, e, k0, kl, t0, t1, tok0, nt, ks, xs, row_gran, red, ring_base, tile_sync); break;
-        case 4: run_tiles<W13, 4>(a, e, k0, kl, t0, t1, tok0, nt, ks, xs, row_gran, red, ring_base, tile_sync); break;
-        case 8: run_tiles<W13, 8>(a, e, k0, kl, t0, t1, tok0, nt, ks, xs, row_gran, red, ring_base, tile_sync); break;
-        default: run_tiles<W13, 16>(a, e, k0, kl, t0, t1, tok0, nt, ks, xs, row_gran, red, ring_base, tile_sync); break;
+        case 2: DYMOE_RUN(2); break;
+        case 4: DYMOE_RUN(4); break;
+        case 8: DYMOE_RUN(8); break;
+        default: DYMOE_RUN(16); break;
       }
+#undef DYMOE_RUN
     }
   }
 }
@@ -398,7 +471,7 @@ size_t smem_bytes(bool w13, int sliceK) {
   const size_t ring = w13 ? (size_t)2 * kWarps * Pipe<true>::STAGES * Ring<2>::STAGE
                           : (size_t)2 * kWarps * Pipe<false>::STAGES * Ring<1>::STAGE;
   return 2 * 2 * kWarps * NM * kRedTile * sizeof(float) + ring +
-         (size_t)kMaxTok * (sliceK / 8 + 4) * 16;
+         (size_t)kMaxTok * x_row_gran(sliceK) * 16;
 }
 
 }  // namespace dec

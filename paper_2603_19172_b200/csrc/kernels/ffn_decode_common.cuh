@@ -13,9 +13,6 @@ struct WT {
   static constexpr int CHUNK_K = 4 * CODES;  // k per chunk (a lane quad covers 64 bytes)
   static constexpr int STEPS = CODES / 4;    // mma k16 steps per chunk
   static constexpr int XU4 = CODES / 8;      // uint4 of x per lane per chunk
-  // row padding (in 16-byte granules, mod 8) that makes the 2 token rows of an LDS.128 phase
-  // hit disjoint bank groups (see x_granule)
-  static constexpr int PAD = BITS == 2 ? 4 : BITS == 4 ? 2 : BITS == 8 ? 1 : 4;
   static constexpr int GPQ = BITS == 2 ? 2 : 1;   // quantization groups a lane quad spans per chunk
 };
 
@@ -62,7 +59,7 @@ __device__ __forceinline__ uint32_t pack_bf2(float lo, float hi) {
 }
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
@@ -74,6 +71,7 @@ __device__ __forceinline__ uint32_t word(const uint4& v, int i) {
 
 struct DQ {
   uint32_t ss, zz;  // bf16x2 (s, s) and (128+z, 128+z)
+  uint32_t zz1, zz2;  // Int2: (32+z, 32+z) and (8+z, 8+z)
   float sf, zf;     // Int8: bf16(s) as float, 2^23 + z
 };
 __device__ __forceinline__ DQ make_dq(float s, uint32_t z) {
@@ -81,14 +79,23 @@ __device__ __forceinline__ DQ make_dq(float s, uint32_t z) {
   const __nv_bfloat16 sb = __float2bfloat16_rn(s);
   const uint32_t sbits = *reinterpret_cast<const uint16_t*>(&sb);
   d.ss = sbits | (sbits << 16);
-  const uint32_t zb = 0x4300u | z;  // bf16(128 + z), exact for z < 128 (Int2/Int4)
-  d.zz = zb | (zb << 16);
+  const uint32_t zl2 = z | (z << 16);
+  d.zz = 0x43004300u + zl2;  // bf16(128 + z), exact for z < 128 (Int2/Int4)
+  d.zz1 = 0x42004200u + zl2 * 4u;
+  d.zz2 = 0x41004100u + zl2 * 16u;
   d.sf = __bfloat162float(sb);
   d.zf = __uint_as_float(0x4B000000u | z);
   return d;
 }
 
 // A-fragment pair (logical k slots lo = {2c, 2c+1}, hi = {2c+8, 2c+9}) for step s of a chunk.
+//
+// Int4: codes j (bits 4j..4j+3 of each 16-bit half) are shifted down and OR-ed into the mantissa
+// of bf16 128 (exponent 7, ulp 1): 128 + q exactly.
+// Int2: no shift for codes at bits 2k..2k+1 (k = 0, 1, 2) of a half: OR-ed into the mantissa of
+// bf16 2^(7-2k) (ulp 4^-k) they read as 2^(7-2k) + q exactly, and subtracting bf16(2^(7-2k) + z)
+// gives q - z exactly; codes 3-5 / 6-7 of a half come from one shift by 6 / 12.  So a word of 16
+// Int2 codes needs 2 shifts instead of 7.
 template <int BITS>
 __device__ __forceinline__ void a_frag(const uint4& w, const DQ& dq, int s, uint32_t& lo,
                                        uint32_t& hi) {
@@ -102,9 +109,21 @@ __device__ __forceinline__ void a_frag(const uint4& w, const DQ& dq, int s, uint
     hi = bf2_mul(bf2_sub(lop_or_and(x >> (sh + 4), 0x000F000Fu, 0x43004300u), dq.zz), dq.ss);
   } else if constexpr (BITS == 2) {
     const uint32_t x = word(w, s >> 2);
-    const int sh = 4 * (s & 3);
-    lo = bf2_mul(bf2_sub(lop_or_and(x >> sh, 0x00030003u, 0x43004300u), dq.zz), dq.ss);
-    hi = bf2_mul(bf2_sub(lop_or_and(x >> (sh + 2), 0x00030003u, 0x43004300u), dq.zz), dq.ss);
+    const int j = 2 * (s & 3);   // codes j (lo) and j + 1 (hi) of each half
+    const uint32_t y0 = x, y1 = x >> 6, y2 = x >> 12;
+    uint32_t v[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int jj = j + t;
+      const int k = jj < 3 ? jj : jj < 6 ? jj - 3 : jj - 6;
+      const uint32_t y = jj < 3 ? y0 : jj < 6 ? y1 : y2;
+      const uint32_t mask = 0x00030003u << (2 * k);
+      const uint32_t magic = 0x43004300u - (uint32_t)k * 0x01000100u;
+      const uint32_t zz = k == 0 ? dq.zz : k == 1 ? dq.zz1 : dq.zz2;
+      v[t] = bf2_mul(bf2_sub(lop_or_and(y, mask, magic), zz), dq.ss);
+    }
+    lo = v[0];
+    hi = v[1];
   } else {  // 8
     // q - z exact in fp32 (2^23 + q minus 2^23 + z), packed to bf16x2 exactly (|q - z| <= 255
     // has 8 significant bits), then one HMUL2 per pair gives RNE((q - z)·s) (D17)
@@ -118,34 +137,32 @@ __device__ __forceinline__ void a_frag(const uint4& w, const DQ& dq, int s, uint
   }
 }
 
-// B fragment (x permuted to a_frag's k order) for step s, from the chunk's x registers.
+// x granules per block and mma steps per block: a block of GPB granules (8 k values each) of the
+// lane's x feeds SPB consecutive k16 steps.
 template <int BITS>
-__device__ __forceinline__ void b_frag(const uint4 (&xv)[WT<BITS>::XU4], int s, uint32_t& b0,
+struct XB {
+  static constexpr int GPB = BITS == 2 ? 2 : 1;
+  static constexpr int SPB = BITS == 2 ? 4 : 2;
+  static constexpr int NB = WT<BITS>::STEPS / SPB;
+};
+
+// B fragment (x permuted to a_frag's k order) for step ss of a block, from the block's x granules.
+template <int BITS>
+__device__ __forceinline__ void b_frag(const uint4 (&xb)[XB<BITS>::GPB], int ss, uint32_t& b0,
                                        uint32_t& b1) {
-  if constexpr (BITS == 16) {
-    b0 = word(xv[0], 2 * s);
-    b1 = word(xv[0], 2 * s + 1);
-  } else if constexpr (BITS == 8) {
-    b0 = word(xv[s >> 1], 2 * (s & 1));
-    b1 = word(xv[s >> 1], 2 * (s & 1) + 1);
+  if constexpr (BITS == 16 || BITS == 8) {
+    b0 = word(xb[0], 2 * ss);
+    b1 = word(xb[0], 2 * ss + 1);
   } else if constexpr (BITS == 4) {
-    const uint4& u = xv[s >> 1];
-    const int j = s & 1;
-    const uint32_t a = word(u, j), c = word(u, j + 2);
+    const uint32_t a = word(xb[0], ss), c = word(xb[0], ss + 2);
     b0 = prmt(a, c, 0x5410u);
     b1 = prmt(a, c, 0x7632u);
   } else {  // 2
-    const int q = s >> 2, j = s & 3;
-    const uint32_t a = word(xv[2 * q], j), c = word(xv[2 * q + 1], j);
+    const uint32_t a = word(xb[0], ss), c = word(xb[1], ss);
     b0 = prmt(a, c, 0x5410u);
     b1 = prmt(a, c, 0x7632u);
   }
 }
-
-// x slice in shared memory: [8 tokens][row_gran granules of 16 B], granule index XOR-swizzled
-// with (g >> 3) & 7 so that the 4 lanes of a quad (k offsets c*XU4 granules apart) hit distinct
-// bank groups; row_gran = sliceK/8 + PAD puts the second token row of a phase on the other four.
-__device__ __forceinline__ int x_granule(int g) { return g ^ ((g >> 3) & 7); }
 
 struct Alloc {
   int n_act;
@@ -157,11 +174,17 @@ struct Alloc {
   int u[DYMOE_MAX_EXPERTS];
 };
 
-__device__ __forceinline__ int wcost(int b) { return b == 16 ? 256 : 16 * b + 5; }
+// Relative time to stream one expert matrix set at width b (per 8-token chunk), measured on B200
+// with every expert forced to one width (tools/decode_width_sweep.py): the narrow widths are
+// bound by dequant issue slots rather than bytes, so they cost more than their bytes suggest.
+__device__ __forceinline__ int wcost(int b, bool w13) {
+  if (w13) return b == 16 ? 256 : b == 8 ? 160 : b == 4 ? 107 : 89;
+  return b == 16 ? 256 : b == 8 ? 200 : b == 4 ? 144 : 129;
+}
 
 // Cost-proportional allocation of `units_total` units to the active experts (largest remainder,
 // ties to the lower list index; every active expert gets >= 1 unit).  Thread 0 only.
-__device__ void compute_alloc(const FfnArgs& a, int units_grid, Alloc& A) {
+__device__ void compute_alloc(const FfnArgs& a, int units_grid, bool w13, Alloc& A) {
   const int n = a.active_list[0];
   A.n_act = n;
   long long* cost = A.cost;
@@ -171,7 +194,7 @@ __device__ void compute_alloc(const FfnArgs& a, int units_grid, Alloc& A) {
     A.expert[i] = e;
     const int rows = a.expert_off[e + 1] - a.expert_off[e];
     const int chunks = (rows + kMaxTok - 1) / kMaxTok;
-    cost[i] = (long long)wcost(a.bits[e]) * chunks;
+    cost[i] = (long long)wcost(a.bits[e], w13) * chunks;
     total += cost[i];
   }
   const int U = units_grid > n ? units_grid : n;

@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
     }
   }
   for (int s = 0; s < k; ++s) wt[s] = renorm ? wt[s] / denom : wt[s];
-  for (int c = threadIdx.x * 4; c < Hd; c += blockDim.x * 4) {
+  // blockIdx.y splits Hd so that a small decode batch still spreads over many SMs
+  for (int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4; c < Hd; c += gridDim.y * blockDim.x * 4) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < k; ++s) {
       if (rows[s] < 0) continue;
@@ -222,8 +223,12 @@ cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, cons
                            const float* topk_w, int T, int k, int Hd, int renorm, int out_dtype,
                            void* y, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  k_combine<<<T, 256, 0, s>>>(y_perm, n_parts, part_rows, inv_row, topk_w, k, Hd, renorm,
-                              out_dtype == DYMOE_OUT_BF16, y);
+  // ~4 CTAs of 128 threads x float4 per SM in total, at least one column chunk per token
+  const int chunks = (Hd + 511) / 512;
+  int gy = (4 * 148 + T - 1) / T;
+  gy = gy < 1 ? 1 : (gy > chunks ? chunks : gy);
+  k_combine<<<dim3(T, gy), 128, 0, s>>>(y_perm, n_parts, part_rows, inv_row, topk_w, k, Hd, renorm,
+                                        out_dtype == DYMOE_OUT_BF16, y);
   return cudaGetLastError();
 }
 
