@@ -9,6 +9,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "dymoe_internal.cuh"
 
 using namespace dymoe;
@@ -18,6 +20,7 @@ struct dymoe_layer {
   std::vector<DevExpert> host;
   DevExpert* dev = nullptr;
   uint32_t* meta_pool = nullptr;   // derived dequant metadata of every resident quantized matrix
+  CUtensorMap* tmap_pool = nullptr;   // TMA descriptors of every resident matrix (device)
 };
 
 namespace {
@@ -286,6 +289,50 @@ int dymoe_quantize_batched(const dymoe_quant_job* jobs, int n_jobs, int group,
 }
 
 // ------------------------------------------------------------------------------------------
+// TMA descriptors (driver entry point fetched once through the runtime: no -lcuda)
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+// tiled map over a row-major tensor of rank 2 or 3 (strides in bytes for dims 1.., box per dim)
+bool encode(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int rank, const uint64_t* dims,
+            const uint64_t* strides, const uint32_t* box, CUtensorMapSwizzle swz) {
+  auto fn = tmap_encoder();
+  if (fn == nullptr) return false;
+  cuuint64_t d[3], st[2];
+  cuuint32_t b[3], es[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    if (i + 1 < rank) st[i] = strides[i];
+  }
+  return fn(m, dt, rank, const_cast<void*>(base), d, st, b, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// codes / bf16 rows: u8 {row_bytes, N}, 128 x 16 boxes, 128-byte swizzle (decode kernel items)
+bool encode_rows(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t N) {
+  const uint64_t dims[2] = {row_bytes, N}, str[1] = {row_bytes};
+  const uint32_t box[2] = {128, 16};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, base, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+// group-major meta [n_mat][gpr][N] u32: boxes {16 rows, gq groups, n_mat}
+bool encode_meta(CUtensorMap* m, const void* base, uint64_t N, uint64_t gpr, int n_mat, uint32_t gq) {
+  const uint64_t dims[3] = {N, gpr, (uint64_t)n_mat}, str[2] = {N * 4, N * gpr * 4};
+  const uint32_t box[3] = {16, gq, (uint32_t)n_mat};
+  return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, base, n_mat > 1 ? 3 : 2, dims, str, box,
+                CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+constexpr int kMapsPerExpert = 21;   // 3 bf16 masters + 3 widths x 3 matrices x (codes, meta)
+}  // namespace
+
 int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
   CHECK_ARG(out != nullptr, "out: must not be NULL");
   *out = nullptr;
@@ -355,9 +402,51 @@ int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
         const size_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
         const size_t n = N * (K / DYMOE_GROUP);
         q.meta = L->meta_pool + at;
-        if (e == cudaSuccess) e = launch_build_meta(q.scales, q.zeros, n, L->meta_pool + at, nullptr);
+        if (e == cudaSuccess)
+          e = launch_build_meta(q.scales, q.zeros, (int)N, (int)(K / DYMOE_GROUP), L->meta_pool + at, nullptr);
         at += n;
       }
+  // TMA descriptors: built on the host, copied next to the expert table
+  std::vector<CUtensorMap> maps((size_t)d->M * kMapsPerExpert);
+  memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
+  if (e == cudaSuccess) e = cudaMalloc(&L->tmap_pool, maps.size() * sizeof(CUtensorMap));
+  bool maps_ok = true;
+  for (int ex = 0; ex < d->M && e == cudaSuccess; ++ex) {
+    DevExpert& y = L->host[ex];
+    CUtensorMap* hm = maps.data() + (size_t)ex * kMapsPerExpert;
+    const CUtensorMap* dm = L->tmap_pool + (size_t)ex * kMapsPerExpert;
+    for (int m = 0; m < 3; ++m) {
+      const uint64_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
+      y.tm_w[m] = nullptr;
+      if (y.w[m] != nullptr) {
+        maps_ok &= encode_rows(&hm[m], y.w[m], 2 * K, N);
+        y.tm_w[m] = dm + m;
+      }
+      for (int wi = 0; wi < 3; ++wi) {
+        DevQMat& q = y.q[wi][m];
+        q.tm_codes = q.tm_meta = nullptr;
+        if (q.codes == nullptr) continue;
+        const int b = wi == 0 ? 8 : wi == 1 ? 4 : 2;
+        const uint32_t gq = (uint32_t)(2 * 512 / b / DYMOE_GROUP);   // groups per 128-byte item
+        const int ic = 3 + (wi * 3 + m) * 2, im = ic + 1;
+        maps_ok &= encode_rows(&hm[ic], q.codes, K * b / 8, N);
+        q.tm_codes = dm + ic;
+        // W2: 2-D meta; W1: 3-D over the adjacent W1 / W3 meta (one box feeds both matrices);
+        // W3's own descriptor is not needed by the kernels
+        const bool pair = m == 0 && y.q[wi][1].codes != nullptr;
+        if (m == 2 || pair) {
+          maps_ok &= encode_meta(&hm[im], q.meta, N, K / DYMOE_GROUP, pair ? 2 : 1, gq);
+          q.tm_meta = dm + im;
+        }
+      }
+    }
+  }
+  if (e == cudaSuccess && !maps_ok) {
+    dymoe_layer_destroy(L);
+    return fail(DYMOE_ERR_CUDA, "dymoe_layer_create: cuTensorMapEncodeTiled failed");
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpy(L->tmap_pool, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(L->dev, L->host.data(), sizeof(DevExpert) * d->M, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -377,7 +466,7 @@ int dymoe_layer_refresh(dymoe_layer* L, dymoe_stream_t stream) {
         const DevQMat& q = L->host[ex].q[wi][m];
         if (q.codes == nullptr) continue;
         const size_t N = m == 2 ? L->Hd : L->F, K = m == 2 ? L->F : L->Hd;
-        CHECK_LAUNCH(launch_build_meta(q.scales, q.zeros, N * (K / DYMOE_GROUP),
+        CHECK_LAUNCH(launch_build_meta(q.scales, q.zeros, (int)N, (int)(K / DYMOE_GROUP),
                                        const_cast<uint32_t*>(q.meta), S(stream)),
                      "dymoe_layer_refresh");
       }
@@ -388,6 +477,7 @@ int dymoe_layer_destroy(dymoe_layer* L) {
   if (!L) return ok();
   if (L->dev) cudaFree(L->dev);
   if (L->meta_pool) cudaFree(L->meta_pool);
+  if (L->tmap_pool) cudaFree(L->tmap_pool);
   delete L;
   return ok();
 }

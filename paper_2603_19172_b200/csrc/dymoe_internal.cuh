@@ -2,6 +2,7 @@
 // Nothing here is visible through include/dymoe.h.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -18,14 +19,24 @@ struct DevQMat {
   const uint8_t* zeros;
   // Derived by the layer handle (dymoe_layer_create / refresh), owned by it: per group
   // (bf16 bits of RNE_bf16(scale)) << 16 | zero — exactly the two values dequant (D17) consumes,
-  // in one 4-byte word, so the decode kernels fetch a group's metadata with one copy.
+  // in one 4-byte word — stored group-major, meta[g * N + n], so that the words of consecutive
+  // rows for one group are contiguous (one TMA box per 16-row tile in the decode kernels,
+  // coalesced per-row loads in the prefill producer).
   const uint32_t* meta;
+  // TMA descriptors (device memory, owned by the layer handle): codes as a 2-D u8 tensor
+  // {row bytes, N} with 128 x 16 boxes, 128-byte swizzle; meta as a u32 tensor {N, K / 128}
+  // with 16 x (groups per 128-byte item) boxes -- 3-D {.., 2} for W1, covering the adjacent W1
+  // and W3 meta with one box (W3's tm_meta is null); 2-D for W2.
+  const CUtensorMap* tm_codes;
+  const CUtensorMap* tm_meta;
 };
-cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, size_t n, uint32_t* meta,
-                              cudaStream_t s);
+// meta[g * N + n] = bf16bits(RNE(scales[n * gpr + g])) << 16 | zeros[n * gpr + g]
+cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, int N, int gpr,
+                              uint32_t* meta, cudaStream_t s);
 struct DevExpert {
-  const uint16_t* w[3];   // bf16 masters W1, W3, W2
-  DevQMat q[3][3];        // [width idx: int8, int4, int2][matrix: W1, W3, W2]
+  const uint16_t* w[3];        // bf16 masters W1, W3, W2
+  const CUtensorMap* tm_w[3];  // their TMA descriptors (u8 {2K, N}, 128 x 16 boxes, swizzled)
+  DevQMat q[3][3];             // [width idx: int8, int4, int2][matrix: W1, W3, W2]
 };
 
 __host__ __device__ inline int width_index(int bits) {

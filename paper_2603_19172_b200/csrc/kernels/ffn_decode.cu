@@ -6,69 +6,56 @@
 // y = h·deq(W2)^T in fp32, deq = RNE_bf16((q - z)·RNE_bf16(s)).
 //
 // Roofline: HBM.  Every active expert's packed W1/W3/W2 is streamed once per 8-token chunk
-// (3·Hd·F·(b/8 + 5/128) bytes per expert).
+// (3·Hd·F·(b/8 + 4/128) bytes per expert).
 //
-// Arithmetic.  At Int2 there are only ~2 ALU issue slots per weight at the HBM rate:
+// Arithmetic (issue slots, not bytes, are the limit at Int4/Int2):
 //  * multiply-adds on the tensor cores: mma.sync m16n8k16, 16 weight rows as A, the (<= 8)
 //    tokens as the N = 8 columns of B, fp32 accumulation;
-//  * dequant in registers straight into A fragments: Int2/Int4 codes are OR-ed into the mantissa
-//    of bf16 128.0 (one LOP3 per 2 weights gives 128+q exactly), HSUB2 (128+z) gives q-z
-//    exactly, HMUL2 by bf16(s) gives RNE((q-z)·s) — bit-identical to D17.  Int8 uses the fp32
-//    magic 2^23+q, FADD, FMUL (exact) and one cvt.rn.bf16x2;
-//  * the dot product is permutation-invariant in k, so A fragments take codes in the order the
-//    LOP3 extracts them (code i and i+4 of a word) and the x values are permuted to match (PRMT
-//    on registers loaded from shared memory).
+//  * dequant in registers straight into A fragments (ffn_decode_common.cuh a_frag): Int4/Int2
+//    codes OR-ed into a bf16 mantissa (exact 2^e + q), HSUB2 of 2^e + z (exact q - z), HMUL2 by
+//    bf16(s) = RNE((q - z)·s), bit-identical to D17; Int8 via the fp32 magic 2^23 + q;
+//  * the dot product is permutation-invariant in k, so A fragments take codes in the order they
+//    are extracted and x is permuted to match (PRMT on registers loaded from shared memory).
 //
 // Work decomposition (one launch per matrix pair, persistent, cost-balanced):
-//  * grid = 1 CTA of two 8-warp groups per SM (alternate tiles, one named barrier per group); each CTA walks "virtual CTAs".  Every CTA computes the same
-//    allocation of virtual CTAs to the active experts, proportional to each expert's streamed
-//    bytes (width x token chunks), so CTAs of Int8 and Int2 experts finish together.
-//  * a virtual CTA = (expert, K-slice, range of 16-row tiles).  Its 8 warps split every tile's K
-//    round-robin by 64-byte chunk and reduce the 16x8 partial tiles through shared memory in
-//    warp order (deterministic, double-buffered, one barrier per tile).  The tokens' x slice is
-//    staged once per virtual CTA in shared memory (XOR-swizzled: conflict-free LDS.128).
-//  * each warp streams its weights through its own cp.async (LDGSTS, L1-bypassing) shared-memory
-//    ring of 4 (W1/W3) or 5 (W2) stages of one 64-byte chunk per row plus the rows' per-group
-//    dequant words, so 2-4 chunks per warp (64 KB per SM) are in flight while it computes.
+//  * grid = 1 CTA of two 8-warp groups per SM (alternating tiles); each CTA walks "virtual
+//    CTAs".  Every CTA computes the same allocation of virtual CTAs to the active experts,
+//    proportional to each expert's measured streaming time (width x token chunks), so CTAs of
+//    Int8 and Int2 experts finish together.
+//  * a virtual CTA = (expert, K-slice, range of 16-row tiles).  The 8 warps of a group split
+//    every tile's K round-robin by 128-byte item and reduce the 16x8 partial tiles through shared
+//    memory in warp order (deterministic; the last warp to arrive reduces, no barrier).  The
+//    tokens' x slice is staged once per virtual CTA in shared memory (x_pos layout below).
+//  * each warp streams its weights through its own TMA ring: an item is one 128 x 16 box per
+//    matrix (128 bytes of each of 16 rows, 128-byte swizzled) plus one box of the group-major
+//    dequant words; lane 0 issues, the warp waits on the stage mbarrier.
 //  * W1/W3 (gate/up): one K-slice (x = 8 x Hd bf16 in smem), SwiGLU applied in the reduction
-//    epilogue, h written as bf16.  W2 (down): K = F is split into SK slices (x slice <= 64 KB),
-//    each writes fp32 partials y_part[slice]; the combine kernel sums the slices in order.
+//    epilogue, h written as bf16.  W2 (down): K = F is split into SK slices, each writes fp32
+//    partials y_part[slice]; the combine kernel sums the slices in order.
 #include "ffn_decode_common.cuh"
 
 namespace dymoe {
 namespace dec {
 
-// partial-tile reduction buffer: [tok 8][row16 + 4 pad] floats (conflict-free fragment stores)
-constexpr int kRedStride = 20;
-constexpr int kRedTile = 8 * kRedStride;
+// partial-tile reduction buffer per warp and matrix: [tok 8][row 16] floats
+constexpr int kRedTile = 8 * 16;
 
-// Per-warp cp.async (LDGSTS) ring.  A pipeline item is (tile, chunk): 64 contiguous bytes of each
-// of the tile's rows (16 rows per matrix) plus those rows' dequant metadata words for the groups
-// the chunk covers.  Copy: 4 lanes per row, 8 rows per instruction (512 contiguous smem bytes);
-// compute reads it back in the mma lane mapping (lane quad c of row g reads granule c), which is
-// bank-conflict free without swizzling.  The metadata copy is one 4/8-byte cp.async per row.
-template <int NM>
-struct Ring {
-  static constexpr int ROWS = NM * 16;
-  static constexpr int W_BYTES = ROWS * 64;
-  static constexpr int META = ROWS * 8;        // up to 2 groups per row per chunk (Int2)
-  static constexpr int STAGE = W_BYTES + META;
-};
+// Shared-memory budget per kernel (one 512-thread CTA per SM, <= 227 KB):
+//   codes ring [warp 16][stage S][m][16 rows][128 B]   (1024-aligned: 128-byte swizzle atoms)
+//   meta ring  [warp 16][stage S][m][gq <= 4][16 rows] words
+//   red        [group 2][buf NB][warp 8][m][tok 8][row 16] floats
+//   x          [tok 8][row_gran granules of 16 B]
+//   Alloc table, tile sync words, ring mbarriers
 template <bool W13>
-struct Pipe {
-  static constexpr int STAGES = W13 ? 3 : 5;
+struct Cfg {
+  static constexpr int NM = W13 ? 2 : 1;
+  static constexpr int S = W13 ? 2 : 4;
+  static constexpr int NB = W13 ? 1 : 2;
+  static constexpr int CODES = NM * 2048;
+  static constexpr int META = NM * 256;
+  static constexpr int RED = 2 * NB * kWarps * NM * kRedTile * 4;
 };
 
-template <int BYTES>
-__device__ __forceinline__ void cp_async(uint32_t saddr, const void* g) {
-  if constexpr (BYTES == 16)
-    asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(saddr), "l"(g));
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(saddr), "l"(g), "n"(BYTES));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 r;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "r"(a));
@@ -85,6 +72,34 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t r;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(a));
   return r;
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t a, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DYMOE_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DYMOE_WAIT_%=;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma3d(uint32_t dst, const CUtensorMap* m, int x, int y, int z,
+                                      uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(z), "r"(bar) : "memory");
 }
 
 // Dequant parameters from a metadata word (bf16 scale bits << 16 | zero).
@@ -105,119 +120,82 @@ __device__ __forceinline__ DQ dq_from_meta(uint32_t w) {
   return d;
 }
 
-// Per-lane producer state: the global addresses this lane copies for the current tile at chunk
-// `warp` (j = 0).  Item j of the tile is these + j * 512 bytes (codes) / + j * GADV words (meta):
-// no per-item address arithmetic beyond one 64-bit add per copy.
-template <int BITS, int NM>
-struct Producer {
-  static constexpr int RG = Ring<NM>::ROWS / 8;               // row groups of 8 rows
-  static constexpr int CK = WT<BITS>::CHUNK_K;
-  static constexpr int GADV = kWarps * CK / DYMOE_GROUP;      // meta words per item step
-  const uint8_t* src[RG];
-  const uint32_t* msrc;
-  size_t tile_step;      // bytes between this lane's rows of tile t and t + 2
-  int mtile_step;        // meta words between ...
-  int k_lane0;           // k of this lane's granule at j = 0 (relative to the slice)
-  bool meta8;            // Int2: the chunk's two metadata words are one aligned 8-byte copy
-
-  __device__ __forceinline__ void init(const uint8_t* const (&mat)[NM],
-                                       const uint32_t* const (&meta)[NM], size_t row_bytes,
-                                       int gpr, int tile, int k0, int warp, int lane) {
-    const int gr = lane & 3;
-    const size_t kbytes = (size_t)k0 * BITS / 8 + (size_t)warp * 64 + gr * 16;
-#pragma unroll
-    for (int i = 0; i < RG; ++i) {
-      const int r = i * 8 + (lane >> 2), m = r >> 4, rr = r & 15;
-      src[i] = mat[m] + (size_t)(tile * 16 + rr) * row_bytes + kbytes;
-    }
-    tile_step = (size_t)32 * row_bytes;
-    k_lane0 = warp * CK + gr * WT<BITS>::CODES;
-    if constexpr (BITS != 16) {
-      const int r = lane < Ring<NM>::ROWS ? lane : 0, m = r >> 4, rr = r & 15;
-      msrc = meta[m] + (size_t)(tile * 16 + rr) * gpr + (k0 + warp * CK) / DYMOE_GROUP;
-      mtile_step = 32 * gpr;
-      meta8 = (((uintptr_t)msrc) & 7) == 0;   // invariant: every step is an even word count
-    }
-  }
-  __device__ __forceinline__ void next_tile() {
-#pragma unroll
-    for (int i = 0; i < RG; ++i) src[i] += tile_step;
-    if constexpr (BITS != 16) msrc += mtile_step;
-  }
-  // copy item j (chunk ci = warp + 8 j) into the stage at shared address st
-  __device__ __forceinline__ void issue(uint32_t st, int j, int ci, int nck, int kl, bool ragged,
-                                       int lane) const {
-    if (ci >= nck) return;
-    const int gr = lane & 3;
-    const uint32_t dst = st + (lane >> 2) * 64 + gr * 16;
-    if (!ragged || k_lane0 + j * kWarps * CK < kl) {
-#pragma unroll
-      for (int i = 0; i < RG; ++i) cp_async<16>(dst + i * 512, src[i] + (size_t)j * 512);
-    }
-    if constexpr (BITS != 16) {
-      if (lane < Ring<NM>::ROWS) {
-        const uint32_t* p = msrc + j * GADV;
-        const uint32_t mdst = st + Ring<NM>::W_BYTES + lane * 8;
-        if constexpr (BITS == 2) {
-          const bool both = !ragged || ci * CK + DYMOE_GROUP < kl;
-          if (both && meta8) {
-            cp_async<8>(mdst, p);
-          } else {
-            cp_async<4>(mdst, p);
-            if (both) cp_async<4>(mdst + 4, p + 1);
-          }
-        } else {
-          cp_async<4>(mdst, p);
-        }
-      }
-    }
-  }
-};
-
 // One virtual CTA: expert e, k-slice [k0, k0 + kl), tiles [t0, t1), nt tokens whose x slice is
 // staged at shared address xs (x_pos layout, row_gran granules per token).  Outputs: W13 -> bf16
-// h at out[tok * ostride + n]; W2 -> fp32 partials at out[tok * ostride + n].
+// h at out[tok * ostride + n]; W2 -> fp32 partials at out[tok * ostride + n].  seq: this warp's
+// running item count (ring slot / mbarrier parity bookkeeping across calls); returns the new one.
+//
+// Item p of a tile (p = warp + 8 j) covers the 64-byte chunks 2p and 2p + 1 of every row of the
+// tile's K slice (CK k values each); its metadata box holds the GQ groups those chunks span.
 template <bool W13, int BITS>
-__device__ __noinline__ void run_tiles(const DevExpert* __restrict__ experts, int e, int K, int k0,
-                                       int kl, int t0, int t1, int nt, void* out, int ostride,
-                                       uint32_t xs, int row_gran, float* red, uint32_t ring_base,
-                                       int* sync) {
+__device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts, int e, int k0,
+                                           int kl, int t0, int t1, int nt, void* out, int ostride,
+                                           uint32_t xs, int row_gran, float* red,
+                                           uint32_t codes_base, uint32_t meta_base,
+                                           uint32_t bar_base, int* sync, uint32_t seq) {
   using Tr = WT<BITS>;
-  constexpr int NM = W13 ? 2 : 1;
-  constexpr int S = Pipe<W13>::STAGES;
-  constexpr int STAGE = Ring<NM>::STAGE;
+  using C = Cfg<W13>;
+  constexpr int NM = C::NM;
+  constexpr int S = C::S;
   constexpr int CK = Tr::CHUNK_K;
+  constexpr int GQ = BITS == 16 ? 0 : 2 * CK / DYMOE_GROUP;   // groups per item: 1, 2, 4
+  constexpr uint32_t TX = NM * 2048 + NM * 64 * GQ;
   const int lane = threadIdx.x & 31;
-  const int grp = threadIdx.x >> 8;                 // warp group: tiles t0 + grp, +2, ...
-  const int warp = (threadIdx.x >> 5) & (kWarps - 1);  // warp within the group
+  const int wid = threadIdx.x >> 5;
+  const int grp = wid >> 3;                          // warp group: tiles t0 + grp, +2, ...
+  const int warp = wid & (kWarps - 1);               // warp within the group
   const int g = lane >> 2, c = lane & 3;
-  const DevExpert& E = experts[e];
-  const int wi = width_index(BITS);
-  const uint8_t* mat[NM];
-  const uint32_t* meta[NM];
-#pragma unroll
-  for (int m = 0; m < NM; ++m) {
-    const int mi = W13 ? m : 2;
-    if constexpr (BITS == 16) {
-      mat[m] = reinterpret_cast<const uint8_t*>(E.w[mi]);
-      meta[m] = nullptr;
-    } else {
-      mat[m] = reinterpret_cast<const uint8_t*>(E.q[wi][mi].codes);
-      meta[m] = E.q[wi][mi].meta;
-    }
-  }
-  const int nck = (kl + CK - 1) / CK;            // chunks per tile (slice)
-  const int cmax = (nck + kWarps - 1) / kWarps;  // per warp (same for all warps)
-  const bool ragged = (kl % CK) != 0;
+  const int nck = (kl + CK - 1) / CK;                // 64-byte chunks per tile row slice
+  const int npr = (nck + 1) >> 1;                    // 128-byte items per tile
+  const int cmax = (npr + kWarps - 1) / kWarps;      // per warp (same for all warps)
   const int my_tiles = (t1 - t0 - grp + 1) / 2;
   const int n_items = (my_tiles > 0 ? my_tiles : 0) * cmax;
-  if (n_items == 0) return;
-  const uint32_t ring = ring_base + (threadIdx.x >> 5) * (S * STAGE);
-  red += grp * (2 * kWarps * NM * kRedTile);
+  if (n_items == 0) return seq;
+  const uint32_t cring = codes_base + wid * (S * C::CODES);
+  const uint32_t mring = meta_base + wid * (S * C::META);
+  const uint32_t bars = bar_base + wid * (S * 8);
+  red += grp * (C::NB * kWarps * NM * kRedTile);
   sync += grp * 4;   // [arrivals buf0, arrivals buf1, generation buf0, generation buf1]
 
-  Producer<BITS, NM> pr;
-  pr.init(mat, meta, (size_t)K * BITS / 8, K / DYMOE_GROUP, t0 + grp, k0, warp, lane);
+  // lane 0 is the producer: this expert's descriptors at this width
+  const CUtensorMap* tmc[NM];
+  const CUtensorMap* tmm = nullptr;
+  if (lane == 0) {
+    const DevExpert& E = experts[e];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) {
+      const int mi = W13 ? m : 2;
+      if constexpr (BITS == 16) {
+        tmc[m] = E.tm_w[mi];
+      } else {
+        tmc[m] = E.q[width_index(BITS)][mi].tm_codes;
+      }
+    }
+    if constexpr (BITS != 16) tmm = E.q[width_index(BITS)][W13 ? 0 : 2].tm_meta;
+  }
+  const int kx0 = k0 * BITS / 8 + warp * 128;        // codes x coordinate (bytes) at j = 0
+  const int gy0 = k0 / DYMOE_GROUP + warp * GQ;      // meta group coordinate at j = 0
+  // item (tile ti, j = jj) into ring position sq
+  auto issue = [&](uint32_t sq, int ti, int jj) {
+    if (lane != 0) return;
+    const uint32_t slot = sq % S;
+    const uint32_t bar = bars + slot * 8;
+    if (warp + kWarps * jj >= npr) {   // nothing to load: complete the phase, keep parity in step
+      mbar_arrive(bar);
+      return;
+    }
+    mbar_expect_tx(bar, TX);
+    const uint32_t cs = cring + slot * C::CODES;
+#pragma unroll
+    for (int m = 0; m < NM; ++m) tma2d(cs + m * 2048, tmc[m], kx0 + jj * (kWarps * 128), ti * 16, bar);
+    if constexpr (BITS != 16) {
+      const uint32_t ms = mring + slot * C::META;
+      if constexpr (W13)
+        tma3d(ms, tmm, ti * 16, gy0 + jj * (kWarps * GQ), 0, bar);
+      else
+        tma2d(ms, tmm, ti * 16, gy0 + jj * (kWarps * GQ), bar);
+    }
+  };
 
   float acc[NM][4];
 #pragma unroll
@@ -225,91 +203,100 @@ __device__ __noinline__ void run_tiles(const DevExpert* __restrict__ experts, in
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
 
-  // producer cursor: the next item to issue is chunk warp + 8 * j_iss of the producer's tile
-  int j_iss = 0;
+  // producer cursor: the next item to issue is j_iss of tile tile_iss
+  int tile_iss = t0 + grp, j_iss = 0;
 #pragma unroll
   for (int p = 0; p < S - 1; ++p) {
-    if (p < n_items) pr.issue(ring + p * STAGE, j_iss, warp + kWarps * j_iss, nck, kl, ragged, lane);
-    cp_commit();
-    if (++j_iss == cmax) { j_iss = 0; pr.next_tile(); }
+    if (p < n_items) issue(seq + p, tile_iss, j_iss);
+    if (++j_iss == cmax) { j_iss = 0; tile_iss += 2; }
   }
 
-  // this lane's x address at chunk 0: token row g, quad position c (x_pos layout)
+  // per-lane shared-memory offsets: x (token row g, quad position c, x_pos layout); codes of
+  // row 8h + g, granule 4 sub + c, 128-byte swizzled (granule ^ row % 8); meta word of row
+  // 8h + g for the group the lane's granule falls in
   const uint32_t xlane = xs + (uint32_t)(g * row_gran + c) * 16;
+  uint32_t wofs[2], mofs[2];
+#pragma unroll
+  for (int sub = 0; sub < 2; ++sub) {
+    wofs[sub] = g * 128 + (((sub * 4 + c) ^ g) * 16);
+    const int gi = BITS == 16 ? 0 : (sub * CK + c * Tr::CODES) / DYMOE_GROUP;
+    mofs[sub] = (gi * 16 + g) * 4;
+  }
   int tile_seq = 0;
   int tile = t0 + grp, j = 0;      // consumer cursor
-  int slot = 0, slot_iss = S - 1;  // ring slots of the consumer / producer
   for (int q = 0; q < n_items; ++q) {
     // refill: item q + S - 1 goes into the slot consumed in the previous iteration
-    if (q + S - 1 < n_items)
-      pr.issue(ring + slot_iss * STAGE, j_iss, warp + kWarps * j_iss, nck, kl, ragged, lane);
-    cp_commit();
-    if (++j_iss == cmax) { j_iss = 0; pr.next_tile(); }
-    if (++slot_iss == S) slot_iss = 0;
-    const int ci = warp + kWarps * j;
-    const bool live = ci < nck;
-    // x for this chunk: beyond the slice the staged x is zero, so stale ring bytes (always
-    // finite: the ring is zeroed at kernel start and only ever holds weights) contribute nothing
-    const uint32_t xa = xlane + (uint32_t)ci * (2 * CK);
-    cp_wait<S - 1>();
-    __syncwarp();   // the stage's rows were copied by other lanes
-    const uint32_t st = ring + slot * STAGE;
-    if (live) {
-      DQ dq[NM][2];
-      if constexpr (BITS != 16) {
-        const int gi = BITS == 2 ? (c >> 1) : 0;            // group within the chunk
+    if (q + S - 1 < n_items) issue(seq + q + S - 1, tile_iss, j_iss);
+    if (++j_iss == cmax) { j_iss = 0; tile_iss += 2; }
+    const uint32_t sq = seq + q;
+    const int p = warp + kWarps * j;
+    if (p < npr) {
+      const uint32_t slot = sq % S;
+      const uint32_t cs = cring + slot * C::CODES;
+      const uint32_t ms = mring + slot * C::META;
+      mbar_wait(bars + slot * 8, (sq / S) & 1);
+#pragma unroll
+      for (int sub = 0; sub < 2; ++sub) {
+        const int ci = 2 * p + sub;
+        if (sub == 1 && ci >= nck) break;
+        // x for this chunk: beyond the slice the staged x is zero, so codes past the slice end
+        // (the next slice's, or TMA's zero fill past the row end) contribute nothing
+        const uint32_t xa = xlane + (uint32_t)ci * (2 * CK);
+        DQ dq[NM][2];
+        if constexpr (BITS != 16) {
+#pragma unroll
+          for (int m = 0; m < NM; ++m)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              dq[m][h] = dq_from_meta<BITS>(lds32(ms + m * (GQ * 64) + h * 32 + mofs[sub]));
+        }
+        uint4 w[NM][2];
 #pragma unroll
         for (int m = 0; m < NM; ++m)
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            dq[m][h] = dq_from_meta<BITS>(lds32(st + Ring<NM>::W_BYTES + (m * 16 + 8 * h + g) * 8 + gi * 4));
-      }
-      uint4 w[NM][2];
+          for (int h = 0; h < 2; ++h) w[m][h] = lds128(cs + m * 2048 + h * 1024 + wofs[sub]);
+        using X = XB<BITS>;
 #pragma unroll
-      for (int m = 0; m < NM; ++m)
+        for (int blk = 0; blk < X::NB; ++blk) {
+          uint4 xb[X::GPB];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) w[m][h] = lds128(st + (m * 16 + 8 * h + g) * 64 + c * 16);
-      using X = XB<BITS>;
+          for (int i = 0; i < X::GPB; ++i) xb[i] = lds128_const(xa + (blk * X::GPB + i) * 64);
 #pragma unroll
-      for (int blk = 0; blk < X::NB; ++blk) {
-        uint4 xb[X::GPB];
+          for (int ss = 0; ss < X::SPB; ++ss) {
+            const int s = blk * X::SPB + ss;
+            uint32_t b0, b1;
+            b_frag<BITS>(xb, ss, b0, b1);
 #pragma unroll
-        for (int i = 0; i < X::GPB; ++i) xb[i] = lds128_const(xa + (blk * X::GPB + i) * 64);
-#pragma unroll
-        for (int ss = 0; ss < X::SPB; ++ss) {
-          const int s = blk * X::SPB + ss;
-          uint32_t b0, b1;
-          b_frag<BITS>(xb, ss, b0, b1);
-#pragma unroll
-          for (int m = 0; m < NM; ++m) {
-            uint32_t glo, ghi, g8lo, g8hi;
-            a_frag<BITS>(w[m][0], dq[m][0], s, glo, ghi);
-            a_frag<BITS>(w[m][1], dq[m][1], s, g8lo, g8hi);
-            mma16816(acc[m], glo, g8lo, ghi, g8hi, b0, b1);
+            for (int m = 0; m < NM; ++m) {
+              uint32_t glo, ghi, g8lo, g8hi;
+              a_frag<BITS>(w[m][0], dq[m][0], s, glo, ghi);
+              a_frag<BITS>(w[m][1], dq[m][1], s, g8lo, g8hi);
+              mma16816(acc[m], glo, g8lo, ghi, g8hi, b0, b1);
+            }
           }
         }
       }
     }
-    __syncwarp();   // every lane is done with this stage before it is refilled
-    if (++slot == S) slot = 0;
+    __syncwarp();   // every lane is done with this stage before lane 0 refills it
     if (++j == cmax) {
-      // end of tile: partials -> red[buf][warp][m][tok][row16 (+pad)]; the LAST warp of the
-      // group to arrive (shared-memory counter) reduces in warp order and applies the
-      // epilogue -- no barrier, so warps drift up to one tile apart.  Buffer b = tile_seq & 1 is
-      // reused by tile_seq + 2 only after its reduction bumped gen[b].
+      // end of tile: partials -> red[buf][warp][m][tok][row16]; the LAST warp of the group to
+      // arrive (shared-memory counter) reduces in warp order and applies the epilogue -- no
+      // barrier, so warps drift up to NB tiles apart.  Buffer b = tile_seq % NB is reused by
+      // tile_seq + NB only after its reduction bumped gen[b].
       j = 0;
-      const int b = tile_seq & 1;
+      const int b = C::NB == 1 ? 0 : (tile_seq & 1);
+      const int gen = C::NB == 1 ? tile_seq : (tile_seq >> 1);
       if (lane == 0)
-        while (*reinterpret_cast<volatile int*>(&sync[2 + b]) != (tile_seq >> 1)) {}
+        while (*reinterpret_cast<volatile int*>(&sync[2 + b]) != gen) {}
       __syncwarp();
       float* rb = red + b * (kWarps * NM * kRedTile);
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
         float* pp = rb + (warp * NM + m) * kRedTile;
-        pp[(2 * c) * kRedStride + g] = acc[m][0];
-        pp[(2 * c + 1) * kRedStride + g] = acc[m][1];
-        pp[(2 * c) * kRedStride + g + 8] = acc[m][2];
-        pp[(2 * c + 1) * kRedStride + g + 8] = acc[m][3];
+        pp[(2 * c) * 16 + g] = acc[m][0];
+        pp[(2 * c + 1) * 16 + g] = acc[m][1];
+        pp[(2 * c) * 16 + g + 8] = acc[m][2];
+        pp[(2 * c + 1) * 16 + g + 8] = acc[m][3];
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
       }
@@ -327,7 +314,7 @@ __device__ __noinline__ void run_tiles(const DevExpert* __restrict__ experts, in
             float s0 = 0.f, s1 = 0.f;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) {
-              const float* pp = rb + (w * NM) * kRedTile + tok * kRedStride + r16;
+              const float* pp = rb + (w * NM) * kRedTile + o;
               s0 = __fadd_rn(s0, pp[0]);
               if (NM == 2) s1 = __fadd_rn(s1, pp[kRedTile]);
             }
@@ -346,14 +333,14 @@ __device__ __noinline__ void run_tiles(const DevExpert* __restrict__ experts, in
         if (lane == 0) {
           sync[b] = 0;
           __threadfence_block();
-          *reinterpret_cast<volatile int*>(&sync[2 + b]) = (tile_seq >> 1) + 1;
+          *reinterpret_cast<volatile int*>(&sync[2 + b]) = gen + 1;
         }
       }
       ++tile_seq;
       tile += 2;
     }
   }
-  cp_wait<0>();
+  return seq + n_items;
 }
 
 // x slice layout in shared memory ("x_pos"): [8 tokens][row_gran granules of 16 B].  Within each
@@ -368,27 +355,50 @@ __device__ __forceinline__ int x_logical(int pos, int xu4) {
 }
 __host__ __device__ inline int x_row_gran(int sliceK) { return (sliceK + 255) / 256 * 32 + 4; }
 
+// dynamic shared-memory carve-up (byte offsets; the base is 1024-aligned)
+template <bool W13>
+struct Smem {
+  static constexpr size_t CODES = (size_t)2 * kWarps * Cfg<W13>::S * Cfg<W13>::CODES;
+  static constexpr size_t META = (size_t)2 * kWarps * Cfg<W13>::S * Cfg<W13>::META;
+  static constexpr size_t RED = Cfg<W13>::RED;
+  static constexpr size_t BARS = (size_t)2 * kWarps * Cfg<W13>::S * 8;
+  static __host__ __device__ size_t x_off() { return CODES + META + RED; }
+  static __host__ __device__ size_t tail_off(int sliceK) {
+    return x_off() + (size_t)kMaxTok * x_row_gran(sliceK) * 16;
+  }
+  static __host__ __device__ size_t bytes(int sliceK) {
+    return tail_off(sliceK) + BARS + 8 * sizeof(int) + sizeof(Alloc);
+  }
+};
+
 template <bool W13>
 __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a, int SK, int sliceK) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  __shared__ Alloc A;
-  __shared__ int tile_sync[8];   // per warp group: arrival counters + generations (run_tiles)
-  constexpr int NM = W13 ? 2 : 1;
-  const size_t red_bytes = 2 * 2 * kWarps * NM * kRedTile * sizeof(float);  // [group][buf]
-  float* red = reinterpret_cast<float*>(smem);
-  const uint32_t ring_base = (uint32_t)__cvta_generic_to_shared(smem + red_bytes);
-  const size_t ring_bytes = (size_t)2 * kWarps * Pipe<W13>::STAGES * Ring<NM>::STAGE;
-  uint4* xs = reinterpret_cast<uint4*>(smem + red_bytes + ring_bytes);
+  extern __shared__ __align__(1024) uint8_t smem[];
+  using C = Cfg<W13>;
+  using L = Smem<W13>;
+  constexpr int NM = C::NM;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  if (sbase & 1023) __trap();   // the swizzled TMA boxes need 1024-byte alignment
+  const size_t tail = L::tail_off(sliceK);
+  uint64_t* ring_bar = reinterpret_cast<uint64_t*>(smem + tail);
+  int* tile_sync = reinterpret_cast<int*>(smem + tail + L::BARS);   // [group][4]
+  Alloc& A = *reinterpret_cast<Alloc*>(smem + tail + L::BARS + 8 * sizeof(int));
+  const uint32_t codes_base = sbase;
+  const uint32_t meta_base = sbase + (uint32_t)L::CODES;
+  float* red = reinterpret_cast<float*>(smem + L::CODES + L::META);
+  uint4* xs = reinterpret_cast<uint4*>(smem + L::x_off());
+  const uint32_t bar_base = (uint32_t)__cvta_generic_to_shared(ring_bar);
   const int K = W13 ? a.Hd : a.F;
   const int N = W13 ? a.F : a.Hd;
   const int NT = N / 16;
   const int row_gran = x_row_gran(sliceK);
-  if (threadIdx.x == 0) compute_alloc(a, gridDim.x / SK, W13, A);
-  {  // zero the weight ring once: stale stage bytes are then always finite (see run_tiles)
-    uint4* rz = reinterpret_cast<uint4*>(smem + red_bytes);
-    const int n16 = (int)(ring_bytes / 16);
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) rz[i] = make_uint4(0, 0, 0, 0);
+  // the codes ring is free until the first TMA: use it as the allocation scratch
+  if (threadIdx.x == 0) compute_alloc(a, gridDim.x / SK, W13, A, *reinterpret_cast<AllocScratch*>(smem));
+  if ((threadIdx.x & 31) == 0) {   // each warp's ring mbarriers (one arrival + tx per phase)
+    for (int i = 0; i < C::S; ++i) mbar_init(bar_base + ((threadIdx.x >> 5) * C::S + i) * 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
   }
+  uint32_t seq = 0;   // this warp's ring position
   __syncthreads();
   if (A.n_act == 0) return;
   const int V = A.units_total * SK;
@@ -413,6 +423,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
       if (be == 16) resident &= E.w[mi] != nullptr;
       else resident &= width_index(be) >= 0 && E.q[width_index(be)][mi].codes != nullptr;
     }
+    if (resident && be != 16) resident &= E.q[width_index(be)][W13 ? 0 : 2].tm_meta != nullptr;
     if (!resident) {
       if (threadIdx.x == 0 && a.status) atomicOr(a.status, (unsigned)DYMOE_STATUS_WIDTH_NOT_RESIDENT);
       for (int r = r_lo; r < r_hi; ++r)
@@ -453,8 +464,9 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
                       : (void*)(a.y_part + ((size_t)ks * a.part_rows + tok0) * a.Hd);
       const int ostride = W13 ? a.F : a.Hd;
       const uint32_t xsa = (uint32_t)__cvta_generic_to_shared(xs);
-#define DYMOE_RUN(B) run_tiles<W13, B>(a.experts, e, K, k0, kl, t0, t1, nt, out, ostride, xsa, \
-                                       row_gran, red, ring_base, tile_sync)
+#define DYMOE_RUN(B) seq = run_tiles<W13, B>(a.experts, e, k0, kl, t0, t1, nt, out, ostride, xsa, \
+                                             row_gran, red, codes_base, meta_base, bar_base,     \
+                                             tile_sync, seq)
       switch (be) {
         case 2: DYMOE_RUN(2); break;
         case 4: DYMOE_RUN(4); break;
@@ -467,11 +479,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
 }
 
 size_t smem_bytes(bool w13, int sliceK) {
-  const int NM = w13 ? 2 : 1;
-  const size_t ring = w13 ? (size_t)2 * kWarps * Pipe<true>::STAGES * Ring<2>::STAGE
-                          : (size_t)2 * kWarps * Pipe<false>::STAGES * Ring<1>::STAGE;
-  return 2 * 2 * kWarps * NM * kRedTile * sizeof(float) + ring +
-         (size_t)kMaxTok * x_row_gran(sliceK) * 16;
+  return w13 ? Smem<true>::bytes(sliceK) : Smem<false>::bytes(sliceK);
 }
 
 }  // namespace dec
@@ -498,8 +506,8 @@ cudaError_t launch_ffn_decode(const FfnArgs& a, cudaStream_t s, void* const* ev)
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // opt in to the maximum once (227 KB per block minus the static Alloc table); the
-    // per-launch size is what each launch requests
+    // opt in to the maximum once (227 KB per block); the per-launch size is what each launch
+    // requests
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa13{}, fa2{};

@@ -164,12 +164,15 @@ __device__ __forceinline__ void b_frag(const uint4 (&xb)[XB<BITS>::GPB], int ss,
   }
 }
 
-struct Alloc {
+struct Alloc {   // compact: it shares the 227 KB shared-memory budget with the rings
   int n_act;
-  int expert[DYMOE_MAX_EXPERTS];
-  int first_unit[DYMOE_MAX_EXPERTS + 1];
-  int units_total;
-  long long cost[DYMOE_MAX_EXPERTS];   // scratch
+  int units_total;                               // <= max(grid, M) < 2^16
+  uint8_t expert[DYMOE_MAX_EXPERTS];             // M <= 256
+  uint16_t first_unit[DYMOE_MAX_EXPERTS + 1];
+};
+// scratch of compute_alloc (lives in shared memory the pipeline has not started using yet)
+struct AllocScratch {
+  long long cost[DYMOE_MAX_EXPERTS];
   long long rem[DYMOE_MAX_EXPERTS];
   int u[DYMOE_MAX_EXPERTS];
 };
@@ -184,14 +187,15 @@ __device__ __forceinline__ int wcost(int b, bool w13) {
 
 // Cost-proportional allocation of `units_total` units to the active experts (largest remainder,
 // ties to the lower list index; every active expert gets >= 1 unit).  Thread 0 only.
-__device__ void compute_alloc(const FfnArgs& a, int units_grid, bool w13, Alloc& A) {
+__device__ void compute_alloc(const FfnArgs& a, int units_grid, bool w13, Alloc& A,
+                              AllocScratch& X) {
   const int n = a.active_list[0];
   A.n_act = n;
-  long long* cost = A.cost;
+  long long* cost = X.cost;
   long long total = 0;
   for (int i = 0; i < n; ++i) {
     const int e = a.active_list[1 + i];
-    A.expert[i] = e;
+    A.expert[i] = (uint8_t)e;
     const int rows = a.expert_off[e + 1] - a.expert_off[e];
     const int chunks = (rows + kMaxTok - 1) / kMaxTok;
     cost[i] = (long long)wcost(a.bits[e], w13) * chunks;
@@ -199,8 +203,8 @@ __device__ void compute_alloc(const FfnArgs& a, int units_grid, bool w13, Alloc&
   }
   const int U = units_grid > n ? units_grid : n;
   A.units_total = U;
-  int* u = A.u;
-  long long* rem = A.rem;
+  int* u = X.u;
+  long long* rem = X.rem;
   int used = 0;
   for (int i = 0; i < n; ++i) {
     const long long num = (long long)(U - n) * cost[i];   // n units reserved (one each)
@@ -218,10 +222,10 @@ __device__ void compute_alloc(const FfnArgs& a, int units_grid, bool w13, Alloc&
   }
   int acc = 0;
   for (int i = 0; i < n; ++i) {
-    A.first_unit[i] = acc;
+    A.first_unit[i] = (uint16_t)acc;
     acc += u[i];
   }
-  A.first_unit[n] = acc;
+  A.first_unit[n] = (uint16_t)acc;
 }
 
 

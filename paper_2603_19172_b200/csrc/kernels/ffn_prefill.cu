@@ -231,7 +231,7 @@ struct RawStage {
 
 template <int BE, int KPER>
 __device__ __forceinline__ void issue_raw(uint32_t raw_base, int tb, int slot, const uint8_t* rowp,
-                                          const uint32_t* metap, int khalf, int kb) {
+                                          const uint32_t* metap, int mstride, int khalf, int kb) {
   constexpr int NB = RawStage<BE, KPER>::NB;
   const size_t kbyte = ((size_t)kb * BK + khalf * KPER) * BE / 8;
   const uint32_t dst = raw_base + slot * RAW_SLOT + tb * 16;
@@ -245,7 +245,7 @@ __device__ __forceinline__ void issue_raw(uint32_t raw_base, int tb, int slot, c
   }
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(raw_base + PF * RAW_SLOT +
                                                                 (slot * kBThreads + tb) * 4),
-               "l"(metap + (kb * BK + khalf * KPER) / DYMOE_GROUP) : "memory");
+               "l"(metap + (size_t)((kb * BK + khalf * KPER) / DYMOE_GROUP) * mstride) : "memory");
 }
 template <int BE, int KPER>
 __device__ __forceinline__ void read_raw(RawStage<BE, KPER>& r, uint32_t raw_base, int tb, int slot) {
@@ -293,7 +293,7 @@ __device__ __forceinline__ void store_stage(const RawStage<BE, KPER>& r, uint32_
 }
 
 template <int BE, int KPER>
-__device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* metap, int khalf,
+__device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* metap, int mstride, int khalf,
                                         int tb, int wr, int j0, int nk, uint32_t sbase,
                                         const uint64_t* full_bar, const uint64_t* empty_bar,
                                         int& stage, uint32_t& phase) {
@@ -311,12 +311,12 @@ __device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* met
     const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;
 #pragma unroll
     for (int p = 0; p < PF - 1; ++p) {
-      if (p < nk) issue_raw<BE, KPER>(raw_base, tb, p, rowp, metap, khalf, p);
+      if (p < nk) issue_raw<BE, KPER>(raw_base, tb, p, rowp, metap, mstride, khalf, p);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     int slot = 0, slot_iss = PF - 1;
     for (int kb = 0; kb < nk; ++kb) {
-      if (kb + PF - 1 < nk) issue_raw<BE, KPER>(raw_base, tb, slot_iss, rowp, metap, khalf, kb + PF - 1);
+      if (kb + PF - 1 < nk) issue_raw<BE, KPER>(raw_base, tb, slot_iss, rowp, metap, mstride, khalf, kb + PF - 1);
       asm volatile("cp.async.commit_group;" ::: "memory");
       if (++slot_iss == PF) slot_iss = 0;
       asm volatile("cp.async.wait_group %0;" ::"n"(PF - 1) : "memory");
@@ -471,12 +471,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a) {
       const size_t row_bytes = (size_t)K * be / 8;
       const int gpr = K / DYMOE_GROUP;
       const uint8_t* rowp = codes + (size_t)row * row_bytes;
-      const uint32_t* metap = meta ? meta + (size_t)row * gpr : nullptr;
+      const uint32_t* metap = meta ? meta + row : nullptr;   // group-major: stride NWR
+      (void)gpr;
       switch (be) {
-        case 2: produce<2, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
-        case 4: produce<4, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
-        case 8: produce<8, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
-        default: produce<16, BK>(rowp, metap, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        case 2: produce<2, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        case 4: produce<4, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        case 8: produce<8, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        default: produce<16, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
       }
       // ---- epilogue: TMEM -> registers -> global
       mbar_wait(smem_u32(&tfull_bar), tphase);

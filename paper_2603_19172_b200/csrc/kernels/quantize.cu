@@ -165,22 +165,27 @@ __global__ void __launch_bounds__(256) k_quantize(const __grid_constant__ QJobs 
   }
 }
 
-// Derived dequant metadata: meta[i] = bf16bits(RNE_bf16(scales[i])) << 16 | zeros[i].
+// Derived dequant metadata, group-major: meta[g * N + n] = bf16bits(RNE_bf16(scales[n * gpr + g]))
+// << 16 | zeros[n * gpr + g].  One thread per output word (coalesced writes).
 __global__ void __launch_bounds__(256) k_build_meta(const float* __restrict__ scales,
-                                                    const uint8_t* __restrict__ zeros, size_t n,
-                                                    uint32_t* __restrict__ meta) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+                                                    const uint8_t* __restrict__ zeros, int N,
+                                                    int gpr, uint32_t* __restrict__ meta) {
+  const size_t n_all = (size_t)N * gpr;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n_all;
        i += (size_t)gridDim.x * blockDim.x) {
-    const __nv_bfloat16 sb = __float2bfloat16_rn(scales[i]);
-    meta[i] = ((uint32_t)*reinterpret_cast<const uint16_t*>(&sb) << 16) | (uint32_t)zeros[i];
+    const size_t g = i / N, n = i - g * N;
+    const size_t src = n * gpr + g;
+    const __nv_bfloat16 sb = __float2bfloat16_rn(scales[src]);
+    meta[i] = ((uint32_t)*reinterpret_cast<const uint16_t*>(&sb) << 16) | (uint32_t)zeros[src];
   }
 }
 
-cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, size_t n, uint32_t* meta,
-                              cudaStream_t s) {
+cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, int N, int gpr,
+                              uint32_t* meta, cudaStream_t s) {
+  const size_t n = (size_t)N * gpr;
   if (n == 0) return cudaSuccess;
   const size_t blocks = (n + 255) / 256 < 8192 ? (n + 255) / 256 : 8192;
-  k_build_meta<<<(unsigned)blocks, 256, 0, s>>>(scales, zeros, n, meta);
+  k_build_meta<<<(unsigned)blocks, 256, 0, s>>>(scales, zeros, N, gpr, meta);
   return cudaGetLastError();
 }
 
