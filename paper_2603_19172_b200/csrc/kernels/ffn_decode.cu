@@ -486,9 +486,9 @@ size_t smem_bytes(bool w13, int sliceK) {
 using namespace dec;
 
 int decode_w2_slice_k(int F) {
-  // K = F is split into slices so that each virtual CTA's x slice (<= 8 tokens of h) stays
-  // L1-resident: 2048 when it divides F, else the smallest multiple of 512 giving <= 4096.
-  if (F % 2048 == 0) return 2048;
+  // K = F is split into the fewest slices of <= 4096 (x slice of 8 tokens <= 64 KB of shared
+  // memory), equal up to a multiple of 512: long slices keep all 8 warps of a group busy even at
+  // Int2 (512 k per 128-byte item) and keep the fp32 partial traffic small.
   const int sk = (F + 4095) / 4096;
   const int per = (F + sk - 1) / sk;
   return (per + 511) / 512 * 512;

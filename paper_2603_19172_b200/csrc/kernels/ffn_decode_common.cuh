@@ -181,8 +181,8 @@ struct AllocScratch {
 // with every expert forced to one width (tools/decode_width_sweep.py): the narrow widths are
 // bound by dequant issue slots rather than bytes, so they cost more than their bytes suggest.
 __device__ __forceinline__ int wcost(int b, bool w13) {
-  if (w13) return b == 16 ? 256 : b == 8 ? 160 : b == 4 ? 107 : 89;
-  return b == 16 ? 256 : b == 8 ? 200 : b == 4 ? 144 : 129;
+  if (w13) return b == 16 ? 256 : b == 8 ? 174 : b == 4 ? 131 : 116;
+  return b == 16 ? 256 : b == 8 ? 139 : b == 4 ? 108 : 93;
 }
 
 // Cost-proportional allocation of `units_total` units to the active experts (largest remainder,
