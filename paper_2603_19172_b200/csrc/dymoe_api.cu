@@ -741,3 +741,12 @@ int dymoe_check_status(const dymoe_layer* L, int T, void* ws, uint32_t* bits_out
 }
 
 }  // extern "C"
+
+// TMA descriptor helper for the kernels' launchers (C++ linkage, outside the C ABI)
+bool dymoe::encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0,
+                           uint64_t d1, uint64_t stride1, uint32_t b0, uint32_t b1,
+                           CUtensorMapSwizzle swz) {
+  const uint64_t dims[2] = {d0, d1}, str[1] = {stride1};
+  const uint32_t box[2] = {b0, b1};
+  return encode(m, dt, base, 2, dims, str, box, swz);
+}

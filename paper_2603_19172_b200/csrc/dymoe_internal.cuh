@@ -82,7 +82,8 @@ struct FfnArgs {
   const int32_t* active_list;  // [M+1]: [0] = count, then expert ids
   uint16_t* h;                 // [T*k][F]
   float* y_perm;               // [T*k][Hd]   (prefill kernels)
-  float* y_part;               // [SK][part_rows][Hd] (decode kernels: W2 K-slice partials)
+  float* y_part;               // [SK][part_rows][Hd] (decode kernels: W2 K-slice partials;
+                               // prefill: scratch for the expert-ordered token rows of GEMM 1)
   int part_rows;               // row capacity of one partial slice (>= T*k)
   uint32_t* status;
 };
@@ -95,6 +96,11 @@ cudaError_t launch_reduce_parts(const float* y_part, int n_parts, int part_rows,
 // ev (nullable, 3 entries, each nullable): recorded before W13, between W13 and W2, after W2.
 cudaError_t launch_ffn_decode(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
 cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
+// 2-D tiled TMA descriptor over a row-major [d1][d0] tensor (stride1 bytes between rows), box
+// b0 x b1, CUtensorMapDataType dt, swizzle swz (host; false if the driver rejects it)
+bool encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0,
+                    uint64_t d1, uint64_t stride1, uint32_t b0, uint32_t b1,
+                    CUtensorMapSwizzle swz);
 
 inline void record_ev(void* const* ev, int i, cudaStream_t s) {
   if (ev != nullptr && ev[i] != nullptr) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);

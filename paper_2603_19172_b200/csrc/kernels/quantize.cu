@@ -13,9 +13,12 @@
 // work (two IEEE divisions, z) is amortised over 128 weights instead of 8, the min/max runs on
 // packed bf16 pairs (HMNMX2, exact), and rint(w*inv) uses the 1.5*2^23 magic add (exact
 // round-half-even for |x| < 2^22) whose bit pattern is the integer, so one IADD also adds z.
-// A warp owns 32 consecutive groups = 8 KB of contiguous input and writes its packed codes
-// contiguously; every 16-byte load hits a 32-byte sector whose other half the next load uses
-// (L1-allocating).  Jobs are padded to whole warps, so a warp never straddles two matrices.
+// A warp owns 32 consecutive groups = 8 KB of contiguous input, which it stages through its own
+// shared-memory buffer with coalesced 16-byte cp.async (each instruction covers 512 contiguous
+// bytes; rows padded to 272 B so that the per-lane 16-byte reads are bank-conflict free), double
+// buffered: the next 8 KB is in flight while the lanes quantize the current one.  Packed codes
+// are written contiguously.  Jobs are padded to whole warps, so a warp never straddles two
+// matrices; groups past a job's end are zero-filled and not stored.
 #include "../dymoe_internal.cuh"
 
 namespace dymoe {
@@ -59,13 +62,33 @@ __device__ __forceinline__ uint32_t qcode(uint32_t u, bool hi, float inv, int zb
   return (uint32_t)q;
 }
 
+constexpr int kQWarps = 4;               // warps per CTA
+constexpr int kRow = 272;                // padded bytes per staged group (256 + 16)
+constexpr int kBuf = 32 * kRow;          // one warp's 32 groups
+
+// stage the 32 groups of warp-item w (global warp index) of job J into smem buffer `buf`
+__device__ __forceinline__ void stage_groups(const QJob& J, long long w, long long first_warp,
+                                             uint32_t buf, int lane) {
+  const long long g0 = (w - first_warp) * 32;
+  const char* base = reinterpret_cast<const char*>(J.W) + g0 * 256;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int gl = 2 * j + (lane >> 4);                 // group within the warp's 32
+    const uint32_t dst = buf + gl * kRow + (lane & 15) * 16;
+    const bool ok = g0 + gl < J.n_groups;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                 "l"(base + j * 512 + lane * 16), "r"(ok ? 16 : 0) : "memory");
+  }
+}
+
 template <int BITS>
-__device__ __forceinline__ void quant_lane_group(const QJob& J, long long g) {
+__device__ __forceinline__ void quant_lane_group(const QJob& J, long long g, uint32_t row) {
   constexpr float maxq = (float)((1 << BITS) - 1);
-  const uint4* src = reinterpret_cast<const uint4*>(J.W) + g * 16;   // 128 bf16 = 16 x 16 B
   uint4 v[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __ldg(src + i);
+  for (int i = 0; i < 16; ++i)
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w) : "r"(row + i * 16));
   // packed min / max over the 64 bf16 pairs (exact), then the two halves, then 0 (GPTQ grid)
   uint32_t mn2 = v[0].x, mx2 = v[0].x;
 #pragma unroll
@@ -147,22 +170,47 @@ __device__ __forceinline__ void quant_lane_group(const QJob& J, long long g) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_quantize(const __grid_constant__ QJobs jobs) {
+__global__ void __launch_bounds__(kQWarps * 32) k_quantize(const __grid_constant__ QJobs jobs) {
+  extern __shared__ __align__(16) uint8_t qsm[];
   const int lane = threadIdx.x & 31;
+  const uint32_t buf0 = (uint32_t)__cvta_generic_to_shared(qsm) + (threadIdx.x >> 5) * (2 * kBuf);
   const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < jobs.total_warps;
-       w += nwarps) {
+  long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  auto job_of = [&](long long ww) {
     int jj = 0;
-    while (jj + 1 < jobs.n && jobs.j[jj + 1].first_warp <= w) ++jj;
+    while (jj + 1 < jobs.n && jobs.j[jj + 1].first_warp <= ww) ++jj;
+    return jj;
+  };
+  if (w >= jobs.total_warps) return;
+  int jj = job_of(w);
+  stage_groups(jobs.j[jj], w, jobs.j[jj].first_warp, buf0, lane);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  for (int it = 0; w < jobs.total_warps; w += nwarps, ++it) {
+    const uint32_t cur = buf0 + (it & 1) * kBuf;
+    // prefetch the next item into the other buffer, then wait for the current one
+    const long long wn = w + nwarps;
+    int jn = jj;
+    if (wn < jobs.total_warps) {
+      jn = job_of(wn);
+      stage_groups(jobs.j[jn], wn, jobs.j[jn].first_warp, buf0 + ((it + 1) & 1) * kBuf, lane);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
     const QJob& J = jobs.j[jj];
     const long long g = (w - J.first_warp) * 32 + lane;
-    if (g >= J.n_groups) continue;
-    switch (J.bits) {
-      case 2: quant_lane_group<2>(J, g); break;
-      case 4: quant_lane_group<4>(J, g); break;
-      default: quant_lane_group<8>(J, g); break;
+    if (g < J.n_groups) {
+      const uint32_t row = cur + lane * kRow;
+      switch (J.bits) {
+        case 2: quant_lane_group<2>(J, g, row); break;
+        case 4: quant_lane_group<4>(J, g, row); break;
+        default: quant_lane_group<8>(J, g, row); break;
+      }
     }
+    __syncwarp();   // every lane has read `cur` before it is refilled (two items later)
+    jj = jn;
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // Derived dequant metadata, group-major: meta[g * N + n] = bf16bits(RNE_bf16(scales[n * gpr + g]))
@@ -190,9 +238,13 @@ cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, int N, 
 }
 
 cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaStream_t s) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, kQWarps * 2 * kBuf);
+  }
   for (int start = 0; start < n_jobs; start += kMaxJobs) {
     QJobs J{};
     J.n = 0;
@@ -210,10 +262,10 @@ cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaSt
     }
     J.total_warps = warps;
     if (warps == 0) continue;
-    long long blocks = (warps + 7) / 8;
-    const long long cap = (long long)sms * 8;   // 8 CTAs of 256 threads per SM (grid-stride)
+    long long blocks = (warps + kQWarps - 1) / kQWarps;
+    const long long cap = (long long)sms * 3;   // 3 CTAs of 4 warps (2 x 8.5 KB each) per SM
     if (blocks > cap) blocks = cap;
-    k_quantize<<<(unsigned)blocks, 256, 0, s>>>(J);
+    k_quantize<<<(unsigned)blocks, kQWarps * 32, kQWarps * 2 * kBuf, s>>>(J);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
