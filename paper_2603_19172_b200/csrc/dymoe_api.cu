@@ -330,7 +330,8 @@ bool encode_meta(CUtensorMap* m, const void* base, uint64_t N, uint64_t gpr, int
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, base, n_mat > 1 ? 3 : 2, dims, str, box,
                 CU_TENSOR_MAP_SWIZZLE_NONE);
 }
-constexpr int kMapsPerExpert = 21;   // 3 bf16 masters + 3 widths x 3 matrices x (codes, meta)
+constexpr int kMapsPerExpert = 24;   // 3 + 3 bf16 masters (decode, prefill boxes) + 3 widths x 3
+                                     // matrices x (codes, meta)
 }  // namespace
 
 int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
@@ -417,10 +418,15 @@ int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
     const CUtensorMap* dm = L->tmap_pool + (size_t)ex * kMapsPerExpert;
     for (int m = 0; m < 3; ++m) {
       const uint64_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
-      y.tm_w[m] = nullptr;
+      y.tm_w[m] = y.tm_wp[m] = nullptr;
       if (y.w[m] != nullptr) {
         maps_ok &= encode_rows(&hm[m], y.w[m], 2 * K, N);
         y.tm_w[m] = dm + m;
+        const uint64_t dims[2] = {K, N}, str[1] = {2 * K};
+        const uint32_t box[2] = {64, 128};
+        maps_ok &= encode(&hm[21 + m], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y.w[m], 2, dims, str, box,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+        y.tm_wp[m] = dm + 21 + m;
       }
       for (int wi = 0; wi < 3; ++wi) {
         DevQMat& q = y.q[wi][m];

@@ -36,6 +36,7 @@ cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, int N, 
 struct DevExpert {
   const uint16_t* w[3];        // bf16 masters W1, W3, W2
   const CUtensorMap* tm_w[3];  // their TMA descriptors (u8 {2K, N}, 128 x 16 boxes, swizzled)
+  const CUtensorMap* tm_wp[3]; // prefill B tiles: bf16 {K, N}, 64 x 128 boxes, 128-byte swizzle
   DevQMat q[3][3];             // [width idx: int8, int4, int2][matrix: W1, W3, W2]
 };
 

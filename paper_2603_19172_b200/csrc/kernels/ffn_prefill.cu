@@ -1,5 +1,5 @@
 // Prefill expert FFN (row a6): fused-dequant grouped GEMM on the 5th-generation tensor cores
-// (tcgen05 / TMEM) for sm_100a.
+// (tcgen05 / TMEM), CTA pairs (cta_group::2), for sm_100a.
 //
 // Paper: P:203 step 4 (executor on a unified mixed-precision weight set), P:312 (Int4/Int2,
 // skip), P:354 (prefill time).  Readings D13, D17, D18, O6: A = xp·deq(W1)^T, B = xp·deq(W3)^T
@@ -8,53 +8,85 @@
 //
 // Roofline: tensor cores (a dense contraction: 2*3*Hd*F flops per routed (token, expert) pair,
 // arithmetic intensity 512-3500 flop/B).  Design:
-//  * CTA tile = 256 tokens (two M=128 UMMA accumulators) x 128 weight rows per matrix; GEMM 1
-//    stacks the W1 and W3 rows of the same output features into one N=256 B tile, so one
-//    tcgen05.mma produces gate and up side by side and SwiGLU is fused in the epilogue.
-//    TMEM: 2 x 256 fp32 columns (GEMM 1) or 2 x 128 (GEMM 2).
-//  * warp roles (11 warps): warps 0-1 gather the token rows (A, bf16) with cp.async into
-//    128B-swizzled K-major smem tiles (rows of x by perm_token for GEMM 1, rows of h for
-//    GEMM 2; rows past the expert's count are zero-filled); warps 2-9 stream the packed codes
-//    + per-group dequant words from HBM (one stage ahead, in registers), dequantize in natural
-//    k order (LOP3/PRMT magic-number extraction, HSUB2 (128+z), HMUL2 s — bit-identical to D17)
-//    and store bf16 into the swizzled B tile, then fence.proxy.async and arrive; one thread of
-//    warp 10 issues tcgen05.mma (kind::f16, bf16 x bf16 -> f32) and tcgen05.commit frees each
-//    smem stage; after the K loop warps 2-9 drain TMEM (tcgen05.ld 32x32b) for the epilogue.
-//  * 3-stage mbarrier pipeline (64 KB per stage), persistent grid of one CTA per SM walking the
-//    (expert, 256-token tile, 128-row tile) list round-robin.  Each dequantized weight tile
-//    feeds 256 tokens, so dequant costs ~2 ALU ops per 512 MMA flops.
+//  * a cluster of 2 CTAs (one TPC) computes a 256-token x 256-column tile with
+//    tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 16): CTA r holds token rows [128r, 128r+128)
+//    of A and B rows [128r, 128r+128) of the tile in its own shared memory, and its TMEM holds
+//    its 128 token rows x all 256 columns.  GEMM 1: B rows 0-127 = W1 rows n0.., 128-255 = the
+//    same W3 rows, so each CTA sees gate and up side by side (SwiGLU in its epilogue); GEMM 2:
+//    256 consecutive W2 rows.  Each CTA reads only its halves of A and B from shared memory
+//    (the pair exchanges operands in the tensor core), halving shared-memory traffic per flop
+//    against one CTA computing the same tile with two M = 128 MMAs.
+//  * warp roles per CTA (14 warps): warp 0 issues the A-tile TMA (128 expert-ordered token rows
+//    x 64 k, 128-byte swizzled; BF16 experts: the B tile too); warp 1 allocates TMEM (both CTAs)
+//    and, in the leader CTA only, one thread issues the MMAs and tcgen05.commit (multicast to
+//    both CTAs' barriers); warps 2-9 dequantize (two threads per B row, 32 k each per stage;
+//    packed codes + dequant word streamed 8 stages ahead by per-thread cp.async into a private
+//    smem ring; natural-k-order LOP3/PRMT extraction; HSUB2/HMUL2 = D17; st.shared into the
+//    swizzled tile; fence.proxy.async; release-arrive on the leader's barrier); warps 10-13 drain
+//    TMEM for the epilogue.  TMEM holds two 256-column accumulators, so the epilogue of tile i
+//    overlaps the main loop of tile i + 1.
+//  * 4-stage pipeline of 32 KB per CTA (A 16 KB + B 16 KB); the leader's full barrier collects
+//    both CTAs' TMA bytes (cta_group::2 TMA signals the leader) and both CTAs' producer arrivals.
+//  * persistent grid: CTA pair c walks the (expert, 256-token tile, 256-column tile) list with
+//    stride (number of pairs).
 #include "../dymoe_internal.cuh"
 
 namespace dymoe {
 namespace pf {
 
-constexpr int BM = 128;           // UMMA M (tokens per accumulator)
-constexpr int MT = 2;             // accumulators per CTA tile -> 256 tokens
-constexpr int TOK = BM * MT;
-constexpr int BN = 128;           // weight rows per matrix per tile
-constexpr int BK = 32;            // k per stage (one 64-byte swizzle atom row)
+constexpr int BM = 128;           // token rows per CTA (UMMA M = 2 * BM across the pair)
+constexpr int TOK = 2 * BM;       // tokens per pair tile
+constexpr int BNH = 128;          // B rows per CTA (UMMA N = 2 * BNH)
+constexpr int NCOL = 2 * BNH;     // TMEM columns per accumulator
+constexpr int BK = 64;            // k per stage (one 128-byte swizzle atom row)
 constexpr int ROWB = BK * 2;      // bytes per tile row (K-major)
-constexpr int CPR = BK / 8;       // 16-byte chunks per tile row
+constexpr int KPER = BK / 2;      // k per B-producer thread per stage (two threads per row)
 constexpr int STAGES = 4;
-constexpr int A_BYTES = TOK * BK * 2;          // 16 KB
-constexpr int B_BYTES_MAX = 2 * BN * BK * 2;   // 16 KB (GEMM 1: W1 + W3 rows)
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES_MAX;
-constexpr int kAWarps = 1, kBWarps = 8;   // warp 0: one thread issues the A-tile TMA loads
-constexpr int kMmaWarp = kAWarps + kBWarps;
-constexpr int kThreads = (kMmaWarp + 1) * 32;   // 352
-constexpr int kAThreads = kAWarps * 32, kBThreads = kBWarps * 32;
-constexpr int kSmemRaw = 8 * (kBWarps * 32 * 16) * 2 + 8 * (kBWarps * 32) * 4;   // B producer ring
-constexpr int kSmem = STAGES * STAGE_BYTES + kSmemRaw + 1024;   // + alignment slack
+constexpr int A_BYTES = BM * BK * 2;            // 16 KB
+constexpr int B_BYTES = BNH * BK * 2;           // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int kBWarps = 8, kEpiWarps = 4;
+constexpr int kBWarp0 = 2, kEpiWarp0 = kBWarp0 + kBWarps;
+constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;   // 448
+constexpr int kBThreads = kBWarps * 32;
+constexpr int PF = 8;                                   // raw stages in flight per thread
+constexpr int RAW_CHUNK = kBThreads * 16;               // one 16-byte granule per thread
+constexpr int RAW_SLOT = ((KPER + 15) / 16) * RAW_CHUNK;  // Int8: KPER bytes per thread per stage
+constexpr int RAW_BYTES = PF * RAW_SLOT + PF * kBThreads * 4;   // + dequant words
+constexpr int kSmem = STAGES * STAGE_BYTES + RAW_BYTES + 1024;   // + alignment slack
+constexpr uint32_t TMEM_COLS = 2 * NCOL;                // two accumulators
 
 // ---------------------------------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
 }
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
+// arrive on a barrier given by its shared::cluster address (default .release.cta semantics: the
+// data the arrival publishes is consumed by the tensor core through the async proxy, which the
+// producers' fence.proxy.async already covers -- cluster-scope release / acquire would cost an
+// MEMBAR per arrive and an L1 invalidate per poll)
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_cl(uint32_t bar_cl, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cl), "r"(tx)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -63,20 +95,12 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void cp_async_zfill(uint32_t saddr, const void* g, uint32_t src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr), "l"(g), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, int x, int y, uint32_t bar) {
+// 2-D TMA load into this CTA's shared memory, completion signalled on the leader's barrier
+__device__ __forceinline__ void tma2d_pair(uint32_t dst, const CUtensorMap* m, int x, int y,
+                                           uint32_t bar_cl) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar_cl) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -87,15 +111,17 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
+// commit this thread's prior MMAs to the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      ::"r"(bar), "h"((uint16_t)0x3) : "memory");
 }
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                       uint32_t idesc, uint32_t accumulate) {
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                            uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -115,26 +141,23 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// UMMA shared-memory descriptor: K-major, ROWB-byte swizzle (64 B: SWIZZLE_64B, 128 B:
-// SWIZZLE_128B), 8-row atoms 8 * ROWB bytes apart.
+// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);        // start address
   d |= (uint64_t)1u << 16;                        // leading byte offset (unused when swizzled)
   d |= (uint64_t)((8u * ROWB) >> 4) << 32;        // stride byte offset: 8 rows
   d |= (uint64_t)1u << 46;                        // descriptor version (sm_100)
-  d |= (uint64_t)(ROWB == 128 ? 2u : 4u) << 61;   // layout: SWIZZLE_128B / SWIZZLE_64B
+  d |= (uint64_t)2u << 61;                        // layout: SWIZZLE_128B
   return d;
 }
 // Instruction descriptor, kind::f16: bf16 A/B, f32 D, both K-major.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-// byte offset of 16-byte chunk j (k = 8j..8j+7) of row r inside a swizzled K-major tile: the
-// chunk index is XOR-ed with address bits [7, 7 + log2(CPR)) of the row start
+// byte offset of 16-byte chunk j (k = 8j..8j+7) of row r inside a 128B-swizzled K-major tile
 __device__ __forceinline__ uint32_t sw_off(int r, int j) {
-  if constexpr (ROWB == 128) return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
-  else return (uint32_t)(r * 64 + ((j ^ ((r >> 1) & 3)) << 4));
+  return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4));
 }
 
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -223,19 +246,14 @@ __device__ __forceinline__ uint32_t deq_int8_pair(uint32_t w, int i, const DQP& 
 }
 
 // ---------------------------------------------------------------------------------------- B producer
-// One thread = one weight row (GEMM 1) or half a row (GEMM 2) of every stage.  Quantized widths:
-// each thread streams its packed bytes (+ the group's dequant word) PF stages ahead with
-// cp.async into a private shared-memory ring ([slot][chunk][thread] 16-byte granules: conflict-
-// free), so no global load is outstanding in registers when the thread fences and arrives; it
-// then dequantizes in natural k order and stores into the 128B-swizzled B tile.
-// BF16 masters: cp.async straight into the tile (arrival on completion).
-constexpr int PF = 8;                                   // raw stages in flight per thread
-constexpr int RAW_CHUNK = kBThreads * 16;               // one 16-byte granule per thread
-constexpr int RAW_SLOT = ((BK + 15) / 16) * RAW_CHUNK;  // Int8: BK bytes per thread per stage
-static_assert(PF * RAW_SLOT + PF * kBThreads * 4 == kSmemRaw, "raw ring size");
-constexpr int RAW_BYTES = PF * RAW_SLOT + PF * kBThreads * 4;   // + dequant words
-
-template <int BE, int KPER>
+// Two threads per B row (k halves of 32), every stage.  Each thread streams its packed bytes
+// (+ the group's dequant word) PF stages ahead with cp.async into a private shared-memory ring
+// ([slot][chunk][thread] 16-byte granules: conflict-free), so no global load is outstanding in
+// registers when the thread fences and arrives; it then dequantizes in natural k order and stores
+// into the 128B-swizzled B tile, fences (generic -> async proxy) and release-arrives on the
+// leader's full barrier.  BF16 experts: the B tile comes by TMA (warp 0); the producers only
+// arrive, to keep the barrier's count.
+template <int BE>
 struct RawStage {
   static constexpr int NB = KPER * BE / 8;        // bytes per thread per stage
   static constexpr int NV = (NB + 15) / 16;
@@ -243,17 +261,17 @@ struct RawStage {
   uint32_t m;
 };
 
-template <int BE, int KPER>
+template <int BE>
 __device__ __forceinline__ void issue_raw(uint32_t raw_base, int tb, int slot, const uint8_t* rowp,
                                           const uint32_t* metap, int mstride, int khalf, int kb) {
-  constexpr int NB = RawStage<BE, KPER>::NB;
+  constexpr int NB = RawStage<BE>::NB;
   const size_t kbyte = ((size_t)kb * BK + khalf * KPER) * BE / 8;
   const uint32_t dst = raw_base + slot * RAW_SLOT + tb * 16;
   if constexpr (NB == 8) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(rowp + kbyte) : "memory");
   } else {
 #pragma unroll
-    for (int i = 0; i < RawStage<BE, KPER>::NV; ++i)
+    for (int i = 0; i < RawStage<BE>::NV; ++i)
       asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst + i * RAW_CHUNK),
                    "l"(rowp + kbyte + 16 * i) : "memory");
   }
@@ -261,19 +279,19 @@ __device__ __forceinline__ void issue_raw(uint32_t raw_base, int tb, int slot, c
                                                                 (slot * kBThreads + tb) * 4),
                "l"(metap + (size_t)((kb * BK + khalf * KPER) / DYMOE_GROUP) * mstride) : "memory");
 }
-template <int BE, int KPER>
-__device__ __forceinline__ void read_raw(RawStage<BE, KPER>& r, uint32_t raw_base, int tb, int slot) {
+template <int BE>
+__device__ __forceinline__ void read_raw(RawStage<BE>& r, uint32_t raw_base, int tb, int slot) {
   const uint32_t src = raw_base + slot * RAW_SLOT + tb * 16;
 #pragma unroll
-  for (int i = 0; i < RawStage<BE, KPER>::NV; ++i)
+  for (int i = 0; i < RawStage<BE>::NV; ++i)
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.v[i].x), "=r"(r.v[i].y), "=r"(r.v[i].z), "=r"(r.v[i].w)
                  : "r"(src + i * RAW_CHUNK));
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r.m) : "r"(raw_base + PF * RAW_SLOT + (slot * kBThreads + tb) * 4));
 }
 
-template <int BE, int KPER>
-__device__ __forceinline__ void store_stage(const RawStage<BE, KPER>& r, uint32_t dst, int wr, int j0) {
+template <int BE>
+__device__ __forceinline__ void store_stage(const RawStage<BE>& r, uint32_t dst, int wr, int j0) {
   const DQP d = dqp_from_meta(r.m);
   if constexpr (BE == 4) {
 #pragma unroll
@@ -306,41 +324,41 @@ __device__ __forceinline__ void store_stage(const RawStage<BE, KPER>& r, uint32_
   }
 }
 
-template <int BE, int KPER>
-__device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* metap, int mstride, int khalf,
-                                        int tb, int wr, int j0, int nk, uint32_t sbase,
-                                        const uint64_t* full_bar, const uint64_t* empty_bar,
-                                        int& stage, uint32_t& phase) {
+// full_cl: shared::cluster address of the leader's full_bar[0] (stage s at + 8 s)
+template <int BE>
+__device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* metap, int mstride,
+                                        int khalf, int tb, int wr, int nk, uint32_t sbase,
+                                        uint32_t full_cl, uint32_t empty_bar, int& stage,
+                                        uint32_t& phase) {
+  const int j0 = khalf * (KPER / 8);
   if constexpr (BE == 16) {
     for (int kb = 0; kb < nk; ++kb) {
-      mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-      const uint32_t dst = sbase + stage * STAGE_BYTES + A_BYTES;
-      const uint8_t* src = rowp + ((size_t)kb * BK + khalf * KPER) * 2;
-#pragma unroll
-      for (int i = 0; i < KPER / 8; ++i) cp_async_zfill(dst + sw_off(wr, j0 + i), src + 16 * i, 16u);
-      cp_async_arrive_noinc(smem_u32(&full_bar[stage]));
+      mbar_wait(empty_bar + stage * 8, phase ^ 1);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive_cl(full_cl + stage * 8);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
   } else {
     const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;
 #pragma unroll
     for (int p = 0; p < PF - 1; ++p) {
-      if (p < nk) issue_raw<BE, KPER>(raw_base, tb, p, rowp, metap, mstride, khalf, p);
+      if (p < nk) issue_raw<BE>(raw_base, tb, p, rowp, metap, mstride, khalf, p);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     int slot = 0, slot_iss = PF - 1;
     for (int kb = 0; kb < nk; ++kb) {
-      if (kb + PF - 1 < nk) issue_raw<BE, KPER>(raw_base, tb, slot_iss, rowp, metap, mstride, khalf, kb + PF - 1);
+      if (kb + PF - 1 < nk) issue_raw<BE>(raw_base, tb, slot_iss, rowp, metap, mstride, khalf, kb + PF - 1);
       asm volatile("cp.async.commit_group;" ::: "memory");
       if (++slot_iss == PF) slot_iss = 0;
       asm volatile("cp.async.wait_group %0;" ::"n"(PF - 1) : "memory");
-      RawStage<BE, KPER> r;
-      read_raw<BE, KPER>(r, raw_base, tb, slot);
+      RawStage<BE> r;
+      read_raw<BE>(r, raw_base, tb, slot);
       if (++slot == PF) slot = 0;
-      mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-      store_stage<BE, KPER>(r, sbase + stage * STAGE_BYTES + A_BYTES, wr, j0);
+      mbar_wait(empty_bar + stage * 8, phase ^ 1);
+      store_stage<BE>(r, sbase + stage * STAGE_BYTES + A_BYTES, wr, j0);
       fence_proxy_async();
-      mbar_arrive(smem_u32(&full_bar[stage]));
+      __syncwarp();   // one release-arrive per warp (the whole warp's writes are fenced)
+      if ((threadIdx.x & 31) == 0) mbar_arrive_cl(full_cl + stage * 8);
       if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -354,7 +372,7 @@ struct Sched {
   int first[DYMOE_MAX_EXPERTS + 1];        // prefix of tiles per expert
 };
 struct Tile {
-  int e, m0, n0, rows;   // expert, first token row (relative), first weight row, valid tokens
+  int e, m0, n0, rows;   // expert, first token row (relative), first output column, valid tokens
 };
 __device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t, int ntiles_n,
                                         int nstep) {
@@ -372,29 +390,30 @@ __device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t,
 }
 
 template <bool W13>
-__global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a,
-                                                               const __grid_constant__ CUtensorMap tmA) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Sched S;
-  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar, tempty_bar;
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int n_tiles_sh;
-  // B tile = 256 weight rows in both GEMMs: GEMM 1 = 128 W1 + the same 128 W3 rows, GEMM 2 =
-  // 256 W2 rows (so every A stage feeds 256 output columns per accumulator).
-  constexpr int NCOL = 2 * BN;                        // TMEM columns per accumulator
-  constexpr uint32_t TMEM_COLS = MT * NCOL <= 256 ? 256 : 512;
-  constexpr uint32_t IDESC = make_idesc(BM, NCOL);
+  constexpr uint32_t IDESC = make_idesc(2 * BM, NCOL);
   const int K = W13 ? a.Hd : a.F;
   const int NWR = W13 ? a.F : a.Hd;                  // weight rows per matrix
-  const int nstep = W13 ? BN : 2 * BN;               // output features per tile
+  const int nstep = W13 ? BNH : NCOL;                // output features per tile
   const int ntiles_n = (NWR + nstep - 1) / nstep;
   const int nk = K / BK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
 
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sbase = smem_u32(smem);
   auto sA = [&](int s) { return sbase + s * STAGE_BYTES; };
   auto sB = [&](int s) { return sbase + s * STAGE_BYTES + A_BYTES; };
+  const uint32_t full0 = smem_u32(&full_bar[0]), empty0 = smem_u32(&empty_bar[0]);
+  const uint32_t full_cl = mapa(full0, 0);                     // the leader's full barriers
+  const uint32_t tempty_cl = mapa(smem_u32(&tempty_bar[0]), 0);
 
   if (threadIdx.x == 0) {
     const int n = a.active_list[0];
@@ -412,106 +431,140 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a,
     S.n = na;
     n_tiles_sh = acc;
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&full_bar[s]), 1 + kBThreads);   // A: expect_tx arrive; B: producers
+      mbar_init(smem_u32(&full_bar[s]), 2 + 2 * kBWarps);   // leader's: both CTAs arrive
       mbar_init(smem_u32(&empty_bar[s]), 1);
     }
-    mbar_init(smem_u32(&tfull_bar), 1);
-    mbar_init(smem_u32(&tempty_bar), kBThreads);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull_bar[b]), 1);
+      mbar_init(smem_u32(&tempty_bar[b]), 2 * kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base_sh)),
                  "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();   // barriers of both CTAs initialised, TMEM allocated in both
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const int n_tiles = n_tiles_sh;
 
-  if (warp < kAWarps) {
-    // ------------------------------------------------------------------ A producer (tokens)
-    // One thread: the A tile of every stage is one TMA box of 256 expert-ordered token rows x BK
-    // (GEMM 1: the rows gathered by perm_token beforehand; GEMM 2: rows of h), 64-byte swizzled
-    // exactly as the UMMA descriptor expects.  Rows past the expert's count hold the next
-    // expert's tokens (or TMA zero fill): their accumulator rows are never stored.
+  if (warp == 0) {
+    // ------------------------------------------------------------------ A (and BF16 B) TMA
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = pair; t < n_tiles; t += npairs) {
         const Tile T = tile_at(S, a, t, ntiles_n, nstep);
-        const int row0 = a.expert_off[T.e] + T.m0;
+        const int row0 = a.expert_off[T.e] + T.m0 + (int)rank * BM;
+        const bool bf = a.bits[T.e] == 16;
+        const CUtensorMap* tmB = nullptr;
+        int brow0 = 0;
+        if (bf) {
+          const DevExpert& E = a.experts[T.e];
+          tmB = E.tm_wp[W13 ? (int)rank : 2];
+          brow0 = T.n0 + (W13 ? 0 : (int)rank * BNH);
+        }
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
-          mbar_expect_tx(smem_u32(&full_bar[stage]), A_BYTES);
-          tma2d(sA(stage), &tmA, kb * BK, row0, smem_u32(&full_bar[stage]));
+          mbar_wait(empty0 + stage * 8, phase ^ 1);
+          mbar_expect_tx_cl(full_cl + stage * 8, A_BYTES + (bf ? B_BYTES : 0));
+          tma2d_pair(sA(stage), &tmA, kb * BK, row0, full_cl + stage * 8);
+          if (bf) tma2d_pair(sB(stage), tmB, kb * BK, brow0, full_cl + stage * 8);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp < kMmaWarp) {
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (leader)
+    if (rank == 0 && lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int i = 0;
+      for (int t = pair; t < n_tiles; t += npairs, ++i) {
+        const int b = i & 1;
+        mbar_wait(smem_u32(&tempty_bar[b]), ((i >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full0 + stage * 8, phase);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk)
+            tc_mma_pair(tmem + b * NCOL, sw_desc(sA(stage) + kk * 32), sw_desc(sB(stage) + kk * 32),
+                        IDESC, (kb | kk) != 0);
+          tc_commit_pair(empty0 + stage * 8);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_pair(smem_u32(&tfull_bar[b]));
+      }
+    }
+  } else if (warp < kEpiWarp0) {
     // ------------------------------------------------------------------ B producer (dequant)
-    const int tb = threadIdx.x - kAThreads;   // 0..255
+    const int tb = threadIdx.x - kBWarp0 * 32;   // 0..255
+    const int wr = tb & (BNH - 1);                // B row within this CTA's half
+    const int khalf = tb >> 7;
     int stage = 0;
-    uint32_t phase = 0, tphase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    uint32_t phase = 0;
+    for (int t = pair; t < n_tiles; t += npairs) {
       const Tile T = tile_at(S, a, t, ntiles_n, nstep);
       const int be = a.bits[T.e];
       const DevExpert& E = a.experts[T.e];
-      // this thread's weight row (GEMM 1: 0-127 W1, 128-255 W3 of the same features; GEMM 2:
-      // 256 consecutive W2 rows, clamped at the end of the matrix -- those outputs are dropped)
-      const int wr = tb;
-      const int mi = W13 ? (wr >= BN ? 1 : 0) : 2;
-      const int row = min(T.n0 + (W13 ? (wr & (BN - 1)) : wr), NWR - 1);
+      // GEMM 1: rank 0 = W1 rows n0.., rank 1 = the same W3 rows; GEMM 2: W2 rows
+      // n0 + 128 rank + wr, clamped at the end of the matrix (those outputs are dropped)
+      const int mi = W13 ? (int)rank : 2;
+      const int row = min(T.n0 + (W13 ? 0 : (int)rank * BNH) + wr, NWR - 1);
       const int wi = width_index(be);
       const uint8_t* codes = be == 16 ? reinterpret_cast<const uint8_t*>(E.w[mi])
                                       : reinterpret_cast<const uint8_t*>(E.q[wi][mi].codes);
       const uint32_t* meta = be == 16 ? nullptr : E.q[wi][mi].meta;
       const size_t row_bytes = (size_t)K * be / 8;
-      const int gpr = K / DYMOE_GROUP;
       const uint8_t* rowp = codes + (size_t)row * row_bytes;
       const uint32_t* metap = meta ? meta + row : nullptr;   // group-major: stride NWR
-      (void)gpr;
       switch (be) {
-        case 2: produce<2, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
-        case 4: produce<4, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
-        case 8: produce<8, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
-        default: produce<16, BK>(rowp, metap, NWR, 0, tb, wr, 0, nk, sbase, full_bar, empty_bar, stage, phase); break;
+        case 2: produce<2>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
+        case 4: produce<4>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
+        case 8: produce<8>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
+        default: produce<16>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
       }
-      // ---- epilogue: TMEM -> registers -> global
-      mbar_wait(smem_u32(&tfull_bar), tphase);
-      tphase ^= 1;
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (TMEM -> global)
+    const int q = warp & 3;                       // TMEM lane quarter this warp may access
+    const int trow = q * 32 + lane;               // token row within this CTA's half
+    int i = 0;
+    for (int t = pair; t < n_tiles; t += npairs, ++i) {
+      const Tile T = tile_at(S, a, t, ntiles_n, nstep);
+      const int b = i & 1;
+      mbar_wait(smem_u32(&tfull_bar[b]), (i >> 1) & 1);
       tc_fence_after();
-      const int q = warp & 3;                         // TMEM lane quarter this warp may access
-      const int mt = (warp - kAWarps) >> 2;           // accumulator (token half) of this warp
-      const int trow = mt * BM + q * 32 + lane;       // token row within the tile
-      const size_t grow = (size_t)(a.expert_off[T.e] + T.m0 + trow);
-      const bool live = trow < T.rows;
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * NCOL);
+      const int mrow = (int)rank * BM + trow;     // row within the pair tile
+      const size_t grow = (size_t)(a.expert_off[T.e] + T.m0 + mrow);
+      const bool live = mrow < T.rows;
+      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NCOL);
 #pragma unroll 1
-      for (int cc = 0; cc < (W13 ? BN : 2 * BN) / 32; ++cc) {
+      for (int cc = 0; cc < (W13 ? BNH : NCOL) / 32; ++cc) {
         if (W13) {
           uint32_t g[32], u[32];
           tmem_ld32(tbase + cc * 32, g);
-          tmem_ld32(tbase + BN + cc * 32, u);
+          tmem_ld32(tbase + BNH + cc * 32, u);
           tmem_ld_wait();
           if (live) {
             uint32_t hv[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int j = 0; j < 16; ++j) {
               float h2[2];
 #pragma unroll
               for (int k2 = 0; k2 < 2; ++k2) {
-                const float A = __uint_as_float(g[2 * i + k2]), B = __uint_as_float(u[2 * i + k2]);
+                const float A = __uint_as_float(g[2 * j + k2]), B = __uint_as_float(u[2 * j + k2]);
                 h2[k2] = __fmul_rn(__fdividef(A, 1.f + __expf(-A)), B);   // fast silu (fp32)
               }
-              hv[i] = pack_bf2(h2[0], h2[1]);
+              hv[j] = pack_bf2(h2[0], h2[1]);
             }
             uint4* dstp = reinterpret_cast<uint4*>(a.h + grow * a.F + T.n0 + cc * 32);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) dstp[i] = make_uint4(hv[4 * i], hv[4 * i + 1], hv[4 * i + 2], hv[4 * i + 3]);
+            for (int j = 0; j < 4; ++j) dstp[j] = make_uint4(hv[4 * j], hv[4 * j + 1], hv[4 * j + 2], hv[4 * j + 3]);
           }
         } else {
           uint32_t v[32];
@@ -520,47 +573,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_prefill_gemm(const FfnArgs a,
           if (live && T.n0 + cc * 32 < NWR) {   // last W2 tile may overhang Hd (clamped rows)
             uint4* dstp = reinterpret_cast<uint4*>(a.y_perm + grow * a.Hd + T.n0 + cc * 32);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) dstp[i] = make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            for (int j = 0; j < 8; ++j) dstp[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           }
         }
       }
       tc_fence_before();
-      mbar_arrive(smem_u32(&tempty_bar));
-    }
-  } else {
-    // ------------------------------------------------------------------ MMA issuer (1 thread)
-    int stage = 0;
-    uint32_t phase = 0, tphase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      if (lane == 0) {
-        mbar_wait(smem_u32(&tempty_bar), tphase ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(smem_u32(&full_bar[stage]), phase);
-          fence_proxy_async();   // A arrived through cp.async (generic proxy) -> tensor core reads
-          tc_fence_after();
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int kk = 0; kk < BK / 16; ++kk) {
-              const uint64_t ad = sw_desc(sA(stage) + mt * (BM * ROWB) + kk * 32);
-              const uint64_t bd = sw_desc(sB(stage) + kk * 32);
-              tc_mma(tmem + mt * NCOL, ad, bd, IDESC, (kb | kk) != 0);
-            }
-          tc_commit(smem_u32(&empty_bar[stage]));
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        tc_commit(smem_u32(&tfull_bar));
-      }
       __syncwarp();
-      tphase ^= 1;
+      if (lane == 0) mbar_arrive_cl(tempty_cl + b * 8);
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
+  cluster_sync();   // both CTAs done (the peer's TMEM and smem are no longer touched)
+  if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
@@ -582,7 +608,7 @@ __global__ void __launch_bounds__(256) k_gather_perm(const uint4* __restrict__ x
 
 cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev) {
   using namespace pf;
-  if (a.Hd % BN || a.F % BN || a.Hd % BK || a.F % BK) return cudaErrorInvalidValue;
+  if (a.Hd % BNH || a.F % BNH || a.Hd % BK || a.F % BK) return cudaErrorInvalidValue;
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -595,9 +621,9 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
   uint16_t* xp = reinterpret_cast<uint16_t*>(a.y_part);   // scratch: [T*k][Hd] bf16
   CUtensorMap tm13, tm2;
   if (!encode_tmap_2d(&tm13, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xp, a.Hd, rows, (uint64_t)a.Hd * 2,
-                      BK, TOK, CU_TENSOR_MAP_SWIZZLE_64B) ||
+                      BK, BM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !encode_tmap_2d(&tm2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.h, a.F, rows, (uint64_t)a.F * 2,
-                      BK, TOK, CU_TENSOR_MAP_SWIZZLE_64B))
+                      BK, BM, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   record_ev(ev, 0, s);
   {
@@ -607,11 +633,12 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
     k_gather_perm<<<blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(a.x), vpr, a.perm_token,
                                          a.expert_off + a.M, rows, reinterpret_cast<uint4*>(xp));
   }
-  k_prefill_gemm<true><<<sms, kThreads, kSmem, s>>>(a, tm13);
+  const int grid = sms / 2 * 2;   // whole CTA pairs, one CTA per SM
+  k_prefill_gemm<true><<<grid, kThreads, kSmem, s>>>(a, tm13);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   record_ev(ev, 1, s);
-  k_prefill_gemm<false><<<sms, kThreads, kSmem, s>>>(a, tm2);
+  k_prefill_gemm<false><<<grid, kThreads, kSmem, s>>>(a, tm2);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   record_ev(ev, 2, s);
