@@ -298,7 +298,8 @@ def run_ours(args, rank, world, device):
                     "algorithmic_flops_per_step": fl / K, "hbm_GBs_ffn": achieved_ffn}
     res = None
     if rank == 0:
-        launches_per_step = 7
+        # route, score, assign, permute, [prefill: gather into expert order], W13, W2, combine
+        launches_per_step = 7 if phase == d.DYMOE_DECODE else 8
         res = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -336,7 +337,7 @@ def run_ep(args, rank, world, device):
     T = args.batch if args.workload == "decode" else args.tokens
     cfg = base.with_tokens(T)
     phase = d.DYMOE_DECODE if args.workload == "decode" else d.DYMOE_PREFILL
-    comm = ep.TorchComm()
+    comm = ep.TorchComm(stage_cpu=torch.distributed.get_backend() != "nccl")
 
     class TimedOps(ep.CudaOps):
         """CudaOps recording CUDA events around the local expert FFN (roofline numerator)."""
@@ -391,13 +392,65 @@ def run_ep(args, rank, world, device):
         torch.cuda.synchronize()
     torch.distributed.barrier()
     ms = t0.elapsed_time(t1)
-    tt = torch.tensor([ms], device=device)
-    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-    ms = float(tt.item())
+    ms = _max_over_ranks(ms, device)
     value = T * K * world / (ms / 1e3)
+    ffn_events = list(ops.events)
+
+    # ---------------- end-to-end: per step the rank's inputs come from pinned host memory and
+    # its output goes back to the host, inside the timed region
+    hx = [inp[0].cpu().pin_memory() for inp in inputs]
+    hl = [inp[1].cpu().pin_memory() for inp in inputs]
+    ha = [inp[2].cpu().pin_memory() for inp in inputs]
+    dx, dl, da = (torch.empty_like(t) for t in inputs[0])
+    hy = torch.empty(T, cfg.hidden, dtype=torch.float32).pin_memory()
+    h2d = hx[0].numel() * 2 + hl[0].numel() * 4 + (ha[0].numel() * 4 if phase == d.DYMOE_PREFILL else 0)
+    d2h = hy.numel() * 4
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    for i in range(K):
+        j = (args.warmup + i) % n_inputs
+        dx.copy_(hx[j], non_blocking=True)
+        dl.copy_(hl[j], non_blocking=True)
+        if phase == d.DYMOE_PREFILL:
+            da.copy_(ha[j], non_blocking=True)
+        y, _ = shards[(args.warmup + i) % len(shards)].forward(
+            dx, dl, ladder, (args.warmup + i) % NUM_LAYERS, NUM_LAYERS, phase, attn_mass=da)
+        hy.copy_(y, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    torch.distributed.barrier()
+    e2e = {"value": T * K * world / (_max_over_ranks(e0.elapsed_time(e1), device) / 1e3), "unit": "tokens/s",
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---------------- decode, batch replicated on every rank (SURVEY §8e latency variant):
+    # the same B tokens everywhere, local experts, one all-reduce of y; strong scaling of one batch
+    rep = None
+    if phase == d.DYMOE_DECODE:
+        xr, lgr, _ = inputs[0]
+        _broadcast(xr)
+        _broadcast(lgr)
+        for i in range(args.warmup):
+            shards[i % len(shards)].forward_replicated(xr, lgr, ladder, i % NUM_LAYERS, NUM_LAYERS)
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        r0.record()
+        for i in range(K):
+            shards[(args.warmup + i) % len(shards)].forward_replicated(
+                xr, lgr, ladder, (args.warmup + i) % NUM_LAYERS, NUM_LAYERS)
+        r1.record()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        rms = _max_over_ranks(r0.elapsed_time(r1), device)
+        rep = {"value": T * K / (rms / 1e3), "unit": "tokens/s", "ms_per_step": rms / K,
+               "scaling": "strong", "global_batch": T,
+               "note": "the same %d-token batch on every rank; local experts + all-reduce(sum) of y" % T}
+
     # local FFN roofline (bytes of the local experts actually streamed / FFN time)
     ffn_ms, ffn_bytes, ffn_flops = 0.0, 0.0, 0.0
-    for e0, e1, bits, off in ops.events:
+    for e0, e1, bits, off in ffn_events:
         ffn_ms += e0.elapsed_time(e1)
         b = bits.cpu().numpy()
         o = off.cpu().numpy()
@@ -431,9 +484,30 @@ def run_ep(args, rank, world, device):
                           "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
                           "weight_copies": args.copies, "l2": "inputs larger than L2 (rotating weight copies)",
                           "parallelism": "ep%d (experts sharded, NCCL all-to-all dispatch/combine)" % world},
-               "roofline": roof, "clocks": clk.summary(), "e2e": None,
-               "gpu_launches": None}
+               "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
+               # libdymoe launches per step and rank: route, score, assign, permute, ep_plan,
+               # gather_rows, local permute, active list, W13, W2, reduce / prefill gather,
+               # unit-weight reorder, weighted combine (NCCL collectives not counted)
+               "gpu_launches": 13 * K,
+               "ep_replicated_decode": rep}
     return res
+
+
+def _max_over_ranks(v, device):
+    """max of a host float over the ranks (CUDA tensor for NCCL, CPU tensor for gloo)."""
+    dev = device if torch.distributed.get_backend() == "nccl" else torch.device("cpu")
+    tt = torch.tensor([v], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    return float(tt.item())
+
+
+def _broadcast(t):
+    if torch.distributed.get_backend() == "nccl":
+        torch.distributed.broadcast(t, 0)
+    else:
+        c = t.cpu()
+        torch.distributed.broadcast(c, 0)
+        t.copy_(c)
 
 
 def load_traffic(kernel_key):
@@ -548,6 +622,9 @@ def main():
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: test hook for several ranks sharing one GPU (collectives staged "
+                         "through host memory); never used for reported numbers")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -560,8 +637,12 @@ def main():
         print(json.dumps(run_reference(args)))
         return
     if world > 1:
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group("gloo")
     if world > 1:
         res = run_ep(args, rank, world, torch.device("cuda", local))
     else:

@@ -201,6 +201,16 @@ int dymoe_expert_ffn(const dymoe_layer* layer, int mode, const uint16_t* x, int 
 int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w, int T,
                   int k, int Hd, int renorm, int out_dtype, void* y, dymoe_stream_t stream);
 
+/* Combine weights against the GLOBAL live set (reading D12), for combines that only see part of
+ * the slots (expert-parallel decode with the batch replicated on every rank):
+ *   w_out[t][s] = bits[topk_idx[t][s]] > 0 ? topk_w[t][s] / d_t : 0,
+ *   d_t = sum over live slots in slot order (fp32) if renorm, else 1; no live slot -> 0.
+ * Combining a subset of the slots with these weights and renorm = 0 gives exactly the terms
+ * dymoe_combine(renorm) would add for those slots.  topk_idx/topk_w/w_out [T][k], bits [M]
+ * device; w_out may alias topk_w.                                                              */
+int dymoe_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uint8_t* bits, int T,
+                         int k, int M, int renorm, float* w_out, dymoe_stream_t stream);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Expert parallelism (BASELINE.json north_star).  Expert e lives on rank
  * floor(e * P / M) (contiguous blocks).  The owner is non-decreasing in e, so the expert-sorted

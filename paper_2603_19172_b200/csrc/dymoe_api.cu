@@ -555,6 +555,17 @@ int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk
   return ok();
 }
 
+int dymoe_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uint8_t* bits, int T,
+                         int k, int M, int renorm, float* w_out, dymoe_stream_t stream) {
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(k >= 1 && k <= 8, "k: must be in [1, 8]");
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  if (T > 0) CHECK_ARG(topk_idx && topk_w && bits && w_out, "topk_idx/topk_w/bits/w_out: must not be NULL");
+  CHECK_LAUNCH(launch_renorm_weights(topk_idx, topk_w, bits, T, k, renorm, w_out, S(stream)),
+               "dymoe_renorm_weights");
+  return ok();
+}
+
 static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, const uint8_t* bits,
                    const int32_t* expert_off, const int32_t* perm_token, const int32_t* active_list,
                    uint16_t* h, float* y_perm, float* y_part, int part_rows, int* parts_out,

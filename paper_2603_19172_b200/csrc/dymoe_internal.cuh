@@ -107,6 +107,8 @@ inline void record_ev(void* const* ev, int i, cudaStream_t s) {
   if (ev != nullptr && ev[i] != nullptr) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
 }
 
+cudaError_t launch_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uint8_t* bits,
+                                  int T, int k, int renorm, float* w_out, cudaStream_t s);
 cudaError_t launch_ep_plan(const int32_t* expert_off, int M, int P, int32_t* send_counts,
                            int32_t* row_expert, cudaStream_t s);
 cudaError_t launch_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n,

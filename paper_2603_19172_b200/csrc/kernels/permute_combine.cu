@@ -232,4 +232,30 @@ cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, cons
   return cudaGetLastError();
 }
 
+// Global-live-set combine weights (D12): one thread per token, slot order, fp32 -- the same
+// arithmetic k_combine applies when it renormalises.
+__global__ void k_renorm_weights(const int32_t* __restrict__ topk_idx, const float* __restrict__ topk_w,
+                                 const uint8_t* __restrict__ bits, int T, int k, int renorm,
+                                 float* __restrict__ w_out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  float w[8];
+  bool live[8];
+  float denom = 0.f;
+  for (int s = 0; s < k; ++s) {
+    w[s] = topk_w[(size_t)t * k + s];
+    live[s] = bits[topk_idx[(size_t)t * k + s]] != 0;
+    if (live[s]) denom += w[s];
+  }
+  for (int s = 0; s < k; ++s)
+    w_out[(size_t)t * k + s] = live[s] ? (renorm ? w[s] / denom : w[s]) : 0.f;
+}
+
+cudaError_t launch_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uint8_t* bits,
+                                  int T, int k, int renorm, float* w_out, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  k_renorm_weights<<<(T + 127) / 128, 128, 0, s>>>(topk_idx, topk_w, bits, T, k, renorm, w_out);
+  return cudaGetLastError();
+}
+
 }  // namespace dymoe

@@ -26,7 +26,7 @@ EXPORTED = [
     "dymoe_layer_create", "dymoe_layer_refresh", "dymoe_layer_destroy", "dymoe_permute", "dymoe_expert_ffn",
     "dymoe_combine", "dymoe_workspace_size", "dymoe_workspace_views", "dymoe_moe_forward",
     "dymoe_check_status", "dymoe_last_error", "dymoe_version", "dymoe_ep_plan",
-    "dymoe_gather_rows",
+    "dymoe_gather_rows", "dymoe_renorm_weights",
 ]
 
 
@@ -110,6 +110,7 @@ def lib():
             "dymoe_version": [],
             "dymoe_ep_plan": [vp, ci, ci, vp, vp, vp],
             "dymoe_gather_rows": [vp, ci, vp, ci, vp, vp],
+            "dymoe_renorm_weights": [vp, vp, vp, ci, ci, ci, ci, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -277,6 +278,15 @@ def dymoe_combine(y_perm, inv_row, topk_w, renorm=True, out_dtype=DYMOE_OUT_F32,
     _check(lib().dymoe_combine(_p(y_perm), _p(inv_row), _p(topk_w), T, k, Hd, int(renorm),
                                out_dtype, _p(y), _stream(stream)))
     return y
+
+
+def dymoe_renorm_weights(topk_idx, topk_w, bits, renorm=True, stream=None):
+    """Combine weights against the global live set (D12; include/dymoe.h)."""
+    T, k = topk_idx.shape
+    out = torch.empty_like(topk_w)
+    _check(lib().dymoe_renorm_weights(_p(topk_idx), _p(topk_w), _p(bits), T, k, bits.shape[0],
+                                      int(renorm), _p(out), _stream(stream)))
+    return out
 
 
 # ---------------------------------------------------------------------------------------------

@@ -21,6 +21,13 @@ step on every rank (each rank owns its own tokens -- weak scaling):
   6. reverse all-to-all of the fp32 rows, and the weighted combine at the source
      (dymoe_combine with the routing weights).
 
+Decode variant with the batch REPLICATED on every rank (decode at B <= 8 is latency
+bound; `forward_replicated`): every rank routes, scores and assigns the same batch (identical
+results, no exchange), runs only its own experts on the pairs routed to them, combines those
+terms with weights renormalised over the GLOBAL live set (dymoe_renorm_weights, D12), and one
+all-reduce(sum) of y [B][Hd] fp32 adds the ranks' partial outputs.  With top-2 each element has at
+most two nonzero terms, so the sum does not depend on the reduction order.
+
 Every step of the math runs in libdymoe kernels; torch.distributed (NCCL on GPUs) carries the
 bytes.  The only host synchronisation is the count exchange needed to size the all-to-all.
 The orchestration is written against two small interfaces -- `ops` (the layer primitives) and
@@ -44,30 +51,39 @@ def owned_range(rank, M, P):
 
 
 class TorchComm:
-    """Collectives over a torch.distributed process group (NCCL between GPUs)."""
+    """Collectives over a torch.distributed process group (NCCL between GPUs).  stage_cpu: move
+    the payloads through host memory (gloo process groups, e.g. several test ranks sharing one
+    GPU); never used for reported numbers."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, stage_cpu=False):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.stage = stage_cpu
 
     def all_reduce_sum(self, t):
+        if self.stage and t.is_cuda:
+            c = t.cpu()
+            self.dist.all_reduce(c, op=self.dist.ReduceOp.SUM, group=self.group)
+            t.copy_(c)
+            return t
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t
 
     def exchange_counts(self, send_counts):
-        recv = torch.empty_like(send_counts)
-        self.dist.all_to_all_single(recv, send_counts, group=self.group)
-        return recv
+        src = send_counts.cpu() if self.stage else send_counts
+        recv = torch.empty_like(src)
+        self.dist.all_to_all_single(recv, src, group=self.group)
+        return recv.to(send_counts.device)
 
     def all_to_all(self, send, send_splits, recv_splits):
+        src = send.contiguous().cpu() if self.stage else send.contiguous()
         out = torch.empty((sum(recv_splits),) + tuple(send.shape[1:]), dtype=send.dtype,
-                          device=send.device)
-        self.dist.all_to_all_single(out, send.contiguous(), recv_splits, send_splits,
-                                    group=self.group)
-        return out
+                          device=src.device)
+        self.dist.all_to_all_single(out, src, recv_splits, send_splits, group=self.group)
+        return out.to(send.device)
 
 
 class ThreadComm:
@@ -157,6 +173,9 @@ class CudaOps:
     def combine(self, y_rows, inv_row, weights, renorm):
         return self.d.dymoe_combine(y_rows, inv_row, weights, renorm=renorm)
 
+    def renorm_weights(self, topk_idx, topk_w, bits, renorm):
+        return self.d.dymoe_renorm_weights(topk_idx, topk_w, bits, renorm=renorm)
+
 
 class EPMoELayer:
     """One rank's shard of an expert-parallel DyMoE layer.
@@ -219,3 +238,37 @@ class EPMoELayer:
         y = ops.combine(y_back, inv, w, renorm)
         return y, dict(bits=bits, importance=imp, topk_idx=idx, topk_w=w, send=send_splits,
                        recv=recv_splits)
+
+    def forward_replicated(self, x, logits, ladder, layer, num_layers, k_tokens=0, renorm=True,
+                           ffn_mode=None):
+        """Decode with the same batch x [B][Hd] on every rank (see the module docstring).
+        Returns (y [B][Hd] summed over the ranks, info)."""
+        ops, comm = self.ops, self.comm
+        M, k = self.M, self.k
+        DECODE = 1
+        B = x.shape[0]
+        idx, w, probs = ops.route(logits, k)
+        imp = ops.score(DECODE, M, k, idx, None, logits, k_tokens)
+        bits = ops.assign_bits(imp, layer, num_layers, ladder, k)
+        wn = ops.renorm_weights(idx, w, bits, renorm)
+        # local view: this rank's experts keep their index (shifted) and width; every other
+        # expert maps to one extra skipped slot M_loc, so its pairs are dropped by the permute
+        M_loc = self.last - self.first
+        mine = (idx >= self.first) & (idx < self.last)
+        idx_loc = torch.where(mine, idx - self.first, torch.full_like(idx, M_loc)).contiguous()
+        bits_loc = torch.cat([bits[self.first:self.last], bits.new_zeros(1)]).contiguous()
+        off, pt, _, inv = ops.permute(idx_loc, M_loc + 1, bits_loc)
+        n_rows = int(off[M_loc].item()) if M_loc > 0 else 0
+        if n_rows > 0:
+            # the local table is a k = 1 layer: hand it the routed rows themselves (expert order)
+            mode = DECODE if ffn_mode is None else ffn_mode
+            x_rows = ops.gather_rows(x, pt[:n_rows].contiguous())
+            ident = torch.arange(n_rows, dtype=torch.int32, device=x.device)
+            y_loc = ops.expert_ffn(self.local, x_rows, bits_loc[:M_loc].contiguous(),
+                                   off[:M_loc + 1].contiguous(), ident, mode)
+        else:
+            y_loc = torch.zeros(1, self.hidden, dtype=ops.y_dtype, device=x.device)
+        y = ops.combine(y_loc, inv, wn, False)
+        if self.P > 1:
+            y = comm.all_reduce_sum(y)
+        return y, dict(bits=bits, importance=imp, topk_idx=idx, topk_w=w, rows=n_rows)

@@ -85,3 +85,13 @@ class OracleOps:
     def combine(self, y_rows, inv_row, weights, renorm):
         return torch.from_numpy(o_moe.combine(y_rows.numpy().astype(np.float64), inv_row.numpy(),
                                               weights.numpy().astype(np.float64), renorm))
+
+    def renorm_weights(self, topk_idx, topk_w, bits, renorm):
+        idx, w, b = topk_idx.numpy(), topk_w.numpy().astype(np.float64), bits.numpy()
+        out = np.zeros_like(w)
+        for t in range(idx.shape[0]):
+            live = [s for s in range(idx.shape[1]) if b[idx[t, s]] > 0]
+            den = sum(w[t, s] for s in live) if renorm else 1.0
+            for s in live:
+                out[t, s] = w[t, s] / den
+        return torch.from_numpy(out)

@@ -99,3 +99,60 @@ def test_ep_two_ranks_equals_unsharded(case):
         assert np.array_equal(y, ref["y"]), np.abs(y - ref["y"]).max()
     # conservation: what rank a sends to b is what b receives from a
     assert out[0][2][1] == out[1][3][0] and out[1][2][0] == out[0][3][1]
+
+
+def _worker_replicated(rank, world, port, bits_t, lams, layer_idx, T, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from ep_oracle_ops import OracleOps, SimpleLadder
+    from paper_2603_19172_b200 import ep
+    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % port, rank=rank,
+                            world_size=world)
+    try:
+        cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+        experts = [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+        first, last = ep.owned_range(rank, cfg.M, world)
+        shard = ep.EPMoELayer(ep.TorchComm(), OracleOps(), experts[first:last], cfg.M, cfg.k,
+                              cfg.hidden, cfg.ffn, make_local_layer=lambda ex: ex)
+        x, lg, _ = _rank_inputs(cfg, 0)          # the SAME batch on every rank
+        y, info = shard.forward_replicated(x, lg, SimpleLadder(bits_t, lams), layer_idx, 32)
+        q.put((rank, y.numpy(), info["bits"].numpy(), info["rows"]))
+    except Exception as e:  # surface worker failures instead of hanging the parent
+        q.put((rank, "error: %r" % e, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", [((8, 4, 2), (0.25, 0.5), 25, 8), ((4, 0), (0.5,), 31, 6),
+                                  ((4, 2), (0.5,), 5, 1)])
+def test_ep_replicated_decode_two_ranks(case):
+    """Decode with the batch replicated on both ranks: local experts + all-reduce(sum) equals the
+    unsharded oracle layer exactly (top-2: at most two nonzero terms per element)."""
+    bits_t, lams, layer, T = case
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_replicated, args=(r, world, port, bits_t, lams, layer, T, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, y, bits, rows = q.get(timeout=300)
+        assert not isinstance(y, str), y
+        out[r] = (y, bits, rows)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+    experts = [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+    x, lg, _ = _rank_inputs(cfg, 0)
+    ref = o_moe.moe_forward(x.numpy(), lg.numpy(), experts, layer, 32, o_sched.Ladder(bits_t, lams), cfg.k)
+    assert out[0][2] + out[1][2] == len(ref["perm_token"])     # every routed pair ran exactly once
+    for r in range(world):
+        y, bits, _ = out[r]
+        assert np.array_equal(bits, ref["bits"])
+        assert np.array_equal(y, ref["y"]), np.abs(y - ref["y"]).max()

@@ -69,3 +69,51 @@ def test_ep_threads_match_unsharded(P, phase, bits_t, lams, layer_idx, T):
                                 o_sched.Ladder(bits_t, lams), cfg.k, forced_bits=bits)
         err = np.abs(y - ref["y"]).max() / np.abs(ref["y"]).max()
         assert err <= 2e-3, (r, err)
+
+
+@pytest.mark.parametrize("P,bits_t,lams,layer_idx,T", [
+    (2, (8, 4, 2), (0.25, 0.5), 25, 8), (4, (8, 4, 2), (0.25, 0.5), 3, 8), (8, (4, 0), (0.5,), 31, 5)])
+def test_ep_replicated_decode_threads(P, bits_t, lams, layer_idx, T):
+    """Decode, batch replicated on P ranks (threads on one GPU): local experts + all-reduce(sum)
+    equals the unsharded single-GPU layer and the oracle."""
+    import paper_2603_19172_b200.dymoe as d
+    from paper_2603_19172_b200 import ep
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+    ex_all = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+    d.quantize_experts(ex_all, (8, 4, 2))
+    x, lg, _ = synthetic.layer_inputs(cfg, 77)
+    lad = d.make_ladder(bits_t, lams)
+    full = d.MoELayer(ex_all, cfg.k, cfg.hidden, cfg.ffn)
+    y_one, _ = full.forward(x.cuda(), lg.cuda(), lad, layer_idx, 32, phase=d.DYMOE_DECODE)
+    torch.cuda.synchronize()
+    comm = ep.ThreadComm(P)
+    ops = ep.CudaOps()
+    results, errors = {}, []
+
+    def worker(r):
+        try:
+            comm.bind(r)
+            first, last = ep.owned_range(r, cfg.M, P)
+            shard = ep.EPMoELayer(comm, ops, ex_all[first:last], cfg.M, cfg.k, cfg.hidden, cfg.ffn,
+                                  make_local_layer=lambda ex: d.MoELayer(ex, 1, cfg.hidden, cfg.ffn))
+            y, info = shard.forward_replicated(x.cuda(), lg.cuda(), lad, layer_idx, 32)
+            torch.cuda.synchronize()
+            results[r] = y.cpu().numpy()
+        except Exception as e:   # pragma: no cover
+            errors.append(e)
+            comm.barrier.abort()
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    experts = [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+    ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, layer_idx, 32,
+                            o_sched.Ladder(bits_t, lams), cfg.k)
+    y1 = y_one.cpu().numpy()
+    for r in range(P):
+        assert np.abs(results[r] - y1).max() <= 1e-6 * np.abs(y1).max(), r
+        err = np.abs(results[r] - ref["y"]).max() / np.abs(ref["y"]).max()
+        assert err <= 2e-3, (r, err)
