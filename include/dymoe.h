@@ -201,6 +201,24 @@ int dymoe_expert_ffn(const dymoe_layer* layer, int mode, const uint16_t* x, int 
 int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w, int T,
                   int k, int Hd, int renorm, int out_dtype, void* y, dymoe_stream_t stream);
 
+/* Look-ahead prediction of the next layer's experts (PAPER.md "Phase-Adaptive
+ * Prefetcher", Eqs. 6-8).  Eq. 6: logits = h · W_g^(l+1)^T (fp32, one rounding per
+ * multiply-add in k order), g_hat = softmax.  PREFILL (Eq. 7): c_e = #{tokens whose top-k_route
+ * predicted experts contain e}; requests = the t experts with the largest c_e (> 0), priority =
+ * c_e.  DECODE (Eq. 8): requests = top-t of the predicted decode importance (B = 1: the predicted
+ * logit row; B > 1: sum over the batch of g_hat), priority = that value.  Order: (value desc,
+ * index asc).  The caller uses the requests to stage the next layer's widths (quantize / pool)
+ * on a side stream while layer l runs.
+ *   h [T][Hd] bf16, w_gate_next [M][Hd] bf16 (Hd multiple of 8, 16-byte aligned), all device.
+ *   ws: dymoe_predict_ws_bytes(T, M, k_route) bytes of device scratch.
+ *   experts [t] i32 / priority [t] f32 out (first *n_out valid), n_out [1] i32 device out;
+ *   logits_out [T][M] f32 (nullable) receives the Eq. 6 logits.
+ * Errors: T < 1, M outside [1, 256], k_route outside [1, min(M, 8)], t outside [1, M].        */
+size_t dymoe_predict_ws_bytes(int T, int M, int k_route);
+int dymoe_predict_next(int phase, const uint16_t* h, const uint16_t* w_gate_next, int T, int Hd,
+                       int M, int k_route, int t, void* ws, size_t ws_bytes, int32_t* experts,
+                       float* priority, int32_t* n_out, float* logits_out, dymoe_stream_t stream);
+
 /* Combine weights against the GLOBAL live set (reading D12), for combines that only see part of
  * the slots (expert-parallel decode with the batch replicated on every rank):
  *   w_out[t][s] = bits[topk_idx[t][s]] > 0 ? topk_w[t][s] / d_t : 0,

@@ -555,6 +555,43 @@ int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk
   return ok();
 }
 
+size_t dymoe_predict_ws_bytes(int T, int M, int k_route) {
+  if (T < 1 || M < 1 || k_route < 1) return 0;
+  const size_t TM = (size_t)T * M, TK = (size_t)T * k_route;
+  return align_up(TM * 4) + align_up(TK * 4) + align_up(TK * 4) + align_up(TM * 4) + align_up((size_t)M * 4);
+}
+
+int dymoe_predict_next(int phase, const uint16_t* h, const uint16_t* w_gate_next, int T, int Hd,
+                       int M, int k_route, int t, void* ws, size_t ws_bytes, int32_t* experts,
+                       float* priority, int32_t* n_out, float* logits_out, dymoe_stream_t stream) {
+  CHECK_ARG(phase == DYMOE_PREFILL || phase == DYMOE_DECODE, "phase: must be DYMOE_PREFILL or DYMOE_DECODE");
+  CHECK_ARG(T >= 1, "T: must be >= 1");
+  CHECK_ARG(Hd > 0 && Hd % 8 == 0, "Hd: must be a positive multiple of 8");
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(k_route >= 1 && k_route <= M && k_route <= 8, "k_route: must satisfy 1 <= k_route <= min(M, 8)");
+  CHECK_ARG(t >= 1 && t <= M, "t: must satisfy 1 <= t <= M");
+  CHECK_ARG(h && w_gate_next && ws && experts && priority && n_out,
+            "h/w_gate_next/ws/experts/priority/n_out: must not be NULL");
+  int rc = check_ptr_align(h, 16, "h");
+  if (rc) return rc;
+  rc = check_ptr_align(w_gate_next, 16, "w_gate_next");
+  if (rc) return rc;
+  if (ws_bytes < dymoe_predict_ws_bytes(T, M, k_route))
+    return fail(DYMOE_ERR_WORKSPACE, "ws_bytes: %zu < dymoe_predict_ws_bytes = %zu", ws_bytes,
+                dymoe_predict_ws_bytes(T, M, k_route));
+  const size_t TM = (size_t)T * M, TK = (size_t)T * k_route;
+  char* b = reinterpret_cast<char*>(ws);
+  float* logits = logits_out ? logits_out : reinterpret_cast<float*>(b);
+  int32_t* tidx = reinterpret_cast<int32_t*>(b + align_up(TM * 4));
+  float* tw = reinterpret_cast<float*>(b + align_up(TM * 4) + align_up(TK * 4));
+  float* probs = reinterpret_cast<float*>(b + align_up(TM * 4) + 2 * align_up(TK * 4));
+  float* value = reinterpret_cast<float*>(b + 2 * align_up(TM * 4) + 2 * align_up(TK * 4));
+  CHECK_LAUNCH(launch_predict_next(phase, h, w_gate_next, T, Hd, M, k_route, t, logits, tidx, tw,
+                                   probs, value, experts, priority, n_out, S(stream)),
+               "dymoe_predict_next");
+  return ok();
+}
+
 int dymoe_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uint8_t* bits, int T,
                          int k, int M, int renorm, float* w_out, dymoe_stream_t stream) {
   CHECK_ARG(T >= 0, "T: must be >= 0");

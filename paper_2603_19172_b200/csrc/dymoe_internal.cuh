@@ -107,6 +107,10 @@ inline void record_ev(void* const* ev, int i, cudaStream_t s) {
   if (ev != nullptr && ev[i] != nullptr) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
 }
 
+cudaError_t launch_predict_next(int phase, const uint16_t* h, const uint16_t* wg, int T, int Hd,
+                                int M, int k, int t, float* logits, int32_t* topk_idx,
+                                float* topk_w, float* probs, float* value, int32_t* experts,
+                                float* priority, int32_t* n_out, cudaStream_t s);
 cudaError_t launch_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uint8_t* bits,
                                   int T, int k, int renorm, float* w_out, cudaStream_t s);
 cudaError_t launch_ep_plan(const int32_t* expert_off, int M, int P, int32_t* send_counts,

@@ -26,7 +26,7 @@ EXPORTED = [
     "dymoe_layer_create", "dymoe_layer_refresh", "dymoe_layer_destroy", "dymoe_permute", "dymoe_expert_ffn",
     "dymoe_combine", "dymoe_workspace_size", "dymoe_workspace_views", "dymoe_moe_forward",
     "dymoe_check_status", "dymoe_last_error", "dymoe_version", "dymoe_ep_plan",
-    "dymoe_gather_rows", "dymoe_renorm_weights",
+    "dymoe_gather_rows", "dymoe_renorm_weights", "dymoe_predict_ws_bytes", "dymoe_predict_next",
 ]
 
 
@@ -111,6 +111,8 @@ def lib():
             "dymoe_ep_plan": [vp, ci, ci, vp, vp, vp],
             "dymoe_gather_rows": [vp, ci, vp, ci, vp, vp],
             "dymoe_renorm_weights": [vp, vp, vp, ci, ci, ci, ci, vp, vp],
+            "dymoe_predict_ws_bytes": [ci, ci, ci],
+            "dymoe_predict_next": [ci, vp, vp, ci, ci, ci, ci, ci, vp, cz, vp, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -119,6 +121,7 @@ def lib():
         L.dymoe_retention_ratio.restype = ctypes.c_double
         L.dymoe_score_scratch_bytes.restype = cz
         L.dymoe_workspace_size.restype = cz
+        L.dymoe_predict_ws_bytes.restype = cz
         L.dymoe_last_error.restype = ctypes.c_char_p
         L.dymoe_version.restype = ctypes.c_char_p
         _lib = L
@@ -287,6 +290,23 @@ def dymoe_renorm_weights(topk_idx, topk_w, bits, renorm=True, stream=None):
     _check(lib().dymoe_renorm_weights(_p(topk_idx), _p(topk_w), _p(bits), T, k, bits.shape[0],
                                       int(renorm), _p(out), _stream(stream)))
     return out
+
+
+def dymoe_predict_next(phase, h, w_gate_next, k_route, t, stream=None):
+    """Eqs. 6-8 look-ahead (include/dymoe.h).  Returns (experts [n] i32, priority [n] f32,
+    logits [T][M] f32) on the device; n = number of valid requests (one host read)."""
+    T, Hd = h.shape
+    M = w_gate_next.shape[0]
+    nbytes = lib().dymoe_predict_ws_bytes(T, M, k_route)
+    ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=h.device)
+    ex = torch.empty(t, dtype=torch.int32, device=h.device)
+    pr = torch.empty(t, dtype=torch.float32, device=h.device)
+    n = torch.empty(1, dtype=torch.int32, device=h.device)
+    lg = torch.empty(T, M, dtype=torch.float32, device=h.device)
+    _check(lib().dymoe_predict_next(phase, _p(_u16(h)), _p(_u16(w_gate_next)), T, Hd, M, k_route, t,
+                                    _p(ws), ws.numel(), _p(ex), _p(pr), _p(n), _p(lg), _stream(stream)))
+    k = int(n.item())
+    return ex[:k], pr[:k], lg
 
 
 # ---------------------------------------------------------------------------------------------
