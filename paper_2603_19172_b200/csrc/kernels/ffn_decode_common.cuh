@@ -125,15 +125,17 @@ __device__ __forceinline__ void a_frag(const uint4& w, const DQ& dq, int s, uint
     lo = v[0];
     hi = v[1];
   } else {  // 8
-    // q - z exact in fp32 (2^23 + q minus 2^23 + z), packed to bf16x2 exactly (|q - z| <= 255
+    // q - z exact in fp32 (2^23 + q minus 2^23 + z), taken to bf16x2 exactly (|q - z| <= 255
     // has 8 significant bits), then one HMUL2 per pair gives RNE((q - z)·s) (D17)
     const uint32_t x = word(w, s);
     const float d0 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7440u)), dq.zf);
     const float d1 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7441u)), dq.zf);
     const float d2 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7442u)), dq.zf);
     const float d3 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7443u)), dq.zf);
-    lo = bf2_mul(pack_bf2(d0, d1), dq.ss);
-    hi = bf2_mul(pack_bf2(d2, d3), dq.ss);
+    // q - z is a small integer (<= 8 significant bits): its fp32 low half is zero, so the bf16
+    // pair is just the two high halves (one PRMT instead of an F2FP conversion)
+    lo = bf2_mul(prmt(__float_as_uint(d0), __float_as_uint(d1), 0x7632u), dq.ss);
+    hi = bf2_mul(prmt(__float_as_uint(d2), __float_as_uint(d3), 0x7632u), dq.ss);
   }
 }
 

@@ -242,7 +242,8 @@ __device__ __forceinline__ void deq_int2_word(uint32_t w, const DQP& d, uint4& l
 __device__ __forceinline__ uint32_t deq_int8_pair(uint32_t w, int i, const DQP& d) {
   const float d0 = __fsub_rn(__uint_as_float(prmt(w, 0x4B000000u, 0x7440u + i)), d.zf);
   const float d1 = __fsub_rn(__uint_as_float(prmt(w, 0x4B000000u, 0x7441u + i)), d.zf);
-  return bf2_mul(pack_bf2(d0, d1), d.ss);
+  // |q - z| <= 255 is exact in bf16: the pair is the two fp32 high halves (PRMT, no F2FP)
+  return bf2_mul(prmt(__float_as_uint(d0), __float_as_uint(d1), 0x7632u), d.ss);
 }
 
 // ---------------------------------------------------------------------------------------- B producer
