@@ -37,7 +37,8 @@ enum {
   DYMOE_ERR_NCCL = 3,        /* reserved for collective failures */
   DYMOE_ERR_WORKSPACE = 4,   /* workspace too small or misaligned */
   DYMOE_ERR_UNSUPPORTED = 5, /* shape or width outside what the kernels implement */
-  DYMOE_ERR_DEVICE = 6       /* dymoe_check_status: a device-side fault was recorded */
+  DYMOE_ERR_DEVICE = 6,      /* dymoe_check_status: a device-side fault was recorded */
+  DYMOE_ERR_CAPACITY = 7     /* dymoe_pool_insert: the entry cannot fit (nothing changed) */
 };
 
 enum { DYMOE_PREFILL = 0, DYMOE_DECODE = 1 };
@@ -200,6 +201,41 @@ int dymoe_expert_ffn(const dymoe_layer* layer, int mode, const uint16_t* x, int 
  * w'·y_perm[inv_row[t][slot]]; E_t empty -> y[t] = 0.  y [T][Hd] f32 or bf16 (out_dtype).     */
 int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk_w, int T,
                   int k, int Hd, int renorm, int out_dtype, void* y, dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Mixed-precision expert pool (PAPER.md "Mixed-Precision Cache Management",
+ * P:303-309; readings P4-P6).  Host-side policy over a caller-owned arena of
+ * `capacity` bytes (typically one device allocation): it decides which (layer, expert) is
+ * resident in which format and where, and therefore when dymoe_quantize must run.
+ *   Rules (bit widths ordered 16 > 8 > 4 > 2, reading P4): No Duplication (one format per key);
+ *   Precision Promotion (request b, narrower cached -> PROMOTE: a miss, load b, evict it);
+ *   Conservative Reuse (request b, wider or equal cached -> HIT served by it).  LRU victims.
+ *   lookup: outcome DYMOE_POOL_HIT / MISS / PROMOTE, served bits, arena offset (HIT only);
+ *     a HIT refreshes recency.
+ *   insert: replaces the key's entry (its range freed first; a pinned key -> INVALID), evicts
+ *     least-recently-used unpinned entries until a contiguous range fits, places first-fit at
+ *     the lowest offset; evicted keys are written as (layer, expert) pairs in eviction order
+ *     (at most max_evicted; *n_evicted is the full count).  If the entry cannot fit even with
+ *     every unpinned entry evicted: DYMOE_ERR_CAPACITY and nothing changes.
+ *   pin / unpin: counted; pinned entries are never evicted.
+ *   snapshot: entries least- to most-recently used.  Not thread-safe (one owner thread).      */
+typedef struct dymoe_pool dymoe_pool;
+enum { DYMOE_POOL_HIT = 0, DYMOE_POOL_MISS = 1, DYMOE_POOL_PROMOTE = 2 };
+typedef struct dymoe_pool_entry {
+  int layer, expert, bits, pins;
+  size_t bytes, offset;
+  unsigned long long last_use;
+} dymoe_pool_entry;
+int dymoe_pool_create(size_t capacity, dymoe_pool** out);
+int dymoe_pool_destroy(dymoe_pool* pool);
+int dymoe_pool_lookup(dymoe_pool* pool, int layer, int expert, int bits, int* outcome,
+                      int* served_bits, size_t* offset);
+int dymoe_pool_insert(dymoe_pool* pool, int layer, int expert, int bits, size_t bytes,
+                      size_t* offset, int32_t* evicted, int max_evicted, int* n_evicted);
+int dymoe_pool_pin(dymoe_pool* pool, int layer, int expert);
+int dymoe_pool_unpin(dymoe_pool* pool, int layer, int expert);
+int dymoe_pool_snapshot(const dymoe_pool* pool, dymoe_pool_entry* out, int max, int* n);
+size_t dymoe_pool_used(const dymoe_pool* pool);
 
 /* Look-ahead prediction of the next layer's experts (PAPER.md "Phase-Adaptive
  * Prefetcher", Eqs. 6-8).  Eq. 6: logits = h · W_g^(l+1)^T (fp32, one rounding per

@@ -804,3 +804,14 @@ bool dymoe::encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* b
   const uint32_t box[2] = {b0, b1};
   return encode(m, dt, base, 2, dims, str, box, swz);
 }
+
+int dymoe::set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+void dymoe::clear_error() { g_err.clear(); }

@@ -44,6 +44,10 @@ __host__ __device__ inline int width_index(int bits) {
   return bits == 8 ? 0 : bits == 4 ? 1 : bits == 2 ? 2 : -1;
 }
 
+// Sets the thread-local error message returned by dymoe_last_error (dymoe_api.cu); returns code.
+int set_error(int code, const char* fmt, ...);
+void clear_error();
+
 // ------------------------------------------------------------------------------------------
 // Launchers (each returns cudaGetLastError() of its launch).
 cudaError_t launch_route(const float* logits, int T, int M, int k, int32_t* topk_idx,

@@ -27,6 +27,8 @@ EXPORTED = [
     "dymoe_combine", "dymoe_workspace_size", "dymoe_workspace_views", "dymoe_moe_forward",
     "dymoe_check_status", "dymoe_last_error", "dymoe_version", "dymoe_ep_plan",
     "dymoe_gather_rows", "dymoe_renorm_weights", "dymoe_predict_ws_bytes", "dymoe_predict_next",
+    "dymoe_pool_create", "dymoe_pool_destroy", "dymoe_pool_lookup", "dymoe_pool_insert",
+    "dymoe_pool_pin", "dymoe_pool_unpin", "dymoe_pool_snapshot", "dymoe_pool_used",
 ]
 
 
@@ -113,6 +115,15 @@ def lib():
             "dymoe_renorm_weights": [vp, vp, vp, ci, ci, ci, ci, vp, vp],
             "dymoe_predict_ws_bytes": [ci, ci, ci],
             "dymoe_predict_next": [ci, vp, vp, ci, ci, ci, ci, ci, vp, cz, vp, vp, vp, vp, vp],
+            "dymoe_pool_create": [cz, ctypes.POINTER(vp)],
+            "dymoe_pool_destroy": [vp],
+            "dymoe_pool_lookup": [vp, ci, ci, ci, ctypes.POINTER(ci), ctypes.POINTER(ci),
+                                  ctypes.POINTER(cz)],
+            "dymoe_pool_insert": [vp, ci, ci, ci, cz, ctypes.POINTER(cz), vp, ci, ctypes.POINTER(ci)],
+            "dymoe_pool_pin": [vp, ci, ci],
+            "dymoe_pool_unpin": [vp, ci, ci],
+            "dymoe_pool_snapshot": [vp, vp, ci, ctypes.POINTER(ci)],
+            "dymoe_pool_used": [vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -122,6 +133,7 @@ def lib():
         L.dymoe_score_scratch_bytes.restype = cz
         L.dymoe_workspace_size.restype = cz
         L.dymoe_predict_ws_bytes.restype = cz
+        L.dymoe_pool_used.restype = cz
         L.dymoe_last_error.restype = ctypes.c_char_p
         L.dymoe_version.restype = ctypes.c_char_p
         _lib = L
@@ -307,6 +319,62 @@ def dymoe_predict_next(phase, h, w_gate_next, k_route, t, stream=None):
                                     _p(ws), ws.numel(), _p(ex), _p(pr), _p(n), _p(lg), _stream(stream)))
     k = int(n.item())
     return ex[:k], pr[:k], lg
+
+
+# ---------------------------------------------------------------------------------------------
+class PoolEntry(ctypes.Structure):
+    _fields_ = [("layer", ctypes.c_int), ("expert", ctypes.c_int), ("bits", ctypes.c_int),
+                ("pins", ctypes.c_int), ("bytes", ctypes.c_size_t), ("offset", ctypes.c_size_t),
+                ("last_use", ctypes.c_ulonglong)]
+
+
+POOL_HIT, POOL_MISS, POOL_PROMOTE = 0, 1, 2
+DYMOE_ERR_CAPACITY = 7
+
+
+class Pool:
+    """dymoe_pool (include/dymoe.h): the mixed-precision expert pool's host-side policy."""
+
+    def __init__(self, capacity):
+        h = ctypes.c_void_p()
+        _check(lib().dymoe_pool_create(capacity, ctypes.byref(h)))
+        self.handle = h
+        self.capacity = capacity
+
+    def __del__(self):
+        if getattr(self, "handle", None) and _lib is not None:
+            _lib.dymoe_pool_destroy(self.handle)
+            self.handle = None
+
+    def lookup(self, layer, expert, bits):
+        out, served, off = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
+        _check(lib().dymoe_pool_lookup(self.handle, layer, expert, bits, ctypes.byref(out),
+                                       ctypes.byref(served), ctypes.byref(off)))
+        return out.value, served.value, (off.value if out.value == POOL_HIT else None)
+
+    def insert(self, layer, expert, bits, nbytes, max_evicted=256):
+        off, n = ctypes.c_size_t(), ctypes.c_int()
+        ev = (ctypes.c_int32 * (2 * max_evicted))()
+        _check(lib().dymoe_pool_insert(self.handle, layer, expert, bits, nbytes, ctypes.byref(off),
+                                       ev, max_evicted, ctypes.byref(n)))
+        return off.value, [(ev[2 * i], ev[2 * i + 1]) for i in range(min(n.value, max_evicted))]
+
+    def pin(self, layer, expert):
+        _check(lib().dymoe_pool_pin(self.handle, layer, expert))
+
+    def unpin(self, layer, expert):
+        _check(lib().dymoe_pool_unpin(self.handle, layer, expert))
+
+    def snapshot(self):
+        n = ctypes.c_int()
+        _check(lib().dymoe_pool_snapshot(self.handle, None, 0, ctypes.byref(n)))
+        arr = (PoolEntry * max(n.value, 1))()
+        _check(lib().dymoe_pool_snapshot(self.handle, arr, n.value, ctypes.byref(n)))
+        return [((e.layer, e.expert), dict(bits=e.bits, nbytes=e.bytes, offset=e.offset,
+                                           last_use=e.last_use, pins=e.pins)) for e in arr[:n.value]]
+
+    def used(self):
+        return lib().dymoe_pool_used(self.handle)
 
 
 # ---------------------------------------------------------------------------------------------
