@@ -167,6 +167,12 @@ typedef struct dymoe_layer_desc {
 typedef struct dymoe_layer dymoe_layer;
 int dymoe_layer_create(const dymoe_layer_desc* desc, dymoe_layer** out);
 int dymoe_layer_refresh(dymoe_layer* layer, dymoe_stream_t stream);
+/* Rebind one expert to new formats (pointers as in dymoe_expert_desc; absent widths NULL), e.g.
+ * after the expert pool placed or evicted a format.  Rebuilds the expert's derived metadata and
+ * TMA descriptors; all device updates are ordered on `stream` before the next forward on it.
+ * The previous formats must stay valid until work already queued on other streams is done.    */
+int dymoe_layer_set_expert(dymoe_layer* layer, int expert, const dymoe_expert_desc* desc,
+                           dymoe_stream_t stream);
 int dymoe_layer_destroy(dymoe_layer* layer);
 
 /* ------------------------------------------------------------------------------------------ */

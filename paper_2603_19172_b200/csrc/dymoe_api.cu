@@ -334,6 +334,97 @@ constexpr int kMapsPerExpert = 24;   // 3 + 3 bf16 masters (decode, prefill boxe
                                      // matrices x (codes, meta)
 }  // namespace
 
+namespace {
+// Expert e's slice of the layer's derived metadata: [width][W1 | W3 | W2] group-major words, W1
+// and W3 adjacent (one 3-D TMA box feeds both).  Allocated for every width at create, so that a
+// format bound later (dymoe_layer_set_expert) has its slot.
+size_t meta_words_per_expert(int Hd, int F) { return (size_t)3 * 3 * F * (Hd / DYMOE_GROUP); }
+uint32_t* meta_slot(dymoe_layer* L, int e, int wi, int m) {
+  const size_t w13 = (size_t)L->F * (L->Hd / DYMOE_GROUP);   // == W2's N * gpr as well
+  return L->meta_pool + (size_t)e * meta_words_per_expert(L->Hd, L->F) + ((size_t)wi * 3 + m) * w13;
+}
+
+int validate_expert(const dymoe_expert_desc& x, int e) {
+  for (int wi = 0; wi < 3; ++wi)
+    for (int m = 0; m < 3; ++m) {
+      if (x.q[wi][m].codes != nullptr && (x.q[wi][m].scales == nullptr || x.q[wi][m].zeros == nullptr))
+        return fail(DYMOE_ERR_INVALID, "desc.experts[%d].q[%d][%d]: scales/zeros must be set with codes", e, wi, m);
+      if (((uintptr_t)x.q[wi][m].codes) % 16)
+        return fail(DYMOE_ERR_INVALID, "desc.experts[%d].q[%d][%d].codes: must be 16-byte aligned", e, wi, m);
+    }
+  const uint16_t* w[3] = {x.w1, x.w3, x.w2};
+  for (int m = 0; m < 3; ++m)
+    if (((uintptr_t)w[m]) % 16)
+      return fail(DYMOE_ERR_INVALID, "desc.experts[%d].w%d: must be 16-byte aligned", e, m == 0 ? 1 : m == 1 ? 3 : 2);
+  return DYMOE_OK;
+}
+
+// (Re)bind expert e to the formats in x: table entry, derived metadata (k_build_meta on stream)
+// and TMA descriptors; the device copies are stream-ordered.
+int bind_expert(dymoe_layer* L, int e, const dymoe_expert_desc& x, cudaStream_t stream) {
+  DevExpert& y = L->host[e];
+  y.w[0] = x.w1;
+  y.w[1] = x.w3;
+  y.w[2] = x.w2;
+  for (int wi = 0; wi < 3; ++wi)
+    for (int m = 0; m < 3; ++m) {
+      DevQMat& q = y.q[wi][m];
+      q.codes = x.q[wi][m].codes;
+      q.scales = x.q[wi][m].scales;
+      q.zeros = x.q[wi][m].zeros;
+      q.meta = nullptr;
+      if (q.codes == nullptr) continue;
+      const size_t N = m == 2 ? L->Hd : L->F, K = m == 2 ? L->F : L->Hd;
+      q.meta = meta_slot(L, e, wi, m);
+      cudaError_t err = launch_build_meta(q.scales, q.zeros, (int)N, (int)(K / DYMOE_GROUP),
+                                          const_cast<uint32_t*>(q.meta), stream);
+      if (err != cudaSuccess) return cuda_fail(err, "bind expert");
+    }
+  std::vector<CUtensorMap> hm(kMapsPerExpert);
+  memset(hm.data(), 0, hm.size() * sizeof(CUtensorMap));
+  const CUtensorMap* dm = L->tmap_pool + (size_t)e * kMapsPerExpert;
+  bool maps_ok = true;
+  for (int m = 0; m < 3; ++m) {
+    const uint64_t N = m == 2 ? L->Hd : L->F, K = m == 2 ? L->F : L->Hd;
+    y.tm_w[m] = y.tm_wp[m] = nullptr;
+    if (y.w[m] != nullptr) {
+      maps_ok &= encode_rows(&hm[m], y.w[m], 2 * K, N);
+      y.tm_w[m] = dm + m;
+      const uint64_t dims[2] = {K, N}, str[1] = {2 * K};
+      const uint32_t box[2] = {64, 128};
+      maps_ok &= encode(&hm[21 + m], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y.w[m], 2, dims, str, box,
+                        CU_TENSOR_MAP_SWIZZLE_128B);
+      y.tm_wp[m] = dm + 21 + m;
+    }
+    for (int wi = 0; wi < 3; ++wi) {
+      DevQMat& q = y.q[wi][m];
+      q.tm_codes = q.tm_meta = nullptr;
+      if (q.codes == nullptr) continue;
+      const int b = wi == 0 ? 8 : wi == 1 ? 4 : 2;
+      const uint32_t gq = (uint32_t)(2 * 512 / b / DYMOE_GROUP);   // groups per 128-byte item
+      const int ic = 3 + (wi * 3 + m) * 2, im = ic + 1;
+      maps_ok &= encode_rows(&hm[ic], q.codes, K * b / 8, N);
+      q.tm_codes = dm + ic;
+      // W2: 2-D meta; W1: 3-D over the adjacent W1 / W3 meta (one box feeds both matrices);
+      // W3's own descriptor is not needed by the kernels
+      const bool pair = m == 0 && y.q[wi][1].codes != nullptr;
+      if (m == 2 || pair) {
+        maps_ok &= encode_meta(&hm[im], q.meta, N, K / DYMOE_GROUP, pair ? 2 : 1, gq);
+        q.tm_meta = dm + im;
+      }
+    }
+  }
+  if (!maps_ok) return fail(DYMOE_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  // pageable sources: the copies are staged before cudaMemcpyAsync returns
+  cudaError_t err = cudaMemcpyAsync(const_cast<CUtensorMap*>(dm), hm.data(),
+                                    hm.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice, stream);
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(L->dev + e, &y, sizeof(DevExpert), cudaMemcpyHostToDevice, stream);
+  if (err != cudaSuccess) return cuda_fail(err, "bind expert");
+  return DYMOE_OK;
+}
+}  // namespace
+
 int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
   CHECK_ARG(out != nullptr, "out: must not be NULL");
   *out = nullptr;
@@ -344,6 +435,10 @@ int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
   CHECK_ARG(d->hidden > 0 && d->hidden % 128 == 0, "desc.hidden: must be a positive multiple of 128");
   CHECK_ARG(d->ffn > 0 && d->ffn % 128 == 0, "desc.ffn: must be a positive multiple of 128");
   CHECK_ARG(d->experts != nullptr, "desc.experts: must not be NULL");
+  for (int e = 0; e < d->M; ++e) {
+    const int rc = validate_expert(d->experts[e], e);
+    if (rc) return rc;
+  }
   dymoe_layer* L = new (std::nothrow) dymoe_layer();
   if (!L) return fail(DYMOE_ERR_INVALID, "out of host memory");
   L->M = d->M;
@@ -351,116 +446,38 @@ int dymoe_layer_create(const dymoe_layer_desc* d, dymoe_layer** out) {
   L->Hd = d->hidden;
   L->F = d->ffn;
   L->host.resize(d->M);
-  for (int e = 0; e < d->M; ++e) {
-    const dymoe_expert_desc& x = d->experts[e];
-    DevExpert& y = L->host[e];
-    y.w[0] = x.w1;
-    y.w[1] = x.w3;
-    y.w[2] = x.w2;
-    for (int wi = 0; wi < 3; ++wi)
-      for (int m = 0; m < 3; ++m) {
-        y.q[wi][m].codes = x.q[wi][m].codes;
-        y.q[wi][m].scales = x.q[wi][m].scales;
-        y.q[wi][m].zeros = x.q[wi][m].zeros;
-        if (x.q[wi][m].codes != nullptr && (x.q[wi][m].scales == nullptr || x.q[wi][m].zeros == nullptr)) {
-          delete L;
-          return fail(DYMOE_ERR_INVALID, "desc.experts[%d].q[%d][%d]: scales/zeros must be set with codes", e, wi, m);
-        }
-        if (((uintptr_t)x.q[wi][m].codes) % 16) {
-          delete L;
-          return fail(DYMOE_ERR_INVALID, "desc.experts[%d].q[%d][%d].codes: must be 16-byte aligned", e, wi, m);
-        }
-      }
-    for (int m = 0; m < 3; ++m)
-      if (((uintptr_t)y.w[m]) % 16) {
-        delete L;
-        return fail(DYMOE_ERR_INVALID, "desc.experts[%d].w%d: must be 16-byte aligned", e, m == 0 ? 1 : m == 1 ? 3 : 2);
-      }
-  }
-  // derived per-group dequant metadata for every resident quantized matrix (one pool)
-  size_t meta_words = 0;
-  for (int ex = 0; ex < d->M; ++ex)
-    for (int wi = 0; wi < 3; ++wi)
-      for (int m = 0; m < 3; ++m)
-        if (L->host[ex].q[wi][m].codes != nullptr) {
-          const size_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
-          meta_words += N * (K / DYMOE_GROUP);
-        }
-  cudaError_t e = cudaSuccess;
-  if (meta_words > 0) e = cudaMalloc(&L->meta_pool, meta_words * sizeof(uint32_t));
+  cudaError_t e = cudaMalloc(&L->meta_pool, meta_words_per_expert(d->hidden, d->ffn) * d->M * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&L->dev, sizeof(DevExpert) * d->M);
+  if (e == cudaSuccess) e = cudaMalloc(&L->tmap_pool, (size_t)d->M * kMapsPerExpert * sizeof(CUtensorMap));
   if (e != cudaSuccess) {
     dymoe_layer_destroy(L);
     return cuda_fail(e, "dymoe_layer_create");
   }
-  size_t at = 0;
-  for (int ex = 0; ex < d->M && e == cudaSuccess; ++ex)
-    for (int wi = 0; wi < 3; ++wi)
-      for (int m = 0; m < 3; ++m) {
-        DevQMat& q = L->host[ex].q[wi][m];
-        q.meta = nullptr;
-        if (q.codes == nullptr) continue;
-        const size_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
-        const size_t n = N * (K / DYMOE_GROUP);
-        q.meta = L->meta_pool + at;
-        if (e == cudaSuccess)
-          e = launch_build_meta(q.scales, q.zeros, (int)N, (int)(K / DYMOE_GROUP), L->meta_pool + at, nullptr);
-        at += n;
-      }
-  // TMA descriptors: built on the host, copied next to the expert table
-  std::vector<CUtensorMap> maps((size_t)d->M * kMapsPerExpert);
-  memset(maps.data(), 0, maps.size() * sizeof(CUtensorMap));
-  if (e == cudaSuccess) e = cudaMalloc(&L->tmap_pool, maps.size() * sizeof(CUtensorMap));
-  bool maps_ok = true;
-  for (int ex = 0; ex < d->M && e == cudaSuccess; ++ex) {
-    DevExpert& y = L->host[ex];
-    CUtensorMap* hm = maps.data() + (size_t)ex * kMapsPerExpert;
-    const CUtensorMap* dm = L->tmap_pool + (size_t)ex * kMapsPerExpert;
-    for (int m = 0; m < 3; ++m) {
-      const uint64_t N = m == 2 ? d->hidden : d->ffn, K = m == 2 ? d->ffn : d->hidden;
-      y.tm_w[m] = y.tm_wp[m] = nullptr;
-      if (y.w[m] != nullptr) {
-        maps_ok &= encode_rows(&hm[m], y.w[m], 2 * K, N);
-        y.tm_w[m] = dm + m;
-        const uint64_t dims[2] = {K, N}, str[1] = {2 * K};
-        const uint32_t box[2] = {64, 128};
-        maps_ok &= encode(&hm[21 + m], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, y.w[m], 2, dims, str, box,
-                          CU_TENSOR_MAP_SWIZZLE_128B);
-        y.tm_wp[m] = dm + 21 + m;
-      }
-      for (int wi = 0; wi < 3; ++wi) {
-        DevQMat& q = y.q[wi][m];
-        q.tm_codes = q.tm_meta = nullptr;
-        if (q.codes == nullptr) continue;
-        const int b = wi == 0 ? 8 : wi == 1 ? 4 : 2;
-        const uint32_t gq = (uint32_t)(2 * 512 / b / DYMOE_GROUP);   // groups per 128-byte item
-        const int ic = 3 + (wi * 3 + m) * 2, im = ic + 1;
-        maps_ok &= encode_rows(&hm[ic], q.codes, K * b / 8, N);
-        q.tm_codes = dm + ic;
-        // W2: 2-D meta; W1: 3-D over the adjacent W1 / W3 meta (one box feeds both matrices);
-        // W3's own descriptor is not needed by the kernels
-        const bool pair = m == 0 && y.q[wi][1].codes != nullptr;
-        if (m == 2 || pair) {
-          maps_ok &= encode_meta(&hm[im], q.meta, N, K / DYMOE_GROUP, pair ? 2 : 1, gq);
-          q.tm_meta = dm + im;
-        }
-      }
+  for (int ex = 0; ex < d->M; ++ex) {
+    const int rc = bind_expert(L, ex, d->experts[ex], nullptr);
+    if (rc) {
+      dymoe_layer_destroy(L);
+      return rc;
     }
   }
-  if (e == cudaSuccess && !maps_ok) {
-    dymoe_layer_destroy(L);
-    return fail(DYMOE_ERR_CUDA, "dymoe_layer_create: cuTensorMapEncodeTiled failed");
-  }
-  if (e == cudaSuccess)
-    e = cudaMemcpy(L->tmap_pool, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess)
-    e = cudaMemcpy(L->dev, L->host.data(), sizeof(DevExpert) * d->M, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     dymoe_layer_destroy(L);
     return cuda_fail(e, "dymoe_layer_create");
   }
   *out = L;
+  return ok();
+}
+
+int dymoe_layer_set_expert(dymoe_layer* L, int expert, const dymoe_expert_desc* desc,
+                           dymoe_stream_t stream) {
+  CHECK_ARG(L != nullptr, "layer: must not be NULL");
+  CHECK_ARG(desc != nullptr, "desc: must not be NULL");
+  CHECK_ARG(expert >= 0 && expert < L->M, "expert: must be in [0, %d)", L->M);
+  const int rc = validate_expert(*desc, expert);
+  if (rc) return rc;
+  const int rb = bind_expert(L, expert, *desc, S(stream));
+  if (rb) return rb;
   return ok();
 }
 

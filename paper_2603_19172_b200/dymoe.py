@@ -29,6 +29,7 @@ EXPORTED = [
     "dymoe_gather_rows", "dymoe_renorm_weights", "dymoe_predict_ws_bytes", "dymoe_predict_next",
     "dymoe_pool_create", "dymoe_pool_destroy", "dymoe_pool_lookup", "dymoe_pool_insert",
     "dymoe_pool_pin", "dymoe_pool_unpin", "dymoe_pool_snapshot", "dymoe_pool_used",
+    "dymoe_layer_set_expert",
 ]
 
 
@@ -124,6 +125,7 @@ def lib():
             "dymoe_pool_unpin": [vp, ci, ci],
             "dymoe_pool_snapshot": [vp, vp, ci, ctypes.POINTER(ci)],
             "dymoe_pool_used": [vp],
+            "dymoe_layer_set_expert": [vp, ci, ctypes.POINTER(ExpertDesc), vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -321,6 +323,19 @@ def dymoe_predict_next(phase, h, w_gate_next, k_route, t, stream=None):
     return ex[:k], pr[:k], lg
 
 
+def _fill_desc(d, ex):
+    for n in ("w1", "w3", "w2"):
+        t = ex.get(n)
+        setattr(d, n, _p(_u16(t)) if t is not None else None)
+    for b, wi in WIDTH_INDEX.items():
+        q = ex.get("q%d" % b)
+        if q is None:
+            continue
+        for mi, n in enumerate(("w1", "w3", "w2")):
+            c, s_, z = q[n]
+            d.q[wi][mi] = QMat(_p(c), _p(s_), _p(z))
+
+
 # ---------------------------------------------------------------------------------------------
 class PoolEntry(ctypes.Structure):
     _fields_ = [("layer", ctypes.c_int), ("expert", ctypes.c_int), ("bits", ctypes.c_int),
@@ -388,20 +403,10 @@ class MoELayer:
         self.k = k_route
         self.hidden = hidden
         self.ffn = ffn
-        self._keep = experts
+        self._keep = list(experts)
         arr = (ExpertDesc * self.M)()
         for e, ex in enumerate(experts):
-            d = arr[e]
-            for n in ("w1", "w3", "w2"):
-                t = ex.get(n)
-                setattr(d, n, _p(_u16(t)) if t is not None else None)
-            for b, wi in WIDTH_INDEX.items():
-                q = ex.get("q%d" % b)
-                if q is None:
-                    continue
-                for mi, n in enumerate(("w1", "w3", "w2")):
-                    c, s, z = q[n]
-                    d.q[wi][mi] = QMat(_p(c), _p(s), _p(z))
+            _fill_desc(arr[e], ex)
         desc = LayerDesc(self.M, k_route, hidden, ffn, arr)
         h = ctypes.c_void_p()
         _check(lib().dymoe_layer_create(ctypes.byref(desc), ctypes.byref(h)))
@@ -414,6 +419,14 @@ class MoELayer:
                 self.handle = None
         except Exception:
             pass
+
+    def set_expert(self, e, expert, stream=None):
+        """dymoe_layer_set_expert: rebind expert e to the formats in `expert` (same dict layout
+        as the constructor's; absent widths are unbound).  Stream-ordered."""
+        d = ExpertDesc()
+        _fill_desc(d, expert)
+        _check(lib().dymoe_layer_set_expert(self.handle, e, ctypes.byref(d), _stream(stream)))
+        self._keep[e] = expert
 
     def refresh(self, stream=None):
         """dymoe_layer_refresh: rebuild the derived dequant metadata after re-quantizing."""
