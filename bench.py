@@ -60,7 +60,7 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled every 50 ms during the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -74,7 +74,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -568,7 +568,8 @@ def cpu_baseline(cfg, args, prefill, frac=8):
     t_ctrl = time.perf_counter() - t0
     # FFN sample: 1/frac of expert 0's rows (W1/W3 rows and the matching W2 columns) at its width
     e0 = ex[0]
-    Fs = cfg.ffn // frac
+    Fs = max(128, cfg.ffn // frac // 128 * 128)   # whole quantization groups of W2's K
+    frac = cfg.ffn / Fs
     sub = {"w1": e0["w1"][:Fs].float().numpy(), "w3": e0["w3"][:Fs].float().numpy(),
            "w2": e0["w2"][:, :Fs].contiguous().float().numpy()}
     b = int(bits[0]) or 4
@@ -582,8 +583,8 @@ def cpu_baseline(cfg, args, prefill, frac=8):
     n_active = int((np.diff(perm["expert_off"]) > 0).sum())
     step_s = t_ctrl + t_ffn * n_active
     return {"value": cfg.T / step_s, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": "route+score+assign+permute for all %d tokens; FFN of 1/%d of one expert "
-                      "(Int%d, %d rows) scaled x%d and x%d active experts" % (cfg.T, frac, b, n_rows, frac, n_active),
+            "sample": "route+score+assign+permute for all %d tokens; FFN of 1/%g of one expert "
+                      "(Int%d, %d rows) scaled x%g and x%d active experts" % (cfg.T, frac, b, n_rows, frac, n_active),
             "blas_threads": torch.get_num_threads()}
 
 
@@ -614,7 +615,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--steps", type=int, default=512)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])
