@@ -19,9 +19,16 @@ One step of layer l (`forward`):
   3. dymoe_moe_forward with the SERVED widths as forced bits.
 `prefetch(l, bits)` runs step 2 ahead of time (e.g. for the widths dymoe_predict_next predicts
 for the next layer), on the caller's stream.
+
+Host-offload variant (the paper's own setting): with masters in (pinned)
+host memory, BF16 becomes a pool format like the packed ones (the arena holds a bf16 copy), and a
+miss first copies the expert's bf16 master host -> device into a staging buffer (the paper's
+PCIe / C2C transfer), then quantizes it into the slot (or, for BF16, copies it into the slot).
 All device work is ordered on one stream, so an arena range is only overwritten after the kernels
 already queued on it have read it.
 """
+import contextlib
+
 import torch
 
 from . import dymoe as d
@@ -35,14 +42,23 @@ def _al(n):
 
 class ExpertStore:
     def __init__(self, masters, k_route, hidden, ffn, capacity, device="cuda"):
-        """masters: [layer][expert] dicts with bf16 'w1', 'w3' [F, Hd] and 'w2' [Hd, F] on the
-        device.  capacity: arena bytes for packed formats."""
+        """masters: [layer][expert] dicts with bf16 'w1', 'w3' [F, Hd] and 'w2' [Hd, F], on the
+        device (packed formats pooled) or in host memory (host-offload: every format pooled,
+        pinned host tensors recommended).  capacity: arena bytes."""
         self.masters = masters
         self.k, self.hidden, self.ffn = k_route, hidden, ffn
         self.L, self.M = len(masters), len(masters[0])
+        self.device = torch.device(device)
+        self.host = not masters[0][0]["w1"].is_cuda
         self.arena = torch.empty(capacity, dtype=torch.uint8, device=device)
         self.pool = d.Pool(capacity)
-        self.layers = [d.MoELayer([dict(e) for e in ml], k_route, hidden, ffn) for ml in masters]
+        if self.host:
+            # one staging buffer for an expert's three bf16 matrices (reused, stream-ordered)
+            self.stage = {n: torch.empty(N, K, dtype=torch.bfloat16, device=device)
+                          for n, N, K in self._shapes()}
+            self.layers = [d.MoELayer([{} for _ in ml], k_route, hidden, ffn) for ml in masters]
+        else:
+            self.layers = [d.MoELayer([dict(e) for e in ml], k_route, hidden, ffn) for ml in masters]
         self.bound = [[None] * self.M for _ in range(self.L)]   # (bits, offset) of the bound format
         self.stats = dict(hits=0, misses=0, promotions=0, evictions=0, quantized_bytes=0)
 
@@ -53,10 +69,19 @@ class ExpertStore:
     def entry_bytes(self, bits):
         n = 0
         for _, N, K in self._shapes():
-            n += _al(N * K * bits // 8) + _al(N * (K // d.GROUP) * 4) + _al(N * (K // d.GROUP))
+            if bits == 16:
+                n += _al(N * K * 2)
+            else:
+                n += _al(N * K * bits // 8) + _al(N * (K // d.GROUP) * 4) + _al(N * (K // d.GROUP))
         return n
 
     def _views(self, off, bits):
+        if bits == 16:
+            out = {}
+            for name, N, K in self._shapes():
+                out[name] = self.arena[off:off + N * K * 2].view(torch.bfloat16).view(N, K)
+                off += _al(N * K * 2)
+            return out
         q = {}
         for name, N, K in self._shapes():
             nc, ns, nz = N * K * bits // 8, N * (K // d.GROUP) * 4, N * (K // d.GROUP)
@@ -70,8 +95,10 @@ class ExpertStore:
         return q
 
     def _bind(self, l, e, bits, off, stream):
-        ex = dict(self.masters[l][e])
-        if bits is not None:
+        ex = {} if self.host else dict(self.masters[l][e])
+        if bits == 16:
+            ex.update(self._views(off, 16))
+        elif bits is not None:
             ex["q%d" % bits] = self._views(off, bits)
         self.layers[l].set_expert(e, ex, stream=stream)
         self.bound[l][e] = (bits, off) if bits is not None else None
@@ -84,7 +111,7 @@ class ExpertStore:
         try:
             for e, b in enumerate(bits):
                 b = int(b)
-                if b in (0, 16):
+                if b == 0 or (b == 16 and not self.host):
                     served[e] = b
                     continue
                 out, sb, off = self.pool.lookup(l, e, b)
@@ -99,9 +126,15 @@ class ExpertStore:
                         self.stats["evictions"] += 1
                         self._bind(l2, e2, None, None, stream)
                     views = self._views(off, b)
-                    jobs = [(self.masters[l][e][n], b, views[n]) for n in ("w1", "w3", "w2")]
-                    d.dymoe_quantize_batched(jobs, stream=stream)
-                    self.stats["quantized_bytes"] += self.entry_bytes(b)
+                    src = self._source(l, e, stream)
+                    if b == 16:
+                        with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
+                            for n in ("w1", "w3", "w2"):
+                                views[n].copy_(src[n], non_blocking=True)
+                    else:
+                        jobs = [(src[n], b, views[n]) for n in ("w1", "w3", "w2")]
+                        d.dymoe_quantize_batched(jobs, stream=stream)
+                        self.stats["quantized_bytes"] += self.entry_bytes(b)
                     self._bind(l, e, b, off, stream)
                     sb = b
                 self.pool.pin(l, e)
@@ -113,6 +146,16 @@ class ExpertStore:
         return served
 
     prefetch = prepare
+
+    def _source(self, l, e, stream):
+        """The expert's bf16 master on the device (host-offload: copied into the staging buffer)."""
+        if not self.host:
+            return self.masters[l][e]
+        with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
+            for n in ("w1", "w3", "w2"):
+                self.stage[n].copy_(self.masters[l][e][n], non_blocking=True)
+        self.stats["h2d_bytes"] = self.stats.get("h2d_bytes", 0) + sum(t.numel() * 2 for t in self.stage.values())
+        return self.stage
 
     def assigned_bits(self, l, x, logits, ladder, num_layers, phase, attn_mass=None, k_tokens=0):
         """Steps route -> score -> assign of dymoe_moe_forward (libdymoe kernels); returns the

@@ -50,3 +50,37 @@ def test_pooled_stack_matches_oracle(phase, T):
         assert err <= FFN_TOL, (step, err)
     s = store.stats
     assert s["hits"] > 0 and s["misses"] > 0 and s["evictions"] > 0, s
+
+
+def test_host_offload_stack_matches_oracle():
+    """Masters in pinned host memory: every format, BF16 included, is a pool entry
+    filled by a host->device copy (+ quantization); steps equal the oracle with served widths."""
+    import paper_2603_19172_b200.dymoe as d
+    from paper_2603_19172_b200.pool import ExpertStore
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(6)
+    L = 3
+    masters = [[{n: t.pin_memory() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 60 + l)]
+               for l in range(L)]
+    probe = ExpertStore([[{n: t.cuda() for n, t in e.items()} for e in masters[0]]], cfg.k,
+                        cfg.hidden, cfg.ffn, 1 << 20)
+    per_layer = cfg.M * (probe.entry_bytes(16) + probe.entry_bytes(8))
+    del probe
+    store = ExpertStore(masters, cfg.k, cfg.hidden, cfg.ffn, int(per_layer * 1.2))
+    assert store.host
+    lad_bits, lad_l = (16, 8, 4, 2), (0.2, 0.5, 0.8)
+    lad = d.make_ladder(lad_bits, lad_l)
+    o_lad = o_sched.Ladder(lad_bits, lad_l)
+    np_masters = [[{n: t.float().numpy() for n, t in e.items()} for e in ml] for ml in masters]
+    for step in range(10):
+        l = step % L
+        x, lg, _ = synthetic.layer_inputs(cfg, 700 + step)
+        y, served, want, forced = store.forward(l, x.cuda(), lg.cuda(), lad, 32)
+        torch.cuda.synchronize()
+        for e in range(cfg.M):
+            if want[e]:
+                assert served[e] >= want[e]
+        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), np_masters[l], l, 32, o_lad, cfg.k,
+                                forced_bits=np.array(forced, np.uint8))
+        err = np.abs(y.cpu().numpy() - ref["y"]).max() / max(np.abs(ref["y"]).max(), 1e-30)
+        assert err <= FFN_TOL, (step, err)
+    assert store.stats["h2d_bytes"] > 0 and store.stats["evictions"] > 0, store.stats
