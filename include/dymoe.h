@@ -243,6 +243,15 @@ int dymoe_pool_unpin(dymoe_pool* pool, int layer, int expert);
 int dymoe_pool_snapshot(const dymoe_pool* pool, dymoe_pool_entry* out, int max, int* n);
 size_t dymoe_pool_used(const dymoe_pool* pool);
 
+/* Heavy-hitter attention mass (the input of Eq. 1, reading R1) without
+ * materializing the attention matrix: a[h][j] = sum_{i >= j} softmax_{j' <= i}(scale *
+ * q[h][i] . k[h][j'])[j] (causal).  Two passes of tensor-core Q K^T tiles (row max / sum, then
+ * column sums of P), fixed summation order.
+ *   q, k [H][T][d] bf16 device (d == 128, 16-byte aligned); scratch [2*H*T] f32 device;
+ *   a_out [H][T] f32 device (the attn_mass argument of dymoe_score / dymoe_fwd_opts).          */
+int dymoe_attention_mass(const uint16_t* q, const uint16_t* k, int H, int T, int d, float scale,
+                         float* scratch, float* a_out, dymoe_stream_t stream);
+
 /* Look-ahead prediction of the next layer's experts (PAPER.md "Phase-Adaptive
  * Prefetcher", Eqs. 6-8).  Eq. 6: logits = h · W_g^(l+1)^T (fp32, one rounding per
  * multiply-add in k order), g_hat = softmax.  PREFILL (Eq. 7): c_e = #{tokens whose top-k_route

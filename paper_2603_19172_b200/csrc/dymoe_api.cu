@@ -572,6 +572,22 @@ int dymoe_combine(const float* y_perm, const int32_t* inv_row, const float* topk
   return ok();
 }
 
+int dymoe_attention_mass(const uint16_t* q, const uint16_t* k, int H, int T, int d, float scale,
+                         float* scratch, float* a_out, dymoe_stream_t stream) {
+  CHECK_ARG(H >= 0 && T >= 0, "H/T: must be >= 0");
+  CHECK_ARG(d == 128, "d: only head dim 128 is implemented");
+  if (H == 0 || T == 0) return ok();
+  CHECK_ARG(q && k && scratch && a_out, "q/k/scratch/a_out: must not be NULL");
+  int rc = check_ptr_align(q, 16, "q");
+  if (rc) return rc;
+  rc = check_ptr_align(k, 16, "k");
+  if (rc) return rc;
+  CHECK_LAUNCH(launch_attention_mass(q, k, H, T, d, scale, scratch, scratch + (size_t)H * T, a_out,
+                                     S(stream)),
+               "dymoe_attention_mass");
+  return ok();
+}
+
 size_t dymoe_predict_ws_bytes(int T, int M, int k_route) {
   if (T < 1 || M < 1 || k_route < 1) return 0;
   const size_t TM = (size_t)T * M, TK = (size_t)T * k_route;

@@ -115,6 +115,9 @@ cudaError_t launch_predict_next(int phase, const uint16_t* h, const uint16_t* wg
                                 int M, int k, int t, float* logits, int32_t* topk_idx,
                                 float* topk_w, float* probs, float* value, int32_t* experts,
                                 float* priority, int32_t* n_out, cudaStream_t s);
+cudaError_t launch_attention_mass(const uint16_t* Q, const uint16_t* K, int H, int T, int d,
+                                  float scale, float* m_scratch, float* l_scratch, float* a_out,
+                                  cudaStream_t s);
 cudaError_t launch_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uint8_t* bits,
                                   int T, int k, int renorm, float* w_out, cudaStream_t s);
 cudaError_t launch_ep_plan(const int32_t* expert_off, int M, int P, int32_t* send_counts,

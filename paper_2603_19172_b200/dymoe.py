@@ -29,7 +29,7 @@ EXPORTED = [
     "dymoe_gather_rows", "dymoe_renorm_weights", "dymoe_predict_ws_bytes", "dymoe_predict_next",
     "dymoe_pool_create", "dymoe_pool_destroy", "dymoe_pool_lookup", "dymoe_pool_insert",
     "dymoe_pool_pin", "dymoe_pool_unpin", "dymoe_pool_snapshot", "dymoe_pool_used",
-    "dymoe_layer_set_expert",
+    "dymoe_layer_set_expert", "dymoe_attention_mass",
 ]
 
 
@@ -126,6 +126,7 @@ def lib():
             "dymoe_pool_snapshot": [vp, vp, ci, ctypes.POINTER(ci)],
             "dymoe_pool_used": [vp],
             "dymoe_layer_set_expert": [vp, ci, ctypes.POINTER(ExpertDesc), vp],
+            "dymoe_attention_mass": [vp, vp, ci, ci, ci, ctypes.c_float, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -295,6 +296,17 @@ def dymoe_combine(y_perm, inv_row, topk_w, renorm=True, out_dtype=DYMOE_OUT_F32,
     _check(lib().dymoe_combine(_p(y_perm), _p(inv_row), _p(topk_w), T, k, Hd, int(renorm),
                                out_dtype, _p(y), _stream(stream)))
     return y
+
+
+def dymoe_attention_mass(q, k, scale=None, stream=None):
+    """Causal attention mass a [H][T] f32 from q, k [H][T][d] bf16 (include/dymoe.h)."""
+    H, T, dd = q.shape
+    scale = dd ** -0.5 if scale is None else scale
+    scratch = torch.empty(2 * H * T, dtype=torch.float32, device=q.device)
+    a = torch.empty(H, T, dtype=torch.float32, device=q.device)
+    _check(lib().dymoe_attention_mass(_p(_u16(q)), _p(_u16(k)), H, T, dd, float(scale), _p(scratch),
+                                      _p(a), _stream(stream)))
+    return a
 
 
 def dymoe_renorm_weights(topk_idx, topk_w, bits, renorm=True, stream=None):
