@@ -294,6 +294,7 @@ def run_ours(args, rank, world, device):
                     "achieved": tfl, "peak": pk, "unit": "TFLOP/s", "frac": tfl / pk,
                     "traffic": traffic, "traffic_capture": tr, "peak_src": peaks["src"] + " bf16 sustained",
                     "frac_of_2250": tfl / 2250.0, "w13_tflops": tfl13,
+                    "w2_tflops": (fl / 3) / (sum(w2_ms) / 1e3) / 1e12,
                     "ffn_share_of_step": ffn_ms / ms if world == 1 else None,
                     "algorithmic_flops_per_step": fl / K, "hbm_GBs_ffn": achieved_ffn}
     res = None

@@ -1,18 +1,30 @@
-timeout 600 python -m pytest tests/test_gpu_attention.py -q -x 2>&1 | tail -5
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "prefill" 2>&1 | tail -1
 python - <<'PY'
-import torch
+import torch, sys
+sys.path.insert(0, '.')
+import synthetic, bench
 import paper_2603_19172_b200.dymoe as d
 d.lib()
-H, T = 32, 2048
-q = torch.randn(H, T, 128, device='cuda').to(torch.bfloat16)
-k = torch.randn(H, T, 128, device='cuda').to(torch.bfloat16)
-for _ in range(3): d.dymoe_attention_mass(q, k)
-torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record()
-for _ in range(10): d.dymoe_attention_mass(q, k)
-e1.record(); torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / 10
-fl = 2 * 2 * T * T * 128 * H / 2
-print('attention mass H=32 T=2048: %.1f us, %.0f TFLOP/s (two causal QK^T passes)' % (ms * 1e3, fl / ms / 1e9))
+dev = torch.device('cuda')
+cfg = synthetic.CONFIGS['mixtral_prefill']
+layers = bench.build_layer_copies(d, cfg, 2, dev)
+lad = d.make_ladder(bench.LADDER_BITS, bench.LADDER_LAMBDAS)
+x, lg, a = synthetic.layer_inputs(cfg, 5, dev)
+for b in (16, 8, 4, 2):
+    forced = torch.full((8,), b, dtype=torch.uint8, device=dev)
+    ws = [L.workspace(cfg.T, dev) for L, _ in layers]
+    for i in range(3): layers[i % 2][0].forward(x, lg, lad, 0, 32, phase=d.DYMOE_PREFILL, attn_mass=a, forced_bits=forced, ws=ws[i % 2])
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(8)]
+    for r in evs:
+        for e in r: e.record()
+    for i in range(8):
+        layers[i % 2][0].forward(x, lg, lad, 0, 32, phase=d.DYMOE_PREFILL, attn_mass=a, forced_bits=forced, ws=ws[i % 2], prof_events=evs[i])
+    torch.cuda.synchronize()
+    off = layers[0][0].views(cfg.T, ws[0])['expert_off'].cpu()
+    n = int(off[-1])
+    fl = 6.0 * cfg.hidden * cfg.ffn * n
+    t13 = sum(e[0].elapsed_time(e[1]) for e in evs) / 8 / 1e3
+    t2 = sum(e[1].elapsed_time(e[2]) for e in evs) / 8 / 1e3
+    print('bits', b, 'W13 %.0f TF/s  W2 %.0f TF/s  rows %d' % (fl * 2 / 3 / t13 / 1e12, fl / 3 / t2 / 1e12, n), flush=True)
 PY

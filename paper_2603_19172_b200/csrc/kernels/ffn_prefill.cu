@@ -29,6 +29,8 @@
 //    both CTAs' TMA bytes (cta_group::2 TMA signals the leader) and both CTAs' producer arrivals.
 //  * persistent grid: CTA pair c walks the (expert, 256-token tile, 256-column tile) list with
 //    stride (number of pairs).
+#include <cstdlib>
+
 #include "../dymoe_internal.cuh"
 
 namespace dymoe {
@@ -41,7 +43,7 @@ constexpr int NCOL = 2 * BNH;     // TMEM columns per accumulator
 constexpr int BK = 64;            // k per stage (one 128-byte swizzle atom row)
 constexpr int ROWB = BK * 2;      // bytes per tile row (K-major)
 constexpr int KPER = BK / 2;      // k per B-producer thread per stage (two threads per row)
-constexpr int STAGES = 4;
+constexpr int STAGES = 5;
 constexpr int A_BYTES = BM * BK * 2;            // 16 KB
 constexpr int B_BYTES = BNH * BK * 2;           // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -49,7 +51,7 @@ constexpr int kBWarps = 8, kEpiWarps = 4;
 constexpr int kBWarp0 = 2, kEpiWarp0 = kBWarp0 + kBWarps;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;   // 448
 constexpr int kBThreads = kBWarps * 32;
-constexpr int PF = 8;                                   // raw stages in flight per thread
+constexpr int PF = 6;                                   // raw stages in flight per thread
 constexpr int RAW_CHUNK = kBThreads * 16;               // one 16-byte granule per thread
 constexpr int RAW_SLOT = ((KPER + 15) / 16) * RAW_CHUNK;  // Int8: KPER bytes per thread per stage
 constexpr int RAW_BYTES = PF * RAW_SLOT + PF * kBThreads * 4;   // + dequant words
@@ -328,12 +330,12 @@ __device__ __forceinline__ void store_stage(const RawStage<BE>& r, uint32_t dst,
 // full_cl: shared::cluster address of the leader's full_bar[0] (stage s at + 8 s)
 template <int BE>
 __device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* metap, int mstride,
-                                        int khalf, int tb, int wr, int nk, uint32_t sbase,
+                                        int khalf, int tb, int wr, int kb0, int kb1, uint32_t sbase,
                                         uint32_t full_cl, uint32_t empty_bar, int& stage,
                                         uint32_t& phase) {
   const int j0 = khalf * (KPER / 8);
   if constexpr (BE == 16) {
-    for (int kb = 0; kb < nk; ++kb) {
+    for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(empty_bar + stage * 8, phase ^ 1);
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive_cl(full_cl + stage * 8);
@@ -343,12 +345,12 @@ __device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* met
     const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;
 #pragma unroll
     for (int p = 0; p < PF - 1; ++p) {
-      if (p < nk) issue_raw<BE>(raw_base, tb, p, rowp, metap, mstride, khalf, p);
+      if (kb0 + p < kb1) issue_raw<BE>(raw_base, tb, p, rowp, metap, mstride, khalf, kb0 + p);
       asm volatile("cp.async.commit_group;" ::: "memory");
     }
     int slot = 0, slot_iss = PF - 1;
-    for (int kb = 0; kb < nk; ++kb) {
-      if (kb + PF - 1 < nk) issue_raw<BE>(raw_base, tb, slot_iss, rowp, metap, mstride, khalf, kb + PF - 1);
+    for (int kb = kb0; kb < kb1; ++kb) {
+      if (kb + PF - 1 < kb1) issue_raw<BE>(raw_base, tb, slot_iss, rowp, metap, mstride, khalf, kb + PF - 1);
       asm volatile("cp.async.commit_group;" ::: "memory");
       if (++slot_iss == PF) slot_iss = 0;
       asm volatile("cp.async.wait_group %0;" ::"n"(PF - 1) : "memory");
@@ -374,15 +376,20 @@ struct Sched {
 };
 struct Tile {
   int e, m0, n0, rows;   // expert, first token row (relative), first output column, valid tokens
+  int kb0, kb1;          // k-block range of this tile (GEMM 2: one of two K halves)
 };
+// ntiles_n counts (n tile, k half) pairs when ksplit == 2
 __device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t, int ntiles_n,
-                                        int nstep) {
+                                        int nstep, int nk, int ksplit) {
   int i = 0;
   while (S.first[i + 1] <= t) ++i;
   Tile r;
   r.e = S.expert[i];
   const int local = t - S.first[i];
-  const int mt = local / ntiles_n, nt = local - mt * ntiles_n;
+  const int mt = local / ntiles_n, ntk = local - mt * ntiles_n;
+  const int nt = ntk / ksplit, kh = ntk - nt * ksplit;
+  r.kb0 = (int)((long long)kh * nk / ksplit);
+  r.kb1 = (int)((long long)(kh + 1) * nk / ksplit);
   const int n_e = a.expert_off[r.e + 1] - a.expert_off[r.e];
   r.m0 = mt * TOK;
   r.n0 = nt * nstep;
@@ -392,7 +399,7 @@ __device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t,
 
 template <bool W13>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
+k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksplit_w2) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ Sched S;
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
@@ -402,7 +409,12 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
   const int K = W13 ? a.Hd : a.F;
   const int NWR = W13 ? a.F : a.Hd;                  // weight rows per matrix
   const int nstep = W13 ? BNH : NCOL;                // output features per tile
-  const int ntiles_n = (NWR + nstep - 1) / nstep;
+  // GEMM 2 (K = F long, only Hd / 256 column tiles per token tile) splits K in two halves whose
+  // fp32 partials are added into the zeroed y_perm: exactly two addends per element, so the
+  // result does not depend on their order (deterministic).  GEMM 1 is not split (SwiGLU needs the
+  // full sums).
+  const int KSPLIT = W13 ? 1 : ksplit_w2;
+  const int ntiles_n = (NWR + nstep - 1) / nstep * KSPLIT;
   const int nk = K / BK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
@@ -459,7 +471,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < n_tiles; t += npairs) {
-        const Tile T = tile_at(S, a, t, ntiles_n, nstep);
+        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
         const int row0 = a.expert_off[T.e] + T.m0 + (int)rank * BM;
         const bool bf = a.bits[T.e] == 16;
         const CUtensorMap* tmB = nullptr;
@@ -469,7 +481,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
           tmB = E.tm_wp[W13 ? (int)rank : 2];
           brow0 = T.n0 + (W13 ? 0 : (int)rank * BNH);
         }
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = T.kb0; kb < T.kb1; ++kb) {
           mbar_wait(empty0 + stage * 8, phase ^ 1);
           mbar_expect_tx_cl(full_cl + stage * 8, A_BYTES + (bf ? B_BYTES : 0));
           tma2d_pair(sA(stage), &tmA, kb * BK, row0, full_cl + stage * 8);
@@ -485,16 +497,17 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
       uint32_t phase = 0;
       int i = 0;
       for (int t = pair; t < n_tiles; t += npairs, ++i) {
+        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
         const int b = i & 1;
         mbar_wait(smem_u32(&tempty_bar[b]), ((i >> 1) & 1) ^ 1);
         tc_fence_after();
-        for (int kb = 0; kb < nk; ++kb) {
+        for (int kb = T.kb0; kb < T.kb1; ++kb) {
           mbar_wait(full0 + stage * 8, phase);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk)
             tc_mma_pair(tmem + b * NCOL, sw_desc(sA(stage) + kk * 32), sw_desc(sB(stage) + kk * 32),
-                        IDESC, (kb | kk) != 0);
+                        IDESC, ((kb - T.kb0) | kk) != 0);
           tc_commit_pair(empty0 + stage * 8);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -509,7 +522,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
     int stage = 0;
     uint32_t phase = 0;
     for (int t = pair; t < n_tiles; t += npairs) {
-      const Tile T = tile_at(S, a, t, ntiles_n, nstep);
+      const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
       const int be = a.bits[T.e];
       const DevExpert& E = a.experts[T.e];
       // GEMM 1: rank 0 = W1 rows n0.., rank 1 = the same W3 rows; GEMM 2: W2 rows
@@ -524,10 +537,10 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
       const uint8_t* rowp = codes + (size_t)row * row_bytes;
       const uint32_t* metap = meta ? meta + row : nullptr;   // group-major: stride NWR
       switch (be) {
-        case 2: produce<2>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
-        case 4: produce<4>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
-        case 8: produce<8>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
-        default: produce<16>(rowp, metap, NWR, khalf, tb, wr, nk, sbase, full_cl, empty0, stage, phase); break;
+        case 2: produce<2>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
+        case 4: produce<4>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
+        case 8: produce<8>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
+        default: produce<16>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
       }
     }
   } else {
@@ -536,7 +549,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
     const int trow = q * 32 + lane;               // token row within this CTA's half
     int i = 0;
     for (int t = pair; t < n_tiles; t += npairs, ++i) {
-      const Tile T = tile_at(S, a, t, ntiles_n, nstep);
+      const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
       const int b = i & 1;
       mbar_wait(smem_u32(&tfull_bar[b]), (i >> 1) & 1);
       tc_fence_after();
@@ -572,9 +585,14 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA) {
           tmem_ld32(tbase + cc * 32, v);
           tmem_ld_wait();
           if (live && T.n0 + cc * 32 < NWR) {   // last W2 tile may overhang Hd (clamped rows)
-            uint4* dstp = reinterpret_cast<uint4*>(a.y_perm + grow * a.Hd + T.n0 + cc * 32);
+            // one of the two K halves: add into the zeroed output (two addends per element)
+            float* dstp = a.y_perm + grow * a.Hd + T.n0 + cc * 32;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) dstp[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 8; ++j)
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dstp + 4 * j),
+                           "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
+                           "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
+                           : "memory");
           }
         }
       }
@@ -635,11 +653,14 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
                                          a.expert_off + a.M, rows, reinterpret_cast<uint4*>(xp));
   }
   const int grid = sms / 2 * 2;   // whole CTA pairs, one CTA per SM
-  k_prefill_gemm<true><<<grid, kThreads, kSmem, s>>>(a, tm13);
+  static const int ksplit = getenv("DYMOE_PREFILL_W2_KSPLIT") ? atoi(getenv("DYMOE_PREFILL_W2_KSPLIT")) : 2;
+  k_prefill_gemm<true><<<grid, kThreads, kSmem, s>>>(a, tm13, 1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   record_ev(ev, 1, s);
-  k_prefill_gemm<false><<<grid, kThreads, kSmem, s>>>(a, tm2);
+  e = cudaMemsetAsync(a.y_perm, 0, (size_t)rows * a.Hd * sizeof(float), s);   // split-K target
+  if (e != cudaSuccess) return e;
+  k_prefill_gemm<false><<<grid, kThreads, kSmem, s>>>(a, tm2, ksplit == 1 ? 1 : 2);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   record_ev(ev, 2, s);
