@@ -273,6 +273,7 @@ def run_ours(args, rank, world, device):
 
     # ---------------- quantize kernel (row a4), alone: one Mixtral expert per width
     quant = measure_quantize(d, layers[0][1], cfg, peaks)
+    extras = measure_extras(d, cfg, phase, device, peaks)
 
     if phase == d.DYMOE_DECODE:
         # dominant kernel: the W1/W3 fused-dequant SwiGLU GEMV (HBM-bound); per launch the
@@ -318,6 +319,7 @@ def run_ours(args, rank, world, device):
             "e2e": e2e,
             "gpu_launches": launches_per_step * K,
             "quantize": quant,
+            "next_rows": extras,
             "tensor_tflops_ffn": fl / (ffn_ms / 1e3) / 1e12,
         }
         if not args.no_cpu_baseline and world == 1:
@@ -521,6 +523,53 @@ def load_traffic(kernel_key):
     with open(p) as f:
         j = json.load(f)
     return j.get(kernel_key)
+
+
+def measure_extras(d, cfg, phase, device, peaks, reps=10):
+    """SURVEY §8f rows built beside the path, timed alone (CUDA events): the look-ahead expert
+    predictor (Eqs. 6-8) on this workload's tokens, and the causal attention mass (f3) for a
+    Mixtral-shaped attention (H = 32, d = 128) over this workload's tokens (prefill)."""
+    out = {}
+    T = cfg.T
+    g = torch.Generator(device=device).manual_seed(11)
+    h = torch.randn(T, cfg.hidden, generator=g, device=device).to(torch.bfloat16)
+    wg = (torch.randn(cfg.M, cfg.hidden, generator=g, device=device) / cfg.hidden ** 0.5).to(torch.bfloat16)
+    nbytes = d.lib().dymoe_predict_ws_bytes(T, cfg.M, cfg.k)
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    ex = torch.empty(cfg.M, dtype=torch.int32, device=device)
+    pr = torch.empty(cfg.M, dtype=torch.float32, device=device)
+    n = torch.empty(1, dtype=torch.int32, device=device)
+    st = torch.cuda.current_stream()
+
+    def predict():
+        d._check(d.lib().dymoe_predict_next(phase, d._p(d._u16(h)), d._p(d._u16(wg)), T, cfg.hidden,
+                                            cfg.M, cfg.k, 2, d._p(ws), nbytes, d._p(ex), d._p(pr),
+                                            d._p(n), None, d._stream(st)))
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e3
+
+    us = timed(predict)
+    out["predict_next"] = {"us": us, "GB/s": (T * cfg.hidden * 2) / (us * 1e-6) / 1e9,
+                           "note": "Eq. 6 gate product + Eq. 7/8 selection, h [T][Hd] read once"}
+    if phase == d.DYMOE_PREFILL:
+        H = 32
+        q = torch.randn(H, T, 128, generator=g, device=device).to(torch.bfloat16)
+        k = torch.randn(H, T, 128, generator=g, device=device).to(torch.bfloat16)
+        us = timed(lambda: d.dymoe_attention_mass(q, k))
+        fl = 2 * 2 * T * T * 128 * H / 2
+        out["attention_mass"] = {"us": us, "TFLOP/s": fl / (us * 1e-6) / 1e12, "H": H, "d": 128,
+                                 "note": "two causal Q.K^T passes (row stats, column sums), mma.sync"}
+    return out
 
 
 def measure_quantize(d, experts, cfg, peaks, reps=5):

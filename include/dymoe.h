@@ -253,8 +253,8 @@ int dymoe_attention_mass(const uint16_t* q, const uint16_t* k, int H, int T, int
                          float* scratch, float* a_out, dymoe_stream_t stream);
 
 /* Look-ahead prediction of the next layer's experts (PAPER.md "Phase-Adaptive
- * Prefetcher", Eqs. 6-8).  Eq. 6: logits = h · W_g^(l+1)^T (fp32, one rounding per
- * multiply-add in k order), g_hat = softmax.  PREFILL (Eq. 7): c_e = #{tokens whose top-k_route
+ * Prefetcher", Eqs. 6-8).  Eq. 6: logits = h · W_g^(l+1)^T (fp32 in the order of
+ * reading P1: 32 lane partial sums over 8-element chunks, then an xor butterfly), g_hat = softmax.  PREFILL (Eq. 7): c_e = #{tokens whose top-k_route
  * predicted experts contain e}; requests = the t experts with the largest c_e (> 0), priority =
  * c_e.  DECODE (Eq. 8): requests = top-t of the predicted decode importance (B = 1: the predicted
  * logit row; B > 1: sum over the batch of g_hat), priority = that value.  Order: (value desc,

@@ -9,10 +9,11 @@ Eq. 7 (prefill): c_e = sum_i 1[e in s_i]; prefetch the top-t experts by c_e.
 Eq. 8 (decode):  prefetch TopK_t(g_hat) of the current token.
 
 Readings:
-  P1  the gate product is evaluated in fp32 with one rounding per multiply-add in k order
-      (bf16 x bf16 products are exact in fp32, so this is the plain definition of an fp32 dot
-      product, written out); TopK over g_hat equals TopK over the logits (softmax is monotonic),
-      ties to the lower index (R11) -- the routing oracle (route.route) is reused as is.
+  P1  the gate product is an fp32 dot product in a fixed, stated order (32 lane partial sums
+      over 8-element chunks, sequential within a lane, then an xor butterfly; see gate_logits);
+      bf16 x bf16 products are exact in fp32.  TopK over g_hat equals TopK over the logits
+      (softmax is monotonic), ties to the lower index (R11) -- the routing oracle (route.route)
+      is reused as is.
   P2  Eq. 7's membership test uses k_route (SPEC S:263 open question; "likely-to-be-activated").
       Experts with c_e = 0 are never requested; requests are ordered by (c_e desc, index asc),
       priority = c_e.
@@ -28,18 +29,28 @@ from . import route as _route
 
 
 def gate_logits(h, w_gate):
-    """P1: logits[t][e] = sum_k h[t][k] * w[e][k], fp32, sequential in k.
+    """P1: logits[t][e] = h[t] . w[e] in fp32 with a fixed order: the k values are dealt to 32
+    lanes in 8-element chunks (lane l takes k = 256 j + 8 l + i, i = 0..7, j = 0, 1, ...), each
+    lane accumulates its k's in increasing order (one rounding per multiply-add; bf16 x bf16
+    products are exact in fp32), then the 32 partial sums are combined by the butterfly
+    s_l <- s_l + s_(l xor o) for o = 16, 8, 4, 2, 1 (every lane ends with the same value).
 
-    h float32 [T, Hd] (bf16 values), w_gate float32 [M, Hd] (bf16 values) -> float32 [T, M].
+    h float32 [T, Hd] (bf16 values), w_gate float32 [M, Hd] (bf16 values), Hd % 8 == 0
+    -> float32 [T, M].
     """
     h = np.asarray(h, dtype=np.float32)
     w = np.asarray(w_gate, dtype=np.float32)
     T, Hd = h.shape
     M = w.shape[0]
-    acc = np.zeros((T, M), dtype=np.float32)
+    lanes = np.zeros((T, M, 32), dtype=np.float32)
     for k in range(Hd):
-        acc = (acc + np.outer(h[:, k], w[:, k]).astype(np.float32)).astype(np.float32)
-    return acc
+        lane = (k // 8) % 32
+        prod = np.outer(h[:, k], w[:, k]).astype(np.float32)
+        lanes[:, :, lane] = (lanes[:, :, lane] + prod).astype(np.float32)
+    for o in (16, 8, 4, 2, 1):
+        partner = lanes[:, :, np.arange(32) ^ o]
+        lanes = (lanes + partner).astype(np.float32)
+    return lanes[:, :, 0].copy()
 
 
 def _top_t(values, t, drop_zero):

@@ -32,8 +32,7 @@ __device__ __forceinline__ void load_block(uint32_t* dst, const uint16_t* src, i
     const int r = i / (D / 8), c = i - r * (D / 8);
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r0 + r < T) v = *reinterpret_cast<const uint4*>(src + (size_t)(r0 + r) * D + c * 8);
-    uint32_t* p = dst + r * RS + c * 4;
-    p[0] = v.x; p[1] = v.y; p[2] = v.z; p[3] = v.w;
+    *reinterpret_cast<uint4*>(dst + r * RS + c * 4) = v;
   }
 }
 
@@ -49,20 +48,31 @@ __device__ __forceinline__ void a_frags(const uint32_t* s, int r0, uint32_t (&a)
   }
 }
 
-// acc[n][.] = (rows of A) x (rows n*8.. of the smem block B)^T, 8 n-tiles of 8 columns
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                        uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+
+// acc[n][.] = (rows of A) x (rows n*8.. of the smem block B)^T, 8 n-tiles of 8 columns.
+// B fragments by ldmatrix.x4: matrices (k 0-7, k 8-15) x (n-tiles 2p, 2p+1) of each k16 step.
 __device__ __forceinline__ void tile_product(const uint32_t (&a)[D / 16][4], const uint32_t* sb,
                                              float (&acc)[8][4]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
+  const int lane = threadIdx.x & 31;
+  // lane l supplies the row address of matrix l / 8: n-tile 2p + (l / 16), k half (l / 8) & 1
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(sb) +
+                        (uint32_t)(((lane >> 4) * 8 + (lane & 7)) * RS * 4 + ((lane >> 3) & 1) * 16);
 #pragma unroll
-  for (int n = 0; n < 8; ++n) {
-    acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+  for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks) {
-      const uint32_t b0 = sb[(n * 8 + g) * RS + ks * 8 + c];
-      const uint32_t b1 = sb[(n * 8 + g) * RS + ks * 8 + 4 + c];
-      mma(acc[n], a[ks][0], a[ks][1], a[ks][2], a[ks][3], b0, b1);
+  for (int ks = 0; ks < D / 16; ++ks)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      uint32_t b00, b01, b10, b11;
+      ldsm_x4(base + p * 16 * RS * 4 + ks * 32, b00, b01, b10, b11);
+      mma(acc[2 * p], a[ks][0], a[ks][1], a[ks][2], a[ks][3], b00, b01);
+      mma(acc[2 * p + 1], a[ks][0], a[ks][1], a[ks][2], a[ks][3], b10, b11);
     }
-  }
 }
 
 // Pass 1: one CTA per (head, 64-query block); warp w owns queries q0 + 16w ..
@@ -70,7 +80,7 @@ __global__ void __launch_bounds__(128) k_row_stats(const uint16_t* __restrict__ 
                                                    const uint16_t* __restrict__ K, int T,
                                                    float scale_log2, float* __restrict__ m_out,
                                                    float* __restrict__ l_out) {
-  __shared__ uint32_t sq[BQ * RS], sk[BQ * RS];
+  __shared__ __align__(16) uint32_t sq[BQ * RS], sk[BQ * RS];
   const int h = blockIdx.y, qb = blockIdx.x, q0 = qb * BQ;
   const uint16_t* Qh = Q + (size_t)h * T * D;
   const uint16_t* Kh = K + (size_t)h * T * D;
@@ -134,8 +144,8 @@ __global__ void __launch_bounds__(128) k_col_sums(const uint16_t* __restrict__ Q
                                                   float scale_log2, const float* __restrict__ m_in,
                                                   const float* __restrict__ l_in,
                                                   float* __restrict__ a_out) {
-  __shared__ uint32_t sk[BQ * RS], sq[BQ * RS];
-  __shared__ float sm[BQ], sl[BQ];
+  __shared__ __align__(16) uint32_t sk[BQ * RS], sq[BQ * RS];
+  __shared__ float sm[BQ], sl[BQ];   // row max (log2 units) and 1 / row sum of the query block
   const int h = blockIdx.y, kb = blockIdx.x, k0 = kb * BQ;
   const uint16_t* Qh = Q + (size_t)h * T * D;
   const uint16_t* Kh = K + (size_t)h * T * D;
@@ -153,7 +163,7 @@ __global__ void __launch_bounds__(128) k_col_sums(const uint16_t* __restrict__ Q
     if (threadIdx.x < BQ) {
       const int i = qb * BQ + threadIdx.x;
       sm[threadIdx.x] = i < T ? m_in[(size_t)h * T + i] : 0.f;
-      sl[threadIdx.x] = i < T ? l_in[(size_t)h * T + i] : 1.f;
+      sl[threadIdx.x] = i < T ? 1.f / l_in[(size_t)h * T + i] : 1.f;
     }
     __syncthreads();
     float acc[8][4];
@@ -165,7 +175,7 @@ __global__ void __launch_bounds__(128) k_col_sums(const uint16_t* __restrict__ Q
         const int qi = n * 8 + 2 * c + (e & 1);
         const int i = qb * BQ + qi;
         const int j = e < 2 ? j0 : j1;
-        const float p = (j <= i && i < T) ? exp2f(acc[n][e] * scale_log2 - sm[qi]) / sl[qi] : 0.f;
+        const float p = (j <= i && i < T) ? exp2f(acc[n][e] * scale_log2 - sm[qi]) * sl[qi] : 0.f;
         if (e < 2) col0 += p;
         else col1 += p;
       }

@@ -1,7 +1,7 @@
 // Look-ahead prediction of the next layer's experts (Eqs. 6-8,
 // P:275-298), for sm_100a.  Readings P1-P3:
-//   Eq. 6  logits = h^(l) · W_g^(l+1)^T, fp32 with one rounding per multiply-add in k order (bf16 x
-//          bf16 products are exact in fp32); g_hat = softmax (the routing kernel);
+//   Eq. 6  logits = h^(l) · W_g^(l+1)^T, fp32 in the fixed order of reading P1 (32 lane partial
+//          sums over 8-element chunks, then an xor butterfly); g_hat = softmax (routing kernel);
 //   Eq. 7  prefill: c_e = #{tokens whose top-k_route predicted experts contain e} (exact ints);
 //   Eq. 8  decode:  predicted demand = decode importance of the predicted gate (B = 1: the
 //          logit row; B > 1: sum_b g_hat[b], fp32 in b order -- the decode scoring kernel);
@@ -11,17 +11,20 @@
 
 namespace dymoe {
 
-// one thread per (token, expert): 16-byte loads, 8 sequential FMAs per load (k order kept)
+// one warp per (token, expert): lane l accumulates the 8-element chunks l, l + 32, l + 64, ...
+// of the dot product in order (16-byte loads, fp32 FMA), then an xor butterfly over the lanes
+// (reading P1: the order oracle/prefetch.py writes out)
 __global__ void __launch_bounds__(256) k_gate_logits(const uint4* __restrict__ h,
                                                      const uint4* __restrict__ w, int T, int Hd,
                                                      int M, float* __restrict__ logits) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (i >= (long long)T * M) return;
   const int t = (int)(i / M), e = (int)(i - (long long)t * M);
   const uint4* hp = h + (size_t)t * (Hd / 8);
   const uint4* wp = w + (size_t)e * (Hd / 8);
   float acc = 0.f;
-  for (int c = 0; c < Hd / 8; ++c) {
+  for (int c = lane; c < Hd / 8; c += 32) {
     const uint4 a = __ldg(hp + c), b = __ldg(wp + c);
     const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, bw[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
@@ -30,7 +33,9 @@ __global__ void __launch_bounds__(256) k_gate_logits(const uint4* __restrict__ h
       acc = __fmaf_rn(__uint_as_float(aw[q] & 0xffff0000u), __uint_as_float(bw[q] & 0xffff0000u), acc);
     }
   }
-  logits[i] = acc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+  if (lane == 0) logits[i] = acc;
 }
 
 __global__ void k_predict_counts(const int32_t* __restrict__ topk_idx, int n, int M,
@@ -72,7 +77,7 @@ cudaError_t launch_predict_next(int phase, const uint16_t* h, const uint16_t* wg
                                 int M, int k, int t, float* logits, int32_t* topk_idx,
                                 float* topk_w, float* probs, float* value, int32_t* experts,
                                 float* priority, int32_t* n_out, cudaStream_t s) {
-  const long long n = (long long)T * M;
+  const long long n = (long long)T * M * 32;   // one warp per (token, expert)
   k_gate_logits<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4*>(h),
                                                            reinterpret_cast<const uint4*>(wg), T,
                                                            Hd, M, logits);
