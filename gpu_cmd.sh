@@ -1,4 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_predict.py -q -x 2>&1 | tail -2
-timeout 600 python bench.py --workload prefill --steps 16 --warmup 3 --no-cpu-baseline > gpurun_out/bp.json 2> gpurun_out/bp.err; tail -2 gpurun_out/bp.err
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
 python -c "
-import json; j=json.load(open('gpurun_out/bp.json'));print(j['next_rows'])"
+import json; j=json.load(open('gpurun_out/bench.json'));r=j['roofline'];print(j['value'], j['ms_per_step'], r['achieved'], r['frac'], r['ffn_w13_plus_w2_GBs'], j.get('e2e'), j['clocks'], j['cpu_baseline'])"

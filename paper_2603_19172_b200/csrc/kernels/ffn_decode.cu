@@ -48,11 +48,15 @@ constexpr int kRedTile = 8 * 16;
 //   Alloc table, tile sync words, ring mbarriers
 template <bool W13>
 struct Cfg {
-  static constexpr int NM = W13 ? 2 : 1;
-  static constexpr int S = W13 ? 2 : 4;
-  static constexpr int NB = W13 ? 1 : 2;
-  static constexpr int CODES = NM * 2048;
-  static constexpr int META = NM * 256;
+  // two 16-row operand blocks per tile: W13 = the W1 and W3 rows of the same features; W2 = two
+  // consecutive 16-row halves of a 32-row tile (4 KB of codes per item in both kernels)
+  static constexpr int NM = 2;
+  static constexpr int TILE_ROWS = W13 ? 16 : 32;
+  static constexpr int S = 2;
+  static constexpr int NB = 1;
+  static constexpr int BOXES = 1;             // 128-byte boxes per operand block per item
+  static constexpr int CODES = NM * BOXES * 2048;
+  static constexpr int META = NM * 256;       // [m][gq <= 4][16 rows] words
   static constexpr int RED = 2 * NB * kWarps * NM * kRedTile * 4;
 };
 
@@ -125,8 +129,10 @@ __device__ __forceinline__ DQ dq_from_meta(uint32_t w) {
 // h at out[tok * ostride + n]; W2 -> fp32 partials at out[tok * ostride + n].  seq: this warp's
 // running item count (ring slot / mbarrier parity bookkeeping across calls); returns the new one.
 //
-// Item p of a tile (p = warp + 8 j) covers the 64-byte chunks 2p and 2p + 1 of every row of the
-// tile's K slice (CK k values each); its metadata box holds the GQ groups those chunks span.
+// Item p of a tile (p = warp + 8 j) covers the 64-byte chunks [NSUB p, NSUB p + NSUB) of every
+// row of the tile's K slice (CK k values each; NSUB = 2 BOXES), one 128 x 16 box per operand
+// block (W13: W1 and W3 rows of the tile's 16 features; W2: the two 16-row halves of a 32-row
+// tile), plus the metadata boxes of the GQ groups those chunks span.
 template <bool W13, int BITS>
 __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts, int e, int k0,
                                            int kl, int t0, int t1, int nt, void* out, int ostride,
@@ -138,15 +144,20 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   constexpr int NM = C::NM;
   constexpr int S = C::S;
   constexpr int CK = Tr::CHUNK_K;
-  constexpr int GQ = BITS == 16 ? 0 : 2 * CK / DYMOE_GROUP;   // groups per item: 1, 2, 4
-  constexpr uint32_t TX = NM * 2048 + NM * 64 * GQ;
+  constexpr int BOXES = C::BOXES;
+  constexpr int NSUB = 2 * BOXES;                               // 64-byte chunks per item
+  constexpr int GQ = BITS == 16 ? 0 : NSUB * CK / DYMOE_GROUP;  // groups per item
+  constexpr uint32_t TX = NM * BOXES * 2048 + NM * 64 * GQ;
+  // meta words of operand block m start at m * MSTRIDE in the stage: W13's 3-D box packs the two
+  // blocks ([m][g][16]); W2's two boxes sit 256 B apart (TMA destinations are 128-B aligned)
+  constexpr int MSTRIDE = W13 ? GQ * 64 : 256;
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
   const int grp = wid >> 3;                          // warp group: tiles t0 + grp, +2, ...
   const int warp = wid & (kWarps - 1);               // warp within the group
   const int g = lane >> 2, c = lane & 3;
   const int nck = (kl + CK - 1) / CK;                // 64-byte chunks per tile row slice
-  const int npr = (nck + 1) >> 1;                    // 128-byte items per tile
+  const int npr = (nck + NSUB - 1) / NSUB;           // items per tile
   const int cmax = (npr + kWarps - 1) / kWarps;      // per warp (same for all warps)
   const int my_tiles = (t1 - t0 - grp + 1) / 2;
   const int n_items = (my_tiles > 0 ? my_tiles : 0) * cmax;
@@ -164,7 +175,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
     const DevExpert& E = experts[e];
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
-      const int mi = W13 ? m : 2;
+      const int mi = W13 ? m : 2;   // W2: both operand blocks come from the W2 matrix
       if constexpr (BITS == 16) {
         tmc[m] = E.tm_w[mi];
       } else {
@@ -173,7 +184,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
     }
     if constexpr (BITS != 16) tmm = E.q[width_index(BITS)][W13 ? 0 : 2].tm_meta;
   }
-  const int kx0 = k0 * BITS / 8 + warp * 128;        // codes x coordinate (bytes) at j = 0
+  const int kx0 = k0 * BITS / 8 + warp * (BOXES * 128);   // codes x coordinate (bytes), j = 0
   const int gy0 = k0 / DYMOE_GROUP + warp * GQ;      // meta group coordinate at j = 0
   // item (tile ti, j = jj) into ring position sq
   auto issue = [&](uint32_t sq, int ti, int jj) {
@@ -187,13 +198,19 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
     mbar_expect_tx(bar, TX);
     const uint32_t cs = cring + slot * C::CODES;
 #pragma unroll
-    for (int m = 0; m < NM; ++m) tma2d(cs + m * 2048, tmc[m], kx0 + jj * (kWarps * 128), ti * 16, bar);
+    for (int m = 0; m < NM; ++m)
+#pragma unroll
+      for (int bx = 0; bx < BOXES; ++bx)
+        tma2d(cs + (m * BOXES + bx) * 2048, tmc[m], kx0 + jj * (kWarps * BOXES * 128) + bx * 128,
+              ti * C::TILE_ROWS + (W13 ? 0 : m * 16), bar);
     if constexpr (BITS != 16) {
       const uint32_t ms = mring + slot * C::META;
-      if constexpr (W13)
+      if constexpr (W13) {
         tma3d(ms, tmm, ti * 16, gy0 + jj * (kWarps * GQ), 0, bar);
-      else
-        tma2d(ms, tmm, ti * 16, gy0 + jj * (kWarps * GQ), bar);
+      } else {
+        tma2d(ms, tmm, ti * 32, gy0 + jj * (kWarps * GQ), bar);
+        tma2d(ms + 256, tmm, ti * 32 + 16, gy0 + jj * (kWarps * GQ), bar);   // 128-B aligned
+      }
     }
   };
 
@@ -215,10 +232,11 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   // row 8h + g, granule 4 sub + c, 128-byte swizzled (granule ^ row % 8); meta word of row
   // 8h + g for the group the lane's granule falls in
   const uint32_t xlane = xs + (uint32_t)(g * row_gran + c) * 16;
-  uint32_t wofs[2], mofs[2];
+  uint32_t wofs[2], mofs[NSUB];
 #pragma unroll
-  for (int sub = 0; sub < 2; ++sub) {
-    wofs[sub] = g * 128 + (((sub * 4 + c) ^ g) * 16);
+  for (int sub = 0; sub < 2; ++sub) wofs[sub] = g * 128 + (((sub * 4 + c) ^ g) * 16);
+#pragma unroll
+  for (int sub = 0; sub < NSUB; ++sub) {
     const int gi = BITS == 16 ? 0 : (sub * CK + c * Tr::CODES) / DYMOE_GROUP;
     mofs[sub] = (gi * 16 + g) * 4;
   }
@@ -236,9 +254,9 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
       const uint32_t ms = mring + slot * C::META;
       mbar_wait(bars + slot * 8, (sq / S) & 1);
 #pragma unroll
-      for (int sub = 0; sub < 2; ++sub) {
-        const int ci = 2 * p + sub;
-        if (sub == 1 && ci >= nck) break;
+      for (int sub = 0; sub < NSUB; ++sub) {
+        const int ci = NSUB * p + sub;
+        if (sub > 0 && ci >= nck) break;
         // x for this chunk: beyond the slice the staged x is zero, so codes past the slice end
         // (the next slice's, or TMA's zero fill past the row end) contribute nothing
         const uint32_t xa = xlane + (uint32_t)ci * (2 * CK);
@@ -248,13 +266,14 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
           for (int m = 0; m < NM; ++m)
 #pragma unroll
             for (int h = 0; h < 2; ++h)
-              dq[m][h] = dq_from_meta<BITS>(lds32(ms + m * (GQ * 64) + h * 32 + mofs[sub]));
+              dq[m][h] = dq_from_meta<BITS>(lds32(ms + m * MSTRIDE + h * 32 + mofs[sub]));
         }
         uint4 w[NM][2];
 #pragma unroll
         for (int m = 0; m < NM; ++m)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) w[m][h] = lds128(cs + m * 2048 + h * 1024 + wofs[sub]);
+          for (int h = 0; h < 2; ++h)
+            w[m][h] = lds128(cs + (m * BOXES + (sub >> 1)) * 2048 + h * 1024 + wofs[sub & 1]);
         using X = XB<BITS>;
 #pragma unroll
         for (int blk = 0; blk < X::NB; ++blk) {
@@ -318,7 +337,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
               s0 = __fadd_rn(s0, pp[0]);
               if (NM == 2) s1 = __fadd_rn(s1, pp[kRedTile]);
             }
-            const int n = tile * 16 + r16;
+            const int n = tile * C::TILE_ROWS + r16;
             if (W13) {
               // silu(A) * B, fast exp / divide (well inside the FFN tolerance)
               const float silu = __fdividef(s0, 1.f + __expf(-s0));
@@ -326,6 +345,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
               reinterpret_cast<__nv_bfloat16*>(out)[(size_t)tok * ostride + n] = hv;
             } else {
               reinterpret_cast<float*>(out)[(size_t)tok * ostride + n] = s0;
+              reinterpret_cast<float*>(out)[(size_t)tok * ostride + n + 16] = s1;
             }
           }
         }
@@ -390,7 +410,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
   const uint32_t bar_base = (uint32_t)__cvta_generic_to_shared(ring_bar);
   const int K = W13 ? a.Hd : a.F;
   const int N = W13 ? a.F : a.Hd;
-  const int NT = N / 16;
+  const int NT = N / C::TILE_ROWS;
   const int row_gran = x_row_gran(sliceK);
   // the codes ring is free until the first TMA: use it as the allocation scratch
   if (threadIdx.x == 0) compute_alloc(a, gridDim.x / SK, W13, A, *reinterpret_cast<AllocScratch*>(smem));
@@ -427,7 +447,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
     if (!resident) {
       if (threadIdx.x == 0 && a.status) atomicOr(a.status, (unsigned)DYMOE_STATUS_WIDTH_NOT_RESIDENT);
       for (int r = r_lo; r < r_hi; ++r)
-        for (int n = t0 * 16 + threadIdx.x; n < t1 * 16; n += blockDim.x) {
+        for (int n = t0 * C::TILE_ROWS + threadIdx.x; n < t1 * C::TILE_ROWS; n += blockDim.x) {
           if (W13) a.h[(size_t)r * a.F + n] = 0;
           else a.y_part[((size_t)ks * a.part_rows + r) * a.Hd + n] = 0.f;
         }
