@@ -308,3 +308,38 @@ def test_invalid_arguments_name_the_field():
         d.dymoe_quantize(torch.zeros(4, 100, dtype=torch.bfloat16, device="cuda"), 4)
     with pytest.raises(d.DymoeError, match="bits:"):
         d.dymoe_quantize(torch.zeros(4, 128, dtype=torch.bfloat16, device="cuda"), 3)
+
+
+# ------------------------------------------------------------------------------------ edges
+@pytest.mark.parametrize("mode", ["decode", "prefill"])
+def test_max_experts_and_multi_pass_decode(mode):
+    """M = 256 experts, top-8 (the ABI maxima), and a decode call whose experts hold more than
+    8 rows (several token passes over the same weights) -- against the oracle."""
+    d = D()
+    for cfg in (synthetic.MoEConfig("m256", M=256, k=8, hidden=256, ffn=256, T=40),
+                synthetic.MoEConfig("multi", M=4, k=2, hidden=256, ffn=384, T=64)):
+        ex = gpu_experts(cfg, 8)
+        layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+        rng = np.random.default_rng(cfg.M)
+        bits = np.array([[16, 8, 4, 2][int(rng.integers(0, 4))] for _ in range(cfg.M)], np.uint8)
+        x, lg, _ = synthetic.layer_inputs(cfg, 8)
+        r_idx, _, _ = o_route.route(lg.numpy(), cfg.k)
+        perm = o_moe.permute(r_idx, bits, cfg.M)
+        if cfg.name == "multi":
+            assert np.diff(perm["expert_off"]).max() > 8          # several decode passes
+        m = d.DYMOE_DECODE if mode == "decode" else d.DYMOE_PREFILL
+        h, y, status = layer.expert_ffn(x.cuda(), torch.from_numpy(bits).cuda(),
+                                        torch.from_numpy(perm["expert_off"]).cuda(),
+                                        torch.from_numpy(perm["perm_token"]).cuda(), m)
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0
+        nx = np_experts(cfg, 8)
+        off = perm["expert_off"]
+        for e in range(cfg.M):
+            lo, hi = int(off[e]), int(off[e + 1])
+            if hi == lo:
+                continue
+            W1, W3, W2 = o_moe.expert_weights(nx[e], int(bits[e]))
+            xr = x.float().numpy()[perm["perm_token"][lo:hi]].astype(np.float64)
+            ref = o_moe.ffn(xr, W1, W3, W2)
+            assert rel_err(y[lo:hi].cpu().numpy(), ref) <= FFN_TOL, (cfg.name, e, int(bits[e]))
