@@ -243,25 +243,54 @@ def run_ours(args, rank, world, device):
         hx = [inp[0].cpu().pin_memory() for inp in inputs]
         hl = [inp[1].cpu().pin_memory() for inp in inputs]
         ha = [inp[2].cpu().pin_memory() for inp in inputs]
-        dx = torch.empty_like(inputs[0][0])
-        dl = torch.empty_like(inputs[0][1])
-        da = torch.empty_like(inputs[0][2])
-        hy = torch.empty(T, cfg.hidden, dtype=torch.float32).pin_memory()
+        # double-buffered device inputs / outputs; the copies run on a side stream so that step
+        # i+1's inputs and step i-1's output move while step i computes (what a serving loop does)
+        dbuf = [tuple(torch.empty_like(t) for t in inputs[0]) for _ in range(2)]
+        obuf = [torch.empty(T, cfg.hidden, dtype=torch.float32, device=device) for _ in range(2)]
+        hy = [torch.empty(T, cfg.hidden, dtype=torch.float32).pin_memory() for _ in range(2)]
         h2d = hx[0].numel() * 2 + hl[0].numel() * 4 + (ha[0].numel() * 4 if phase == d.DYMOE_PREFILL else 0)
-        d2h = hy.numel() * 4
+        d2h = hy[0].numel() * 4
+        cstream = torch.cuda.Stream(device=device)
+        in_ready = [torch.cuda.Event() for _ in range(2)]
+        out_ready = [torch.cuda.Event() for _ in range(2)]
+        buf_free = [torch.cuda.Event() for _ in range(2)]
+        out_free = [torch.cuda.Event() for _ in range(2)]
+
+        def stage_in(i):
+            _, _, j = plan(args.warmup + i)
+            b = i & 1
+            with torch.cuda.stream(cstream):
+                cstream.wait_event(buf_free[b])
+                dbuf[b][0].copy_(hx[j], non_blocking=True)
+                dbuf[b][1].copy_(hl[j], non_blocking=True)
+                if phase == d.DYMOE_PREFILL:
+                    dbuf[b][2].copy_(ha[j], non_blocking=True)
+                in_ready[b].record(cstream)
+
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for ev_ in buf_free + out_free:
+            ev_.record(stream)
         torch.cuda.synchronize()
         e0.record(stream)
+        cstream.wait_event(e0)          # no copy starts before the timed region
+        stage_in(0)
         for i in range(K):
             c, l, j = plan(args.warmup + i)
-            dx.copy_(hx[j], non_blocking=True)
-            dl.copy_(hl[j], non_blocking=True)
-            if phase == d.DYMOE_PREFILL:
-                da.copy_(ha[j], non_blocking=True)
+            b = i & 1
+            if i + 1 < K:
+                stage_in(i + 1)
+            stream.wait_event(in_ready[b])
+            stream.wait_event(out_free[b])          # step i-2's output has left the device
+            dx, dl, da = dbuf[b]
             layers[c][0].forward(dx, dl, ladder, l, NUM_LAYERS, phase=phase, attn_mass=da,
-                                 ws=ws[c], out=out)
-            hy.copy_(out, non_blocking=True)
-        e1.record(stream)
+                                 ws=ws[c], out=obuf[b])
+            buf_free[b].record(stream)
+            out_ready[b].record(stream)
+            with torch.cuda.stream(cstream):
+                cstream.wait_event(out_ready[b])
+                hy[b].copy_(obuf[b], non_blocking=True)
+                out_free[b].record(cstream)
+        e1.record(cstream)                            # after the last output copy
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
         if world > 1:
