@@ -330,8 +330,8 @@ bool encode_meta(CUtensorMap* m, const void* base, uint64_t N, uint64_t gpr, int
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, base, n_mat > 1 ? 3 : 2, dims, str, box,
                 CU_TENSOR_MAP_SWIZZLE_NONE);
 }
-constexpr int kMapsPerExpert = 24;   // 3 + 3 bf16 masters (decode, prefill boxes) + 3 widths x 3
-                                     // matrices x (codes, meta)
+constexpr int kMapsPerExpert = 42;   // 3 + 3 bf16 masters (decode, prefill boxes) + 3 widths x 3
+                                     // matrices x (codes, meta) x (decode, prefill boxes)
 }  // namespace
 
 namespace {
@@ -398,13 +398,28 @@ int bind_expert(dymoe_layer* L, int e, const dymoe_expert_desc& x, cudaStream_t 
     }
     for (int wi = 0; wi < 3; ++wi) {
       DevQMat& q = y.q[wi][m];
-      q.tm_codes = q.tm_meta = nullptr;
+      q.tm_codes = q.tm_meta = q.tm_raw = q.tm_rawmeta = nullptr;
       if (q.codes == nullptr) continue;
       const int b = wi == 0 ? 8 : wi == 1 ? 4 : 2;
       const uint32_t gq = (uint32_t)(2 * 512 / b / DYMOE_GROUP);   // groups per 128-byte item
       const int ic = 3 + (wi * 3 + m) * 2, im = ic + 1;
       maps_ok &= encode_rows(&hm[ic], q.codes, K * b / 8, N);
       q.tm_codes = dm + ic;
+      {  // prefill producer boxes: 64 k x 128 rows of codes, one group's words of 128 rows
+        const int ir = 24 + (wi * 3 + m) * 2, irm = ir + 1;
+        const uint64_t rb = K * b / 8;
+        const uint64_t dims[2] = {rb, N}, str[1] = {rb};
+        const uint32_t box[2] = {(uint32_t)(64 * b / 8), 128};
+        const CUtensorMapSwizzle swz = b == 8 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                     : b == 4 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
+        maps_ok &= encode(&hm[ir], CU_TENSOR_MAP_DATA_TYPE_UINT8, q.codes, 2, dims, str, box, swz);
+        const uint64_t mdims[2] = {N, K / DYMOE_GROUP}, mstr[1] = {N * 4};
+        const uint32_t mbox[2] = {128, 1};
+        maps_ok &= encode(&hm[irm], CU_TENSOR_MAP_DATA_TYPE_UINT32, q.meta, 2, mdims, mstr, mbox,
+                          CU_TENSOR_MAP_SWIZZLE_NONE);
+        q.tm_raw = dm + ir;
+        q.tm_rawmeta = dm + irm;
+      }
       // W2: 2-D meta; W1: 3-D over the adjacent W1 / W3 meta (one box feeds both matrices);
       // W3's own descriptor is not needed by the kernels
       const bool pair = m == 0 && y.q[wi][1].codes != nullptr;

@@ -29,6 +29,10 @@ struct DevQMat {
   // and W3 meta with one box (W3's tm_meta is null); 2-D for W2.
   const CUtensorMap* tm_codes;
   const CUtensorMap* tm_meta;
+  // prefill producer boxes: codes {64 k of 128 rows} (Int8 64-byte, Int4 32-byte swizzle, Int2
+  // none) and the 128 rows' words of one group (meta {128, 1})
+  const CUtensorMap* tm_raw;
+  const CUtensorMap* tm_rawmeta;
 };
 // meta[g * N + n] = bf16bits(RNE(scales[n * gpr + g])) << 16 | zeros[n * gpr + g]
 cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, int N, int gpr,

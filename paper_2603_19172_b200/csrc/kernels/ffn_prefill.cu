@@ -50,11 +50,10 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int kBWarps = 8, kEpiWarps = 4;
 constexpr int kBWarp0 = 2, kEpiWarp0 = kBWarp0 + kBWarps;
 constexpr int kThreads = (kEpiWarp0 + kEpiWarps) * 32;   // 448
-constexpr int kBThreads = kBWarps * 32;
-constexpr int PF = 6;                                   // raw stages in flight per thread
-constexpr int RAW_CHUNK = kBThreads * 16;               // one 16-byte granule per thread
-constexpr int RAW_SLOT = ((KPER + 15) / 16) * RAW_CHUNK;  // Int8: KPER bytes per thread per stage
-constexpr int RAW_BYTES = PF * RAW_SLOT + PF * kBThreads * 4;   // + dequant words
+constexpr int PF = 6;                       // raw ring slots (stages of packed codes in flight)
+constexpr int RAW_CODES = 128 * 64;         // per slot: 128 B rows x up to 64 bytes (Int8)
+constexpr int RAW_SLOT = RAW_CODES + 1024;  // + the 128 rows' dequant words (512 B), 1 KB aligned
+constexpr int RAW_BYTES = PF * RAW_SLOT;
 constexpr int kSmem = STAGES * STAGE_BYTES + RAW_BYTES + 1024;   // + alignment slack
 constexpr uint32_t TMEM_COLS = 2 * NCOL;                // two accumulators
 
@@ -103,6 +102,19 @@ __device__ __forceinline__ void tma2d_pair(uint32_t dst, const CUtensorMap* m, i
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar_cl) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_local(uint32_t bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+// 2-D TMA load into this CTA's shared memory, completion on this CTA's barrier
+__device__ __forceinline__ void tma2d_local(uint32_t dst, const CUtensorMap* m, int x, int y,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -249,13 +261,13 @@ __device__ __forceinline__ uint32_t deq_int8_pair(uint32_t w, int i, const DQP& 
 }
 
 // ---------------------------------------------------------------------------------------- B producer
-// Two threads per B row (k halves of 32), every stage.  Each thread streams its packed bytes
-// (+ the group's dequant word) PF stages ahead with cp.async into a private shared-memory ring
-// ([slot][chunk][thread] 16-byte granules: conflict-free), so no global load is outstanding in
-// registers when the thread fences and arrives; it then dequantizes in natural k order and stores
-// into the 128B-swizzled B tile, fences (generic -> async proxy) and release-arrives on the
-// leader's full barrier.  BF16 experts: the B tile comes by TMA (warp 0); the producers only
-// arrive, to keep the barrier's count.
+// The packed codes of the CTA's 128 B rows arrive by TMA into a PF-slot ring (one thread issues
+// them, PF stages ahead: a 64 k x 128 row box, Int8 64-byte / Int4 32-byte swizzled, plus the
+// rows' dequant words of the stage's group).  Two producer threads per B row (k halves of 32)
+// read their codes back from the slot, release it (one arrive per warp), dequantize in natural k
+// order, store into the 128B-swizzled B tile, fence (generic -> async proxy) and arrive on the
+// leader's full barrier.  No producer thread has a memory load in flight at its proxy fence.
+// BF16 experts: the B tile comes by TMA (warp 0); the producers only arrive, to keep the count.
 template <int BE>
 struct RawStage {
   static constexpr int NB = KPER * BE / 8;        // bytes per thread per stage
@@ -264,33 +276,27 @@ struct RawStage {
   uint32_t m;
 };
 
+// this thread's codes (row wr, k half khalf) from a raw slot, undoing the TMA swizzle
 template <int BE>
-__device__ __forceinline__ void issue_raw(uint32_t raw_base, int tb, int slot, const uint8_t* rowp,
-                                          const uint32_t* metap, int mstride, int khalf, int kb) {
-  constexpr int NB = RawStage<BE>::NB;
-  const size_t kbyte = ((size_t)kb * BK + khalf * KPER) * BE / 8;
-  const uint32_t dst = raw_base + slot * RAW_SLOT + tb * 16;
-  if constexpr (NB == 8) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(rowp + kbyte) : "memory");
-  } else {
+__device__ __forceinline__ void read_raw(RawStage<BE>& r, uint32_t slot, int wr, int khalf) {
+  if constexpr (BE == 8) {          // 64-byte rows, 64B swizzle: granule g at g ^ ((row >> 1) & 3)
 #pragma unroll
-    for (int i = 0; i < RawStage<BE>::NV; ++i)
-      asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst + i * RAW_CHUNK),
-                   "l"(rowp + kbyte + 16 * i) : "memory");
-  }
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(raw_base + PF * RAW_SLOT +
-                                                                (slot * kBThreads + tb) * 4),
-               "l"(metap + (size_t)((kb * BK + khalf * KPER) / DYMOE_GROUP) * mstride) : "memory");
-}
-template <int BE>
-__device__ __forceinline__ void read_raw(RawStage<BE>& r, uint32_t raw_base, int tb, int slot) {
-  const uint32_t src = raw_base + slot * RAW_SLOT + tb * 16;
-#pragma unroll
-  for (int i = 0; i < RawStage<BE>::NV; ++i)
+    for (int i = 0; i < 2; ++i) {
+      const int g = (2 * khalf + i) ^ ((wr >> 1) & 3);
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(r.v[i].x), "=r"(r.v[i].y), "=r"(r.v[i].z), "=r"(r.v[i].w)
+                   : "r"(slot + wr * 64 + g * 16));
+    }
+  } else if constexpr (BE == 4) {   // 32-byte rows, 32B swizzle: granule g at g ^ ((row >> 2) & 1)
+    const int g = khalf ^ ((wr >> 2) & 1);
     asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.v[i].x), "=r"(r.v[i].y), "=r"(r.v[i].z), "=r"(r.v[i].w)
-                 : "r"(src + i * RAW_CHUNK));
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r.m) : "r"(raw_base + PF * RAW_SLOT + (slot * kBThreads + tb) * 4));
+                 : "=r"(r.v[0].x), "=r"(r.v[0].y), "=r"(r.v[0].z), "=r"(r.v[0].w)
+                 : "r"(slot + wr * 32 + g * 16));
+  } else {                          // 16-byte rows, no swizzle
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(r.v[0].x), "=r"(r.v[0].y)
+                 : "r"(slot + wr * 16 + khalf * 8));
+  }
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r.m) : "r"(slot + RAW_CODES + wr * 4));
 }
 
 template <int BE>
@@ -307,7 +313,7 @@ __device__ __forceinline__ void store_stage(const RawStage<BE>& r, uint32_t dst,
       }
     }
   } else if constexpr (BE == 2) {
-    const uint32_t wv[4] = {r.v[0].x, r.v[0].y, r.v[0].z, r.v[0].w};
+    const uint32_t wv[2] = {r.v[0].x, r.v[0].y};
 #pragma unroll
     for (int q = 0; q < KPER / 16; ++q) {
       uint4 lo, hi;
@@ -327,44 +333,32 @@ __device__ __forceinline__ void store_stage(const RawStage<BE>& r, uint32_t dst,
   }
 }
 
-// full_cl: shared::cluster address of the leader's full_bar[0] (stage s at + 8 s)
+// One tile's k-blocks [kb0, kb1).  full_cl: shared::cluster address of the leader's full_bar[0]
+// (stage s at + 8 s); raw ring position (rslot, rphase) shared with the issuer's order.
 template <int BE>
-__device__ __forceinline__ void produce(const uint8_t* rowp, const uint32_t* metap, int mstride,
-                                        int khalf, int tb, int wr, int kb0, int kb1, uint32_t sbase,
+__device__ __forceinline__ void produce(int khalf, int wr, int kb0, int kb1, uint32_t sbase,
+                                        uint32_t raw_base, uint32_t raw_full0, uint32_t raw_empty0,
                                         uint32_t full_cl, uint32_t empty_bar, int& stage,
-                                        uint32_t& phase) {
+                                        uint32_t& phase, int& rslot, uint32_t& rphase) {
   const int j0 = khalf * (KPER / 8);
-  if constexpr (BE == 16) {
-    for (int kb = kb0; kb < kb1; ++kb) {
-      mbar_wait(empty_bar + stage * 8, phase ^ 1);
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive_cl(full_cl + stage * 8);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
-    }
-  } else {
-    const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;
-#pragma unroll
-    for (int p = 0; p < PF - 1; ++p) {
-      if (kb0 + p < kb1) issue_raw<BE>(raw_base, tb, p, rowp, metap, mstride, khalf, kb0 + p);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    int slot = 0, slot_iss = PF - 1;
-    for (int kb = kb0; kb < kb1; ++kb) {
-      if (kb + PF - 1 < kb1) issue_raw<BE>(raw_base, tb, slot_iss, rowp, metap, mstride, khalf, kb + PF - 1);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      if (++slot_iss == PF) slot_iss = 0;
-      asm volatile("cp.async.wait_group %0;" ::"n"(PF - 1) : "memory");
+  const bool lane0 = (threadIdx.x & 31) == 0;
+  for (int kb = kb0; kb < kb1; ++kb) {
+    if constexpr (BE != 16) {
       RawStage<BE> r;
-      read_raw<BE>(r, raw_base, tb, slot);
-      if (++slot == PF) slot = 0;
+      mbar_wait(raw_full0 + rslot * 8, rphase);
+      read_raw<BE>(r, raw_base + rslot * RAW_SLOT, wr, khalf);
+      __syncwarp();
+      if (lane0) mbar_arrive_local(raw_empty0 + rslot * 8);
+      if (++rslot == PF) { rslot = 0; rphase ^= 1; }
       mbar_wait(empty_bar + stage * 8, phase ^ 1);
       store_stage<BE>(r, sbase + stage * STAGE_BYTES + A_BYTES, wr, j0);
       fence_proxy_async();
-      __syncwarp();   // one release-arrive per warp (the whole warp's writes are fenced)
-      if ((threadIdx.x & 31) == 0) mbar_arrive_cl(full_cl + stage * 8);
-      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    } else {
+      mbar_wait(empty_bar + stage * 8, phase ^ 1);
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();   // one release-arrive per warp (the whole warp's writes are fenced)
+    if (lane0) mbar_arrive_cl(full_cl + stage * 8);
+    if (++stage == STAGES) { stage = 0; phase ^= 1; }
   }
 }
 
@@ -403,6 +397,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
   extern __shared__ uint8_t smem_raw[];
   __shared__ Sched S;
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t raw_full[PF], raw_empty[PF];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int n_tiles_sh;
   constexpr uint32_t IDESC = make_idesc(2 * BM, NCOL);
@@ -425,6 +420,8 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
   auto sA = [&](int s) { return sbase + s * STAGE_BYTES; };
   auto sB = [&](int s) { return sbase + s * STAGE_BYTES + A_BYTES; };
   const uint32_t full0 = smem_u32(&full_bar[0]), empty0 = smem_u32(&empty_bar[0]);
+  const uint32_t raw_base = sbase + STAGES * STAGE_BYTES;   // 1 KB aligned slots
+  const uint32_t raw_full0 = smem_u32(&raw_full[0]), raw_empty0 = smem_u32(&raw_empty[0]);
   const uint32_t full_cl = mapa(full0, 0);                     // the leader's full barriers
   const uint32_t tempty_cl = mapa(smem_u32(&tempty_bar[0]), 0);
 
@@ -450,6 +447,10 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&tfull_bar[b]), 1);
       mbar_init(smem_u32(&tempty_bar[b]), 2 * kEpiWarps);
+    }
+    for (int r = 0; r < PF; ++r) {
+      mbar_init(smem_u32(&raw_full[r]), 1);         // issuer's expect_tx arrive + TMA bytes
+      mbar_init(smem_u32(&raw_empty[r]), kBWarps);  // one arrive per producer warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -489,6 +490,26 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+    } else if (lane == 1) {
+      // packed codes + dequant words of this CTA's 128 B rows, PF stages ahead of the producers
+      int rslot = 0;
+      uint32_t rphase = 0;
+      for (int t = pair; t < n_tiles; t += npairs) {
+        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
+        const int be = a.bits[T.e];
+        if (be == 16) continue;
+        const DevQMat& q = a.experts[T.e].q[width_index(be)][W13 ? (int)rank : 2];
+        const int row0 = T.n0 + (W13 ? 0 : (int)rank * BNH);   // rows past the end: zero fill
+        const int rb = BK * be / 8;                              // code bytes per row per stage
+        for (int kb = T.kb0; kb < T.kb1; ++kb) {
+          mbar_wait(raw_empty0 + rslot * 8, rphase ^ 1);
+          mbar_expect_tx_local(raw_full0 + rslot * 8, 128 * rb + 128 * 4);
+          tma2d_local(raw_base + rslot * RAW_SLOT, q.tm_raw, kb * rb, row0, raw_full0 + rslot * 8);
+          tma2d_local(raw_base + rslot * RAW_SLOT + RAW_CODES, q.tm_rawmeta, row0,
+                      kb * BK / DYMOE_GROUP, raw_full0 + rslot * 8);
+          if (++rslot == PF) { rslot = 0; rphase ^= 1; }
+        }
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (leader)
@@ -519,29 +540,20 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     const int tb = threadIdx.x - kBWarp0 * 32;   // 0..255
     const int wr = tb & (BNH - 1);                // B row within this CTA's half
     const int khalf = tb >> 7;
-    int stage = 0;
-    uint32_t phase = 0;
+    int stage = 0, rslot = 0;
+    uint32_t phase = 0, rphase = 0;
     for (int t = pair; t < n_tiles; t += npairs) {
       const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
       const int be = a.bits[T.e];
-      const DevExpert& E = a.experts[T.e];
-      // GEMM 1: rank 0 = W1 rows n0.., rank 1 = the same W3 rows; GEMM 2: W2 rows
-      // n0 + 128 rank + wr, clamped at the end of the matrix (those outputs are dropped)
-      const int mi = W13 ? (int)rank : 2;
-      const int row = min(T.n0 + (W13 ? 0 : (int)rank * BNH) + wr, NWR - 1);
-      const int wi = width_index(be);
-      const uint8_t* codes = be == 16 ? reinterpret_cast<const uint8_t*>(E.w[mi])
-                                      : reinterpret_cast<const uint8_t*>(E.q[wi][mi].codes);
-      const uint32_t* meta = be == 16 ? nullptr : E.q[wi][mi].meta;
-      const size_t row_bytes = (size_t)K * be / 8;
-      const uint8_t* rowp = codes + (size_t)row * row_bytes;
-      const uint32_t* metap = meta ? meta + row : nullptr;   // group-major: stride NWR
+#define DYMOE_PRODUCE(B) produce<B>(khalf, wr, T.kb0, T.kb1, sbase, raw_base, raw_full0, raw_empty0, \
+                                    full_cl, empty0, stage, phase, rslot, rphase)
       switch (be) {
-        case 2: produce<2>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
-        case 4: produce<4>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
-        case 8: produce<8>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
-        default: produce<16>(rowp, metap, NWR, khalf, tb, wr, T.kb0, T.kb1, sbase, full_cl, empty0, stage, phase); break;
+        case 2: DYMOE_PRODUCE(2); break;
+        case 4: DYMOE_PRODUCE(4); break;
+        case 8: DYMOE_PRODUCE(8); break;
+        default: DYMOE_PRODUCE(16); break;
       }
+#undef DYMOE_PRODUCE
     }
   } else {
     // ------------------------------------------------------------------ epilogue (TMEM -> global)
