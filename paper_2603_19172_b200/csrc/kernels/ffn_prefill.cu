@@ -96,6 +96,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity)
       : "memory");
 }
+// wait with back-off, for the epilogue warps (idle for most of a tile): their polling would
+// otherwise take issue slots from the dequant producers on the same SM sub-partition
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity, uint32_t ns) {
+  uint32_t done = 0;
+  while (true) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    if (done) break;
+    __nanosleep(ns);
+  }
+}
 // 2-D TMA load into this CTA's shared memory, completion signalled on the leader's barrier
 __device__ __forceinline__ void tma2d_pair(uint32_t dst, const CUtensorMap* m, int x, int y,
                                            uint32_t bar_cl) {
@@ -563,7 +576,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     for (int t = pair; t < n_tiles; t += npairs, ++i) {
       const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
       const int b = i & 1;
-      mbar_wait(smem_u32(&tfull_bar[b]), (i >> 1) & 1);
+      mbar_wait_sleep(smem_u32(&tfull_bar[b]), (i >> 1) & 1, 256);
       tc_fence_after();
       const int mrow = (int)rank * BM + trow;     // row within the pair tile
       const size_t grow = (size_t)(a.expert_off[T.e] + T.m0 + mrow);
