@@ -151,21 +151,25 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   // meta words of operand block m start at m * MSTRIDE in the stage: W13's 3-D box packs the two
   // blocks ([m][g][16]); W2's two boxes sit 256 B apart (TMA destinations are 128-B aligned)
   constexpr int MSTRIDE = W13 ? GQ * 64 : 256;
+  // warps sharing a tile: 8, or 4 at Int4 / Int2, whose 512 / 1024-k items would otherwise
+  // leave each warp only 1-2 items per tile (a cross-warp reduction per item or two)
+  constexpr int WPT = (BITS == 2 || BITS == 4) ? 4 : kWarps;
+  constexpr int NSG = 2 * kWarps / WPT;              // subgroups per CTA, on interleaved tiles
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
-  const int grp = wid >> 3;                          // warp group: tiles t0 + grp, +2, ...
-  const int warp = wid & (kWarps - 1);               // warp within the group
+  const int grp = wid / WPT;                         // subgroup: tiles t0 + grp, + NSG, ...
+  const int warp = wid % WPT;                        // warp within the subgroup
   const int g = lane >> 2, c = lane & 3;
   const int nck = (kl + CK - 1) / CK;                // 64-byte chunks per tile row slice
   const int npr = (nck + NSUB - 1) / NSUB;           // items per tile
-  const int cmax = (npr + kWarps - 1) / kWarps;      // per warp (same for all warps)
-  const int my_tiles = (t1 - t0 - grp + 1) / 2;
+  const int cmax = (npr + WPT - 1) / WPT;            // per warp (same for all warps)
+  const int my_tiles = (t1 - t0 - grp + NSG - 1) / NSG;
   const int n_items = (my_tiles > 0 ? my_tiles : 0) * cmax;
   if (n_items == 0) return seq;
   const uint32_t cring = codes_base + wid * (S * C::CODES);
   const uint32_t mring = meta_base + wid * (S * C::META);
   const uint32_t bars = bar_base + wid * (S * 8);
-  red += grp * (C::NB * kWarps * NM * kRedTile);
+  red += grp * (C::NB * WPT * NM * kRedTile);
   sync += grp * 4;   // [arrivals buf0, arrivals buf1, generation buf0, generation buf1]
 
   // lane 0 is the producer: this expert's descriptors at this width
@@ -191,7 +195,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
     if (lane != 0) return;
     const uint32_t slot = sq % S;
     const uint32_t bar = bars + slot * 8;
-    if (warp + kWarps * jj >= npr) {   // nothing to load: complete the phase, keep parity in step
+    if (warp + WPT * jj >= npr) {   // nothing to load: complete the phase, keep parity in step
       mbar_arrive(bar);
       return;
     }
@@ -201,15 +205,15 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
     for (int m = 0; m < NM; ++m)
 #pragma unroll
       for (int bx = 0; bx < BOXES; ++bx)
-        tma2d(cs + (m * BOXES + bx) * 2048, tmc[m], kx0 + jj * (kWarps * BOXES * 128) + bx * 128,
+        tma2d(cs + (m * BOXES + bx) * 2048, tmc[m], kx0 + jj * (WPT * BOXES * 128) + bx * 128,
               ti * C::TILE_ROWS + (W13 ? 0 : m * 16), bar);
     if constexpr (BITS != 16) {
       const uint32_t ms = mring + slot * C::META;
       if constexpr (W13) {
-        tma3d(ms, tmm, ti * 16, gy0 + jj * (kWarps * GQ), 0, bar);
+        tma3d(ms, tmm, ti * 16, gy0 + jj * (WPT * GQ), 0, bar);
       } else {
-        tma2d(ms, tmm, ti * 32, gy0 + jj * (kWarps * GQ), bar);
-        tma2d(ms + 256, tmm, ti * 32 + 16, gy0 + jj * (kWarps * GQ), bar);   // 128-B aligned
+        tma2d(ms, tmm, ti * 32, gy0 + jj * (WPT * GQ), bar);
+        tma2d(ms + 256, tmm, ti * 32 + 16, gy0 + jj * (WPT * GQ), bar);   // 128-B aligned
       }
     }
   };
@@ -225,7 +229,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
 #pragma unroll
   for (int p = 0; p < S - 1; ++p) {
     if (p < n_items) issue(seq + p, tile_iss, j_iss);
-    if (++j_iss == cmax) { j_iss = 0; tile_iss += 2; }
+    if (++j_iss == cmax) { j_iss = 0; tile_iss += NSG; }
   }
 
   // per-lane shared-memory offsets: x (token row g, quad position c, x_pos layout); codes of
@@ -245,9 +249,9 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   for (int q = 0; q < n_items; ++q) {
     // refill: item q + S - 1 goes into the slot consumed in the previous iteration
     if (q + S - 1 < n_items) issue(seq + q + S - 1, tile_iss, j_iss);
-    if (++j_iss == cmax) { j_iss = 0; tile_iss += 2; }
+    if (++j_iss == cmax) { j_iss = 0; tile_iss += NSG; }
     const uint32_t sq = seq + q;
-    const int p = warp + kWarps * j;
+    const int p = warp + WPT * j;
     if (p < npr) {
       const uint32_t slot = sq % S;
       const uint32_t cs = cring + slot * C::CODES;
@@ -308,7 +312,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
       if (lane == 0)
         while (*reinterpret_cast<volatile int*>(&sync[2 + b]) != gen) {}
       __syncwarp();
-      float* rb = red + b * (kWarps * NM * kRedTile);
+      float* rb = red + b * (WPT * NM * kRedTile);
 #pragma unroll
       for (int m = 0; m < NM; ++m) {
         float* pp = rb + (warp * NM + m) * kRedTile;
@@ -324,7 +328,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
       int old = 0;
       if (lane == 0) old = atomicAdd(&sync[b], 1);
       old = __shfl_sync(0xffffffffu, old, 0);
-      if (old == kWarps - 1) {
+      if (old == WPT - 1) {
         __threadfence_block();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -332,7 +336,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
           if (tok < nt) {
             float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) {
+            for (int w = 0; w < WPT; ++w) {
               const float* pp = rb + (w * NM) * kRedTile + o;
               s0 = __fadd_rn(s0, pp[0]);
               if (NM == 2) s1 = __fadd_rn(s1, pp[kRedTile]);
@@ -357,7 +361,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
         }
       }
       ++tile_seq;
-      tile += 2;
+      tile += NSG;
     }
   }
   return seq + n_items;
@@ -382,12 +386,13 @@ struct Smem {
   static constexpr size_t META = (size_t)2 * kWarps * Cfg<W13>::S * Cfg<W13>::META;
   static constexpr size_t RED = Cfg<W13>::RED;
   static constexpr size_t BARS = (size_t)2 * kWarps * Cfg<W13>::S * 8;
+  static constexpr int SYNC_INTS = 16;   // 4 words per tile subgroup, up to 4 subgroups
   static __host__ __device__ size_t x_off() { return CODES + META + RED; }
   static __host__ __device__ size_t tail_off(int sliceK) {
     return x_off() + (size_t)kMaxTok * x_row_gran(sliceK) * 16;
   }
   static __host__ __device__ size_t bytes(int sliceK) {
-    return tail_off(sliceK) + BARS + 8 * sizeof(int) + sizeof(Alloc);
+    return tail_off(sliceK) + BARS + SYNC_INTS * sizeof(int) + sizeof(Alloc);
   }
 };
 
@@ -402,7 +407,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
   const size_t tail = L::tail_off(sliceK);
   uint64_t* ring_bar = reinterpret_cast<uint64_t*>(smem + tail);
   int* tile_sync = reinterpret_cast<int*>(smem + tail + L::BARS);   // [group][4]
-  Alloc& A = *reinterpret_cast<Alloc*>(smem + tail + L::BARS + 8 * sizeof(int));
+  Alloc& A = *reinterpret_cast<Alloc*>(smem + tail + L::BARS + L::SYNC_INTS * sizeof(int));
   const uint32_t codes_base = sbase;
   const uint32_t meta_base = sbase + (uint32_t)L::CODES;
   float* red = reinterpret_cast<float*>(smem + L::CODES + L::META);
@@ -467,7 +472,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
       const int nt = min(kMaxTok, r_hi - tok0);
       // stage the x slice of this pass's tokens (zero rows beyond nt), x_pos layout
       __syncthreads();  // the previous pass is done with xs / red / tile_sync
-      if (threadIdx.x < 8) tile_sync[threadIdx.x] = 0;
+      if (threadIdx.x < L::SYNC_INTS) tile_sync[threadIdx.x] = 0;
       for (int idx = threadIdx.x; idx < kMaxTok * npos; idx += blockDim.x) {
         const int t = idx / npos, pos = idx - t * npos;
         const int gl = x_logical(pos, xu4);

@@ -183,8 +183,8 @@ struct AllocScratch {
 // with every expert forced to one width (tools/decode_width_sweep.py): the narrow widths are
 // bound by dequant issue slots rather than bytes, so they cost more than their bytes suggest.
 __device__ __forceinline__ int wcost(int b, bool w13) {
-  if (w13) return b == 16 ? 256 : b == 8 ? 172 : b == 4 ? 131 : 115;
-  return b == 16 ? 256 : b == 8 ? 201 : b == 4 ? 158 : 137;
+  if (w13) return b == 16 ? 256 : b == 8 ? 173 : b == 4 ? 125 : 111;
+  return b == 16 ? 256 : b == 8 ? 203 : b == 4 ? 155 : 134;
 }
 
 // Cost-proportional allocation of `units_total` units to the active experts (largest remainder,
