@@ -99,6 +99,36 @@ __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, int x,
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
       ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar) : "memory");
 }
+// Warp-collective forms: every lane executes them with warp-uniform operands and one elected
+// lane (e != 0) issues, so the operands go to uniform registers without a per-lane loop around
+// each TMA instruction
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n}" : "=r"(e));
+  return e;
+}
+__device__ __forceinline__ void tma2d_e(uint32_t e, uint32_t dst, const CUtensorMap* m, int x, int y,
+                                        uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n}"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar), "r"(e) : "memory");
+}
+__device__ __forceinline__ void tma3d_e(uint32_t e, uint32_t dst, const CUtensorMap* m, int x, int y,
+                                        int z, uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %6, 0;\n\t"
+      "@p cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n}"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(z), "r"(bar), "r"(e) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_e(uint32_t e, uint32_t a, uint32_t tx) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
+               "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}" ::"r"(a), "r"(tx), "r"(e) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_e(uint32_t e, uint32_t a) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+               "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n}" ::"r"(a), "r"(e) : "memory");
+}
 __device__ __forceinline__ void tma3d(uint32_t dst, const CUtensorMap* m, int x, int y, int z,
                                       uint32_t bar) {
   asm volatile(
@@ -172,10 +202,10 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   red += grp * (C::NB * WPT * NM * kRedTile);
   sync += grp * 4;   // [arrivals buf0, arrivals buf1, generation buf0, generation buf1]
 
-  // lane 0 is the producer: this expert's descriptors at this width
+  // the producer (warp-collective issue, one elected lane): this expert's descriptors at this width
   const CUtensorMap* tmc[NM];
   const CUtensorMap* tmm = nullptr;
-  if (lane == 0) {
+  {   // every lane: the issue is warp-collective
     const DevExpert& E = experts[e];
 #pragma unroll
     for (int m = 0; m < NM; ++m) {
@@ -191,29 +221,30 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   const int kx0 = k0 * BITS / 8 + warp * (BOXES * 128);   // codes x coordinate (bytes), j = 0
   const int gy0 = k0 / DYMOE_GROUP + warp * GQ;      // meta group coordinate at j = 0
   // item (tile ti, j = jj) into ring position sq
+  // warp-collective: all lanes call it with the same arguments, one elected lane issues
   auto issue = [&](uint32_t sq, int ti, int jj) {
-    if (lane != 0) return;
+    const uint32_t el = elect_one();
     const uint32_t slot = sq % S;
     const uint32_t bar = bars + slot * 8;
     if (warp + WPT * jj >= npr) {   // nothing to load: complete the phase, keep parity in step
-      mbar_arrive(bar);
+      mbar_arrive_e(el, bar);
       return;
     }
-    mbar_expect_tx(bar, TX);
+    mbar_expect_tx_e(el, bar, TX);
     const uint32_t cs = cring + slot * C::CODES;
 #pragma unroll
     for (int m = 0; m < NM; ++m)
 #pragma unroll
       for (int bx = 0; bx < BOXES; ++bx)
-        tma2d(cs + (m * BOXES + bx) * 2048, tmc[m], kx0 + jj * (WPT * BOXES * 128) + bx * 128,
-              ti * C::TILE_ROWS + (W13 ? 0 : m * 16), bar);
+        tma2d_e(el, cs + (m * BOXES + bx) * 2048, tmc[m], kx0 + jj * (WPT * BOXES * 128) + bx * 128,
+                ti * C::TILE_ROWS + (W13 ? 0 : m * 16), bar);
     if constexpr (BITS != 16) {
       const uint32_t ms = mring + slot * C::META;
       if constexpr (W13) {
-        tma3d(ms, tmm, ti * 16, gy0 + jj * (WPT * GQ), 0, bar);
+        tma3d_e(el, ms, tmm, ti * 16, gy0 + jj * (WPT * GQ), 0, bar);
       } else {
-        tma2d(ms, tmm, ti * 32, gy0 + jj * (WPT * GQ), bar);
-        tma2d(ms + 256, tmm, ti * 32 + 16, gy0 + jj * (WPT * GQ), bar);   // 128-B aligned
+        tma2d_e(el, ms, tmm, ti * 32, gy0 + jj * (WPT * GQ), bar);
+        tma2d_e(el, ms + 256, tmm, ti * 32 + 16, gy0 + jj * (WPT * GQ), bar);   // 128-B aligned
       }
     }
   };
@@ -477,10 +508,19 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
         const int t = idx / npos, pos = idx - t * npos;
         const int gl = x_logical(pos, xu4);
         uint4 v4 = make_uint4(0, 0, 0, 0);
-        if (t < nt && gl < gran) {
+        if (t < nt) {
           const int r = tok0 + t;
-          const uint16_t* src = W13 ? a.x + (size_t)a.perm_token[r] * a.Hd : a.h + (size_t)r * a.F;
-          v4 = *reinterpret_cast<const uint4*>(src + k0 + gl * 8);
+          const uint16_t* src = (W13 ? a.x + (size_t)a.perm_token[r] * a.Hd : a.h + (size_t)r * a.F) + k0;
+          const uint4 z4 = make_uint4(0, 0, 0, 0);
+          if (be == 2) {   // granule pair (gb, gb + 1), element-interleaved (x_perm)
+            const int gb = gl & ~1;
+            const uint4 ga = gb < gran ? *reinterpret_cast<const uint4*>(src + gb * 8) : z4;
+            const uint4 gc = gb + 1 < gran ? *reinterpret_cast<const uint4*>(src + gb * 8 + 8) : z4;
+            v4 = x_perm<2>(ga, gc, gl & 1);
+          } else if (gl < gran) {
+            v4 = *reinterpret_cast<const uint4*>(src + gl * 8);
+            if (be == 4) v4 = x_perm<4>(v4, v4, 0);
+          }
         }
         xs[t * row_gran + pos] = v4;
       }

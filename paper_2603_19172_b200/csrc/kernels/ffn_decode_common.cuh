@@ -70,28 +70,16 @@ __device__ __forceinline__ uint32_t word(const uint4& v, int i) {
 }
 
 struct DQ {
-  uint32_t ss, zz;  // bf16x2 (s, s) and (128+z, 128+z)
+  uint32_t ss, zz;    // bf16x2 (s, s) and (128+z, 128+z)
   uint32_t zz1, zz2;  // Int2: (32+z, 32+z) and (8+z, 8+z)
-  float sf, zf;     // Int8: bf16(s) as float, 2^23 + z
+  float sf, zf;       // Int8: bf16(s) as float, 2^23 + z
 };
-__device__ __forceinline__ DQ make_dq(float s, uint32_t z) {
-  DQ d;
-  const __nv_bfloat16 sb = __float2bfloat16_rn(s);
-  const uint32_t sbits = *reinterpret_cast<const uint16_t*>(&sb);
-  d.ss = sbits | (sbits << 16);
-  const uint32_t zl2 = z | (z << 16);
-  d.zz = 0x43004300u + zl2;  // bf16(128 + z), exact for z < 128 (Int2/Int4)
-  d.zz1 = 0x42004200u + zl2 * 4u;
-  d.zz2 = 0x41004100u + zl2 * 16u;
-  d.sf = __bfloat162float(sb);
-  d.zf = __uint_as_float(0x4B000000u | z);
-  return d;
-}
 
 // A-fragment pair (logical k slots lo = {2c, 2c+1}, hi = {2c+8, 2c+9}) for step s of a chunk.
 //
 // Int4: codes j (bits 4j..4j+3 of each 16-bit half) are shifted down and OR-ed into the mantissa
-// of bf16 128 (exponent 7, ulp 1): 128 + q exactly.
+// of bf16 128 (exponent 7, ulp 1): 128 + q exactly.  (A code at bits 4..7 would reach the
+// exponent's lowest bit, so every code but the lowest needs its shift.)
 // Int2: no shift for codes at bits 2k..2k+1 (k = 0, 1, 2) of a half: OR-ed into the mantissa of
 // bf16 2^(7-2k) (ulp 4^-k) they read as 2^(7-2k) + q exactly, and subtracting bf16(2^(7-2k) + z)
 // gives q - z exactly; codes 3-5 / 6-7 of a half come from one shift by 6 / 12.  So a word of 16
@@ -148,21 +136,39 @@ struct XB {
   static constexpr int NB = WT<BITS>::STEPS / SPB;
 };
 
-// B fragment (x permuted to a_frag's k order) for step ss of a block, from the block's x granules.
+// B fragment (x in a_frag's k order) for step ss of a block, from the block's x granules.  The x
+// staging already permuted the elements of each granule into that order (x_perm), so a fragment is
+// two words of a granule at every width.
 template <int BITS>
 __device__ __forceinline__ void b_frag(const uint4 (&xb)[XB<BITS>::GPB], int ss, uint32_t& b0,
                                        uint32_t& b1) {
-  if constexpr (BITS == 16 || BITS == 8) {
+  if constexpr (BITS == 2) {
+    b0 = word(xb[ss >> 1], 2 * (ss & 1));
+    b1 = word(xb[ss >> 1], 2 * (ss & 1) + 1);
+  } else {
     b0 = word(xb[0], 2 * ss);
     b1 = word(xb[0], 2 * ss + 1);
-  } else if constexpr (BITS == 4) {
-    const uint32_t a = word(xb[0], ss), c = word(xb[0], ss + 2);
-    b0 = prmt(a, c, 0x5410u);
-    b1 = prmt(a, c, 0x7632u);
-  } else {  // 2
-    const uint32_t a = word(xb[0], ss), c = word(xb[1], ss);
-    b0 = prmt(a, c, 0x5410u);
-    b1 = prmt(a, c, 0x7632u);
+  }
+}
+
+// Element order of the staged x granules: a_frag's step s pairs, per lane, k values that are not
+// adjacent in x (Int4: codes j and j + 4 of a byte pair; Int2: the same code position of two
+// consecutive granules), so the staging stores
+//   Int4: granule (e0 .. e7) as (e0 e4 e1 e5 e2 e6 e3 e7);
+//   Int2: granule pair A, C as (a0 c0 a1 c1 a2 c2 a3 c3), (a4 c4 a5 c5 a6 c6 a7 c7) (half 0, 1);
+//   BF16 / Int8: unchanged.
+template <int BITS>
+__device__ __forceinline__ uint4 x_perm(const uint4& a, const uint4& c, int half) {
+  if constexpr (BITS == 4) {
+    return make_uint4(prmt(a.x, a.z, 0x5410u), prmt(a.x, a.z, 0x7632u), prmt(a.y, a.w, 0x5410u),
+                      prmt(a.y, a.w, 0x7632u));
+  } else if constexpr (BITS == 2) {
+    const uint32_t a0 = half ? a.z : a.x, a1 = half ? a.w : a.y;
+    const uint32_t c0 = half ? c.z : c.x, c1 = half ? c.w : c.y;
+    return make_uint4(prmt(a0, c0, 0x5410u), prmt(a0, c0, 0x7632u), prmt(a1, c1, 0x5410u),
+                      prmt(a1, c1, 0x7632u));
+  } else {
+    return a;
   }
 }
 
@@ -183,8 +189,8 @@ struct AllocScratch {
 // with every expert forced to one width (tools/decode_width_sweep.py): the narrow widths are
 // bound by dequant issue slots rather than bytes, so they cost more than their bytes suggest.
 __device__ __forceinline__ int wcost(int b, bool w13) {
-  if (w13) return b == 16 ? 256 : b == 8 ? 173 : b == 4 ? 125 : 111;
-  return b == 16 ? 256 : b == 8 ? 203 : b == 4 ? 155 : 134;
+  if (w13) return b == 16 ? 256 : b == 8 ? 172 : b == 4 ? 118 : 107;
+  return b == 16 ? 256 : b == 8 ? 196 : b == 4 ? 144 : 131;
 }
 
 // Cost-proportional allocation of `units_total` units to the active experts (largest remainder,
