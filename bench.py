@@ -329,8 +329,9 @@ def run_ours(args, rank, world, device):
                     "algorithmic_flops_per_step": fl / K, "hbm_GBs_ffn": achieved_ffn}
     res = None
     if rank == 0:
-        # route, score, assign, permute, [prefill: gather into expert order], W13, W2, combine
-        launches_per_step = 7 if phase == d.DYMOE_DECODE else 8
+        # decode: fused front (route+score+assign+permute), W13, W2, combine; prefill: route, score,
+        # assign, permute, gather into expert order, W13, W2, combine
+        launches_per_step = 4 if phase == d.DYMOE_DECODE else 8
         res = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

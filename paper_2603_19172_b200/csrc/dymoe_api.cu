@@ -796,23 +796,33 @@ int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logi
   int32_t* active_list = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + W.active_list);
   cudaStream_t s = S(stream);
 
-  CHECK_LAUNCH(launch_route(logits, T, L->M, L->k, v.topk_idx, v.topk_w, v.probs, s), "route");
   const uint8_t* bits = o->forced_bits;
-  if (bits == nullptr) {
-    if (o->phase == DYMOE_PREFILL) {
-      CHECK_LAUNCH(launch_score_prefill(o->attn_mass, o->heads, v.topk_idx, T, L->M, L->k, k_tokens,
-                                        v.importance, v.heavy,
-                                        reinterpret_cast<float*>(v.score_scratch), s),
-                   "score");
-    } else {
-      CHECK_LAUNCH(launch_score_decode(logits, T, L->M, v.importance, s), "score");
+  if (o->phase == DYMOE_DECODE && T <= kFrontDecodeMaxT) {
+    // decode batch: route, score, assign and permute in one launch
+    CHECK_LAUNCH(launch_front_decode(logits, T, L->M, L->k, ap, bits, v.topk_idx, v.topk_w, v.probs,
+                                     v.importance, v.bits, v.active, v.expert_off, v.perm_token,
+                                     v.perm_slot, v.inv_row, active_list, s),
+                 "front");
+    if (bits == nullptr) bits = v.bits;
+  } else {
+    CHECK_LAUNCH(launch_route(logits, T, L->M, L->k, v.topk_idx, v.topk_w, v.probs, s), "route");
+    if (bits == nullptr) {
+      if (o->phase == DYMOE_PREFILL) {
+        CHECK_LAUNCH(launch_score_prefill(o->attn_mass, o->heads, v.topk_idx, T, L->M, L->k,
+                                          k_tokens, v.importance, v.heavy,
+                                          reinterpret_cast<float*>(v.score_scratch), s),
+                     "score");
+      } else {
+        CHECK_LAUNCH(launch_score_decode(logits, T, L->M, v.importance, s), "score");
+      }
+      CHECK_LAUNCH(launch_assign(v.importance, nullptr, v.topk_idx, T, ap, v.bits, v.active, s),
+                   "assign");
+      bits = v.bits;
     }
-    CHECK_LAUNCH(launch_assign(v.importance, nullptr, v.topk_idx, T, ap, v.bits, v.active, s), "assign");
-    bits = v.bits;
+    CHECK_LAUNCH(launch_permute(v.topk_idx, T, L->k, L->M, bits, v.expert_off, v.perm_token,
+                                v.perm_slot, v.inv_row, active_list, s),
+                 "permute");
   }
-  CHECK_LAUNCH(launch_permute(v.topk_idx, T, L->k, L->M, bits, v.expert_off, v.perm_token,
-                              v.perm_slot, v.inv_row, active_list, s),
-               "permute");
   const int mode = o->ffn_mode == -1 ? o->phase : o->ffn_mode;
   float* y_part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + W.y_part);
   int n_parts = 0;

@@ -74,6 +74,15 @@ cudaError_t launch_assign(const float* importance, const uint8_t* active_mask,
                           const int32_t* topk_idx, int T, const AssignParams& p, uint8_t* bits,
                           uint8_t* active_out, cudaStream_t s);
 
+// Fused decode front (route -> [score -> assign] -> permute), one single-CTA launch; the same
+// arithmetic as launch_route + launch_score_decode + launch_assign + launch_permute.
+constexpr int kFrontDecodeMaxT = 256;
+cudaError_t launch_front_decode(const float* logits, int T, int M, int k, const AssignParams& p,
+                                const uint8_t* forced_bits, int32_t* topk_idx, float* topk_w,
+                                float* probs, float* importance, uint8_t* bits, uint8_t* active,
+                                int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot,
+                                int32_t* inv_row, int32_t* active_list, cudaStream_t s);
+
 cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaStream_t s);
 
 cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,

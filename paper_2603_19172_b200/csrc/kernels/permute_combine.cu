@@ -8,12 +8,12 @@
 // from __match_any_sync).  Integer-only, bit-exact by construction.
 //
 // Combine (reading D12): y[t] = sum_slot w'[t,slot] * y_perm[inv_row[t,slot]], slot order, fp32.
-#include "../dymoe_internal.cuh"
+#include "front_common.cuh"
 
 namespace dymoe {
 
-constexpr int kPermThreads = 1024;
-constexpr int kPermWarps = kPermThreads / 32;
+using front::kPermThreads;
+using front::kPermWarps;
 
 __global__ void __launch_bounds__(kPermThreads)
 k_permute(const int32_t* __restrict__ topk_idx, int T, int k, int M,
@@ -21,68 +21,10 @@ k_permute(const int32_t* __restrict__ topk_idx, int T, int k, int M,
           int32_t* __restrict__ perm_token, int32_t* __restrict__ perm_slot,
           int32_t* __restrict__ inv_row, int32_t* __restrict__ active_list) {
   __shared__ int running[DYMOE_MAX_EXPERTS];
-  __shared__ int warp_cnt[kPermWarps][DYMOE_MAX_EXPERTS];
+  __shared__ int warp_cnt[kPermWarps * DYMOE_MAX_EXPERTS];
   __shared__ uint8_t keep[DYMOE_MAX_EXPERTS];
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int P = T * k;
-  for (int e = tid; e < M; e += kPermThreads) {
-    running[e] = 0;
-    keep[e] = bits[e] != 0;
-  }
-  __syncthreads();
-  // pass 1: counts per expert
-  for (int p = tid; p < P; p += kPermThreads) {
-    const int e = topk_idx[p];
-    if (keep[e]) atomicAdd(&running[e], 1);
-  }
-  __syncthreads();
-  // exclusive scan of counts (M <= 256: warp 0 does it serially per lane-chunk)
-  if (tid == 0) {
-    int acc = 0, na = 0;
-    for (int e = 0; e < M; ++e) {
-      const int c = running[e];
-      expert_off[e] = acc;
-      running[e] = acc;
-      if (c > 0) active_list[1 + na++] = e;
-      acc += c;
-    }
-    expert_off[M] = acc;
-    active_list[0] = na;
-  }
-  __syncthreads();
-  // pass 2: stable placement, chunk by chunk in (token, slot) order
-  for (int c0 = 0; c0 < P; c0 += kPermThreads) {
-    for (int q = tid; q < kPermWarps * M; q += kPermThreads) (&warp_cnt[0][0])[
-        (q / M) * DYMOE_MAX_EXPERTS + (q % M)] = 0;
-    __syncthreads();
-    const int p = c0 + tid;
-    int e = -1;
-    if (p < P) {
-      e = topk_idx[p];
-      if (!keep[e]) {
-        inv_row[p] = -1;
-        e = -1;
-      }
-    }
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    const int rank_in_warp = __popc(peers & ((1u << lane) - 1u));
-    if (e >= 0 && rank_in_warp == 0) warp_cnt[w][e] = __popc(peers);
-    __syncthreads();
-    if (e >= 0) {
-      int r = running[e] + rank_in_warp;
-      for (int q = 0; q < w; ++q) r += warp_cnt[q][e];
-      perm_token[r] = p / k;
-      perm_slot[r] = p - (p / k) * k;
-      inv_row[p] = r;
-    }
-    __syncthreads();
-    for (int e2 = tid; e2 < M; e2 += kPermThreads) {
-      int add = 0;
-      for (int q = 0; q < kPermWarps; ++q) add += warp_cnt[q][e2];
-      running[e2] += add;
-    }
-    __syncthreads();
-  }
+  front::permute(topk_idx, T, k, M, bits, expert_off, perm_token, perm_slot, inv_row, active_list,
+                 running, warp_cnt, keep);
 }
 
 cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,

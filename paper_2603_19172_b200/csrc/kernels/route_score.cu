@@ -6,96 +6,22 @@
 //
 // All three are latency-bound (a few KB of input per layer); they are written for one launch
 // each with no host round trip so that a decode step can be captured in a CUDA graph.
-#include <cfloat>
-#include <math.h>
-
-#include "../dymoe_internal.cuh"
+#include "front_common.cuh"
 
 namespace dymoe {
 
 // ===========================================================================================
-// Route: one warp per token.  Each lane holds up to 8 logits (M <= 256).  Top-k is k rounds of
-// a warp arg-max under the total order (value desc, index asc); comparisons are plain float
-// compares, so -0.0 == +0.0 (reading D11).
+// Route: one warp per token (front::route_token: top-k by (logit desc, index asc), softmax over
+// the k, full softmax).
 // ===========================================================================================
-__device__ __forceinline__ bool better(float va, int ia, float vb, int ib) {
-  return va > vb || (va == vb && ia < ib);
-}
-
 __global__ void __launch_bounds__(256) k_route(const float* __restrict__ logits, int T, int M,
                                                int k, int32_t* __restrict__ topk_idx,
                                                float* __restrict__ topk_w,
                                                float* __restrict__ probs) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
   if (warp >= T) return;
-  const float* row = logits + (size_t)warp * M;
-  float v[8];
-  uint32_t taken = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int j = lane + 32 * i;
-    v[i] = j < M ? row[j] : -FLT_MAX;
-  }
-  float sel_v[8];
-  int sel_i[8];
-  for (int r = 0; r < k; ++r) {
-    float bv = 0.f;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int j = lane + 32 * i;
-      if (j < M && !(taken >> i & 1u) && (bi == 0x7fffffff || better(v[i], j, bv, bi))) {
-        bv = v[i];
-        bi = j;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    sel_v[r] = bv;
-    sel_i[r] = bi;
-    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-  }
-  // softmax over the selected logits (max = the first selected), fp32, slot order
-  const float vmax = sel_v[0];
-  float e[8];
-  float z = 0.f;
-  for (int r = 0; r < k; ++r) {
-    e[r] = expf(sel_v[r] - vmax);
-    z += e[r];
-  }
-  if (lane < k) {
-    float my_e = 0.f;
-    int my_i = 0;
-    for (int r = 0; r < k; ++r)
-      if (r == lane) { my_e = e[r]; my_i = sel_i[r]; }
-    topk_idx[(size_t)warp * k + lane] = my_i;
-    topk_w[(size_t)warp * k + lane] = my_e / z;
-  }
-  if (probs != nullptr) {
-    float ev[8];
-    float zs = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int j = lane + 32 * i;
-      ev[i] = j < M ? expf(v[i] - vmax) : 0.f;
-      zs += ev[i];
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) zs += __shfl_xor_sync(0xffffffffu, zs, off);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      int j = lane + 32 * i;
-      if (j < M) probs[(size_t)warp * M + j] = ev[i] / zs;
-    }
-  }
+  front::route_token(logits + (size_t)warp * M, M, k, threadIdx.x & 31, topk_idx + (size_t)warp * k,
+                     topk_w + (size_t)warp * k, probs != nullptr ? probs + (size_t)warp * M : nullptr);
 }
 
 cudaError_t launch_route(const float* logits, int T, int M, int k, int32_t* topk_idx,
@@ -260,48 +186,12 @@ cudaError_t launch_score_prefill(const float* attn, int H, const int32_t* topk_i
 
 // ===========================================================================================
 // Decode score (Eq. 3, reading D10): B == 1 -> the logit row; B > 1 -> sum_b softmax(l_b)
-// (fp32, b ascending).  One CTA, one thread per expert, block reductions per token.
+// (fp32, b ascending; each softmax exactly route's probs).  One CTA of 8 warps.
 // ===========================================================================================
 __global__ void __launch_bounds__(256) k_score_decode(const float* __restrict__ logits, int B,
                                                       int M, float* __restrict__ importance) {
-  __shared__ float red[8];
-  __shared__ float bc[2];
-  const int j = threadIdx.x;
-  const int lane = j & 31, w = j >> 5;
-  if (B == 1) {
-    if (j < M) importance[j] = logits[j];
-    return;
-  }
-  float acc = 0.f;
-  for (int b = 0; b < B; ++b) {
-    const float l = j < M ? logits[(size_t)b * M + j] : -FLT_MAX;
-    float m = l;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    if (lane == 0) red[w] = m;
-    __syncthreads();
-    if (j == 0) {
-      float mm = red[0];
-      for (int q = 1; q < 8; ++q) mm = fmaxf(mm, red[q]);
-      bc[0] = mm;
-    }
-    __syncthreads();
-    const float e = j < M ? expf(l - bc[0]) : 0.f;
-    float z = e;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
-    if (lane == 0) red[w] = z;
-    __syncthreads();
-    if (j == 0) {
-      float zz = 0.f;
-      for (int q = 0; q < 8; ++q) zz += red[q];
-      bc[1] = zz;
-    }
-    __syncthreads();
-    acc += e / bc[1];
-    __syncthreads();
-  }
-  if (j < M) importance[j] = acc;
+  __shared__ float sp[8 * DYMOE_MAX_EXPERTS];
+  front::decode_importance(logits, B, M, sp, importance);
 }
 
 cudaError_t launch_score_decode(const float* logits, int B, int M, float* importance,
@@ -311,9 +201,8 @@ cudaError_t launch_score_decode(const float* logits, int B, int M, float* import
 }
 
 // ===========================================================================================
-// Assign bits (Eq. 5 + tiers, readings D5, D7-D9, D11): one CTA, thread j = expert j.
-// rank_j = #{i in candidates : I_i > I_j or (I_i == I_j and i < j)}; t_k = ceil(r_k*M_eff - 1e-9)
-// in fp64 (no contraction: explicit _rn intrinsics) from the host-evaluated r_k.
+// Assign bits (Eq. 5 + tiers, readings D5, D7-D9, D11): one CTA, thread j = expert j
+// (front::assign_bits).
 // ===========================================================================================
 __global__ void __launch_bounds__(256) k_assign(const float* __restrict__ importance,
                                                 const uint8_t* __restrict__ active_mask,
@@ -323,48 +212,58 @@ __global__ void __launch_bounds__(256) k_assign(const float* __restrict__ import
   __shared__ float I[DYMOE_MAX_EXPERTS];
   __shared__ int act[DYMOE_MAX_EXPERTS];
   __shared__ int n_act;
-  const int j = threadIdx.x;
-  if (j < p.M) {
-    I[j] = importance[j];
-    act[j] = p.m_active ? (active_mask != nullptr ? (active_mask[j] != 0) : 0) : 1;
-  }
-  if (j == 0) n_act = 0;
-  __syncthreads();
-  if (p.m_active && active_mask == nullptr) {
-    for (int q = j; q < T * p.k_route; q += blockDim.x) act[topk_idx[q]] = 1;  // benign race
-    __syncthreads();
-  }
-  if (j < p.M && act[j]) atomicAdd(&n_act, 1);
-  __syncthreads();
-  if (j >= p.M) return;
-  if (active_out != nullptr) active_out[j] = (uint8_t)act[j];
-  const int M_eff = n_act;
-  if (!act[j]) {
-    bits[j] = (uint8_t)p.bits[p.n_tiers - 1];
-    return;
-  }
-  const float Ij = I[j];
-  int rank = 0;
-  for (int i = 0; i < p.M; ++i)
-    if (act[i] && (I[i] > Ij || (I[i] == Ij && i < j))) ++rank;
-  int tier = p.n_tiers - 1;
-  int prev = 0;
-  for (int q = 0; q < p.n_tiers - 1; ++q) {
-    double x = __dsub_rn(__dmul_rn(p.r[q], (double)M_eff), 1e-9);
-    int t = (int)ceil(x);
-    if (q == 0 && p.clamp_to_k) t = max(t, min(p.k_route, M_eff));
-    t = max(t, prev);
-    t = min(t, M_eff);
-    prev = t;
-    if (rank < t && tier == p.n_tiers - 1) tier = q;
-  }
-  bits[j] = (uint8_t)p.bits[tier];
+  front::assign_bits(importance, active_mask, topk_idx, T, p, bits, active_out, I, act, &n_act);
 }
 
 cudaError_t launch_assign(const float* importance, const uint8_t* active_mask,
                           const int32_t* topk_idx, int T, const AssignParams& p, uint8_t* bits,
                           uint8_t* active_out, cudaStream_t s) {
   k_assign<<<1, 256, 0, s>>>(importance, active_mask, topk_idx, T, p, bits, active_out);
+  return cudaGetLastError();
+}
+
+// ===========================================================================================
+// Fused decode front: route -> score -> assign -> permute in ONE single-CTA launch (1024
+// threads) for a decode batch, with exactly the arithmetic of the four standalone kernels (the
+// same front:: bodies).  A decode step's front is latency-bound (a few KB), so three launches and
+// their gaps were ~10 % of the step.  forced_bits != nullptr skips score/assign.
+// ===========================================================================================
+__global__ void __launch_bounds__(front::kPermThreads)
+k_front_decode(const float* logits, int T, int M, int k, AssignParams p,
+               const uint8_t* forced_bits, int32_t* topk_idx, float* topk_w, float* probs,
+               float* importance, uint8_t* bits, uint8_t* active, int32_t* expert_off,
+               int32_t* perm_token, int32_t* perm_slot, int32_t* inv_row, int32_t* active_list) {
+  // phase buffers: the score's per-warp softmax rows and the permute's per-warp histograms are
+  // never live at the same time (block barriers between the phases)
+  __shared__ __align__(16) int big[front::kPermWarps * DYMOE_MAX_EXPERTS];
+  __shared__ int running[DYMOE_MAX_EXPERTS];
+  __shared__ float I[DYMOE_MAX_EXPERTS];
+  __shared__ int act[DYMOE_MAX_EXPERTS];
+  __shared__ uint8_t keep[DYMOE_MAX_EXPERTS];
+  __shared__ int n_act;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int t = w; t < T; t += front::kPermWarps)
+    front::route_token(logits + (size_t)t * M, M, k, lane, topk_idx + (size_t)t * k,
+                       topk_w + (size_t)t * k, probs != nullptr ? probs + (size_t)t * M : nullptr);
+  __syncthreads();
+  const uint8_t* b = forced_bits;
+  if (b == nullptr) {
+    front::decode_importance(logits, T, M, reinterpret_cast<float*>(big), importance);
+    front::assign_bits(importance, nullptr, topk_idx, T, p, bits, active, I, act, &n_act);
+    b = bits;
+  }
+  front::permute(topk_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row, active_list,
+                 running, big, keep);
+}
+
+cudaError_t launch_front_decode(const float* logits, int T, int M, int k, const AssignParams& p,
+                                const uint8_t* forced_bits, int32_t* topk_idx, float* topk_w,
+                                float* probs, float* importance, uint8_t* bits, uint8_t* active,
+                                int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot,
+                                int32_t* inv_row, int32_t* active_list, cudaStream_t s) {
+  k_front_decode<<<1, front::kPermThreads, 0, s>>>(logits, T, M, k, p, forced_bits, topk_idx, topk_w,
+                                                   probs, importance, bits, active, expert_off,
+                                                   perm_token, perm_slot, inv_row, active_list);
   return cudaGetLastError();
 }
 

@@ -343,3 +343,42 @@ def test_max_experts_and_multi_pass_decode(mode):
             xr = x.float().numpy()[perm["perm_token"][lo:hi]].astype(np.float64)
             ref = o_moe.ffn(xr, W1, W3, W2)
             assert rel_err(y[lo:hi].cpu().numpy(), ref) <= FFN_TOL, (cfg.name, e, int(bits[e]))
+
+
+# ------------------------------------------------------------------------------------ fused decode front
+@pytest.mark.parametrize("M,k,T,m_active,forced", [(8, 2, 1, False, False), (8, 2, 8, False, False),
+                                                   (64, 6, 33, False, False), (64, 6, 40, True, False),
+                                                   (256, 8, 256, False, False), (16, 4, 257, False, False),
+                                                   (8, 2, 5, False, True)])
+def test_fused_decode_front_equals_kernels(M, k, T, m_active, forced):
+    """dymoe_moe_forward's decode front (one launch: route -> score -> assign -> permute, T <= 256)
+    is bit-identical to the standalone dymoe_route / dymoe_score / dymoe_assign_bits /
+    dymoe_permute calls on the same inputs (T = 257 takes the four-launch path)."""
+    d = D()
+    cfg = synthetic.MoEConfig("front", M=M, k=k, hidden=128, ffn=128, T=T)
+    ex = gpu_experts(cfg, 3, widths=(8, 4, 2))
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    x, _, _ = synthetic.layer_inputs(cfg, 3)
+    lg = synthetic.random_logits(T, M, seed=T + M, ties=(T % 2 == 1)).cuda()
+    ladder = d.make_ladder((8, 4, 2), (0.25, 0.5), m_active=m_active)
+    fb = torch.from_numpy(np.array([(8, 4, 2)[e % 3] for e in range(M)], np.uint8)).cuda() if forced else None
+    _, ws = layer.forward(x.cuda(), lg, ladder, 29, 32, phase=d.DYMOE_DECODE, forced_bits=fb)
+    torch.cuda.synchronize()
+    v = layer.views(T, ws)
+    idx, w, p = d.dymoe_route(lg, k)
+    assert torch.equal(v["topk_idx"], idx) and torch.equal(v["topk_w"], w) and torch.equal(v["probs"], p)
+    if forced:
+        bits = fb
+    else:
+        imp, _ = d.dymoe_score(d.DYMOE_DECODE, M, logits=lg)
+        assert torch.equal(v["importance"], imp)
+        mask = None
+        if m_active:
+            mask = torch.zeros(M, dtype=torch.uint8, device="cuda")
+            mask[idx.long().flatten()] = 1
+        bits, _ = d.dymoe_assign_bits(imp, 29, 32, ladder, k, active_mask=mask)
+        assert torch.equal(v["bits"], bits)
+    off, pt, ps, inv = d.dymoe_permute(idx, M, bits)
+    n = int(off[-1].item())
+    assert torch.equal(v["expert_off"], off) and torch.equal(v["inv_row"], inv)
+    assert torch.equal(v["perm_token"][:n], pt[:n]) and torch.equal(v["perm_slot"][:n], ps[:n])
