@@ -1,6 +1,7 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -q -x 2>&1 | tail -5 > gpurun_out/pytest_gpu.txt
 cat gpurun_out/pytest_gpu.txt
+timeout 300 python tools/decode_width_sweep.py 2>&1 | tail -4
 timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err
 python -c "
 import json
