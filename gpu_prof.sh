@@ -1,6 +1,7 @@
 mkdir -p gpurun_out
-./tools/micro/pipe_rates > gpurun_out/micro_pipe_rates.txt 2>&1
-timeout 60 ./tools/micro/tmem_a > gpurun_out/micro_tmem_a.txt 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_|gemv|gemm|attn" -c 200 --csv --log-file gpurun_out/r01_launches_decode.csv python bench.py --steps 8 --warmup 3 --copies 1 --no-cpu-baseline > gpurun_out/b_dec.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_|gemv|gemm|attn" -c 200 --csv --log-file gpurun_out/r01_launches_prefill.csv python bench.py --workload prefill --steps 4 --warmup 3 --copies 1 --no-cpu-baseline > gpurun_out/b_pf.log 2>&1
-tail -c 300 gpurun_out/b_dec.log; tail -c 300 gpurun_out/b_pf.log
+python tools/profile_step.py --workload decode > gpurun_out/step_decode.json 2>/dev/null
+ncu --set full --clock-control none --import-source on -k regex:k_decode_gemv -s 4 -c 2 -o gpurun_out/r01_decode_full -f python tools/profile_step.py --workload decode > gpurun_out/ncu_dec.log 2>&1
+python tools/profile_step.py --workload prefill > gpurun_out/step_prefill.json 2>/dev/null
+ncu --set full --clock-control none --import-source on -k regex:k_prefill_gemm -s 4 -c 2 -o gpurun_out/r01_prefill_full -f python tools/profile_step.py --workload prefill > gpurun_out/ncu_pf.log 2>&1
+tail -3 gpurun_out/ncu_dec.log gpurun_out/ncu_pf.log
+ls -la gpurun_out/*.ncu-rep
