@@ -692,13 +692,131 @@ def run_reference(args):
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def run_stack(args, device):
+    """SURVEY §8d C5 (BASELINE.json configs[4]) on one GPU: a 32-layer Mixtral-8x7B-shaped stack
+    on the bf16 residual stream (paper_2603_19172_b200.stack.MoEStack: RMSNorm -> router -> MoE ->
+    residual add per layer), every layer its own random
+    experts (packed Int8/Int4/Int2 resident, bf16 masters dropped after quantization: 84 GB) and
+    its own router, depth-adaptive bits.  A step = one pass of the whole stack for `batch` decode
+    tokens (or `tokens` prefill tokens).  value = tokens through all 32 layers per second."""
+    import paper_2603_19172_b200.dymoe as d
+    from paper_2603_19172_b200.stack import MoEStack
+    d.lib()
+    torch.cuda.set_device(device)
+    peaks = load_peaks()
+    prefill = args.workload == "stack_prefill"
+    T = args.tokens if prefill else args.batch
+    cfg = synthetic.CONFIGS["stack"].with_tokens(T)
+    L = cfg.layers
+    phase = d.DYMOE_PREFILL if prefill else d.DYMOE_DECODE
+    layers, gates = [], []
+    for l in range(L):
+        ex = [{n: t for n, t in e.items()} for e in synthetic.expert_weights(cfg, 3000 + l, device)]
+        d.quantize_experts(ex, (8, 4, 2))
+        torch.cuda.synchronize()
+        for e in ex:          # the ladder has no BF16 tier: keep only the packed widths
+            for n in ("w1", "w3", "w2"):
+                del e[n]
+        layers.append(ex)
+        gates.append(synthetic.stack_gate(cfg, l, 7, device))
+    torch.cuda.empty_cache()
+    st = MoEStack(layers, gates, cfg.k, cfg.hidden, cfg.ffn)
+    x = synthetic.hidden_states(cfg, 8, device)
+    attn = [synthetic.attention_mass(cfg, 400 + l, device) for l in range(L)] if prefill else None
+    ladder = d.make_ladder(LADDER_BITS, LADDER_LAMBDAS)
+    ws = st.workspace(T, device)
+    bufs = (torch.empty_like(x), torch.empty_like(x), torch.empty_like(x))
+    logits = torch.empty(T, cfg.M, dtype=torch.float32, device=device)
+    # census of one pass (bits and loads are data-dependent per layer)
+    _, tr = st.forward(x, ladder, phase, attn, ws=ws, bufs=bufs, logits=logits, trace=True)
+    b_tot = fl_tot = 0.0
+    widths = {}
+    for l in range(L):
+        bits = tr[l][3].cpu().numpy()
+        lgl = tr[l][2]
+        r_idx = torch.topk(lgl, cfg.k, dim=1).indices.cpu().numpy()   # loads only (census)
+        off = np.zeros(cfg.M + 1, np.int64)
+        for e in range(cfg.M):
+            off[e + 1] = off[e] + int((r_idx == e).sum()) * int(bits[e] != 0)
+        b13, b2 = algorithmic_bytes(cfg, bits, off)
+        b_tot += b13 + b2
+        fl_tot += algorithmic_flops(cfg, off, bits)
+        for b in bits.tolist():
+            widths[b] = widths.get(b, 0) + 1
+    del tr
+    stream = torch.cuda.current_stream()
+
+    def one_step():
+        st.forward(x, ladder, phase, attn, ws=ws, bufs=bufs, logits=logits)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    K = args.steps
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t0.record(stream)
+        for _ in range(K):
+            one_step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    # e2e: x from pinned host memory in, the final stream out, every step
+    hx = x.cpu().pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    dx = torch.empty_like(x)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(K):
+        dx.copy_(hx, non_blocking=True)
+        y, _ = st.forward(dx, ladder, phase, attn, ws=ws, bufs=bufs, logits=logits)
+        hy.copy_(y, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    step_s = ms / K / 1e3
+    if prefill:
+        ach = fl_tot / step_s / 1e12
+        pk = peaks["bf16_sus"] or peaks["bf16"]
+        roof = {"bound": "tensor", "kernel": "whole stack (32 x (rmsnorm, gate, front, tcgen05 W13/W2 GEMMs, combine))",
+                "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
+                "peak_src": peaks["src"] + " bf16 sustained", "algorithmic_flops_per_step": fl_tot}
+    else:
+        ach = b_tot / step_s / 1e9
+        roof = {"bound": "hbm", "kernel": "whole stack (32 x (rmsnorm, gate, front, W13/W2 GEMVs, combine))",
+                "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
+                "traffic": None, "peak_src": peaks["src"], "algorithmic_bytes_per_step": b_tot}
+    # rmsnorm, gate, (decode: fused front | prefill: route, score, assign, permute, gather), W13,
+    # W2, combine
+    per_layer = 6 if not prefill else 10
+    return {"metric": METRIC, "value": T * K / (ms / 1e3), "unit": "tokens/s", "n_gpus": 1, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
+            "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts and routers per layer)",
+            "config": {"workload": "mixtral_stack32_%s" % ("prefill" if prefill else "decode"),
+                       "layers": L, "hidden": cfg.hidden, "ffn": cfg.ffn, "experts": cfg.M, "top_k": cfg.k,
+                       "tokens_per_step": T, "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
+                       "resident_packed_GB": round(torch.cuda.memory_allocated() / 1e9, 1),
+                       "widths_assigned": {str(k): v for k, v in sorted(widths.items())},
+                       "l2": "inputs larger than L2 (32 distinct layers, 84 GB of packed weights)",
+                       "parallelism": "single GPU"},
+            "ms_per_layer": ms / K / L, "roofline": roof, "clocks": clk.summary(),
+            "e2e": {"value": T * K / (e_ms / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hy.numel() * 2)},
+            "gpu_launches": per_layer * L * K}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=512)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])
+    ap.add_argument("--workload", default="decode",
+                    choices=["decode", "prefill", "stack", "stack_prefill"],
+                    help="decode / prefill: one Mixtral layer (configs[1] / [2]); stack / "
+                         "stack_prefill: the 32-layer stack of configs[4] on one GPU")
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--copies", type=int, default=4)
@@ -724,7 +842,11 @@ def main():
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             torch.distributed.init_process_group("gloo")
-    if world > 1:
+    if args.workload.startswith("stack"):
+        if world > 1:
+            raise SystemExit("--workload stack runs on one GPU (the EP stack needs 8 GPUs)")
+        res = run_stack(args, torch.device("cuda", local))
+    elif world > 1:
         res = run_ep(args, rank, world, torch.device("cuda", local))
     else:
         res = run_ours(args, rank, world, torch.device("cuda", local))

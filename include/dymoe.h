@@ -270,6 +270,27 @@ int dymoe_predict_next(int phase, const uint16_t* h, const uint16_t* w_gate_next
                        int M, int k_route, int t, void* ws, size_t ws_bytes, int32_t* experts,
                        float* priority, int32_t* n_out, float* logits_out, dymoe_stream_t stream);
 
+/* Router / gate logits (P:111 router; the gate product of Eq. 6, reading P1):
+ *   logits[t][e] = h[t] · w_gate[e] + bias[e],
+ * the dot product in fp32 in the order of reading P1 (32 lane partial sums over 8-element chunks,
+ * sequential within a lane, one rounding per multiply-add -- bf16 products are exact -- then an
+ * xor butterfly), then one fp32 add of bias[e] (bias nullable = 0).  Used to route each layer of a
+ * stack from its own hidden state on the device.
+ *   h [T][Hd] bf16, w_gate [M][Hd] bf16 (Hd multiple of 8, 16-byte aligned), bias [M] f32,
+ *   logits [T][M] f32 out; all device.
+ * Errors: T < 0, M outside [1, 256], Hd not a positive multiple of 8, NULL or misaligned
+ * pointers (INVALID).                                                                          */
+int dymoe_gate_logits(const uint16_t* h, const uint16_t* w_gate, const float* bias, int T, int Hd,
+                      int M, float* logits, dymoe_stream_t stream);
+
+/* RMSNorm of the residual stream before each layer of a stack (the MoE input of a
+ * Mixtral block, unit weight for random-init weights):
+ *   u[t][i] = RNE_bf16(x[t][i] / sqrt(mean_j x[t][j]^2 + eps)),
+ * the mean of squares in fp32 (per-thread sums in order, then fixed-order reductions), one rsqrt.
+ *   x, u [T][Hd] bf16 device (16-byte aligned, Hd multiple of 8); u may not alias x.
+ * Errors: T < 0, Hd not a positive multiple of 8, eps < 0, NULL / misaligned pointers.          */
+int dymoe_rmsnorm(const uint16_t* x, int T, int Hd, float eps, uint16_t* u, dymoe_stream_t stream);
+
 /* Combine weights against the GLOBAL live set (reading D12), for combines that only see part of
  * the slots (expert-parallel decode with the batch replicated on every rank):
  *   w_out[t][s] = bits[topk_idx[t][s]] > 0 ? topk_w[t][s] / d_t : 0,
@@ -309,6 +330,11 @@ typedef struct dymoe_fwd_opts {
   void* prof_events[3];      /* nullable cudaEvent_t's recorded on `stream` before the gate/up
                                 (W1/W3) FFN kernel, between it and the down (W2) kernel, and
                                 after the down kernel (live per-kernel timing for benchmarks) */
+  const uint16_t* residual;  /* device [T][Hd] bf16, nullable: the residual stream of a layer
+                                stack (x_{l+1} = bf16(x_l + y_l)).  When set the
+                                combine adds it after the slot sum (one fp32 add per element)
+                                before the output rounding: y = out_dtype(residual + sum).  May
+                                alias x but not y. */
 } dymoe_fwd_opts;
 
 /* Workspace: one device buffer of dymoe_workspace_size(...) bytes (256-byte aligned); it holds

@@ -24,10 +24,11 @@ Modules and the passages they follow (PAPER.md line numbers, "P:"):
   prefetch    look-ahead prediction of the next layer's experts, Eqs. 6-8
   pool        mixed-precision expert pool policy, P:303-309 (SPEC cache module)
   attention   causal attention mass a[h][j] (the input of Eq. 1, reading R1)
+  stack       L layers on the bf16 residual stream, each routed by its own gate (config C5)
 
 Pinning status (what each function is checked against) is listed in DESIGN.md §4
 and in tests/test_oracle_*.py.  Functions without an independent pin say
 "parity unpinned" in their docstring.
 """
 
-from . import bf16, route, importance, schedule, quant, moe, prefetch, pool, attention  # noqa: F401
+from . import bf16, route, importance, schedule, quant, moe, prefetch, pool, attention, stack  # noqa: F401

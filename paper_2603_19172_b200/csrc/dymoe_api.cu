@@ -609,6 +609,39 @@ size_t dymoe_predict_ws_bytes(int T, int M, int k_route) {
   return align_up(TM * 4) + align_up(TK * 4) + align_up(TK * 4) + align_up(TM * 4) + align_up((size_t)M * 4);
 }
 
+int dymoe_rmsnorm(const uint16_t* x, int T, int Hd, float eps, uint16_t* u, dymoe_stream_t stream) {
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(Hd > 0 && Hd % 8 == 0, "Hd: must be a positive multiple of 8");
+  CHECK_ARG(eps >= 0.f, "eps: must be >= 0");
+  if (T == 0) return ok();
+  CHECK_ARG(x != nullptr, "x: must not be NULL");
+  CHECK_ARG(u != nullptr, "u: must not be NULL");
+  CHECK_ARG(x != u, "u: must not alias x");
+  int rc = check_ptr_align(x, 16, "x");
+  if (rc) return rc;
+  rc = check_ptr_align(u, 16, "u");
+  if (rc) return rc;
+  CHECK_LAUNCH(launch_rmsnorm(x, T, Hd, eps, u, S(stream)), "dymoe_rmsnorm");
+  return ok();
+}
+
+int dymoe_gate_logits(const uint16_t* h, const uint16_t* w_gate, const float* bias, int T, int Hd,
+                      int M, float* logits, dymoe_stream_t stream) {
+  CHECK_ARG(T >= 0, "T: must be >= 0");
+  CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
+  CHECK_ARG(Hd > 0 && Hd % 8 == 0, "Hd: must be a positive multiple of 8");
+  if (T == 0) return ok();
+  CHECK_ARG(h != nullptr, "h: must not be NULL");
+  CHECK_ARG(w_gate != nullptr, "w_gate: must not be NULL");
+  CHECK_ARG(logits != nullptr, "logits: must not be NULL");
+  int rc = check_ptr_align(h, 16, "h");
+  if (rc) return rc;
+  rc = check_ptr_align(w_gate, 16, "w_gate");
+  if (rc) return rc;
+  CHECK_LAUNCH(launch_gate_logits(h, w_gate, bias, T, Hd, M, logits, S(stream)), "dymoe_gate_logits");
+  return ok();
+}
+
 int dymoe_predict_next(int phase, const uint16_t* h, const uint16_t* w_gate_next, int T, int Hd,
                        int M, int k_route, int t, void* ws, size_t ws_bytes, int32_t* experts,
                        float* priority, int32_t* n_out, float* logits_out, dymoe_stream_t stream) {
@@ -781,6 +814,10 @@ int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logi
   if (rc) return rc;
   rc = check_ptr_align(ws, 256, "workspace");
   if (rc) return rc;
+  if (o->residual != nullptr) {
+    rc = check_ptr_align(o->residual, 16, "opts.residual");
+    if (rc) return rc;
+  }
   const WsLayout W = ws_layout(L->M, L->k, L->Hd, L->F, T);
   if (ws_bytes < W.total)
     return fail(DYMOE_ERR_WORKSPACE, "ws_bytes: %zu < dymoe_workspace_size() = %zu", ws_bytes, W.total);
@@ -831,7 +868,7 @@ int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logi
   if (rc) return rc;
   CHECK_LAUNCH(launch_combine(n_parts > 0 ? y_part : v.y_perm, n_parts > 0 ? n_parts : 1, T * L->k,
                               v.inv_row, v.topk_w, T, L->k, L->Hd, o->ladder.renorm_on_skip,
-                              o->out_dtype, y, s),
+                              o->out_dtype, y, s, o->residual),
                "combine");
   return ok();
 }

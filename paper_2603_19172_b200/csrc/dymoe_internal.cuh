@@ -140,9 +140,15 @@ cudaError_t launch_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, i
 
 // y_perm may hold n_parts partial slices [n_parts][part_rows][Hd]; they are summed in slice order
 // before weighting (n_parts = 1, part_rows ignored for a plain y_perm).
+// residual (nullable, [T][Hd] bf16): added after the slot sum, before the output rounding.
 cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, const int32_t* inv_row,
                            const float* topk_w, int T, int k, int Hd, int renorm, int out_dtype,
-                           void* y, cudaStream_t s);
+                           void* y, cudaStream_t s, const uint16_t* residual = nullptr);
+// u[t] = bf16(x[t] / sqrt(mean(x[t]^2) + eps))  (stack RMSNorm, Hd multiple of 8)
+cudaError_t launch_rmsnorm(const uint16_t* x, int T, int Hd, float eps, uint16_t* u, cudaStream_t s);
+// logits[t][e] = h[t] . wg[e] (fp32, reading P1 order) + bias[e] (nullable)
+cudaError_t launch_gate_logits(const uint16_t* h, const uint16_t* wg, const float* bias, int T,
+                               int Hd, int M, float* logits, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------------
 // Small device helpers.

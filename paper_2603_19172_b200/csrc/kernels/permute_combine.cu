@@ -120,7 +120,9 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
                                                  int part_rows,
                                                  const int32_t* __restrict__ inv_row,
                                                  const float* __restrict__ topk_w, int k, int Hd,
-                                                 int renorm, int out_bf16, void* __restrict__ y) {
+                                                 int renorm, int out_bf16,
+                                                 const uint16_t* __restrict__ residual,
+                                                 void* __restrict__ y) {
   const size_t part_stride = (size_t)part_rows * Hd;
   const int t = blockIdx.x;
   int rows[8];
@@ -147,6 +149,13 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
       acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], v.z));
       acc.w = __fadd_rn(acc.w, __fmul_rn(wt[s], v.w));
     }
+    if (residual != nullptr) {   // x_{l+1} = x_l + y_l (one fp32 add), rounded below if bf16
+      const uint2 r = *reinterpret_cast<const uint2*>(residual + (size_t)t * Hd + c);
+      acc.x = __fadd_rn(__uint_as_float(r.x << 16), acc.x);
+      acc.y = __fadd_rn(__uint_as_float(r.x & 0xffff0000u), acc.y);
+      acc.z = __fadd_rn(__uint_as_float(r.y << 16), acc.z);
+      acc.w = __fadd_rn(__uint_as_float(r.y & 0xffff0000u), acc.w);
+    }
     if (out_bf16) {
       __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y);
       __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z, acc.w);
@@ -163,14 +172,14 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
 
 cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, const int32_t* inv_row,
                            const float* topk_w, int T, int k, int Hd, int renorm, int out_dtype,
-                           void* y, cudaStream_t s) {
+                           void* y, cudaStream_t s, const uint16_t* residual) {
   if (T == 0) return cudaSuccess;
   // ~4 CTAs of 128 threads x float4 per SM in total, at least one column chunk per token
   const int chunks = (Hd + 511) / 512;
   int gy = (4 * 148 + T - 1) / T;
   gy = gy < 1 ? 1 : (gy > chunks ? chunks : gy);
   k_combine<<<dim3(T, gy), 128, 0, s>>>(y_perm, n_parts, part_rows, inv_row, topk_w, k, Hd, renorm,
-                                        out_dtype == DYMOE_OUT_BF16, y);
+                                        out_dtype == DYMOE_OUT_BF16, residual, y);
   return cudaGetLastError();
 }
 

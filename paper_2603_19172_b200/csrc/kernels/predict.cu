@@ -16,7 +16,8 @@ namespace dymoe {
 // (reading P1: the order oracle/prefetch.py writes out)
 __global__ void __launch_bounds__(256) k_gate_logits(const uint4* __restrict__ h,
                                                      const uint4* __restrict__ w, int T, int Hd,
-                                                     int M, float* __restrict__ logits) {
+                                                     int M, const float* __restrict__ bias,
+                                                     float* __restrict__ logits) {
   const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= (long long)T * M) return;
@@ -35,7 +36,17 @@ __global__ void __launch_bounds__(256) k_gate_logits(const uint4* __restrict__ h
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-  if (lane == 0) logits[i] = acc;
+  if (lane == 0) logits[i] = bias != nullptr ? __fadd_rn(acc, bias[e]) : acc;
+}
+
+cudaError_t launch_gate_logits(const uint16_t* h, const uint16_t* wg, const float* bias, int T,
+                               int Hd, int M, float* logits, cudaStream_t s) {
+  const long long n = (long long)T * M * 32;   // one warp per (token, expert)
+  if (n == 0) return cudaSuccess;
+  k_gate_logits<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4*>(h),
+                                                           reinterpret_cast<const uint4*>(wg), T,
+                                                           Hd, M, bias, logits);
+  return cudaGetLastError();
 }
 
 __global__ void k_predict_counts(const int32_t* __restrict__ topk_idx, int n, int M,
@@ -77,11 +88,7 @@ cudaError_t launch_predict_next(int phase, const uint16_t* h, const uint16_t* wg
                                 int M, int k, int t, float* logits, int32_t* topk_idx,
                                 float* topk_w, float* probs, float* value, int32_t* experts,
                                 float* priority, int32_t* n_out, cudaStream_t s) {
-  const long long n = (long long)T * M * 32;   // one warp per (token, expert)
-  k_gate_logits<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4*>(h),
-                                                           reinterpret_cast<const uint4*>(wg), T,
-                                                           Hd, M, logits);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_gate_logits(h, wg, nullptr, T, Hd, M, logits, s);
   if (e != cudaSuccess) return e;
   if (phase == DYMOE_PREFILL) {
     e = launch_route(logits, T, M, k, topk_idx, topk_w, probs, s);

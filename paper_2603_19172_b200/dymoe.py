@@ -29,7 +29,8 @@ EXPORTED = [
     "dymoe_gather_rows", "dymoe_renorm_weights", "dymoe_predict_ws_bytes", "dymoe_predict_next",
     "dymoe_pool_create", "dymoe_pool_destroy", "dymoe_pool_lookup", "dymoe_pool_insert",
     "dymoe_pool_pin", "dymoe_pool_unpin", "dymoe_pool_snapshot", "dymoe_pool_used",
-    "dymoe_layer_set_expert", "dymoe_attention_mass",
+    "dymoe_layer_set_expert", "dymoe_attention_mass", "dymoe_gate_logits",
+    "dymoe_rmsnorm",
 ]
 
 
@@ -70,7 +71,8 @@ class FwdOpts(ctypes.Structure):
     _fields_ = [("phase", ctypes.c_int), ("layer", ctypes.c_int), ("num_layers", ctypes.c_int),
                 ("ladder", Ladder), ("attn_mass", ctypes.c_void_p), ("heads", ctypes.c_int),
                 ("k_tokens", ctypes.c_int), ("ffn_mode", ctypes.c_int), ("out_dtype", ctypes.c_int),
-                ("forced_bits", ctypes.c_void_p), ("prof_events", ctypes.c_void_p * 3)]
+                ("forced_bits", ctypes.c_void_p), ("prof_events", ctypes.c_void_p * 3),
+                ("residual", ctypes.c_void_p)]
 
 
 class WsViews(ctypes.Structure):
@@ -127,6 +129,8 @@ def lib():
             "dymoe_pool_used": [vp],
             "dymoe_layer_set_expert": [vp, ci, ctypes.POINTER(ExpertDesc), vp],
             "dymoe_attention_mass": [vp, vp, ci, ci, ci, ctypes.c_float, vp, vp, vp],
+            "dymoe_gate_logits": [vp, vp, vp, ci, ci, ci, vp, vp],
+            "dymoe_rmsnorm": [vp, ci, ci, ctypes.c_float, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -318,6 +322,24 @@ def dymoe_renorm_weights(topk_idx, topk_w, bits, renorm=True, stream=None):
     return out
 
 
+def dymoe_rmsnorm(x, eps=1e-5, out=None, stream=None):
+    """u [T][Hd] bf16 = bf16(x / sqrt(mean(x^2) + eps)), x bf16 [T][Hd]."""
+    T, Hd = x.shape
+    u = out if out is not None else torch.empty_like(x)
+    _check(lib().dymoe_rmsnorm(_p(_u16(x)), T, Hd, eps, _p(_u16(u)), _stream(stream)))
+    return u
+
+
+def dymoe_gate_logits(h, w_gate, bias=None, out=None, stream=None):
+    """logits [T][M] f32 = h [T][Hd] bf16 . w_gate [M][Hd] bf16 (reading P1 order) + bias [M]."""
+    T, Hd = h.shape
+    M = w_gate.shape[0]
+    lg = out if out is not None else torch.empty(T, M, dtype=torch.float32, device=h.device)
+    _check(lib().dymoe_gate_logits(_p(_u16(h)), _p(_u16(w_gate)), _p(bias), T, Hd, M, _p(lg),
+                                   _stream(stream)))
+    return lg
+
+
 def dymoe_predict_next(phase, h, w_gate_next, k_route, t, stream=None):
     """Eqs. 6-8 look-ahead (include/dymoe.h).  Returns (experts [n] i32, priority [n] f32,
     logits [T][M] f32) on the device; n = number of valid requests (one host read)."""
@@ -481,7 +503,7 @@ class MoELayer:
 
     def forward(self, x, logits, ladder, layer, num_layers, phase=DYMOE_DECODE, attn_mass=None,
                 k_tokens=0, out_dtype=DYMOE_OUT_F32, forced_bits=None, ffn_mode=-1, ws=None,
-                out=None, stream=None, prof_events=None):
+                out=None, stream=None, prof_events=None, residual=None):
         """dymoe_moe_forward.  Returns (y, ws).  prof_events: optional 3 torch.cuda.Events
         (already recorded once so that they exist) recorded around the FFN kernels."""
         T = x.shape[0]
@@ -501,6 +523,7 @@ class MoELayer:
         o.ffn_mode = ffn_mode
         o.out_dtype = out_dtype
         o.forced_bits = _p(forced_bits)
+        o.residual = _p(_u16(residual)) if residual is not None else None
         if prof_events is not None:
             for i, ev in enumerate(prof_events):
                 o.prof_events[i] = ev.cuda_event

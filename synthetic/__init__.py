@@ -87,6 +87,18 @@ def router_logits(cfg, x, seed, device="cpu"):
     return (x.float() @ wg.t() + beta).contiguous()
 
 
+def stack_gate(cfg, layer, seed, device="cpu"):
+    """Router of stack layer `layer`: (W_g bf16 [M, Hd] ~ N(0, 1/Hd), beta f32 [M]) with
+    beta_{pi(r)} = -alpha ln(r+1) (Zipf, permutation drawn per layer so the hot experts move
+    with depth)."""
+    g = generator(seed * 1000 + 29 + 7919 * layer, device)
+    wg = (torch.randn(cfg.M, cfg.hidden, generator=g, device=device) / math.sqrt(cfg.hidden))
+    perm = torch.randperm(cfg.M, generator=g, device=device)
+    beta = torch.empty(cfg.M, device=device)
+    beta[perm] = -ZIPF_ALPHA * torch.log(torch.arange(cfg.M, device=device, dtype=torch.float32) + 1.0)
+    return wg.to(torch.bfloat16).contiguous(), beta.contiguous()
+
+
 def attention_mass(cfg, seed, device="cpu", T=None):
     """a[h][i] >= 0, fp32 [H, T]: 20% heavy tokens ~ U(4,8)(1+0.1 N(0,1)), rest U(0,1)."""
     g = generator(seed * 1000 + 17, device)

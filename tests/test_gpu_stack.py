@@ -1,0 +1,101 @@
+"""GPU parity of the C5 layer stack (paper_2603_19172_b200.stack.MoEStack): 32 layers on the bf16
+residual stream (pre-norm: RMSNorm -> router -> MoE -> residual add), each layer routed by its own
+gate on the device, depth-adaptive bits.  Teacher-forced layer by layer against oracle.stack: the
+GPU's normed input u_l is within one bf16 ulp of the oracle's RMSNorm of the GPU's x_l (fp32 vs
+fp64 mean of squares; rare), and, fed the GPU's u_l, the oracle must give bit-identical router
+logits (reading P1 + one fp32 bias add) and bits, and x_{l+1} within
+|x_gpu - x_ref| <= 2e-3 max|y_ref| + ulp_bf16(x_ref) elementwise (the FFN bar of north_star plus one
+rounding of the bf16 stream)."""
+import numpy as np
+import pytest
+import torch
+
+import synthetic
+from oracle import stack as o_stack, schedule as o_sched
+
+pytestmark = pytest.mark.gpu
+
+
+def D():
+    import paper_2603_19172_b200.dymoe as d
+    d.lib()
+    return d
+
+
+def _ulp_bf16(v):
+    a = np.abs(v)
+    e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+    return np.where(a > 0, 2.0 ** (e - 7), 2.0 ** -133)
+
+
+@pytest.mark.parametrize("phase,T", [("decode", 8), ("prefill", 40)])
+def test_stack_32_layers_teacher_forced(phase, T):
+    d = D()
+    from paper_2603_19172_b200.stack import MoEStack
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+    L = 32
+    masters = [synthetic.expert_weights(cfg, 100 + l) for l in range(L)]
+    gpu_layers = []
+    for l in range(L):
+        ex = [{n: t.cuda() for n, t in e.items()} for e in masters[l]]
+        d.quantize_experts(ex, (8, 4, 2))
+        gpu_layers.append(ex)
+    gates = [synthetic.stack_gate(cfg, l, 5) for l in range(L)]
+    st = MoEStack(gpu_layers, [(w.cuda(), b.cuda()) for w, b in gates], cfg.k, cfg.hidden, cfg.ffn)
+    x0 = synthetic.hidden_states(cfg, 6).cuda()
+    attn = [synthetic.attention_mass(cfg, 200 + l).cuda() for l in range(L)] if phase == "prefill" else None
+    bits_t, lams = (8, 4, 2), (0.25, 0.5)
+    ph = d.DYMOE_PREFILL if phase == "prefill" else d.DYMOE_DECODE
+    xL, trace = st.forward(x0, d.make_ladder(bits_t, lams), phase=ph, attn_masses=attn, trace=True)
+    torch.cuda.synchronize()
+    lad = o_sched.Ladder(bits_t, lams)
+    seen = set()
+    n_u_diff = 0
+    for l in range(L):
+        x_in = trace[l][0].float().cpu().numpy()
+        u_gpu = trace[l][1].float().cpu().numpy().astype(np.float64)
+        u_ref = o_stack.rmsnorm(x_in)
+        assert (np.abs(u_gpu - u_ref) <= _ulp_bf16(u_ref)).all(), "rmsnorm, layer %d" % l
+        n_u_diff += int((u_gpu != u_ref).sum())
+        x_out = (trace[l + 1][0] if l + 1 < L else xL).float().cpu().numpy().astype(np.float64)
+        np_ex = [{n: t.float().numpy() for n, t in e.items()} for e in masters[l]]
+        wg, beta = gates[l]
+        x_ref, lg_ref, out = o_stack.stack_layer(
+            x_in, wg.float().numpy(), beta.numpy(), np_ex, l, L, lad, cfg.k, phase=phase,
+            attn_mass=attn[l].cpu().numpy() if attn is not None else None, u=u_gpu)
+        assert np.array_equal(trace[l][2].cpu().numpy(), lg_ref), "router logits, layer %d" % l
+        bits = trace[l][3].cpu().numpy()
+        assert np.array_equal(bits, out["bits"]), "bits, layer %d" % l
+        seen.update(int(b) for b in bits)
+        bound = 2e-3 * np.abs(out["y"]).max() + _ulp_bf16(x_ref)
+        assert (np.abs(x_out - x_ref) <= bound).all(), "stream, layer %d" % l
+    assert np.isfinite(xL.float().cpu().numpy()).all()
+    assert n_u_diff <= 0.01 * L * T * cfg.hidden          # 1-ulp norm differences are rare
+    assert {8, 4, 2} <= seen          # the depth schedule used every tier along the stack
+
+
+def test_rmsnorm_kernel():
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"]
+    x = (synthetic.hidden_states(cfg, 9).float() * 7.5).to(torch.bfloat16)
+    u = d.dymoe_rmsnorm(x.cuda()).float().cpu().numpy().astype(np.float64)
+    ref = o_stack.rmsnorm(x.float().numpy())
+    assert (np.abs(u - ref) <= _ulp_bf16(ref)).all()
+    assert (u != ref).mean() < 0.01
+    with pytest.raises(d.DymoeError):
+        xc = x.cuda()
+        d.dymoe_rmsnorm(xc, out=xc)                                  # u aliases x
+
+
+def test_gate_logits_bias_and_residual_args():
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"]
+    wg, beta = synthetic.stack_gate(cfg, 3, 1)
+    x = synthetic.hidden_states(cfg, 2)
+    lg = d.dymoe_gate_logits(x.cuda(), wg.cuda(), beta.cuda()).cpu().numpy()
+    ref = o_stack.router_logits(x.float().numpy(), wg.float().numpy(), beta.numpy())
+    assert np.array_equal(lg, ref)
+    lg0 = d.dymoe_gate_logits(x.cuda(), wg.cuda()).cpu().numpy()
+    assert np.array_equal(lg0, o_stack.router_logits(x.float().numpy(), wg.float().numpy()))
+    with pytest.raises(d.DymoeError):
+        d.dymoe_gate_logits(x.cuda()[:, :100].contiguous(), wg.cuda()[:, :100].contiguous())   # Hd % 8 != 0
