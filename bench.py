@@ -206,13 +206,31 @@ def run_ours(args, rank, world, device):
         for e_ in row:
             e_.record(stream)   # creates the CUDA event so its handle can be passed down
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # the K steps (4 launches each in decode, no host synchronisation inside dymoe_moe_forward)
+    # are captured once as a CUDA graph -- per-kernel events included -- and replayed in the timed
+    # region, as a serving loop would: launch gaps and host-side marshalling leave the step
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream(device=device)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                for i in range(K):
+                    one_step(args.warmup + i, ev[i])
+        stream.wait_stream(side)
+        graph.replay()          # one untimed replay (the warm-up steps above ran call by call)
+        torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0.record(stream)
-        for i in range(K):
-            one_step(args.warmup + i, ev[i])
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(K):
+                one_step(args.warmup + i, ev[i])
         t1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -348,6 +366,7 @@ def run_ours(args, rank, world, device):
             "clocks": clk.summary(),
             "e2e": e2e,
             "gpu_launches": launches_per_step * K,
+            "cuda_graph": graph is not None,
             "quantize": quant,
             "next_rows": extras,
             "tensor_tflops_ffn": fl / (ffn_ms / 1e3) / 1e12,
@@ -752,12 +771,29 @@ def run_stack(args, device):
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
+    # the whole 32-layer pass (6-10 launches per layer, no host synchronisation inside) captured
+    # once as a CUDA graph and replayed: launch gaps and host marshalling leave the timed loop
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            with torch.cuda.graph(graph, stream=side):
+                one_step()
+        stream.wait_stream(side)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     K = args.steps
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         t0.record(stream)
         for _ in range(K):
-            one_step()
+            if graph is not None:
+                graph.replay()
+            else:
+                one_step()
         t1.record(stream)
         torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
@@ -772,6 +808,7 @@ def run_stack(args, device):
         dx.copy_(hx, non_blocking=True)
         y, _ = st.forward(dx, ladder, phase, attn, ws=ws, bufs=bufs, logits=logits)
         hy.copy_(y, non_blocking=True)
+    # (e2e runs the public API call by call, no graph: what a caller of MoEStack.forward gets)
     e1.record(stream)
     torch.cuda.synchronize()
     e_ms = e0.elapsed_time(e1)
@@ -801,7 +838,7 @@ def run_stack(args, device):
                        "widths_assigned": {str(k): v for k, v in sorted(widths.items())},
                        "l2": "inputs larger than L2 (32 distinct layers, 84 GB of packed weights)",
                        "parallelism": "single GPU"},
-            "ms_per_layer": ms / K / L, "roofline": roof, "clocks": clk.summary(),
+            "ms_per_layer": ms / K / L, "cuda_graph": graph is not None, "roofline": roof, "clocks": clk.summary(),
             "e2e": {"value": T * K / (e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hy.numel() * 2)},
             "gpu_launches": per_layer * L * K}
@@ -821,6 +858,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time the steps call by call instead "
+                    "of replaying their CUDA graph (single-GPU decode / prefill / stack workloads)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test hook for several ranks sharing one GPU (collectives staged "
                          "through host memory); never used for reported numbers")

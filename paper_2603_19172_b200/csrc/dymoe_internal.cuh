@@ -120,8 +120,15 @@ bool encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, ui
                     uint64_t d1, uint64_t stride1, uint32_t b0, uint32_t b1,
                     CUtensorMapSwizzle swz);
 
+// Inside a stream capture the record becomes a graph event-record node (cudaEventRecordExternal),
+// so the events time the kernels when the graph is replayed.
 inline void record_ev(void* const* ev, int i, cudaStream_t s) {
-  if (ev != nullptr && ev[i] != nullptr) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
+  if (ev == nullptr || ev[i] == nullptr) return;
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(reinterpret_cast<cudaEvent_t>(ev[i]), s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
 }
 
 cudaError_t launch_predict_next(int phase, const uint16_t* h, const uint16_t* wg, int T, int Hd,
