@@ -113,13 +113,13 @@ __global__ void k_check(const uint16_t* A, const uint16_t* B, int nb_rows, uint3
 }
 
 // ----------------------------------------------------------------------------- (2) throughput
-template <int NW, int S, bool NOMMA = false>
+template <int NW, int S, bool NOMMA = false, int NN = 16>
 __global__ void k_tput(int steps, uint32_t seed, float* out, long long* cyc) {
-  __shared__ __align__(1024) uint8_t xs[1024 * 4];
+  __shared__ __align__(1024) uint8_t xs[NN >= 64 ? NN * 128 : 1024 * 4];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t full[S], empty[S], done;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) reinterpret_cast<uint32_t*>(xs)[i] = 0x3f803f80u;
+  for (int i = threadIdx.x; i < (int)sizeof(xs) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(xs)[i] = 0x3f803f80u;
   if (warp == NW) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -160,7 +160,7 @@ __global__ void k_tput(int steps, uint32_t seed, float* out, long long* cyc) {
         }
       }
       w = w * 1664525u + 1013904223u;
-      ST32(tm + ((uint32_t)(q * 32) << 16) + 64 + s * 32, r);
+      ST32(tm + ((uint32_t)(q * 32) << 16) + (NN >= 64 ? NN : 64) + s * 32, r);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
@@ -178,7 +178,8 @@ __global__ void k_tput(int steps, uint32_t seed, float* out, long long* cyc) {
       } else {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          mma_ts(tm + (i & 1) * 16, tm + 64 + s * 32 + kk * 8, sw_desc(smem_u32(xs) + kk * 32, 0), make_idesc(128, 16), kk > 0);
+          mma_ts(NN >= 64 ? tm : tm + (i & 1) * 16, tm + (NN >= 64 ? NN : 64) + s * 32 + kk * 8,
+                 sw_desc(smem_u32(xs) + kk * 32, NN >= 64 ? 1024 : 0), make_idesc(128, NN), kk > 0);
         commit(smem_u32(&empty[s]));
       }
     }
@@ -320,6 +321,10 @@ int main() {
     mr(k_mma_rate<64, 8, true>, 64, 8, "TS");
     mr(k_mma_rate<64, 8, false>, 64, 8, "SS");
   }
+  run(k_tput<8, 4, false, 256>, 8, "N=256: 8 writer warps, 4 stages (A in TMEM, prefill shape)");
+  run(k_tput<8, 4, true, 256>, 8, "N=256 NO MMA: 8 writer warps, 4 stages");
+  run(k_tput<4, 4, false, 256>, 4, "N=256: 4 writer warps, 4 stages");
+  run(k_tput<8, 6, false, 128>, 8, "N=128: 8 writer warps, 6 stages");
   run(k_tput<4, 4, true>, 4, "NO MMA: 4 writer warps, 4 stages");
   run(k_tput<8, 4, true>, 8, "NO MMA: 8 writer warps, 4 stages");
   run(k_tput<4, 4>, 4, "4 writer warps, 4 stages");
