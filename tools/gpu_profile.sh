@@ -1,3 +1,5 @@
+# ncu captures for profiles/ (run from the repo root on a B200): full captures of the decode and
+# prefill FFN kernels of one bench step (tools/profile_step.py), summarised by tools/ncu_summary.py.
 mkdir -p gpurun_out
 python tools/profile_step.py --workload decode > gpurun_out/step_decode.json 2>/dev/null
 ncu --set full --clock-control none --import-source on -k regex:k_decode_gemv -s 4 -c 2 -o gpurun_out/r01_decode_full -f python tools/profile_step.py --workload decode > gpurun_out/ncu_dec.log 2>&1
