@@ -16,9 +16,13 @@
 // A warp owns 32 consecutive groups = 8 KB of contiguous input, which it stages through its own
 // shared-memory buffer with coalesced 16-byte cp.async (each instruction covers 512 contiguous
 // bytes; rows padded to 272 B so that the per-lane 16-byte reads are bank-conflict free), double
-// buffered: the next 8 KB is in flight while the lanes quantize the current one.  Packed codes
-// are written contiguously.  Jobs are padded to whole warps, so a warp never straddles two
-// matrices; groups past a job's end are zero-filled and not stored.
+// buffered: the next 8 KB is in flight while the lanes quantize the current one.  Each lane
+// writes its group's packed codes back into its own staging row (it has read the row into
+// registers), and the warp then stores the 32 groups' codes -- one contiguous 1-4 KB range --
+// with 16-byte stores of 512 contiguous bytes per instruction (a lane storing its own 128-byte
+// group directly made every store instruction touch 32 separate lines).  Jobs are padded to whole
+// warps, so a warp never straddles two matrices; groups past a job's end are zero-filled and not
+// stored.
 #include "../dymoe_internal.cuh"
 
 namespace dymoe {
@@ -115,8 +119,12 @@ __device__ __forceinline__ void quant_lane_group(const QJob& J, long long g, uin
   const int zbias = 0x4B400000 - z;
   J.scales[g] = s;
   J.zeros[g] = (uint8_t)z;
-  // codes: group g occupies 128*BITS/8 contiguous bytes of its row (rows are whole groups)
-  uint4* dst = reinterpret_cast<uint4*>(J.codes) + g * (BITS * 128 / 8 / 16);
+  // codes: group g's 128*BITS/8 bytes go to the start of this lane's staging row (already read
+  // into v); the warp stores them to global memory afterwards (store_codes)
+  auto sts = [&](int i, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(row + i * 16), "r"(a), "r"(b), "r"(c),
+                 "r"(d) : "memory");
+  };
   if constexpr (BITS == 8) {
 #pragma unroll
     for (int i = 0; i < 16; i += 2) {   // 16 codes per 16-byte store
@@ -129,7 +137,7 @@ __device__ __forceinline__ void quant_lane_group(const QJob& J, long long g, uin
         o[2 * h + 1] = qcode<8>(a.z, false, inv, zbias) | qcode<8>(a.z, true, inv, zbias) << 8 |
                        qcode<8>(a.w, false, inv, zbias) << 16 | qcode<8>(a.w, true, inv, zbias) << 24;
       }
-      dst[i / 2] = make_uint4(o[0], o[1], o[2], o[3]);
+      sts(i / 2, o[0], o[1], o[2], o[3]);
     }
   } else if constexpr (BITS == 4) {
 #pragma unroll
@@ -145,7 +153,7 @@ __device__ __forceinline__ void quant_lane_group(const QJob& J, long long g, uin
           word |= (qcode<4>(w4[j], false, inv, zbias) | qcode<4>(w4[j], true, inv, zbias) << 4) << (8 * j);
         o[h] = word;
       }
-      dst[i / 4] = make_uint4(o[0], o[1], o[2], o[3]);
+      sts(i / 4, o[0], o[1], o[2], o[3]);
     }
   } else {   // 2
 #pragma unroll
@@ -165,8 +173,24 @@ __device__ __forceinline__ void quant_lane_group(const QJob& J, long long g, uin
         }
         o[h] = word;
       }
-      dst[i / 8] = make_uint4(o[0], o[1], o[2], o[3]);
+      sts(i / 8, o[0], o[1], o[2], o[3]);
     }
+  }
+}
+
+// The warp's 32 staged groups (BITS 16-byte chunks each, at the start of each staging row) ->
+// contiguous global codes, 32 consecutive chunks per store instruction.
+__device__ __forceinline__ void store_codes(const QJob& J, long long g0, uint32_t buf, int lane) {
+  const long long left = J.n_groups - g0;
+  const int ng = left < 32 ? (int)left : 32;
+  const int nch = ng * J.bits;                    // 16-byte chunks (BITS per group)
+  uint4* dst = reinterpret_cast<uint4*>(J.codes) + g0 * J.bits;
+  for (int c = lane; c < nch; c += 32) {
+    const int gl = c / J.bits, off = c - gl * J.bits;
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(buf + gl * kRow + off * 16));
+    dst[c] = v;
   }
 }
 
@@ -207,6 +231,8 @@ __global__ void __launch_bounds__(kQWarps * 32) k_quantize(const __grid_constant
         default: quant_lane_group<8>(J, g, row); break;
       }
     }
+    __syncwarp();   // every lane's codes are staged
+    store_codes(J, (w - J.first_warp) * 32, cur, lane);
     __syncwarp();   // every lane has read `cur` before it is refilled (two items later)
     jj = jn;
   }
