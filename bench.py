@@ -684,7 +684,17 @@ def cpu_baseline(cfg, args, prefill, frac=8):
     return {"value": cfg.T / step_s, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": "route+score+assign+permute for all %d tokens; FFN of 1/%g of one expert "
                       "(Int%d, %d rows) scaled x%g and x%d active experts" % (cfg.T, frac, b, n_rows, frac, n_active),
-            "blas_threads": torch.get_num_threads()}
+            "blas_threads": torch.get_num_threads(), "cpu_model": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(args):
