@@ -195,13 +195,15 @@ __device__ __forceinline__ void assign_bits(const float* importance, const uint8
 }
 
 // Permute (P:203 step 3): stable counting sort of the T*k (token, slot) pairs by expert id,
-// pairs of skipped experts (bits == 0) dropped; 1024 threads.  Token-major chunks of 1024 pairs:
-// a pair's stable rank = running offset + same-expert pairs of earlier warps (per-warp histogram)
-// + same-expert lanes before it (__match_any_sync).  Shared: running [M] ints, warp_cnt
-// [32][kMaxE] ints, keep [M] bytes.  Integer-only, bit-exact by construction.
+// pairs of skipped experts (bits == 0) dropped; a block of NT threads.  Token-major chunks of NT
+// pairs: a pair's stable rank = running offset + same-expert pairs of earlier warps (per-warp
+// histogram) + same-expert lanes before it (__match_any_sync).  Shared: running [M] ints,
+// warp_cnt [NT/32][kMaxE] ints, keep [M] bytes.  Integer-only, bit-exact by construction (the
+// result does not depend on NT).
 constexpr int kPermThreads = 1024;
 constexpr int kPermWarps = kPermThreads / 32;
 
+template <int NT = kPermThreads>
 __device__ __forceinline__ void permute(const int32_t* topk_idx, int T, int k, int M,
                                         const uint8_t* bits, int32_t* expert_off,
                                         int32_t* perm_token, int32_t* perm_slot, int32_t* inv_row,
@@ -209,12 +211,12 @@ __device__ __forceinline__ void permute(const int32_t* topk_idx, int T, int k, i
                                         uint8_t* keep) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int P = T * k;
-  for (int e = tid; e < M; e += kPermThreads) {
+  for (int e = tid; e < M; e += NT) {
     running[e] = 0;
     keep[e] = bits[e] != 0;
   }
   __syncthreads();
-  for (int p = tid; p < P; p += kPermThreads) {   // counts per expert
+  for (int p = tid; p < P; p += NT) {   // counts per expert
     const int e = topk_idx[p];
     if (keep[e]) atomicAdd(&running[e], 1);
   }
@@ -232,8 +234,8 @@ __device__ __forceinline__ void permute(const int32_t* topk_idx, int T, int k, i
     active_list[0] = na;
   }
   __syncthreads();
-  for (int c0 = 0; c0 < P; c0 += kPermThreads) {   // stable placement, chunk by chunk
-    for (int q = tid; q < kPermWarps * M; q += kPermThreads)
+  for (int c0 = 0; c0 < P; c0 += NT) {   // stable placement, chunk by chunk
+    for (int q = tid; q < (NT / 32) * M; q += NT)
       warp_cnt[(q / M) * DYMOE_MAX_EXPERTS + (q % M)] = 0;
     __syncthreads();
     const int p = c0 + tid;
@@ -257,9 +259,9 @@ __device__ __forceinline__ void permute(const int32_t* topk_idx, int T, int k, i
       inv_row[p] = r;
     }
     __syncthreads();
-    for (int e2 = tid; e2 < M; e2 += kPermThreads) {
+    for (int e2 = tid; e2 < M; e2 += NT) {
       int add = 0;
-      for (int q = 0; q < kPermWarps; ++q) add += warp_cnt[q * DYMOE_MAX_EXPERTS + e2];
+      for (int q = 0; q < (NT / 32); ++q) add += warp_cnt[q * DYMOE_MAX_EXPERTS + e2];
       running[e2] += add;
     }
     __syncthreads();

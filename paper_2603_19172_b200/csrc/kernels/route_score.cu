@@ -223,37 +223,69 @@ cudaError_t launch_assign(const float* importance, const uint8_t* active_mask,
 }
 
 // ===========================================================================================
-// Fused decode front: route -> score -> assign -> permute in ONE single-CTA launch (1024
-// threads) for a decode batch, with exactly the arithmetic of the four standalone kernels (the
-// same front:: bodies).  A decode step's front is latency-bound (a few KB), so three launches and
-// their gaps were ~10 % of the step.  forced_bits != nullptr skips score/assign.
+// Fused decode front: route -> score -> assign -> permute in ONE single-CTA launch of 256 threads
+// for a decode batch, with exactly the arithmetic of the four standalone kernels (the same front::
+// bodies; none of their results depends on the block size).  The intermediates the later phases
+// read back (top-k indices, importance, bits) stay in shared memory and are copied out at the
+// end.  A decode step's front is latency-bound (a few KB), so three launches and their gaps were
+// ~10 % of the step.  forced_bits != nullptr skips score/assign.
 // ===========================================================================================
-__global__ void __launch_bounds__(front::kPermThreads)
+constexpr int kFrontThreads = 256;
+
+__global__ void __launch_bounds__(kFrontThreads)
 k_front_decode(const float* logits, int T, int M, int k, AssignParams p,
                const uint8_t* forced_bits, int32_t* topk_idx, float* topk_w, float* probs,
                float* importance, uint8_t* bits, uint8_t* active, int32_t* expert_off,
                int32_t* perm_token, int32_t* perm_slot, int32_t* inv_row, int32_t* active_list) {
+  constexpr int NW = kFrontThreads / 32;
   // phase buffers: the score's per-warp softmax rows and the permute's per-warp histograms are
   // never live at the same time (block barriers between the phases)
-  __shared__ __align__(16) int big[front::kPermWarps * DYMOE_MAX_EXPERTS];
+  __shared__ __align__(16) int big[NW * DYMOE_MAX_EXPERTS];
   __shared__ int running[DYMOE_MAX_EXPERTS];
   __shared__ float I[DYMOE_MAX_EXPERTS];
   __shared__ int act[DYMOE_MAX_EXPERTS];
   __shared__ uint8_t keep[DYMOE_MAX_EXPERTS];
   __shared__ int n_act;
+  __shared__ int32_t s_idx[kFrontDecodeMaxT * 8];
+  __shared__ float s_imp[DYMOE_MAX_EXPERTS];
+  __shared__ uint8_t s_bits[DYMOE_MAX_EXPERTS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int t = w; t < T; t += front::kPermWarps)
-    front::route_token(logits + (size_t)t * M, M, k, lane, topk_idx + (size_t)t * k,
-                       topk_w + (size_t)t * k, probs != nullptr ? probs + (size_t)t * M : nullptr);
+  // T <= NW (one token per warp): route's full-softmax rows go to shared memory, where the score
+  // phase sums them -- they are exactly the rows decode_importance would recompute
+  // (front::softmax_row), so the importance is unchanged; copied to `probs` below
+  const bool rows_in_smem = T <= NW && T > 1;
+  float* sp = reinterpret_cast<float*>(big);
+  for (int t = w; t < T; t += NW)
+    front::route_token(logits + (size_t)t * M, M, k, lane, s_idx + (size_t)t * k,
+                       topk_w + (size_t)t * k,
+                       rows_in_smem ? sp + t * M : (probs != nullptr ? probs + (size_t)t * M : nullptr));
   __syncthreads();
   const uint8_t* b = forced_bits;
   if (b == nullptr) {
-    front::decode_importance(logits, T, M, reinterpret_cast<float*>(big), importance);
-    front::assign_bits(importance, nullptr, topk_idx, T, p, bits, active, I, act, &n_act);
-    b = bits;
+    if (rows_in_smem) {
+      if ((int)threadIdx.x < M) {   // Eq. 3, b ascending (decode_importance's sum)
+        float acc = 0.f;
+        for (int q = 0; q < T; ++q) acc = __fadd_rn(acc, sp[q * M + threadIdx.x]);
+        s_imp[threadIdx.x] = acc;
+      }
+      __syncthreads();
+    } else {
+      front::decode_importance(logits, T, M, sp, s_imp);
+    }
+    front::assign_bits(s_imp, nullptr, s_idx, T, p, s_bits, active, I, act, &n_act);
+    b = s_bits;
   }
-  front::permute(topk_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row, active_list,
-                 running, big, keep);
+  if (rows_in_smem && probs != nullptr)
+    for (int i = threadIdx.x; i < T * M; i += kFrontThreads) probs[i] = sp[i];
+  __syncthreads();   // sp (= big) is reused by the permute's histograms
+  front::permute<kFrontThreads>(s_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row,
+                                active_list, running, big, keep);
+  for (int i = threadIdx.x; i < T * k; i += kFrontThreads) topk_idx[i] = s_idx[i];
+  if (forced_bits == nullptr)
+    for (int j = threadIdx.x; j < M; j += kFrontThreads) {
+      importance[j] = s_imp[j];
+      bits[j] = s_bits[j];
+    }
 }
 
 cudaError_t launch_front_decode(const float* logits, int T, int M, int k, const AssignParams& p,
@@ -261,7 +293,7 @@ cudaError_t launch_front_decode(const float* logits, int T, int M, int k, const 
                                 float* probs, float* importance, uint8_t* bits, uint8_t* active,
                                 int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot,
                                 int32_t* inv_row, int32_t* active_list, cudaStream_t s) {
-  k_front_decode<<<1, front::kPermThreads, 0, s>>>(logits, T, M, k, p, forced_bits, topk_idx, topk_w,
+  k_front_decode<<<1, kFrontThreads, 0, s>>>(logits, T, M, k, p, forced_bits, topk_idx, topk_w,
                                                    probs, importance, bits, active, expert_off,
                                                    perm_token, perm_slot, inv_row, active_list);
   return cudaGetLastError();
