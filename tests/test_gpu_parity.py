@@ -382,3 +382,40 @@ def test_fused_decode_front_equals_kernels(M, k, T, m_active, forced):
     n = int(off[-1].item())
     assert torch.equal(v["expert_off"], off) and torch.equal(v["inv_row"], inv)
     assert torch.equal(v["perm_token"][:n], pt[:n]) and torch.equal(v["perm_slot"][:n], ps[:n])
+
+
+@pytest.mark.parametrize("T", [1, 5, 16, 17])
+@pytest.mark.parametrize("out_dtype", ["f32", "bf16_residual"])
+def test_decode_combine_paths(T, out_dtype):
+    """The decode combine (K-slice partials summed, weights renormalised over executed slots, D12,
+    optional residual and bf16 output) equals the oracle, including a step where every routed
+    expert is skipped (y = 0, or exactly the residual) and one with a skipped expert."""
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+    ex = gpu_experts(cfg, 4)
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    nx = np_experts(cfg, 4)
+    x, lg, _ = synthetic.layer_inputs(cfg, 4)
+    od = d.DYMOE_OUT_F32 if out_dtype == "f32" else d.DYMOE_OUT_BF16
+    res = x.cuda() if out_dtype != "f32" else None
+    for forced in (np.zeros(cfg.M, np.uint8), np.array([[8, 4, 2, 0][e % 4] for e in range(cfg.M)], np.uint8)):
+        y, ws = layer.forward(x.cuda(), lg.cuda(), d.make_ladder((8, 4, 2), (0.25, 0.5)), 7, 32,
+                              forced_bits=torch.from_numpy(forced).cuda(), out_dtype=od, residual=res)
+        torch.cuda.synchronize()
+        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), nx, 7, 32,
+                                o_sched.Ladder((8, 4, 2), (0.25, 0.5)), cfg.k, forced_bits=forced)["y"]
+        yg = y.float().cpu().numpy().astype(np.float64)
+        if res is None:
+            if not forced.any():
+                assert (yg == 0).all()
+            else:
+                assert rel_err(yg, ref) <= FFN_TOL
+        else:
+            xr = x.float().numpy().astype(np.float64)
+            if not forced.any():
+                assert np.array_equal(yg, xr)
+            else:
+                from oracle import stack as o_stack
+                full = o_stack.residual(xr, ref)
+                bound = FFN_TOL * np.abs(ref).max() + np.abs(full) * 2.0 ** -7
+                assert (np.abs(yg - full) <= bound).all()
