@@ -115,7 +115,7 @@ __global__ void k_check(const uint16_t* A, const uint16_t* B, int nb_rows, uint3
 // ----------------------------------------------------------------------------- (2) throughput
 template <int NW, int S, bool NOMMA = false, int NN = 16>
 __global__ void k_tput(int steps, uint32_t seed, float* out, long long* cyc) {
-  __shared__ __align__(1024) uint8_t xs[NN >= 64 ? NN * 128 : 1024 * 4];
+  __shared__ __align__(1024) uint8_t xs[NN >= 64 ? ((NN + 7) / 8) * 1024 : 1024 * 4];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t full[S], empty[S], done;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -325,6 +325,8 @@ int main() {
   run(k_tput<8, 4, true, 256>, 8, "N=256 NO MMA: 8 writer warps, 4 stages");
   run(k_tput<4, 4, false, 256>, 4, "N=256: 4 writer warps, 4 stages");
   run(k_tput<8, 6, false, 128>, 8, "N=128: 8 writer warps, 6 stages");
+  run(k_tput<8, 4, false, 192>, 8, "N=192: 8 writer warps, 4 stages (MMA-bound = 21.3)");
+  run(k_tput<8, 4, false, 160>, 8, "N=160: 8 writer warps, 4 stages (MMA-bound = 25.6)");
   run(k_tput<4, 4, true>, 4, "NO MMA: 4 writer warps, 4 stages");
   run(k_tput<8, 4, true>, 8, "NO MMA: 8 writer warps, 4 stages");
   run(k_tput<4, 4>, 4, "4 writer warps, 4 stages");
