@@ -174,13 +174,14 @@ def run_ours(args, rank, world, device):
         return i % len(layers), i % NUM_LAYERS, i % n_inputs
 
     events = None
+    ffn_mode = d.DYMOE_FFN_PREFILL_TS if (phase == d.DYMOE_PREFILL and args.prefill_kernel == "ts") else -1
 
     def one_step(i, ev=None):
         c, l, j = plan(i)
         L = layers[c][0]
         x, lg, a = inputs[j]
         L.forward(x, lg, ladder, l, NUM_LAYERS, phase=phase, attn_mass=a, ws=ws[c], out=out,
-                  prof_events=ev)
+                  prof_events=ev, ffn_mode=ffn_mode)
 
     # census: algorithmic bytes / flops of every distinct step (bits are data-dependent)
     census = {}
@@ -367,6 +368,7 @@ def run_ours(args, rank, world, device):
             "e2e": e2e,
             "gpu_launches": launches_per_step * K,
             "cuda_graph": graph is not None,
+            "prefill_kernel": args.prefill_kernel if phase == d.DYMOE_PREFILL else None,
             "quantize": quant,
             "next_rows": extras,
             "tensor_tflops_ffn": fl / (ffn_ms / 1e3) / 1e12,
@@ -868,6 +870,9 @@ def main():
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prefill-kernel", default="ss", choices=["ss", "ts"],
+                    help="prefill expert GEMM: ss = dequantized weights through shared memory "
+                         "(default), ts = the experimental operand-swapped kernel (weights in TMEM)")
     ap.add_argument("--no-graph", action="store_true", help="time the steps call by call instead "
                     "of replaying their CUDA graph (single-GPU decode / prefill / stack workloads)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],

@@ -42,6 +42,10 @@ enum {
 };
 
 enum { DYMOE_PREFILL = 0, DYMOE_DECODE = 1 };
+/* Expert-FFN kernel selector only (dymoe_expert_ffn mode, dymoe_fwd_opts.ffn_mode): the
+ * experimental operand-swapped tcgen05 prefill GEMM (dequantized weights as the A operand in
+ * TMEM, tokens as B).  Same function as DYMOE_PREFILL; measured slower. */
+enum { DYMOE_FFN_PREFILL_TS = 2 };
 enum { DYMOE_M_TOTAL = 0, DYMOE_M_ACTIVE = 1 };  /* reading D5: meaning of M in Eq. 5 */
 enum { DYMOE_OUT_F32 = 0, DYMOE_OUT_BF16 = 1 };
 
@@ -195,7 +199,8 @@ int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* b
  * deq = RNE_bf16((q - z)·RNE_bf16(s)) (D17) or the bf16 master for bits == 16.
  *   x [T][Hd] bf16; h_ws [T*k][F] bf16 scratch (intermediate); y_perm [T*k][Hd] f32 out.
  * mode: DYMOE_DECODE = fused-dequant GEMV kernels (intended for <= 8 rows per expert),
- *       DYMOE_PREFILL = fused-dequant tcgen05 grouped GEMM.  Both compute the same function.
+ *       DYMOE_PREFILL = fused-dequant tcgen05 grouped GEMM, DYMOE_FFN_PREFILL_TS = its
+ *       operand-swapped experimental variant.  All compute the same function.
  * status: device u32 word (nullable) receiving DYMOE_STATUS_* bits.                           */
 int dymoe_expert_ffn(const dymoe_layer* layer, int mode, const uint16_t* x, int T,
                      const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,

@@ -708,9 +708,10 @@ static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, con
   a.part_rows = part_rows;
   a.status = status;
   // decode kernels write K-slice partials of W2; the prefill grouped GEMM writes y_perm directly
-  *parts_out = mode == DYMOE_PREFILL ? 0 : decode_w2_slices(L->F);
+  *parts_out = mode == DYMOE_DECODE ? decode_w2_slices(L->F) : 0;
   if (T == 0) return DYMOE_OK;
-  cudaError_t e = mode == DYMOE_PREFILL ? launch_ffn_prefill(a, s, ev) : launch_ffn_decode(a, s, ev);
+  cudaError_t e = mode == DYMOE_DECODE ? launch_ffn_decode(a, s, ev)
+                                       : launch_ffn_prefill(a, s, ev, mode == DYMOE_FFN_PREFILL_TS);
   if (e != cudaSuccess) return cuda_fail(e, "expert ffn");
   return DYMOE_OK;
 }
@@ -729,7 +730,8 @@ int dymoe_expert_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T,
                      const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,
                      uint16_t* h_ws, float* y_perm, uint32_t* status, dymoe_stream_t stream) {
   CHECK_ARG(L != nullptr, "layer: must not be NULL");
-  CHECK_ARG(mode == DYMOE_PREFILL || mode == DYMOE_DECODE, "mode: must be DYMOE_PREFILL or DYMOE_DECODE");
+  CHECK_ARG(mode == DYMOE_PREFILL || mode == DYMOE_DECODE || mode == DYMOE_FFN_PREFILL_TS,
+            "mode: must be DYMOE_PREFILL, DYMOE_DECODE or DYMOE_FFN_PREFILL_TS");
   CHECK_ARG(T >= 0, "T: must be >= 0");
   if (T == 0) return ok();
   CHECK_ARG(x && bits && expert_off && perm_token && h_ws && y_perm,
@@ -797,8 +799,9 @@ int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logi
   CHECK_ARG(T >= 0, "T: must be >= 0");
   CHECK_ARG(o->phase == DYMOE_PREFILL || o->phase == DYMOE_DECODE, "opts.phase: must be DYMOE_PREFILL or DYMOE_DECODE");
   CHECK_ARG(o->out_dtype == DYMOE_OUT_F32 || o->out_dtype == DYMOE_OUT_BF16, "opts.out_dtype: must be DYMOE_OUT_F32 or DYMOE_OUT_BF16");
-  CHECK_ARG(o->ffn_mode == -1 || o->ffn_mode == DYMOE_PREFILL || o->ffn_mode == DYMOE_DECODE,
-            "opts.ffn_mode: must be -1, DYMOE_PREFILL or DYMOE_DECODE");
+  CHECK_ARG(o->ffn_mode == -1 || o->ffn_mode == DYMOE_PREFILL || o->ffn_mode == DYMOE_DECODE ||
+                o->ffn_mode == DYMOE_FFN_PREFILL_TS,
+            "opts.ffn_mode: must be -1, DYMOE_PREFILL, DYMOE_DECODE or DYMOE_FFN_PREFILL_TS");
   AssignParams ap{};
   int rc = fill_assign_params(&o->ladder, L->M, L->k, o->layer, o->num_layers, ap);
   if (rc) {

@@ -113,7 +113,8 @@ cudaError_t launch_reduce_parts(const float* y_part, int n_parts, int part_rows,
                                 float* y_perm, cudaStream_t s);
 // ev (nullable, 3 entries, each nullable): recorded before W13, between W13 and W2, after W2.
 cudaError_t launch_ffn_decode(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
-cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
+cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr,
+                               bool operand_swapped = false);
 // 2-D tiled TMA descriptor over a row-major [d1][d0] tensor (stride1 bytes between rows), box
 // b0 x b1, CUtensorMapDataType dt, swizzle swz (host; false if the driver rejects it)
 bool encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0,

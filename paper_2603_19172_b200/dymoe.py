@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(_HERE, "libdymoe.so")
 
 DYMOE_OK = 0
 DYMOE_PREFILL, DYMOE_DECODE = 0, 1
+DYMOE_FFN_PREFILL_TS = 2   # expert-FFN kernel selector: the operand-swapped prefill GEMM (experimental)
 DYMOE_M_TOTAL, DYMOE_M_ACTIVE = 0, 1
 DYMOE_OUT_F32, DYMOE_OUT_BF16 = 0, 1
 MAX_TIERS = 5

@@ -202,7 +202,7 @@ FFN_CFGS = [synthetic.CONFIGS["tiny"],
 
 
 @pytest.mark.parametrize("cfg", FFN_CFGS, ids=lambda c: c.name)
-@pytest.mark.parametrize("mode", ["decode", "prefill"])
+@pytest.mark.parametrize("mode", ["decode", "prefill", "prefill_ts"])
 def test_expert_ffn_all_widths(cfg, mode):
     d = D()
     ex = gpu_experts(cfg, 1)
@@ -213,7 +213,7 @@ def test_expert_ffn_all_widths(cfg, mode):
     x, lg, _ = synthetic.layer_inputs(cfg, 1)
     r_idx, _, _ = o_route.route(lg.numpy(), cfg.k)
     perm = o_moe.permute(r_idx, bits, cfg.M)
-    m = d.DYMOE_DECODE if mode == "decode" else d.DYMOE_PREFILL
+    m = {"decode": d.DYMOE_DECODE, "prefill": d.DYMOE_PREFILL, "prefill_ts": d.DYMOE_FFN_PREFILL_TS}[mode]
     h, y, status = layer.expert_ffn(x.cuda(), torch.from_numpy(bits).cuda(),
                                     torch.from_numpy(perm["expert_off"]).cuda(),
                                     torch.from_numpy(perm["perm_token"]).cuda(), m)
@@ -419,3 +419,26 @@ def test_decode_combine_paths(T, out_dtype):
                 full = o_stack.residual(xr, ref)
                 bound = FFN_TOL * np.abs(ref).max() + np.abs(full) * 2.0 ** -7
                 assert (np.abs(yg - full) <= bound).all()
+
+
+@pytest.mark.parametrize("T", [600, 1000])
+def test_prefill_operand_swapped_multi_tile(T):
+    """The operand-swapped prefill kernel (DYMOE_FFN_PREFILL_TS) on enough tokens that experts span
+    several 192-token tiles plus a ragged tail (N rounded up to 32): the whole layer equals the
+    oracle (bits exact, y within the FFN bar)."""
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+    ex = gpu_experts(cfg, 8)
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    x, lg, a = synthetic.layer_inputs(cfg, 8)
+    y, ws = layer.forward(x.cuda(), lg.cuda(), d.make_ladder((16, 8, 4, 2), (0.2, 0.5, 0.8)), 9, 32,
+                          phase=d.DYMOE_PREFILL, attn_mass=a.cuda(), ffn_mode=d.DYMOE_FFN_PREFILL_TS)
+    torch.cuda.synchronize()
+    ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), np_experts(cfg, 8), 9, 32,
+                            o_sched.Ladder((16, 8, 4, 2), (0.2, 0.5, 0.8)), cfg.k, phase="prefill",
+                            attn_mass=a.numpy())
+    v = layer.views(T, ws)
+    assert np.array_equal(v["bits"].cpu().numpy(), ref["bits"])
+    counts = np.diff(ref["expert_off"])
+    assert counts.max() > 192            # at least one expert spans several tiles
+    assert rel_err(y.cpu().numpy(), ref["y"]) <= FFN_TOL
