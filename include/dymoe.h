@@ -319,6 +319,74 @@ int dymoe_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n, uin
                       dymoe_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
+/* Expert-parallel dispatch and combine over peer memory (the NVLink /
+ * NVSwitch replacement of the NCCL all-to-all pair).  Every rank owns one symmetric WINDOW of
+ * dymoe_ep_window_bytes(P, M, Hd, cap_rows) device bytes, mapped into every other rank's address
+ * space (CUDA IPC between processes; the same pointer between threads of one process):
+ *   flags  u32[P]          barrier counters, flags[src] written by rank src
+ *   cnt    i32[2][P][M]    cnt[parity][src][e] = rows rank src routes to expert e (double-
+ *                          buffered by step parity so a step's publish never races a peer's
+ *                          previous combine)
+ *   recv_x bf16[cap][Hd]   rows received by this rank, EXPERT-MAJOR: local expert e's rows are
+ *                          [Σ_{e'<e} Σ_src cnt[src][e'], ...) and within an expert by source rank,
+ *                          then in the source's (token, slot) order -- i.e. exactly the order
+ *                          the expert FFN wants, no regrouping on the receiver
+ *   y_out  f32[cap][Hd]    the local experts' outputs, row-aligned with recv_x
+ * One step (3 barriers):
+ *   dymoe_ep_publish_counts   write this rank's per-expert counts (from dymoe_permute's
+ *                             expert_off) into cnt[parity][rank][*] of every window
+ *   dymoe_ep_barrier
+ *   dymoe_ep_dispatch         fused gather + all-to-all: x[perm_token[j]] is stored straight
+ *                             into the owner's recv_x row (16-byte stores over NVLink); also
+ *                             writes recv_off [M_loc+1] (local expert offsets of recv_x)
+ *   dymoe_ep_barrier
+ *   dymoe_expert_ffn          on recv_x with recv_off, identity perm, y_perm = the window's y_out
+ *   dymoe_ep_barrier
+ *   dymoe_ep_combine          fused reverse all-to-all + weighted combine: every live (t, slot)
+ *                             pulls its output row from the owner's y_out (NVLink loads) and the
+ *                             dymoe_combine arithmetic (reading D12, slot order, fp32) applies.
+ * dymoe_ep_window: P ranks, this rank, M experts (expert e on rank floor(e P / M)), Hd, cap_rows
+ *   (>= the rows any rank can receive; T_max * k * P is always enough), parity (step & 1) and
+ *   peers: a DEVICE array [P] of the windows' base pointers as mapped in this process
+ *   (peers[rank] = own window).
+ * Barrier: thread p stores `epoch` into flags[rank] of window p (release, system scope), then
+ * waits until every flags[src] of its own window is >= epoch (acquire, system scope).  The
+ * caller increments epoch by one per barrier call on every rank.  A wait longer than ~10 s sets
+ * DYMOE_STATUS_EP_TIMEOUT in *status (nullable) and returns (never hangs the device).
+ * Window memory: dymoe_ep_window_alloc (cudaMalloc, zeroed; ipc_handle receives the 64-byte
+ * cudaIpcMemHandle_t, nullable), dymoe_ep_window_open (cudaIpcOpenMemHandle with lazy peer
+ * access, another process's window), dymoe_ep_window_close / _free.  The caller owns them.
+ * Errors: INVALID for NULL pointers, P outside [1, min(M, 64)], rank outside [0, P), Hd not a
+ * positive multiple of 8, cap_rows < 0; CUDA for allocation / IPC failures.                   */
+enum { DYMOE_STATUS_EP_TIMEOUT = 2 };
+typedef struct dymoe_ep_window {
+  int P, rank, M, Hd, cap_rows, parity;
+  void* const* peers;
+} dymoe_ep_window;
+size_t dymoe_ep_window_bytes(int P, int M, int Hd, int cap_rows);
+int dymoe_ep_window_alloc(size_t bytes, void** base, void* ipc_handle);
+int dymoe_ep_window_open(const void* ipc_handle, void** base);
+int dymoe_ep_window_close(void* base);
+int dymoe_ep_window_free(void* base);
+int dymoe_ep_publish_counts(const dymoe_ep_window* w, const int32_t* expert_off,
+                            dymoe_stream_t stream);
+int dymoe_ep_barrier(const dymoe_ep_window* w, uint32_t epoch, uint32_t* status,
+                     dymoe_stream_t stream);
+/* x [T][Hd] bf16; expert_off [M+1], perm_token [T*k] from dymoe_permute (skips dropped);
+ * recv_off [M_loc+1] i32 out, M_loc = experts owned by this rank.  Rows that would exceed
+ * cap_rows are not stored and set DYMOE_STATUS_EP_TIMEOUT's sibling bit
+ * DYMOE_STATUS_EP_OVERFLOW in *status.                                                         */
+enum { DYMOE_STATUS_EP_OVERFLOW = 4 };
+int dymoe_ep_dispatch(const dymoe_ep_window* w, const uint16_t* x, int T,
+                      const int32_t* expert_off, const int32_t* perm_token, int32_t* recv_off,
+                      uint32_t* status, dymoe_stream_t stream);
+/* inv_row [T][k], topk_w [T][k], expert_off [M+1] of this rank's dymoe_permute; y [T][Hd]
+ * (out_dtype) out.  Same result as dymoe_combine on the unsharded layer.                      */
+int dymoe_ep_combine(const dymoe_ep_window* w, const int32_t* inv_row, const float* topk_w,
+                     int T, int k, const int32_t* expert_off, int renorm, int out_dtype, void* y,
+                     dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
 /* The whole layer, one step: route -> score -> assign -> permute -> FFN
  * -> combine, all on `stream` with no host synchronisation (graph-capturable).               */
 typedef struct dymoe_fwd_opts {

@@ -31,8 +31,11 @@ EXPORTED = [
     "dymoe_pool_create", "dymoe_pool_destroy", "dymoe_pool_lookup", "dymoe_pool_insert",
     "dymoe_pool_pin", "dymoe_pool_unpin", "dymoe_pool_snapshot", "dymoe_pool_used",
     "dymoe_layer_set_expert", "dymoe_attention_mass", "dymoe_gate_logits",
-    "dymoe_rmsnorm",
+    "dymoe_rmsnorm", "dymoe_ep_window_bytes", "dymoe_ep_window_alloc", "dymoe_ep_window_open",
+    "dymoe_ep_window_close", "dymoe_ep_window_free", "dymoe_ep_publish_counts", "dymoe_ep_barrier",
+    "dymoe_ep_dispatch", "dymoe_ep_combine",
 ]
+DYMOE_STATUS_EP_TIMEOUT, DYMOE_STATUS_EP_OVERFLOW = 2, 4
 
 
 class DymoeError(RuntimeError):
@@ -85,6 +88,11 @@ class WsViews(ctypes.Structure):
 _lib = None
 
 
+class EpWindow(ctypes.Structure):
+    _fields_ = [("P", ctypes.c_int), ("rank", ctypes.c_int), ("M", ctypes.c_int), ("Hd", ctypes.c_int),
+                ("cap_rows", ctypes.c_int), ("parity", ctypes.c_int), ("peers", ctypes.c_void_p)]
+
+
 def lib():
     """Load libdymoe.so once; raise loudly if it is missing (no fallback)."""
     global _lib
@@ -132,6 +140,15 @@ def lib():
             "dymoe_attention_mass": [vp, vp, ci, ci, ci, ctypes.c_float, vp, vp, vp],
             "dymoe_gate_logits": [vp, vp, vp, ci, ci, ci, vp, vp],
             "dymoe_rmsnorm": [vp, ci, ci, ctypes.c_float, vp, vp],
+            "dymoe_ep_window_bytes": [ci, ci, ci, ci],
+            "dymoe_ep_window_alloc": [cz, ctypes.POINTER(vp), vp],
+            "dymoe_ep_window_open": [vp, ctypes.POINTER(vp)],
+            "dymoe_ep_window_close": [vp],
+            "dymoe_ep_window_free": [vp],
+            "dymoe_ep_publish_counts": [ctypes.POINTER(EpWindow), vp, vp],
+            "dymoe_ep_barrier": [ctypes.POINTER(EpWindow), ctypes.c_uint32, vp, vp],
+            "dymoe_ep_dispatch": [ctypes.POINTER(EpWindow), vp, ci, vp, vp, vp, vp, vp],
+            "dymoe_ep_combine": [ctypes.POINTER(EpWindow), vp, vp, ci, ci, vp, ci, ci, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -142,6 +159,7 @@ def lib():
         L.dymoe_workspace_size.restype = cz
         L.dymoe_predict_ws_bytes.restype = cz
         L.dymoe_pool_used.restype = cz
+        L.dymoe_ep_window_bytes.restype = cz
         L.dymoe_last_error.restype = ctypes.c_char_p
         L.dymoe_version.restype = ctypes.c_char_p
         _lib = L
@@ -291,6 +309,55 @@ def dymoe_gather_rows(x, rows, stream=None):
     _check(lib().dymoe_gather_rows(_p(_u16(x)), x.shape[1], _p(rows), n, _p(_u16(out)) if n else None,
                                    _stream(stream)))
     return out
+
+
+def dymoe_ep_window_bytes(P, M, Hd, cap_rows):
+    return lib().dymoe_ep_window_bytes(P, M, Hd, cap_rows)
+
+
+def dymoe_ep_window_alloc(nbytes):
+    """(base pointer int, 64-byte CUDA IPC handle) of a zeroed device window (caller frees)."""
+    base = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(64)
+    _check(lib().dymoe_ep_window_alloc(nbytes, ctypes.byref(base), h))
+    return base.value, bytes(h.raw)
+
+
+def dymoe_ep_window_open(handle):
+    base = ctypes.c_void_p()
+    _check(lib().dymoe_ep_window_open(ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(base)))
+    return base.value
+
+
+def dymoe_ep_window_close(base):
+    _check(lib().dymoe_ep_window_close(ctypes.c_void_p(base)))
+
+
+def dymoe_ep_window_free(base):
+    _check(lib().dymoe_ep_window_free(ctypes.c_void_p(base)))
+
+
+def dymoe_ep_publish_counts(win, expert_off, stream=None):
+    _check(lib().dymoe_ep_publish_counts(ctypes.byref(win), _p(expert_off), _stream(stream)))
+
+
+def dymoe_ep_barrier(win, epoch, status=None, stream=None):
+    _check(lib().dymoe_ep_barrier(ctypes.byref(win), epoch & 0xffffffff, _p(status), _stream(stream)))
+
+
+def dymoe_ep_dispatch(win, x, expert_off, perm_token, recv_off, status=None, stream=None):
+    _check(lib().dymoe_ep_dispatch(ctypes.byref(win), _p(_u16(x)), x.shape[0], _p(expert_off),
+                                   _p(perm_token), _p(recv_off), _p(status), _stream(stream)))
+
+
+def dymoe_ep_combine(win, inv_row, topk_w, expert_off, renorm=True, out_dtype=DYMOE_OUT_F32,
+                     stream=None):
+    T, k = inv_row.shape
+    y = torch.empty(T, win.Hd, dtype=torch.float32 if out_dtype == DYMOE_OUT_F32 else torch.bfloat16,
+                    device=inv_row.device)
+    _check(lib().dymoe_ep_combine(ctypes.byref(win), _p(inv_row), _p(topk_w), T, k, _p(expert_off),
+                                  int(renorm), out_dtype, _p(y) if T else None, _stream(stream)))
+    return y
 
 
 def dymoe_combine(y_perm, inv_row, topk_w, renorm=True, out_dtype=DYMOE_OUT_F32, stream=None):
@@ -492,6 +559,14 @@ class MoELayer:
             perm_token=view("perm_token", (T * k,), torch.int32), perm_slot=view("perm_slot", (T * k,), torch.int32),
             inv_row=view("inv_row", (T, k), torch.int32), h=view("h", (T * k, F), torch.bfloat16),
             y_perm=view("y_perm", (T * k, Hd), torch.float32), status=view("status", (1,), torch.int32))
+
+    def expert_ffn_into(self, x_ptr, T, bits, expert_off, perm_token, mode, y_ptr, h, status,
+                        stream=None):
+        """dymoe_expert_ffn on raw device rows (x_ptr [T][Hd] bf16) writing y_perm to y_ptr
+        ([T*k][Hd] f32), e.g. an expert-parallel peer window; h [T*k][F] bf16 scratch."""
+        _check(lib().dymoe_expert_ffn(self.handle, mode, ctypes.c_void_p(x_ptr), T, _p(bits),
+                                      _p(expert_off), _p(perm_token), _p(h), ctypes.c_void_p(y_ptr),
+                                      _p(status), _stream(stream)))
 
     def expert_ffn(self, x, bits, expert_off, perm_token, mode, stream=None):
         T = x.shape[0]

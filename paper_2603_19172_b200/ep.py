@@ -28,6 +28,15 @@ terms with weights renormalised over the GLOBAL live set (dymoe_renorm_weights, 
 all-reduce(sum) of y [B][Hd] fp32 adds the ranks' partial outputs.  With top-2 each element has at
 most two nonzero terms, so the sum does not depend on the reduction order.
 
+Peer-memory variant (`forward_p2p`, SURVEY §8e over NVLink / NVSwitch): the two all-to-alls are
+replaced by libdymoe kernels that move the rows themselves through symmetric windows mapped into
+every rank (PeerWindows; CUDA IPC between processes): dymoe_ep_dispatch gathers each permuted row
+and stores it straight into its owner's window at its final expert-major row (no regrouping on the
+receiver), the FFN writes its outputs into the own window, and dymoe_ep_combine pulls every live
+slot's output row from its owner and applies the weighted combine in the same kernel.  Three
+flag barriers per step (dymoe_ep_barrier); the receive count is read once on the host to size
+the FFN launch.
+
 Every step of the math runs in libdymoe kernels; torch.distributed (NCCL on GPUs) carries the
 bytes.  The only host synchronisation is the count exchange needed to size the all-to-all.
 The orchestration is written against two small interfaces -- `ops` (the layer primitives) and
@@ -137,6 +146,71 @@ class ThreadComm:
         return out
 
 
+class PeerWindows:
+    """This rank's symmetric expert-parallel window and every peer's, mapped into this process
+    (include/dymoe.h "Expert-parallel dispatch and combine over peer memory").
+
+    comm: ThreadComm (ranks are threads of one process: the base pointers are shared directly) or
+    TorchComm (one process per rank: 64-byte CUDA IPC handles are all-gathered and opened).
+    barrier: "device" -- flag barriers in the windows (dymoe_ep_barrier, no host involvement);
+    "host" -- stream synchronise + process-group barrier (ranks time-sharing ONE GPU from several
+    processes, where a spinning device barrier would wait on context switches)."""
+
+    def __init__(self, comm, M, hidden, cap_rows, barrier="device", device=None):
+        from . import dymoe as d
+        self.d, self.comm = d, comm
+        self.P, self.rank = comm.world, comm.rank
+        self.M, self.hidden, self.cap = M, hidden, cap_rows
+        self.barrier_mode = barrier
+        self.nbytes = d.dymoe_ep_window_bytes(self.P, M, hidden, cap_rows)
+        self.base, handle = d.dymoe_ep_window_alloc(self.nbytes)
+        self.opened = []
+        if isinstance(comm, ThreadComm):
+            bases = comm._exchange(self.base)
+        else:
+            handles = [None] * self.P
+            comm.dist.all_gather_object(handles, handle, group=comm.group)
+            bases = []
+            for r, h in enumerate(handles):
+                if r == self.rank:
+                    bases.append(self.base)
+                else:
+                    b = d.dymoe_ep_window_open(h)
+                    self.opened.append(b)
+                    bases.append(b)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.peers = torch.tensor(bases, dtype=torch.int64, device=dev)
+        self.win = d.EpWindow(self.P, self.rank, M, hidden, cap_rows, 0, self.peers.data_ptr())
+        # the window's sections (include/dymoe.h): flags, cnt[2][P][M], recv_x, y_out
+        a = lambda v: (v + 255) // 256 * 256
+        cnt = a(self.P * 4)
+        self.recv_x_ptr = self.base + cnt + a(2 * self.P * M * 4)
+        self.y_out_ptr = self.recv_x_ptr + a(cap_rows * hidden * 2)
+        self.epoch = 0
+        self.status = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.ident = torch.arange(max(cap_rows, 1), dtype=torch.int32, device=dev)
+
+    def barrier(self):
+        if self.barrier_mode == "host":
+            torch.cuda.current_stream().synchronize()
+            if isinstance(self.comm, ThreadComm):
+                self.comm.barrier.wait()
+            else:
+                self.comm.dist.barrier(group=self.comm.group)
+            return
+        self.epoch += 1
+        self.d.dymoe_ep_barrier(self.win, self.epoch, self.status)
+
+    def close(self):
+        for b in self.opened:
+            self.d.dymoe_ep_window_close(b)
+        self.opened = []
+        if self.base:
+            torch.cuda.synchronize()
+            self.d.dymoe_ep_window_free(self.base)
+            self.base = None
+
+
 class CudaOps:
     """The layer primitives on the CUDA path (libdymoe C ABI)."""
 
@@ -238,6 +312,42 @@ class EPMoELayer:
         y = ops.combine(y_back, inv, w, renorm)
         return y, dict(bits=bits, importance=imp, topk_idx=idx, topk_w=w, send=send_splits,
                        recv=recv_splits)
+
+    def forward_p2p(self, win, x, logits, ladder, layer, num_layers, phase, attn_mass=None,
+                    k_tokens=0, renorm=True, ffn_mode=None):
+        """forward() with dispatch and combine over peer memory (`win`: PeerWindows).  Same
+        result as forward(), bit for bit: the receive layout is the expert-major order forward()
+        regroups into, and the combine is dymoe_combine's arithmetic."""
+        ops, comm, d = self.ops, self.comm, win.d
+        M, k, P = self.M, self.k, self.P
+        PREFILL, DECODE = 0, 1
+        idx, w, probs = ops.route(logits, k)
+        if phase == DECODE and P > 1 and x.shape[0] == 1:
+            imp = probs[0].clone()
+        else:
+            imp = ops.score(phase, M, k, idx, attn_mass, logits, k_tokens)
+        if P > 1:
+            imp = comm.all_reduce_sum(imp)
+        bits = ops.assign_bits(imp, layer, num_layers, ladder, k)
+        off, pt, ps, inv = ops.permute(idx, M, bits)
+        # counts into every window, then the rows straight to their owners
+        d.dymoe_ep_publish_counts(win.win, off)
+        win.barrier()
+        M_loc = self.last - self.first
+        recv_off = torch.empty(M_loc + 1, dtype=torch.int32, device=x.device)
+        d.dymoe_ep_dispatch(win.win, x, off, pt, recv_off, win.status)
+        win.barrier()
+        n_recv = int(recv_off[M_loc].item())      # sizes the FFN launch (one host read)
+        if n_recv > 0:
+            mode = (PREFILL if n_recv > 64 else DECODE) if ffn_mode is None else ffn_mode
+            bits_loc = bits[self.first:self.last].contiguous()
+            h = torch.empty(n_recv, self.ffn, dtype=torch.bfloat16, device=x.device)
+            self.local.expert_ffn_into(win.recv_x_ptr, n_recv, bits_loc, recv_off,
+                                       win.ident[:n_recv], mode, win.y_out_ptr, h, win.status)
+        win.barrier()
+        y = d.dymoe_ep_combine(win.win, inv, w, off, renorm=renorm)
+        win.win.parity ^= 1
+        return y, dict(bits=bits, importance=imp, topk_idx=idx, topk_w=w, recv=n_recv)
 
     def forward_replicated(self, x, logits, ladder, layer, num_layers, k_tokens=0, renorm=True,
                            ffn_mode=None):

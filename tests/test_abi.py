@@ -100,3 +100,29 @@ def test_no_cpu_fallback(d):
     import torch
     with pytest.raises(ValueError, match="CUDA"):
         d.dymoe_route(torch.zeros(2, 8), 2)
+
+
+def test_ep_window_layout_and_validation(d):
+    """Host-side parts of the peer-memory EP calls: the window size formula (flags, cnt[2][P][M],
+    recv_x bf16 and y_out f32 sections, each 256-byte aligned) and field-naming validation."""
+    a = lambda v: (v + 255) // 256 * 256
+    for P, M, Hd, cap in [(2, 8, 256, 64), (8, 64, 2048, 98304), (1, 1, 8, 0), (3, 7, 24, 5)]:
+        want = a(P * 4) + a(2 * P * M * 4) + a(cap * Hd * 2) + a(cap * Hd * 4)
+        assert d.dymoe_ep_window_bytes(P, M, Hd, cap) == want
+    assert d.dymoe_ep_window_bytes(0, 8, 256, 4) == 0
+    L = d.lib()
+    w = d.EpWindow(4, 0, 2, 256, 16, 0, 0x100000)
+    rc, msg = _err(d, L.dymoe_ep_publish_counts(ctypes.byref(w), FAKE, None))
+    assert rc == 1 and msg.startswith("window.P:")
+    w = d.EpWindow(2, 2, 8, 256, 16, 0, 0x100000)
+    rc, msg = _err(d, L.dymoe_ep_barrier(ctypes.byref(w), 1, None, None))
+    assert rc == 1 and msg.startswith("window.rank:")
+    w = d.EpWindow(2, 0, 8, 100, 16, 0, 0x100000)
+    rc, msg = _err(d, L.dymoe_ep_dispatch(ctypes.byref(w), FAKE, 4, FAKE, FAKE, FAKE, None, None))
+    assert rc == 1 and msg.startswith("window.Hd:")
+    w = d.EpWindow(2, 0, 8, 256, 16, 2, 0x100000)
+    rc, msg = _err(d, L.dymoe_ep_combine(ctypes.byref(w), FAKE, FAKE, 4, 2, FAKE, 1, 0, FAKE, None))
+    assert rc == 1 and msg.startswith("window.parity:")
+    w = d.EpWindow(2, 0, 8, 256, 16, 0, None)
+    rc, msg = _err(d, L.dymoe_ep_combine(ctypes.byref(w), FAKE, FAKE, 4, 2, FAKE, 1, 0, FAKE, None))
+    assert rc == 1 and msg.startswith("window.peers:")
