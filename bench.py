@@ -502,6 +502,41 @@ def run_ep(args, rank, world, device):
                "scaling": "strong", "global_batch": T,
                "note": "the same %d-token batch on every rank; local experts + all-reduce(sum) of y" % T}
 
+    # ---------------- the same weak-scaling steps with dispatch / combine over peer memory
+    # (forward_p2p: fused gather+store and pull+combine kernels, flag barriers)
+    p2p = None
+    try:
+        gloo = torch.distributed.get_backend() != "nccl"
+        win = ep.PeerWindows(comm, cfg.M, cfg.hidden, T * cfg.k * world,
+                             barrier="host" if gloo else "device", device=device)
+
+        def p2p_step(i):
+            x, lg, a = inputs[i % n_inputs]
+            return shards[i % len(shards)].forward_p2p(win, x, lg, ladder, i % NUM_LAYERS, NUM_LAYERS,
+                                                       phase, attn_mass=a)
+
+        for i in range(args.warmup):
+            p2p_step(i)
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        q0.record()
+        for i in range(K):
+            p2p_step(args.warmup + i)
+        q1.record()
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        qms = _max_over_ranks(q0.elapsed_time(q1), device)
+        st = int(win.status.item())
+        torch.distributed.barrier()
+        win.close()
+        p2p = {"value": T * K * world / (qms / 1e3), "unit": "tokens/s", "ms_per_step": qms / K,
+               "scaling": "weak", "barrier": win.barrier_mode, "status": st,
+               "note": "dymoe_ep_dispatch / dymoe_ep_combine over peer windows (CUDA IPC), "
+                       "no NCCL on the data path; 3 flag barriers + 1 count read per step"}
+    except Exception as ex:   # reported, never fatal for the main line
+        p2p = {"error": "%s: %s" % (type(ex).__name__, str(ex)[:300])}
+
     # local FFN roofline (bytes of the local experts actually streamed / FFN time)
     ffn_ms, ffn_bytes, ffn_flops = 0.0, 0.0, 0.0
     for e0, e1, bits, off in ffn_events:
@@ -543,7 +578,7 @@ def run_ep(args, rank, world, device):
                # gather_rows, local permute, active list, W13, W2, reduce / prefill gather,
                # unit-weight reorder, weighted combine (NCCL collectives not counted)
                "gpu_launches": 13 * K,
-               "ep_replicated_decode": rep}
+               "ep_replicated_decode": rep, "ep_p2p": p2p}
     return res
 
 

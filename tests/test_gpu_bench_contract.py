@@ -50,3 +50,21 @@ def test_stack_line():
     j = _run("--workload", "stack", "--steps", "2", "--warmup", "3")
     _common(j)
     assert j["config"]["workload"] == "mixtral_stack32_decode" and j["config"]["layers"] == 32
+
+
+def test_ep_two_ranks_line_with_p2p():
+    """N = 2 bench path (two processes time-sharing the one GPU over gloo -- a test hook, never a
+    reported number): the EP line, the replicated-decode and the peer-memory variants."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29641", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--dist-backend", "gloo", "--steps", "3", "--warmup", "3", "--copies", "1"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["value"] > 0 and j["scaling"] == "weak"
+    assert j["ep_replicated_decode"]["value"] > 0
+    p = j["ep_p2p"]
+    assert "error" not in p, p
+    assert p["value"] > 0 and p["status"] == 0 and p["barrier"] == "host"
