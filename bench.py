@@ -13,6 +13,9 @@ Workloads:
           l = step mod 32 of a 32-layer stack, 4 rotating copies of the layer's weights so that
           no step re-reads weights another step left in L2 (each copy >= 5 GB > 126 MB L2).
   prefill (configs[2]): 2048 tokens per step, same rotation.
+  finegrained / finegrained_decode (configs[3]'s layer: 64 experts, top-6, hidden 2048, ffn
+          1408): 2048 tokens / B tokens per step; with N > 1 the expert-parallel layer of
+          configs[3].
 
 N > 1 (torchrun): expert parallelism (paper_2603_19172_b200/ep.py): experts sharded in
 contiguous blocks over the ranks, NCCL all-to-all token dispatch/combine, every rank bringing its
@@ -153,15 +156,26 @@ def algorithmic_flops(cfg, off, bits):
     return 6.0 * cfg.hidden * cfg.ffn * n
 
 
+def workload_cfg(args):
+    """(config, is_decode, workload name) of a layer workload: decode / prefill are BASELINE.json
+    configs[1] / [2] (Mixtral-8x7B-shaped); finegrained / finegrained_decode are configs[3]'s
+    layer (64 experts, top-6, hidden 2048, ffn 1408)."""
+    decode = args.workload in ("decode", "finegrained_decode")
+    fine = args.workload.startswith("finegrained")
+    base = synthetic.CONFIGS["finegrained" if fine else ("mixtral_decode" if decode else "mixtral_prefill")]
+    T = args.batch if decode else args.tokens
+    name = ("finegrained_" if fine else "mixtral_") + ("decode" if decode else "prefill")
+    return base.with_tokens(T), decode, name
+
+
 def run_ours(args, rank, world, device):
     import paper_2603_19172_b200.dymoe as d
     d.lib()
     torch.cuda.set_device(device)
     peaks = load_peaks()
-    base = synthetic.CONFIGS["mixtral_decode" if args.workload == "decode" else "mixtral_prefill"]
-    T = args.batch if args.workload == "decode" else args.tokens
-    cfg = base.with_tokens(T)
-    phase = d.DYMOE_DECODE if args.workload == "decode" else d.DYMOE_PREFILL
+    cfg, is_decode, wname = workload_cfg(args)
+    T = cfg.T
+    phase = d.DYMOE_DECODE if is_decode else d.DYMOE_PREFILL
     layers = build_layer_copies(d, cfg, args.copies, device)
     n_inputs = 8
     inputs = step_inputs(cfg, n_inputs, device)
@@ -253,7 +267,9 @@ def run_ours(args, rank, world, device):
     ffn_ms = sum(w13_ms) + sum(w2_ms)
     achieved_w13 = b13 / (sum(w13_ms) / 1e3) / 1e9
     achieved_ffn = (b13 + b2) / (ffn_ms / 1e3) / 1e9
-    tr = load_traffic("k_decode_gemv<W13>" if phase == d.DYMOE_DECODE else "k_prefill_gemm<W13>")
+    # the committed ncu capture is of the Mixtral layer's kernels
+    tr = load_traffic("k_decode_gemv<W13>" if phase == d.DYMOE_DECODE else "k_prefill_gemm<W13>") \
+        if wname.startswith("mixtral") else None
     traffic = tr["traffic"] if tr else None
 
     # ---------------- end-to-end through the public API with host buffers
@@ -356,12 +372,14 @@ def run_ours(args, rank, world, device):
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
             "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
-            "config": {"workload": "mixtral_%s" % args.workload, "hidden": cfg.hidden, "ffn": cfg.ffn,
+            "config": {"workload": wname, "hidden": cfg.hidden, "ffn": cfg.ffn,
                        "experts": cfg.M, "top_k": cfg.k, "tokens_per_step": T,
                        "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
                        "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
                        "weight_copies": args.copies,
-                       "l2": "inputs larger than L2: %d rotating weight copies, each >= 5 GB" % args.copies,
+                       "l2": "inputs larger than L2: %d rotating weight copies of %.1f GB each (L2 126 MB)" % (
+                           args.copies, cfg.M * 3 * cfg.hidden * cfg.ffn * sum(
+                               bytes_per_weight(b) for b in (16, 8, 4, 2)) / 1e9),
                        "parallelism": "replicas" if world > 1 else "single GPU"},
             "roofline": roofline,
             "clocks": clk.summary(),
@@ -387,10 +405,9 @@ def run_ep(args, rank, world, device):
     d.lib()
     torch.cuda.set_device(device)
     peaks = load_peaks()
-    base = synthetic.CONFIGS["mixtral_decode" if args.workload == "decode" else "mixtral_prefill"]
-    T = args.batch if args.workload == "decode" else args.tokens
-    cfg = base.with_tokens(T)
-    phase = d.DYMOE_DECODE if args.workload == "decode" else d.DYMOE_PREFILL
+    cfg, is_decode, wname = workload_cfg(args)
+    T = cfg.T
+    phase = d.DYMOE_DECODE if is_decode else d.DYMOE_PREFILL
     comm = ep.TorchComm(stage_cpu=torch.distributed.get_backend() != "nccl")
 
     class TimedOps(ep.CudaOps):
@@ -566,7 +583,7 @@ def run_ep(args, rank, world, device):
                "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
                "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
-               "config": {"workload": "mixtral_%s" % args.workload, "hidden": cfg.hidden, "ffn": cfg.ffn,
+               "config": {"workload": wname, "hidden": cfg.hidden, "ffn": cfg.ffn,
                           "experts": cfg.M, "top_k": cfg.k, "tokens_per_step_per_rank": T,
                           "global_batch": T * world,
                           "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
@@ -736,10 +753,9 @@ def _cpu_model():
 
 def run_reference(args):
     """Reference arm: the CPU oracle on the same workload, bounded sample per step."""
-    base = synthetic.CONFIGS["mixtral_decode" if args.workload == "decode" else "mixtral_prefill"]
-    T = args.batch if args.workload == "decode" else args.tokens
-    cfg = base.with_tokens(T)
-    prefill = args.workload == "prefill"
+    cfg, is_decode, wname = workload_cfg(args)
+    T = cfg.T
+    prefill = not is_decode
     for _ in range(args.warmup):
         cpu_baseline(cfg, args, prefill, frac=64)
     vals = []
@@ -753,7 +769,7 @@ def run_reference(args):
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (oracle)",
-            "data": "synthetic", "config": {"workload": "mixtral_%s" % args.workload, "tokens_per_step": T},
+            "data": "synthetic", "config": {"workload": wname, "tokens_per_step": T},
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
@@ -898,8 +914,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="decode",
-                    choices=["decode", "prefill", "stack", "stack_prefill"],
-                    help="decode / prefill: one Mixtral layer (configs[1] / [2]); stack / "
+                    choices=["decode", "prefill", "finegrained", "finegrained_decode", "stack",
+                             "stack_prefill"],
+                    help="decode / prefill: one Mixtral layer (configs[1] / [2]); finegrained / "
+                         "finegrained_decode: the 64-expert top-6 layer of configs[3]; stack / "
                          "stack_prefill: the 32-layer stack of configs[4] on one GPU")
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--tokens", type=int, default=2048)

@@ -232,3 +232,15 @@ def test_ep_p2p_ipc_processes(tmp_path):
     for rank in range(2):
         res = json.load(open("%s.%d" % (out, rank)))
         assert res["ok"] and res["status"] == 0, res
+
+
+@pytest.mark.parametrize("phase,T", [(0, 256), (1, 8)])
+def test_ep_p2p_finegrained_p8(phase, T):
+    """BASELINE.json configs[3]'s layer (64 experts, top-6, hidden 2048, ffn 1408) over 8 ranks
+    (threads, 8 experts each): peer-memory dispatch/combine equals the all-to-all path."""
+    cfg = synthetic.CONFIGS["finegrained"].with_tokens(T)
+    res = _run_p2p(8, phase, (8, 4, 2), (0.25, 0.5), 17, cfg, steps=2)
+    for r in range(8):
+        for y1, y2, n2, n1, status in res[r]:
+            assert status == 0 and n1 == n2 and n2 > 0
+            assert np.array_equal(y1, y2), (r, np.abs(y1 - y2).max())
