@@ -717,13 +717,18 @@ static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, con
 }
 
 // Builds the active list (experts with rows) from expert_off on device.
+// One warp, 32 experts per ballot round, list order = expert order.
 __global__ void k_active_from_off(const int32_t* __restrict__ off, int M, int32_t* list) {
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int e = 0; e < M; ++e)
-      if (off[e + 1] > off[e]) list[1 + n++] = e;
-    list[0] = n;
+  const int lane = threadIdx.x & 31;
+  int n = 0;
+  for (int e0 = 0; e0 < M; e0 += 32) {
+    const int e = e0 + lane;
+    const bool act = e < M && off[e + 1] > off[e];
+    const unsigned bal = __ballot_sync(0xffffffffu, act);
+    if (act) list[1 + n + __popc(bal & ((1u << lane) - 1))] = e;
+    n += __popc(bal);
   }
+  if (lane == 0) list[0] = n;
 }
 
 int dymoe_expert_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T,

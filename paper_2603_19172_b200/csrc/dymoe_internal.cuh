@@ -104,6 +104,7 @@ struct FfnArgs {
                                // prefill: scratch for the expert-ordered token rows of GEMM 1)
   int part_rows;               // row capacity of one partial slice (>= T*k)
   uint32_t* status;
+  int min_items;               // decode: min 128-byte items per warp per tile (set by the launcher)
 };
 // Number of K-slices (and slice length) the decode W2 kernel splits F into.
 int decode_w2_slices(int F);

@@ -32,6 +32,8 @@
 //  * W1/W3 (gate/up): one K-slice (x = 8 x Hd bf16 in smem), SwiGLU applied in the reduction
 //    epilogue, h written as bf16.  W2 (down): K = F is split into SK slices, each writes fp32
 //    partials y_part[slice]; the combine kernel sums the slices in order.
+#include <cstdlib>
+
 #include "ffn_decode_common.cuh"
 
 namespace dymoe {
@@ -163,7 +165,7 @@ __device__ __forceinline__ DQ dq_from_meta(uint32_t w) {
 // row of the tile's K slice (CK k values each; NSUB = 2 BOXES), one 128 x 16 box per operand
 // block (W13: W1 and W3 rows of the tile's 16 features; W2: the two 16-row halves of a 32-row
 // tile), plus the metadata boxes of the GQ groups those chunks span.
-template <bool W13, int BITS>
+template <bool W13, int BITS, int WPT>
 __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts, int e, int k0,
                                            int kl, int t0, int t1, int nt, void* out, int ostride,
                                            uint32_t xs, int row_gran, float* red,
@@ -181,9 +183,7 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   // meta words of operand block m start at m * MSTRIDE in the stage: W13's 3-D box packs the two
   // blocks ([m][g][16]); W2's two boxes sit 256 B apart (TMA destinations are 128-B aligned)
   constexpr int MSTRIDE = W13 ? GQ * 64 : 256;
-  // warps sharing a tile: 8, or 4 at Int4 / Int2, whose 512 / 1024-k items would otherwise
-  // leave each warp only 1-2 items per tile (a cross-warp reduction per item or two)
-  constexpr int WPT = (BITS == 2 || BITS == 4) ? 4 : kWarps;
+  // WPT = warps sharing a tile (wpt_for below): K split over fewer warps when the slice is short
   constexpr int NSG = 2 * kWarps / WPT;              // subgroups per CTA, on interleaved tiles
   const int lane = threadIdx.x & 31;
   const int wid = threadIdx.x >> 5;
@@ -398,6 +398,20 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   return seq + n_items;
 }
 
+// Warps sharing a tile (each takes every WPT-th 128-byte item of the tile's K slice and the
+// group reduces the partial tiles): 8 at BF16 / Int8, 4 at Int4 / Int2 (whose 512 / 1024-k
+// items would otherwise leave each warp 1-2 items per tile), halved (down to 2) while a warp
+// would get fewer than `min_items` items per tile -- short K slices (the fine-grained layer's
+// K = 2048 / 1408) then keep whole items per warp instead of a cross-warp reduction per item.
+constexpr int kDecodeMinItems = 6;   // DYMOE_DECODE_MIN_ITEMS overrides (measurement knob)
+__device__ __forceinline__ int wpt_for(int bits, int kl, int min_items) {
+  const int ck = 4 * (128 / bits);                         // WT<BITS>::CHUNK_K
+  const int npr = ((kl + ck - 1) / ck + 1) / 2;            // items per tile (2 chunks each)
+  int w = (bits == 2 || bits == 4) ? 4 : kWarps;
+  while (w > 2 && (npr + w - 1) / w < min_items) w >>= 1;
+  return w;
+}
+
 // x slice layout in shared memory ("x_pos"): [8 tokens][row_gran granules of 16 B].  Within each
 // chunk of CK k values (4 * XU4 granules), the granule lane quad position c reads as its i-th
 // (logical granule c * XU4 + i) is stored at position i * 4 + c, so a lane's XU4 loads are 64 B
@@ -417,7 +431,7 @@ struct Smem {
   static constexpr size_t META = (size_t)2 * kWarps * Cfg<W13>::S * Cfg<W13>::META;
   static constexpr size_t RED = Cfg<W13>::RED;
   static constexpr size_t BARS = (size_t)2 * kWarps * Cfg<W13>::S * 8;
-  static constexpr int SYNC_INTS = 16;   // 4 words per tile subgroup, up to 4 subgroups
+  static constexpr int SYNC_INTS = 32;   // 4 words per tile subgroup, up to 8 subgroups
   static __host__ __device__ size_t x_off() { return CODES + META + RED; }
   static __host__ __device__ size_t tail_off(int sliceK) {
     return x_off() + (size_t)kMaxTok * x_row_gran(sliceK) * 16;
@@ -449,7 +463,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
   const int NT = N / C::TILE_ROWS;
   const int row_gran = x_row_gran(sliceK);
   // the codes ring is free until the first TMA: use it as the allocation scratch
-  if (threadIdx.x == 0) compute_alloc(a, gridDim.x / SK, W13, A, *reinterpret_cast<AllocScratch*>(smem));
+  if (threadIdx.x < 32) compute_alloc(a, gridDim.x / SK, W13, A, *reinterpret_cast<AllocScratch*>(smem));
   if ((threadIdx.x & 31) == 0) {   // each warp's ring mbarriers (one arrival + tx per phase)
     for (int i = 0; i < C::S; ++i) mbar_init(bar_base + ((threadIdx.x >> 5) * C::S + i) * 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
@@ -529,14 +543,21 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
                       : (void*)(a.y_part + ((size_t)ks * a.part_rows + tok0) * a.Hd);
       const int ostride = W13 ? a.F : a.Hd;
       const uint32_t xsa = (uint32_t)__cvta_generic_to_shared(xs);
-#define DYMOE_RUN(B) seq = run_tiles<W13, B>(a.experts, e, k0, kl, t0, t1, nt, out, ostride, xsa, \
-                                             row_gran, red, codes_base, meta_base, bar_base,     \
-                                             tile_sync, seq)
-      switch (be) {
-        case 2: DYMOE_RUN(2); break;
-        case 4: DYMOE_RUN(4); break;
-        case 8: DYMOE_RUN(8); break;
-        default: DYMOE_RUN(16); break;
+      const int wpt = wpt_for(be, kl, a.min_items);
+#define DYMOE_RUN(B, W) seq = run_tiles<W13, B, W>(a.experts, e, k0, kl, t0, t1, nt, out, ostride, \
+                                                   xsa, row_gran, red, codes_base, meta_base,    \
+                                                   bar_base, tile_sync, seq)
+      switch (be * 16 + wpt) {
+        case 2 * 16 + 4: DYMOE_RUN(2, 4); break;
+        case 2 * 16 + 2: DYMOE_RUN(2, 2); break;
+        case 4 * 16 + 4: DYMOE_RUN(4, 4); break;
+        case 4 * 16 + 2: DYMOE_RUN(4, 2); break;
+        case 8 * 16 + 8: DYMOE_RUN(8, 8); break;
+        case 8 * 16 + 4: DYMOE_RUN(8, 4); break;
+        case 8 * 16 + 2: DYMOE_RUN(8, 2); break;
+        case 16 * 16 + 8: DYMOE_RUN(16, 8); break;
+        case 16 * 16 + 4: DYMOE_RUN(16, 4); break;
+        default: DYMOE_RUN(16, 2); break;
       }
 #undef DYMOE_RUN
     }
@@ -563,8 +584,14 @@ int decode_w2_slices(int F) {
   return (F + sl - 1) / sl;
 }
 
-cudaError_t launch_ffn_decode(const FfnArgs& a, cudaStream_t s, void* const* ev) {
+cudaError_t launch_ffn_decode(const FfnArgs& args, cudaStream_t s, void* const* ev) {
   static int sms = 0, dyn_max13 = 0, dyn_max2 = 0;
+  static const int min_items = [] {
+    const char* v = getenv("DYMOE_DECODE_MIN_ITEMS");
+    return v ? atoi(v) : kDecodeMinItems;
+  }();
+  FfnArgs a = args;
+  a.min_items = min_items;
   const int SK = decode_w2_slices(a.F), sliceK = decode_w2_slice_k(a.F);
   const size_t sm13 = smem_bytes(true, a.Hd), sm2 = smem_bytes(false, sliceK);
   if (sms == 0) {

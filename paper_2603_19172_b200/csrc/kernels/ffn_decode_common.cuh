@@ -193,47 +193,48 @@ __device__ __forceinline__ int wcost(int b, bool w13) {
   return b == 16 ? 256 : b == 8 ? 196 : b == 4 ? 144 : 131;
 }
 
-// Cost-proportional allocation of `units_total` units to the active experts (largest remainder,
-// ties to the lower list index; every active expert gets >= 1 unit).  Thread 0 only.
+// Cost-proportional allocation of `units_total` units to the active experts, every active
+// expert >= 1 unit: with C_i the exclusive prefix of the costs in list order and R = U - n,
+// first_unit[i] = i + floor(R * C_i / total) (so expert i gets 1 + floor(R C_{i+1} / total) -
+// floor(R C_i / total) units and the total is exactly U).  Warp 0, all 32 lanes: the list, row
+// counts and widths are loaded in parallel (one dependent round trip instead of a serial walk
+// over the experts -- the serial version held the whole CTA at its first barrier for tens of
+// microseconds with 20-60 active experts) and the prefix is a warp scan over contiguous blocks.
+// Every CTA computes the identical allocation; it only partitions tiles, never the arithmetic.
 __device__ void compute_alloc(const FfnArgs& a, int units_grid, bool w13, Alloc& A,
                               AllocScratch& X) {
+  const int lane = threadIdx.x & 31;
   const int n = a.active_list[0];
-  A.n_act = n;
-  long long* cost = X.cost;
-  long long total = 0;
-  for (int i = 0; i < n; ++i) {
+  const int per = (n + 31) / 32;
+  const int i0 = lane * per, i1 = min(n, i0 + per);
+  long long local = 0;
+  for (int i = i0; i < i1; ++i) {
     const int e = a.active_list[1 + i];
-    A.expert[i] = (uint8_t)e;
     const int rows = a.expert_off[e + 1] - a.expert_off[e];
-    const int chunks = (rows + kMaxTok - 1) / kMaxTok;
-    cost[i] = (long long)wcost(a.bits[e], w13) * chunks;
-    total += cost[i];
+    const long long c = (long long)wcost(a.bits[e], w13) * ((rows + kMaxTok - 1) / kMaxTok);
+    A.expert[i] = (uint8_t)e;
+    X.cost[i] = c;
+    local += c;
   }
+  long long incl = local;   // inclusive warp scan of the block sums
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const long long total = __shfl_sync(0xffffffffu, incl, 31);
   const int U = units_grid > n ? units_grid : n;
-  A.units_total = U;
-  int* u = X.u;
-  long long* rem = X.rem;
-  int used = 0;
-  for (int i = 0; i < n; ++i) {
-    const long long num = (long long)(U - n) * cost[i];   // n units reserved (one each)
-    u[i] = 1 + (int)(num / total);
-    rem[i] = num % total;
-    used += u[i];
+  const long long R = U - n;
+  long long cum = incl - local;
+  for (int i = i0; i < i1; ++i) {
+    A.first_unit[i] = (uint16_t)(i + (total > 0 ? (int)(R * cum / total) : 0));
+    cum += X.cost[i];
   }
-  while (used < U) {  // hand out the rest by largest remainder
-    int best = 0;
-    for (int i = 1; i < n; ++i)
-      if (rem[i] > rem[best]) best = i;
-    u[best] += 1;
-    rem[best] = -1;
-    ++used;
+  if (lane == 0) {
+    A.n_act = n;
+    A.units_total = U;
+    A.first_unit[n] = (uint16_t)U;
   }
-  int acc = 0;
-  for (int i = 0; i < n; ++i) {
-    A.first_unit[i] = (uint16_t)acc;
-    acc += u[i];
-  }
-  A.first_unit[n] = (uint16_t)acc;
 }
 
 

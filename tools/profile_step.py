@@ -18,7 +18,10 @@ import synthetic  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])
+    ap.add_argument("--workload", default="decode",
+                    choices=["decode", "prefill", "finegrained", "finegrained_decode"])
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--layer", type=int, default=20)
     ap.add_argument("--input", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=2)
@@ -27,8 +30,8 @@ def main():
     import paper_2603_19172_b200.dymoe as d
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    cfg = synthetic.CONFIGS["mixtral_decode" if args.workload == "decode" else "mixtral_prefill"]
-    phase = d.DYMOE_DECODE if args.workload == "decode" else d.DYMOE_PREFILL
+    cfg, is_decode, _ = bench.workload_cfg(args)
+    phase = d.DYMOE_DECODE if is_decode else d.DYMOE_PREFILL
     (layer, _), = bench.build_layer_copies(d, cfg, 1, dev)
     inputs = bench.step_inputs(cfg, args.input + 1, dev)
     x, lg, a = inputs[args.input]
