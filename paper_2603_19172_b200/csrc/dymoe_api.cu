@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -80,6 +81,8 @@ int check_ladder(const dymoe_ladder* L) {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+constexpr int kPrefillSmallRows = 16;
+
 struct WsLayout {
   size_t topk_idx, topk_w, probs, importance, heavy, bits, active, active_list, expert_off,
       perm_token, perm_slot, inv_row, h, y_perm, y_part, status, score_scratch, total;
@@ -101,7 +104,7 @@ WsLayout ws_layout(int M, int k, int Hd, int F, int T) {
   L.heavy = take((size_t)T * 4);
   L.bits = take((size_t)M);
   L.active = take((size_t)M);
-  L.active_list = take((size_t)(M + 1) * 4);
+  L.active_list = take((size_t)3 * (M + 1) * 4);   // + the two lists of the prefill split
   L.expert_off = take((size_t)(M + 1) * 4);
   L.perm_token = take(TK * 4);
   L.perm_slot = take(TK * 4);
@@ -684,6 +687,40 @@ int dymoe_renorm_weights(const int32_t* topk_idx, const float* topk_w, const uin
   return ok();
 }
 
+// Prefill: experts with at most this many rows run on the decode GEMV kernels (0 = never).
+// DYMOE_PREFILL_SMALL_ROWS overrides (measurement knob).
+static int prefill_small_rows() {
+  static const int v = getenv("DYMOE_PREFILL_SMALL_ROWS") ? atoi(getenv("DYMOE_PREFILL_SMALL_ROWS"))
+                                                          : kPrefillSmallRows;
+  return v;
+}
+
+// Splits the active list (list order kept) into experts with > small rows and those with
+// 1..small rows.  One warp, 32 entries per ballot round.
+__global__ void k_split_active(const int32_t* __restrict__ off, const int32_t* __restrict__ list,
+                               int small, int32_t* __restrict__ large_list,
+                               int32_t* __restrict__ small_list) {
+  const int lane = threadIdx.x & 31;
+  const int n = list[0];
+  int nl = 0, ns = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const int e = i < n ? list[1 + i] : 0;
+    const int rows = i < n ? off[e + 1] - off[e] : 0;
+    const bool is_l = rows > small, is_s = rows > 0 && rows <= small;
+    const unsigned bl = __ballot_sync(0xffffffffu, is_l), bs = __ballot_sync(0xffffffffu, is_s);
+    const unsigned below = (1u << lane) - 1;
+    if (is_l) large_list[1 + nl + __popc(bl & below)] = e;
+    if (is_s) small_list[1 + ns + __popc(bs & below)] = e;
+    nl += __popc(bl);
+    ns += __popc(bs);
+  }
+  if (lane == 0) {
+    large_list[0] = nl;
+    small_list[0] = ns;
+  }
+}
+
 static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, const uint8_t* bits,
                    const int32_t* expert_off, const int32_t* perm_token, const int32_t* active_list,
                    uint16_t* h, float* y_perm, float* y_part, int part_rows, int* parts_out,
@@ -710,8 +747,31 @@ static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, con
   // decode kernels write K-slice partials of W2; the prefill grouped GEMM writes y_perm directly
   *parts_out = mode == DYMOE_DECODE ? decode_w2_slices(L->F) : 0;
   if (T == 0) return DYMOE_OK;
-  cudaError_t e = mode == DYMOE_DECODE ? launch_ffn_decode(a, s, ev)
-                                       : launch_ffn_prefill(a, s, ev, mode == DYMOE_FFN_PREFILL_TS);
+  cudaError_t e;
+  const int small = prefill_small_rows();
+  if (mode == DYMOE_PREFILL && small > 0 && decode_w2_slices(L->F) == 1) {
+    // Prefill with small experts split off (active_list has room for 3 lists of M + 1): experts
+    // with <= `small` rows would fill a 256-token pair tile mostly with padding, so the GEMV
+    // kernels stream their weights once per 8 tokens instead; the W2 GEMV (one K slice) writes
+    // its rows of y_perm directly, after the grouped GEMM zeroed y_perm and added its own rows.
+    int32_t* large_list = const_cast<int32_t*>(active_list) + (L->M + 1);
+    int32_t* small_list = large_list + (L->M + 1);
+    k_split_active<<<1, 32, 0, s>>>(expert_off, active_list, small, large_list, small_list);
+    FfnArgs al = a;
+    al.active_list = large_list;
+    void* ev2[3] = {ev ? ev[0] : nullptr, ev ? ev[1] : nullptr, nullptr};
+    e = launch_ffn_prefill(al, s, ev ? ev2 : nullptr, false);
+    if (e == cudaSuccess) {
+      FfnArgs as = a;
+      as.active_list = small_list;
+      as.y_part = y_perm;
+      e = launch_ffn_decode(as, s, nullptr);
+    }
+    if (e == cudaSuccess && ev) record_ev(ev, 2, s);
+  } else {
+    e = mode == DYMOE_DECODE ? launch_ffn_decode(a, s, ev)
+                             : launch_ffn_prefill(a, s, ev, mode == DYMOE_FFN_PREFILL_TS);
+  }
   if (e != cudaSuccess) return cuda_fail(e, "expert ffn");
   return DYMOE_OK;
 }
@@ -747,7 +807,7 @@ int dymoe_expert_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T,
   const int SK = decode_w2_slices(L->F);
   int32_t* active = nullptr;
   float* parts = nullptr;
-  cudaError_t e = cudaMallocAsync(&active, (L->M + 1) * sizeof(int32_t), S(stream));
+  cudaError_t e = cudaMallocAsync(&active, 3 * (L->M + 1) * sizeof(int32_t), S(stream));
   if (e == cudaSuccess)
     e = cudaMallocAsync(&parts, (size_t)SK * rows * L->Hd * sizeof(float), S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dymoe_expert_ffn");

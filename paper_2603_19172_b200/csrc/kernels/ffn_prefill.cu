@@ -1051,7 +1051,11 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
                                          a.expert_off + a.M, rows, reinterpret_cast<uint4*>(xp));
   }
   const int grid = sms / 2 * 2;   // whole CTA pairs, one CTA per SM
-  static const int ksplit = getenv("DYMOE_PREFILL_W2_KSPLIT") ? atoi(getenv("DYMOE_PREFILL_W2_KSPLIT")) : 2;
+  // GEMM 2's K = F split in two halves only when it is long (Mixtral F = 14336: 224 k-blocks,
+  // 749 vs 722 TFLOP/s); a short K (the fine-grained layer's F = 1408: 22 k-blocks) keeps whole
+  // tiles (W2 269 -> 334 TFLOP/s).  DYMOE_PREFILL_W2_KSPLIT overrides (measurement knob).
+  static const int ks_env = getenv("DYMOE_PREFILL_W2_KSPLIT") ? atoi(getenv("DYMOE_PREFILL_W2_KSPLIT")) : 0;
+  const int ksplit = ks_env > 0 ? ks_env : (a.F / BK >= 64 ? 2 : 1);
   if (operand_swapped) {
     static bool attr = false;
     if (!attr) {
