@@ -359,6 +359,12 @@ int dymoe_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n, uin
  * Errors: INVALID for NULL pointers, P outside [1, min(M, 64)], rank outside [0, P), Hd not a
  * positive multiple of 8, cap_rows < 0; CUDA for allocation / IPC failures.                   */
 enum { DYMOE_STATUS_EP_TIMEOUT = 2 };
+/* Loads every kernel of the library on the current device now.  Under CUDA lazy loading a
+ * kernel's first launch waits for the device to go idle, which never happens while a peer's
+ * dymoe_ep_barrier spins waiting for this rank (the barrier then times out).
+ * dymoe_ep_window_alloc calls it; call it yourself before the first barrier otherwise.
+ * Errors: CUDA.                                                                               */
+int dymoe_preload(void);
 typedef struct dymoe_ep_window {
   int P, rank, M, Hd, cap_rows, parity;
   void* const* peers;

@@ -295,14 +295,14 @@ int dymoe_quantize_batched(const dymoe_quant_job* jobs, int n_jobs, int group,
 // TMA descriptors (driver entry point fetched once through the runtime: no -lcuda)
 namespace {
 PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (fn == nullptr) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+  }();
   return fn;
 }
 // tiled map over a row-major tensor of rank 2 or 3 (strides in bytes for dims 1.., box per dim)
@@ -978,3 +978,5 @@ int dymoe::set_error(int code, const char* fmt, ...) {
   return code;
 }
 void dymoe::clear_error() { g_err.clear(); }
+
+cudaError_t dymoe::preload_api() { return preload_kernels(k_split_active, k_active_from_off); }

@@ -11,6 +11,27 @@
 
 namespace dymoe {
 
+// Kernel preloading.  Under CUDA lazy loading (the default) a kernel's first launch loads it, and
+// loading waits for the device to go idle -- which never happens while a peer rank's
+// dymoe_ep_barrier kernel spins waiting for this rank.  cudaFuncGetAttributes loads a kernel
+// without launching it; each translation unit lists its kernels in a preload_* function.
+template <class... K>
+inline cudaError_t preload_kernels(K... k) {
+  cudaError_t r = cudaSuccess;
+  cudaFuncAttributes fa;
+  ((r = (r == cudaSuccess ? cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(k)) : r)), ...);
+  return r;
+}
+cudaError_t preload_route_score();
+cudaError_t preload_permute_combine();
+cudaError_t preload_ffn_decode();
+cudaError_t preload_ffn_prefill();
+cudaError_t preload_quantize();
+cudaError_t preload_attn_mass();
+cudaError_t preload_predict();
+cudaError_t preload_norm();
+cudaError_t preload_api();
+
 // ------------------------------------------------------------------------------------------
 // Device-side expert table (one entry per expert; copied to device by dymoe_layer_create).
 struct DevQMat {

@@ -247,6 +247,17 @@ int done(cudaError_t e, const char* where) {
 
 extern "C" {
 
+int dymoe_preload(void) {
+  using namespace dymoe;
+  cudaError_t e = preload_kernels(k_ep_publish, k_ep_barrier, k_ep_dispatch, k_ep_combine);
+  cudaError_t (*const fns[])() = {preload_route_score, preload_permute_combine, preload_ffn_decode,
+                                  preload_ffn_prefill,  preload_quantize,        preload_attn_mass,
+                                  preload_predict,      preload_norm,            preload_api};
+  for (auto f : fns)
+    if (e == cudaSuccess) e = f();
+  return done(e, "dymoe_preload");
+}
+
 size_t dymoe_ep_window_bytes(int P, int M, int Hd, int cap_rows) {
   if (P < 1 || M < 1 || Hd < 1 || cap_rows < 0) return 0;
   return win_layout(P, M, Hd, cap_rows).total;
@@ -256,6 +267,9 @@ int dymoe_ep_window_alloc(size_t bytes, void** base, void* ipc_handle) {
   if (!base) return dymoe::set_error(DYMOE_ERR_INVALID, "base: must not be NULL");
   if (bytes == 0) return dymoe::set_error(DYMOE_ERR_INVALID, "bytes: must be > 0");
   *base = nullptr;
+  // every kernel loaded before any peer can spin in a barrier (see dymoe_preload)
+  int rc = dymoe_preload();
+  if (rc) return rc;
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, bytes);
   if (e != cudaSuccess) return cuda_err(e, "dymoe_ep_window_alloc");

@@ -208,4 +208,6 @@ cudaError_t launch_attention_mass(const uint16_t* Q, const uint16_t* K, int H, i
   return cudaGetLastError();
 }
 
+cudaError_t preload_attn_mass() { return preload_kernels(attn::k_row_stats, attn::k_col_sums); }
+
 }  // namespace dymoe

@@ -585,7 +585,28 @@ int decode_w2_slices(int F) {
 }
 
 cudaError_t launch_ffn_decode(const FfnArgs& args, cudaStream_t s, void* const* ev) {
-  static int sms = 0, dyn_max13 = 0, dyn_max2 = 0;
+  // one-time setup, thread-safe (C++11 magic static): several host threads may launch the first
+  // layer step concurrently (expert-parallel ranks simulated by threads)
+  struct Setup { int sms, dyn_max13, dyn_max2; };
+  static const Setup setup = [] {
+    Setup r{};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&r.sms, cudaDevAttrMultiProcessorCount, dev);
+    // opt in to the maximum once (227 KB per block); the per-launch size is what each launch
+    // requests
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa13{}, fa2{};
+    cudaFuncGetAttributes(&fa13, k_decode_gemv<true>);
+    cudaFuncGetAttributes(&fa2, k_decode_gemv<false>);
+    r.dyn_max13 = optin - (int)fa13.sharedSizeBytes;
+    r.dyn_max2 = optin - (int)fa2.sharedSizeBytes;
+    cudaFuncSetAttribute(k_decode_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, r.dyn_max13);
+    cudaFuncSetAttribute(k_decode_gemv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, r.dyn_max2);
+    return r;
+  }();
+  const int sms = setup.sms, dyn_max13 = setup.dyn_max13, dyn_max2 = setup.dyn_max2;
   static const int min_items = [] {
     const char* v = getenv("DYMOE_DECODE_MIN_ITEMS");
     return v ? atoi(v) : kDecodeMinItems;
@@ -594,22 +615,6 @@ cudaError_t launch_ffn_decode(const FfnArgs& args, cudaStream_t s, void* const* 
   a.min_items = min_items;
   const int SK = decode_w2_slices(a.F), sliceK = decode_w2_slice_k(a.F);
   const size_t sm13 = smem_bytes(true, a.Hd), sm2 = smem_bytes(false, sliceK);
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // opt in to the maximum once (227 KB per block); the per-launch size is what each launch
-    // requests
-    int optin = 0;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa13{}, fa2{};
-    cudaFuncGetAttributes(&fa13, k_decode_gemv<true>);
-    cudaFuncGetAttributes(&fa2, k_decode_gemv<false>);
-    dyn_max13 = optin - (int)fa13.sharedSizeBytes;
-    dyn_max2 = optin - (int)fa2.sharedSizeBytes;
-    cudaFuncSetAttribute(k_decode_gemv<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max13);
-    cudaFuncSetAttribute(k_decode_gemv<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_max2);
-  }
   if ((int)sm13 > dyn_max13 || (int)sm2 > dyn_max2) return cudaErrorInvalidConfiguration;
   const int grid = sms;   // one 512-thread CTA (two 8-warp groups) per SM
   record_ev(ev, 0, s);
@@ -623,6 +628,10 @@ cudaError_t launch_ffn_decode(const FfnArgs& args, cudaStream_t s, void* const* 
   if (e != cudaSuccess) return e;
   record_ev(ev, 2, s);
   return cudaSuccess;
+}
+
+cudaError_t preload_ffn_decode() {
+  return preload_kernels(dec::k_decode_gemv<true>, dec::k_decode_gemv<false>);
 }
 
 }  // namespace dymoe

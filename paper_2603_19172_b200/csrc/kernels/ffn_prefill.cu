@@ -1026,14 +1026,16 @@ __global__ void __launch_bounds__(256) k_gather_perm(const uint4* __restrict__ x
 cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev, bool operand_swapped) {
   using namespace pf;
   if (a.Hd % BNH || a.F % BNH || a.Hd % BK || a.F % BK) return cudaErrorInvalidValue;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
+  static const int sms = [] {   // one-time setup, thread-safe (magic static)
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_prefill_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     cudaFuncSetAttribute(k_prefill_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-  }
+    cudaFuncSetAttribute(k_prefill_ts<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts::kSmemT);
+    cudaFuncSetAttribute(k_prefill_ts<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts::kSmemT);
+    return n;
+  }();
   const int rows = a.T * a.k;
   uint16_t* xp = reinterpret_cast<uint16_t*>(a.y_part);   // scratch: [T*k][Hd] bf16
   CUtensorMap tm13, tm2;
@@ -1057,12 +1059,6 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
   static const int ks_env = getenv("DYMOE_PREFILL_W2_KSPLIT") ? atoi(getenv("DYMOE_PREFILL_W2_KSPLIT")) : 0;
   const int ksplit = ks_env > 0 ? ks_env : (a.F / BK >= 64 ? 2 : 1);
   if (operand_swapped) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_prefill_ts<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts::kSmemT);
-      cudaFuncSetAttribute(k_prefill_ts<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts::kSmemT);
-      attr = true;
-    }
     // token tiles: this CTA's ts::NT / 2 rows of 64 k per TMA box
     CUtensorMap tb13, tb2;
     if (!encode_tmap_2d(&tb13, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xp, a.Hd, rows, (uint64_t)a.Hd * 2,
@@ -1093,6 +1089,11 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
   if (e != cudaSuccess) return e;
   record_ev(ev, 2, s);
   return cudaSuccess;
+}
+
+cudaError_t preload_ffn_prefill() {
+  return preload_kernels(k_gather_perm, pf::k_prefill_gemm<true>, pf::k_prefill_gemm<false>,
+                         pf::k_prefill_ts<true>, pf::k_prefill_ts<false>);
 }
 
 }  // namespace dymoe

@@ -221,17 +221,32 @@ __device__ __forceinline__ void permute(const int32_t* topk_idx, int T, int k, i
     if (keep[e]) atomicAdd(&running[e], 1);
   }
   __syncthreads();
-  if (tid == 0) {   // exclusive scan of the counts (M <= 256), active list
-    int acc = 0, na = 0;
-    for (int e = 0; e < M; ++e) {
+  if (tid < 32) {   // exclusive scan of the counts (M <= 256) and the active list, one warp
+    const int per = (M + 31) / 32;
+    const int e0 = lane * per, e1 = min(M, e0 + per);
+    int sum = 0, nz = 0;
+    for (int e = e0; e < e1; ++e) {
+      sum += running[e];
+      nz += running[e] > 0;
+    }
+    int is = sum, in = nz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int vs = __shfl_up_sync(0xffffffffu, is, o), vn = __shfl_up_sync(0xffffffffu, in, o);
+      if (lane >= o) { is += vs; in += vn; }
+    }
+    int acc = is - sum, na = in - nz;
+    for (int e = e0; e < e1; ++e) {
       const int c = running[e];
       expert_off[e] = acc;
       running[e] = acc;
       if (c > 0) active_list[1 + na++] = e;
       acc += c;
     }
-    expert_off[M] = acc;
-    active_list[0] = na;
+    if (lane == 31) {
+      expert_off[M] = acc;
+      active_list[0] = na;
+    }
   }
   __syncthreads();
   for (int c0 = 0; c0 < P; c0 += NT) {   // stable placement, chunk by chunk

@@ -52,4 +52,6 @@ cudaError_t launch_rmsnorm(const uint16_t* x, int T, int Hd, float eps, uint16_t
   return cudaGetLastError();
 }
 
+cudaError_t preload_norm() { return preload_kernels(k_rmsnorm); }
+
 }  // namespace dymoe

@@ -209,4 +209,9 @@ cudaError_t launch_renorm_weights(const int32_t* topk_idx, const float* topk_w, 
   return cudaGetLastError();
 }
 
+cudaError_t preload_permute_combine() {
+  return preload_kernels(k_permute, k_ep_plan, k_gather_rows, k_reduce_parts, k_combine,
+                         k_renorm_weights);
+}
+
 }  // namespace dymoe

@@ -103,4 +103,8 @@ cudaError_t launch_predict_next(int phase, const uint16_t* h, const uint16_t* wg
   return cudaGetLastError();
 }
 
+cudaError_t preload_predict() {
+  return preload_kernels(k_gate_logits, k_predict_counts, k_select_top);
+}
+
 }  // namespace dymoe

@@ -264,13 +264,13 @@ cudaError_t launch_build_meta(const float* scales, const uint8_t* zeros, int N, 
 }
 
 cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaStream_t s) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
+  static const int sms = [] {   // one-time setup, thread-safe (magic static)
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_quantize, cudaFuncAttributeMaxDynamicSharedMemorySize, kQWarps * 2 * kBuf);
-  }
+    return n;
+  }();
   for (int start = 0; start < n_jobs; start += kMaxJobs) {
     QJobs J{};
     J.n = 0;
@@ -297,5 +297,7 @@ cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaSt
   }
   return cudaSuccess;
 }
+
+cudaError_t preload_quantize() { return preload_kernels(k_build_meta, k_quantize); }
 
 }  // namespace dymoe

@@ -90,7 +90,15 @@ k_score_prefill(const float* __restrict__ attn, int H, const int32_t* __restrict
   // 1. token scores, sequential over heads (coalesced over tokens)
   for (int i = tid; i < T; i += kScoreThreads) {
     float acc = attn[i];
-    for (int h = 1; h < H; ++h) acc = __fadd_rn(acc, attn[(size_t)h * T + i]);
+    int h = 1;
+    for (; h + 8 <= H; h += 8) {   // 8 loads in flight, then the adds in head order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = attn[(size_t)(h + u) * T + i];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = __fadd_rn(acc, v[u]);
+    }
+    for (; h < H; ++h) acc = __fadd_rn(acc, attn[(size_t)h * T + i]);
     S[i] = acc;
   }
   for (int j = tid; j < M; j += kScoreThreads) cnt[j] = 0;
@@ -297,6 +305,10 @@ cudaError_t launch_front_decode(const float* logits, int T, int M, int k, const 
                                                    probs, importance, bits, active, expert_off,
                                                    perm_token, perm_slot, inv_row, active_list);
   return cudaGetLastError();
+}
+
+cudaError_t preload_route_score() {
+  return preload_kernels(k_route, k_score_prefill, k_score_decode, k_assign, k_front_decode);
 }
 
 }  // namespace dymoe

@@ -33,7 +33,7 @@ EXPORTED = [
     "dymoe_layer_set_expert", "dymoe_attention_mass", "dymoe_gate_logits",
     "dymoe_rmsnorm", "dymoe_ep_window_bytes", "dymoe_ep_window_alloc", "dymoe_ep_window_open",
     "dymoe_ep_window_close", "dymoe_ep_window_free", "dymoe_ep_publish_counts", "dymoe_ep_barrier",
-    "dymoe_ep_dispatch", "dymoe_ep_combine",
+    "dymoe_ep_dispatch", "dymoe_ep_combine", "dymoe_preload",
 ]
 DYMOE_STATUS_EP_TIMEOUT, DYMOE_STATUS_EP_OVERFLOW = 2, 4
 
@@ -141,6 +141,7 @@ def lib():
             "dymoe_gate_logits": [vp, vp, vp, ci, ci, ci, vp, vp],
             "dymoe_rmsnorm": [vp, ci, ci, ctypes.c_float, vp, vp],
             "dymoe_ep_window_bytes": [ci, ci, ci, ci],
+            "dymoe_preload": [],
             "dymoe_ep_window_alloc": [cz, ctypes.POINTER(vp), vp],
             "dymoe_ep_window_open": [vp, ctypes.POINTER(vp)],
             "dymoe_ep_window_close": [vp],
