@@ -85,7 +85,7 @@ constexpr int kPrefillSmallRows = 16;
 
 struct WsLayout {
   size_t topk_idx, topk_w, probs, importance, heavy, bits, active, active_list, expert_off,
-      perm_token, perm_slot, inv_row, h, y_perm, y_part, status, score_scratch, total;
+      perm_token, perm_slot, inv_row, h, y_perm, y_part, status, score_scratch, perm_scratch, total;
 };
 
 WsLayout ws_layout(int M, int k, int Hd, int F, int T) {
@@ -114,6 +114,7 @@ WsLayout ws_layout(int M, int k, int Hd, int F, int T) {
   L.y_part = take((size_t)decode_w2_slices(F) * TK * Hd * 4);
   L.status = take(4);
   L.score_scratch = take((size_t)T * 4);
+  L.perm_scratch = take(permute_scratch_bytes(T, k, M));
   L.total = o;
   return L;
 }
@@ -538,10 +539,14 @@ int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* b
   }
   // the active list is an internal by-product; use a small temporary
   int32_t* active = nullptr;
+  int32_t* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&active, (M + 1) * sizeof(int32_t), S(stream));
+  if (e == cudaSuccess && T > 0)
+    e = cudaMallocAsync(&scratch, permute_scratch_bytes(T, k, M), S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dymoe_permute");
   e = launch_permute(topk_idx, T, k, M, bits, expert_off, perm_token, perm_slot, inv_row, active,
-                     S(stream));
+                     S(stream), scratch);
+  if (scratch) cudaFreeAsync(scratch, S(stream));
   cudaFreeAsync(active, S(stream));
   if (e != cudaSuccess) return cuda_fail(e, "dymoe_permute");
   return ok();
@@ -925,7 +930,8 @@ int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logi
       bits = v.bits;
     }
     CHECK_LAUNCH(launch_permute(v.topk_idx, T, L->k, L->M, bits, v.expert_off, v.perm_token,
-                                v.perm_slot, v.inv_row, active_list, s),
+                                v.perm_slot, v.inv_row, active_list, s,
+                                reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ws) + W.perm_scratch)),
                  "permute");
   }
   const int mode = o->ffn_mode == -1 ? o->phase : o->ffn_mode;

@@ -106,9 +106,14 @@ cudaError_t launch_front_decode(const float* logits, int T, int M, int k, const 
 
 cudaError_t launch_quantize(const dymoe_quant_job* jobs_host, int n_jobs, cudaStream_t s);
 
+// scratch (nullable, permute_scratch_bytes): with it, pair lists of more than
+// kPermMultiMinChunks chunks of 1024 pairs take the multi-CTA path (same arrays, bit for bit).
+constexpr int kPermMultiMinChunks = 4;
+size_t permute_scratch_bytes(int T, int k, int M);
 cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
                            int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot,
-                           int32_t* inv_row, int32_t* active_list, cudaStream_t s);
+                           int32_t* inv_row, int32_t* active_list, cudaStream_t s,
+                           int32_t* scratch = nullptr);
 
 struct FfnArgs {
   const DevExpert* experts;

@@ -27,9 +27,123 @@ k_permute(const int32_t* __restrict__ topk_idx, int T, int k, int M,
                  running, warp_cnt, keep);
 }
 
+// Multi-CTA permute for long pair lists: the single-CTA kernel walks its token-major chunks of
+// kPermThreads pairs one after another; here chunk c is CTA c.  k_perm_count: per-chunk expert
+// counts; k_perm_scan: per expert, the exclusive prefix over chunks plus the expert offset (one
+// CTA; the expert scan and active list exactly as front::permute); k_perm_place: the body of one
+// iteration of front::permute's chunk loop with running[] = that prefix.  Same placement order
+// (chunk, warp, lane), so the same arrays bit for bit.
+__global__ void __launch_bounds__(kPermThreads)
+k_perm_count(const int32_t* __restrict__ topk_idx, int P, int M, const uint8_t* __restrict__ bits,
+             int32_t* __restrict__ cnt) {
+  __shared__ int c_sh[DYMOE_MAX_EXPERTS];
+  for (int e = threadIdx.x; e < M; e += kPermThreads) c_sh[e] = 0;
+  __syncthreads();
+  const int p = blockIdx.x * kPermThreads + threadIdx.x;
+  if (p < P) {
+    const int e = topk_idx[p];
+    if (bits[e] != 0) atomicAdd(&c_sh[e], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < M; e += kPermThreads) cnt[(size_t)blockIdx.x * M + e] = c_sh[e];
+}
+
+__global__ void __launch_bounds__(256)
+k_perm_scan(int G, int M, int32_t* __restrict__ cnt, int32_t* __restrict__ expert_off,
+            int32_t* __restrict__ active_list) {
+  __shared__ int tot[DYMOE_MAX_EXPERTS];
+  for (int e = threadIdx.x; e < M; e += blockDim.x) {
+    int acc = 0;
+    for (int c = 0; c < G; ++c) {
+      const int v = cnt[(size_t)c * M + e];
+      cnt[(size_t)c * M + e] = acc;
+      acc += v;
+    }
+    tot[e] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int per = (M + 31) / 32;
+    const int e0 = lane * per, e1 = min(M, e0 + per);
+    int sum = 0, nz = 0;
+    for (int e = e0; e < e1; ++e) {
+      sum += tot[e];
+      nz += tot[e] > 0;
+    }
+    int is = sum, in = nz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int vs = __shfl_up_sync(0xffffffffu, is, o), vn = __shfl_up_sync(0xffffffffu, in, o);
+      if (lane >= o) { is += vs; in += vn; }
+    }
+    int acc = is - sum, na = in - nz;
+    for (int e = e0; e < e1; ++e) {
+      const int c = tot[e];
+      expert_off[e] = acc;
+      tot[e] = acc;   // now the expert's first row
+      if (c > 0) active_list[1 + na++] = e;
+      acc += c;
+    }
+    if (lane == 31) {
+      expert_off[M] = acc;
+      active_list[0] = na;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < M; e += blockDim.x)
+    for (int c = 0; c < G; ++c) cnt[(size_t)c * M + e] += tot[e];
+}
+
+__global__ void __launch_bounds__(kPermThreads)
+k_perm_place(const int32_t* __restrict__ topk_idx, int T, int k, int M,
+             const uint8_t* __restrict__ bits, const int32_t* __restrict__ base,
+             int32_t* __restrict__ perm_token, int32_t* __restrict__ perm_slot,
+             int32_t* __restrict__ inv_row) {
+  __shared__ int warp_cnt[kPermWarps * DYMOE_MAX_EXPERTS];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int P = T * k;
+  for (int q = tid; q < kPermWarps * M; q += kPermThreads)
+    warp_cnt[(q / M) * DYMOE_MAX_EXPERTS + (q % M)] = 0;
+  __syncthreads();
+  const int p = blockIdx.x * kPermThreads + tid;
+  int e = -1;
+  if (p < P) {
+    e = topk_idx[p];
+    if (bits[e] == 0) {
+      inv_row[p] = -1;
+      e = -1;
+    }
+  }
+  const unsigned peers = __match_any_sync(0xffffffffu, e);
+  const int rank_in_warp = __popc(peers & ((1u << lane) - 1u));
+  if (e >= 0 && rank_in_warp == 0) warp_cnt[w * DYMOE_MAX_EXPERTS + e] = __popc(peers);
+  __syncthreads();
+  if (e >= 0) {
+    int r = base[(size_t)blockIdx.x * M + e] + rank_in_warp;
+    for (int q = 0; q < w; ++q) r += warp_cnt[q * DYMOE_MAX_EXPERTS + e];
+    perm_token[r] = p / k;
+    perm_slot[r] = p - (p / k) * k;
+    inv_row[p] = r;
+  }
+}
+
+size_t permute_scratch_bytes(int T, int k, int M) {
+  return (size_t)((T * k + kPermThreads - 1) / kPermThreads) * M * sizeof(int32_t);
+}
+
 cudaError_t launch_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
                            int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot,
-                           int32_t* inv_row, int32_t* active_list, cudaStream_t s) {
+                           int32_t* inv_row, int32_t* active_list, cudaStream_t s,
+                           int32_t* scratch) {
+  const int G = (T * k + kPermThreads - 1) / kPermThreads;
+  if (scratch != nullptr && G > kPermMultiMinChunks) {
+    k_perm_count<<<G, kPermThreads, 0, s>>>(topk_idx, T * k, M, bits, scratch);
+    k_perm_scan<<<1, 256, 0, s>>>(G, M, scratch, expert_off, active_list);
+    k_perm_place<<<G, kPermThreads, 0, s>>>(topk_idx, T, k, M, bits, scratch, perm_token,
+                                            perm_slot, inv_row);
+    return cudaGetLastError();
+  }
   k_permute<<<1, kPermThreads, 0, s>>>(topk_idx, T, k, M, bits, expert_off, perm_token,
                                        perm_slot, inv_row, active_list);
   return cudaGetLastError();
@@ -210,7 +324,7 @@ cudaError_t launch_renorm_weights(const int32_t* topk_idx, const float* topk_w, 
 }
 
 cudaError_t preload_permute_combine() {
-  return preload_kernels(k_permute, k_ep_plan, k_gather_rows, k_reduce_parts, k_combine,
+  return preload_kernels(k_permute, k_perm_count, k_perm_scan, k_perm_place, k_ep_plan, k_gather_rows, k_reduce_parts, k_combine,
                          k_renorm_weights);
 }
 

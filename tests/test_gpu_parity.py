@@ -146,7 +146,8 @@ def test_quantize_batched_mixed_jobs():
 
 
 # ------------------------------------------------------------------------------------ permute / combine
-@pytest.mark.parametrize("T,M,k", [(1, 8, 2), (16, 8, 2), (2048, 8, 2), (1500, 64, 6), (3, 256, 8), (0, 8, 2)])
+@pytest.mark.parametrize("T,M,k", [(1, 8, 2), (16, 8, 2), (2048, 8, 2), (1500, 64, 6), (3, 256, 8), (0, 8, 2),
+                                   (2048, 64, 6), (4096, 8, 2), (6000, 256, 8), (2561, 8, 2)])
 def test_permute(T, M, k):
     d = D()
     rng = np.random.default_rng(T + M)
