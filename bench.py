@@ -467,6 +467,58 @@ def run_ep(args, rank, world, device):
     value = T * K * world / (ms / 1e3)
     ffn_events = list(ops.events)
 
+    # ---------------- the same weak-scaling steps with dispatch / combine over peer memory
+    # (forward_p2p: fused gather+store and pull+combine kernels, flag barriers).  It
+    # is the main line when it runs clean on every rank; the NCCL all-to-all line is kept beside it
+    p2p, win = None, None
+    nccl_ms = ms
+    try:
+        gloo = torch.distributed.get_backend() != "nccl"
+        win = ep.PeerWindows(comm, cfg.M, cfg.hidden, T * cfg.k * world,
+                             barrier="host" if gloo else "device", device=device)
+
+        def p2p_step(i, x=None, lg=None, a=None):
+            if x is None:
+                x, lg, a = inputs[i % n_inputs]
+            return shards[i % len(shards)].forward_p2p(win, x, lg, ladder, i % NUM_LAYERS, NUM_LAYERS,
+                                                       phase, attn_mass=a)
+
+        p2p_step(0)   # one step, then check every rank's status before timing anything
+        torch.cuda.synchronize()
+        st = torch.tensor([float(win.status.item())], device=device if not gloo else "cpu",
+                          dtype=torch.float64)
+        torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.MAX)
+        if st.item() != 0:
+            raise RuntimeError("peer-memory step reported status %d" % int(st.item()))
+        for i in range(1, args.warmup):
+            p2p_step(i)
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(torch.cuda.current_device()) as clk_p2p:
+            q0.record()
+            for i in range(K):
+                p2p_step(args.warmup + i)
+            q1.record()
+            torch.cuda.synchronize()
+        torch.distributed.barrier()
+        qms = _max_over_ranks(q0.elapsed_time(q1), device)
+        st = torch.tensor([float(win.status.item())], device=device if not gloo else "cpu",
+                          dtype=torch.float64)
+        torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.MAX)
+        p2p = {"value": T * K * world / (qms / 1e3), "unit": "tokens/s", "ms_per_step": qms / K,
+               "scaling": "weak", "barrier": win.barrier_mode, "status": int(st.item()),
+               "note": "dymoe_ep_dispatch / dymoe_ep_combine over peer windows (CUDA IPC), "
+                       "no NCCL on the data path; 3 flag barriers + 1 count read per step"}
+    except Exception as ex:   # reported, never fatal for the NCCL line
+        p2p = {"error": "%s: %s" % (type(ex).__name__, str(ex)[:300])}
+    use_p2p = p2p is not None and "error" not in p2p and p2p["status"] == 0 and \
+        args.ep_main != "nccl" and (torch.distributed.get_backend() == "nccl" or args.ep_main == "p2p")
+    nccl_line = {"value": value, "unit": "tokens/s", "ms_per_step": nccl_ms / K, "scaling": "weak",
+                 "note": "NCCL all_to_all_single dispatch / combine (counts exchanged first)"}
+    if use_p2p:
+        ms, value, clk = qms, p2p["value"], clk_p2p
+
     # ---------------- end-to-end: per step the rank's inputs come from pinned host memory and
     # its output goes back to the host, inside the timed region
     hx = [inp[0].cpu().pin_memory() for inp in inputs]
@@ -486,14 +538,21 @@ def run_ep(args, rank, world, device):
         dl.copy_(hl[j], non_blocking=True)
         if phase == d.DYMOE_PREFILL:
             da.copy_(ha[j], non_blocking=True)
-        y, _ = shards[(args.warmup + i) % len(shards)].forward(
-            dx, dl, ladder, (args.warmup + i) % NUM_LAYERS, NUM_LAYERS, phase, attn_mass=da)
+        if use_p2p:
+            y, _ = p2p_step(args.warmup + i, dx, dl, da)
+        else:
+            y, _ = shards[(args.warmup + i) % len(shards)].forward(
+                dx, dl, ladder, (args.warmup + i) % NUM_LAYERS, NUM_LAYERS, phase, attn_mass=da)
         hy.copy_(y, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
     torch.distributed.barrier()
     e2e = {"value": T * K * world / (_max_over_ranks(e0.elapsed_time(e1), device) / 1e3), "unit": "tokens/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    if win is not None:
+        torch.distributed.barrier()
+        win.close()
 
     # ---------------- decode, batch replicated on every rank (SURVEY §8e latency variant):
     # the same B tokens everywhere, local experts, one all-reduce of y; strong scaling of one batch
@@ -518,41 +577,6 @@ def run_ep(args, rank, world, device):
         rep = {"value": T * K / (rms / 1e3), "unit": "tokens/s", "ms_per_step": rms / K,
                "scaling": "strong", "global_batch": T,
                "note": "the same %d-token batch on every rank; local experts + all-reduce(sum) of y" % T}
-
-    # ---------------- the same weak-scaling steps with dispatch / combine over peer memory
-    # (forward_p2p: fused gather+store and pull+combine kernels, flag barriers)
-    p2p = None
-    try:
-        gloo = torch.distributed.get_backend() != "nccl"
-        win = ep.PeerWindows(comm, cfg.M, cfg.hidden, T * cfg.k * world,
-                             barrier="host" if gloo else "device", device=device)
-
-        def p2p_step(i):
-            x, lg, a = inputs[i % n_inputs]
-            return shards[i % len(shards)].forward_p2p(win, x, lg, ladder, i % NUM_LAYERS, NUM_LAYERS,
-                                                       phase, attn_mass=a)
-
-        for i in range(args.warmup):
-            p2p_step(i)
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.distributed.barrier()
-        torch.cuda.synchronize()
-        q0.record()
-        for i in range(K):
-            p2p_step(args.warmup + i)
-        q1.record()
-        torch.cuda.synchronize()
-        torch.distributed.barrier()
-        qms = _max_over_ranks(q0.elapsed_time(q1), device)
-        st = int(win.status.item())
-        torch.distributed.barrier()
-        win.close()
-        p2p = {"value": T * K * world / (qms / 1e3), "unit": "tokens/s", "ms_per_step": qms / K,
-               "scaling": "weak", "barrier": win.barrier_mode, "status": st,
-               "note": "dymoe_ep_dispatch / dymoe_ep_combine over peer windows (CUDA IPC), "
-                       "no NCCL on the data path; 3 flag barriers + 1 count read per step"}
-    except Exception as ex:   # reported, never fatal for the main line
-        p2p = {"error": "%s: %s" % (type(ex).__name__, str(ex)[:300])}
 
     # local FFN roofline (bytes of the local experts actually streamed / FFN time)
     ffn_ms, ffn_bytes, ffn_flops = 0.0, 0.0, 0.0
@@ -589,13 +613,15 @@ def run_ep(args, rank, world, device):
                           "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
                           "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
                           "weight_copies": args.copies, "l2": "inputs larger than L2 (rotating weight copies)",
-                          "parallelism": "ep%d (experts sharded, NCCL all-to-all dispatch/combine)" % world},
+                          "parallelism": ("ep%d (experts sharded, peer-memory dispatch/combine kernels)" % world)
+                          if use_p2p else ("ep%d (experts sharded, NCCL all-to-all dispatch/combine)" % world)},
                "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
                # libdymoe launches per step and rank: route, score, assign, permute, ep_plan,
                # gather_rows, local permute, active list, W13, W2, reduce / prefill gather,
                # unit-weight reorder, weighted combine (NCCL collectives not counted)
-               "gpu_launches": 13 * K,
-               "ep_replicated_decode": rep, "ep_p2p": p2p}
+               "gpu_launches": (15 if use_p2p else 13) * K,
+               "ep_path": "p2p" if use_p2p else "nccl_all_to_all",
+               "ep_replicated_decode": rep, "ep_p2p": p2p, "ep_nccl_all_to_all": nccl_line}
     return res
 
 
@@ -928,6 +954,9 @@ def main():
                          "(default), ts = the experimental operand-swapped kernel (weights in TMEM)")
     ap.add_argument("--no-graph", action="store_true", help="time the steps call by call instead "
                     "of replaying their CUDA graph (single-GPU decode / prefill / stack workloads)")
+    ap.add_argument("--ep-main", default="auto", choices=["auto", "nccl", "p2p"],
+                    help="N > 1: the main line's dispatch/combine path (auto: the peer-memory path "
+                         "when it runs clean under NCCL, else the NCCL all-to-all)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test hook for several ranks sharing one GPU (collectives staged "
                          "through host memory); never used for reported numbers")

@@ -351,7 +351,7 @@ int dymoe_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n, uin
  *   (peers[rank] = own window).
  * Barrier: thread p stores `epoch` into flags[rank] of window p (release, system scope), then
  * waits until every flags[src] of its own window is >= epoch (acquire, system scope).  The
- * caller increments epoch by one per barrier call on every rank.  A wait longer than ~10 s sets
+ * caller increments epoch by one per barrier call on every rank.  A wait longer than ~5 s sets
  * DYMOE_STATUS_EP_TIMEOUT in *status (nullable) and returns (never hangs the device).
  * Window memory: dymoe_ep_window_alloc (cudaMalloc, zeroed; ipc_handle receives the 64-byte
  * cudaIpcMemHandle_t, nullable), dymoe_ep_window_open (cudaIpcOpenMemHandle with lazy peer

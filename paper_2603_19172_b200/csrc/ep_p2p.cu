@@ -16,7 +16,7 @@
 namespace {
 
 constexpr int kMaxP = 64;
-constexpr unsigned long long kBarrierTimeoutNs = 10ull * 1000 * 1000 * 1000;
+constexpr unsigned long long kBarrierTimeoutNs = 5ull * 1000 * 1000 * 1000;
 
 struct WinLayout {
   size_t flags, cnt, recv_x, y_out, total;

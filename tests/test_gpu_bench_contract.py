@@ -68,3 +68,18 @@ def test_ep_two_ranks_line_with_p2p():
     p = j["ep_p2p"]
     assert "error" not in p, p
     assert p["value"] > 0 and p["status"] == 0 and p["barrier"] == "host"
+
+
+def test_ep_two_ranks_p2p_main_line():
+    """The N = 2 main line on the peer-memory path (forced under the gloo test hook), e2e included."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29643", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--dist-backend", "gloo", "--steps", "3", "--warmup", "3", "--copies", "1",
+           "--ep-main", "p2p", "--workload", "finegrained", "--tokens", "256"]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    j = json.loads(lines[0])
+    assert j["ep_path"] == "p2p" and j["value"] == j["ep_p2p"]["value"] and j["e2e"]["value"] > 0
+    assert j["ep_nccl_all_to_all"]["value"] > 0 and "peer-memory" in j["config"]["parallelism"]
