@@ -29,3 +29,16 @@ def test_algorithmic_flops_counts_executed_pairs_only():
     bits = np.array([8, 0, 2, 16], np.uint8)
     off = np.array([0, 2, 3, 3, 6])
     assert bench.algorithmic_flops(cfg, off, bits) == 6.0 * 256 * 512 * (2 + 0 + 0 + 3)
+
+
+def test_workload_configs_match_baseline_configs():
+    """bench.py workloads -> BASELINE.json configs: [1] Mixtral decode (B tokens), [2] Mixtral
+    prefill 2048, [3]'s fine-grained layer (64 experts, top-6, hidden 2048, ffn 1408)."""
+    import argparse
+    for w, (M, k, Hd, F, T, dec, name) in {
+            "decode": (8, 2, 4096, 14336, 8, True, "mixtral_decode"),
+            "prefill": (8, 2, 4096, 14336, 2048, False, "mixtral_prefill"),
+            "finegrained": (64, 6, 2048, 1408, 2048, False, "finegrained_prefill"),
+            "finegrained_decode": (64, 6, 2048, 1408, 8, True, "finegrained_decode")}.items():
+        cfg, is_dec, wname = bench.workload_cfg(argparse.Namespace(workload=w, batch=8, tokens=2048))
+        assert (cfg.M, cfg.k, cfg.hidden, cfg.ffn, cfg.T, is_dec, wname) == (M, k, Hd, F, T, dec, name)

@@ -4,7 +4,7 @@ import torch, bench, synthetic
 import paper_2603_19172_b200.dymoe as d
 from torch.profiler import profile, ProfilerActivity
 dev = torch.device("cuda", 0)
-cfg = synthetic.CONFIGS["mixtral_decode"].with_tokens(8)
+cfg = synthetic.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "mixtral_decode"].with_tokens(8)
 (layer, _), = bench.build_layer_copies(d, cfg, 1, dev)
 inputs = bench.step_inputs(cfg, 4, dev)
 ws = layer.workspace(8, dev)
@@ -36,17 +36,17 @@ print("per step %.1f us" % span)
 # the front's phases as standalone kernels (same bodies), warm, for attribution
 x, lg, a = inputs[0]
 for i in range(5):
-    idx, w, pr = d.dymoe_route(lg, 2)
-    imp, _ = d.dymoe_score(d.DYMOE_DECODE, 8, logits=lg)
-    bits, _ = d.dymoe_assign_bits(imp, 20, 32, lad, 2)
-    d.dymoe_permute(idx, 8, bits)
+    idx, w, pr = d.dymoe_route(lg, cfg.k)
+    imp, _ = d.dymoe_score(d.DYMOE_DECODE, cfg.M, logits=lg)
+    bits, _ = d.dymoe_assign_bits(imp, 20, 32, lad, cfg.k)
+    d.dymoe_permute(idx, cfg.M, bits)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA]) as p2:
     for i in range(20):
-        idx, w, pr = d.dymoe_route(lg, 2)
-        imp, _ = d.dymoe_score(d.DYMOE_DECODE, 8, logits=lg)
-        bits, _ = d.dymoe_assign_bits(imp, 20, 32, lad, 2)
-        d.dymoe_permute(idx, 8, bits)
+        idx, w, pr = d.dymoe_route(lg, cfg.k)
+        imp, _ = d.dymoe_score(d.DYMOE_DECODE, cfg.M, logits=lg)
+        bits, _ = d.dymoe_assign_bits(imp, 20, 32, lad, cfg.k)
+        d.dymoe_permute(idx, cfg.M, bits)
     torch.cuda.synchronize()
 dur = collections.defaultdict(list)
 for e in p2.events():
