@@ -189,8 +189,8 @@ struct AllocScratch {
 // with every expert forced to one width (tools/decode_width_sweep.py): the narrow widths are
 // bound by dequant issue slots rather than bytes, so they cost more than their bytes suggest.
 __device__ __forceinline__ int wcost(int b, bool w13) {
-  if (w13) return b == 16 ? 256 : b == 8 ? 172 : b == 4 ? 118 : 107;
-  return b == 16 ? 256 : b == 8 ? 196 : b == 4 ? 144 : 131;
+  if (w13) return b == 16 ? 256 : b == 8 ? 167 : b == 4 ? 116 : 103;
+  return b == 16 ? 256 : b == 8 ? 180 : b == 4 ? 133 : 129;
 }
 
 // Cost-proportional allocation of `units_total` units to the active experts, every active
