@@ -575,7 +575,12 @@ int decode_w2_slice_k(int F) {
   // K = F is split into the fewest slices of <= 4096 (x slice of 8 tokens <= 64 KB of shared
   // memory), equal up to a multiple of 512: long slices keep all 8 warps of a group busy even at
   // Int2 (512 k per 128-byte item) and keep the fp32 partial traffic small.
-  const int sk = (F + 4095) / 4096;
+  static const int max_k = [] {   // DYMOE_DECODE_W2_SLICE_MAX overrides (measurement knob)
+    const char* v = getenv("DYMOE_DECODE_W2_SLICE_MAX");
+    const int m = v ? atoi(v) : 4096;
+    return m >= 512 && m <= 4096 ? m : 4096;
+  }();
+  const int sk = (F + max_k - 1) / max_k;
   const int per = (F + sk - 1) / sk;
   return (per + 511) / 512 * 512;
 }
