@@ -49,10 +49,16 @@ __device__ __forceinline__ int32_t* cnt_of(const WinArgs& a, int p) {
 }
 
 // Row layout of the step (computed from this rank's own, complete count matrix):
-//   row0[e] = row of this rank's first pair of expert e in the owner's recv_x
-//           = sum_{owner's experts e' < e} sum_src cnt[src][e'] + sum_{src < rank} cnt[src][e]
-//   base[e] = sum_{owner's experts e' < e} sum_src cnt[src][e'] (expert e's first row there).
-__device__ void ep_layout(const WinArgs& a, int* s_row0, int* s_base, int* s_tot) {
+//   tot[e]  = sum_src cnt[src][e];  gex[e] = sum_{e' < e} tot[e'] (global exclusive prefix)
+//   base(e) = gex[e] - gex[first expert of owner(e)]  (expert e's first row in its owner's recv_x)
+//   row0[e] = base(e) + sum_{src < rank} cnt[src][e]   (this rank's first row of expert e there)
+// The prefix is one warp scan over contiguous blocks of experts (owners hold contiguous expert
+// blocks, so a per-owner base is a difference of the global prefix).
+__device__ __forceinline__ int first_of_owner(int o, int M, int P) {
+  return (int)(((long long)o * M + P - 1) / P);
+}
+
+__device__ void ep_layout(const WinArgs& a, int* s_row0, int* s_gex, int* s_tot) {
   const int32_t* cnt = cnt_of(a, a.rank);
   for (int e = threadIdx.x; e < a.M; e += blockDim.x) {
     int tot = 0, pre = 0;
@@ -65,16 +71,27 @@ __device__ void ep_layout(const WinArgs& a, int* s_row0, int* s_base, int* s_tot
     s_row0[e] = pre;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int running = 0;
-    for (int x = 0; x < a.M; ++x) {
-      if (x == 0 || owner_of(x, a.M, a.P) != owner_of(x - 1, a.M, a.P)) running = 0;
-      s_base[x] = running;
-      running += s_tot[x];
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int per = (a.M + 31) / 32;
+    const int e0 = lane * per, e1 = min(a.M, e0 + per);
+    int sum = 0;
+    for (int e = e0; e < e1; ++e) sum += s_tot[e];
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int acc = incl - sum;
+    for (int e = e0; e < e1; ++e) {
+      s_gex[e] = acc;
+      acc += s_tot[e];
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < a.M; e += blockDim.x) s_row0[e] += s_base[e];
+  for (int e = threadIdx.x; e < a.M; e += blockDim.x)
+    s_row0[e] += s_gex[e] - s_gex[first_of_owner(owner_of(e, a.M, a.P), a.M, a.P)];
   __syncthreads();
 }
 
@@ -125,17 +142,17 @@ __global__ void __launch_bounds__(256) k_ep_dispatch(WinArgs a, const uint4* __r
                                                       const int32_t* __restrict__ perm_token,
                                                       int32_t* __restrict__ recv_off,
                                                       uint32_t* status) {
-  __shared__ int s_row0[DYMOE_MAX_EXPERTS], s_base[DYMOE_MAX_EXPERTS], s_tot[DYMOE_MAX_EXPERTS];
+  __shared__ int s_row0[DYMOE_MAX_EXPERTS], s_gex[DYMOE_MAX_EXPERTS], s_tot[DYMOE_MAX_EXPERTS];
   __shared__ int s_off[DYMOE_MAX_EXPERTS + 1];
-  ep_layout(a, s_row0, s_base, s_tot);
+  ep_layout(a, s_row0, s_gex, s_tot);
   for (int e = threadIdx.x; e <= a.M; e += blockDim.x) s_off[e] = off[e];
   if (blockIdx.x == 0) {
     // local experts' offsets in this rank's own recv_x (the receiver side of the same layout)
-    const int first = (int)(((long long)a.rank * a.M + a.P - 1) / a.P);
-    const int last = (int)(((long long)(a.rank + 1) * a.M + a.P - 1) / a.P);
+    const int first = first_of_owner(a.rank, a.M, a.P);
+    const int last = first_of_owner(a.rank + 1, a.M, a.P);
     for (int i = threadIdx.x; i <= last - first; i += blockDim.x)
-      recv_off[i] = i < last - first ? s_base[first + i]
-                                     : (last > first ? s_base[last - 1] + s_tot[last - 1] : 0);
+      recv_off[i] = i < last - first ? s_gex[first + i] - s_gex[first]
+                                     : (last > first ? s_gex[last - 1] + s_tot[last - 1] - s_gex[first] : 0);
   }
   __syncthreads();
   const int R = s_off[a.M];
@@ -160,8 +177,10 @@ __global__ void __launch_bounds__(128) k_ep_combine(WinArgs a, const int32_t* __
                                                      const float* __restrict__ topk_w, int k,
                                                      const int32_t* __restrict__ off, int renorm,
                                                      int out_bf16, void* __restrict__ y) {
-  __shared__ int s_row0[DYMOE_MAX_EXPERTS], s_base[DYMOE_MAX_EXPERTS], s_tot[DYMOE_MAX_EXPERTS];
-  ep_layout(a, s_row0, s_base, s_tot);
+  __shared__ int s_row0[DYMOE_MAX_EXPERTS], s_gex[DYMOE_MAX_EXPERTS], s_tot[DYMOE_MAX_EXPERTS];
+  __shared__ int s_off[DYMOE_MAX_EXPERTS + 1];
+  for (int e = threadIdx.x; e <= a.M; e += blockDim.x) s_off[e] = off[e];
+  ep_layout(a, s_row0, s_gex, s_tot);   // ends with a barrier: s_off is visible below
   const int t = blockIdx.x;
   const float* src[8];
   float wt[8];
@@ -172,8 +191,8 @@ __global__ void __launch_bounds__(128) k_ep_combine(WinArgs a, const int32_t* __
     src[s] = nullptr;
     if (j >= 0) {
       denom += wt[s];
-      const int e = expert_of_row(off, a.M, j);
-      const int row = s_row0[e] + (j - off[e]);
+      const int e = expert_of_row(s_off, a.M, j);
+      const int row = s_row0[e] + (j - s_off[e]);
       src[s] = reinterpret_cast<const float*>(a.peers[owner_of(e, a.M, a.P)] + a.L.y_out) +
                (size_t)row * a.Hd;
     }
