@@ -255,13 +255,30 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
   // blockIdx.y splits Hd so that a small decode batch still spreads over many SMs
   for (int c = (blockIdx.y * blockDim.x + threadIdx.x) * 4; c < Hd; c += gridDim.y * blockDim.x * 4) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < k; ++s) {
-      if (rows[s] < 0) continue;
-      const float4 v = load_row(y_perm, n_parts, part_stride, rows[s], Hd, c);
-      acc.x = __fadd_rn(acc.x, __fmul_rn(wt[s], v.x));
-      acc.y = __fadd_rn(acc.y, __fmul_rn(wt[s], v.y));
-      acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], v.z));
-      acc.w = __fadd_rn(acc.w, __fmul_rn(wt[s], v.w));
+    if (n_parts == 1) {
+      // every live slot's row loaded first (k loads in flight), then summed in slot order
+      float4 v[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < k && rows[s] >= 0)
+          v[s] = *reinterpret_cast<const float4*>(y_perm + (size_t)rows[s] * Hd + c);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {
+        if (s >= k || rows[s] < 0) continue;
+        acc.x = __fadd_rn(acc.x, __fmul_rn(wt[s], v[s].x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(wt[s], v[s].y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], v[s].z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(wt[s], v[s].w));
+      }
+    } else {
+      for (int s = 0; s < k; ++s) {
+        if (rows[s] < 0) continue;
+        const float4 v = load_row(y_perm, n_parts, part_stride, rows[s], Hd, c);
+        acc.x = __fadd_rn(acc.x, __fmul_rn(wt[s], v.x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(wt[s], v.y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], v.z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(wt[s], v.w));
+      }
     }
     if (residual != nullptr) {   // x_{l+1} = x_l + y_l (one fp32 add), rounded below if bf16
       const uint2 r = *reinterpret_cast<const uint2*>(residual + (size_t)t * Hd + c);
