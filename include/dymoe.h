@@ -258,8 +258,8 @@ int dymoe_attention_mass(const uint16_t* q, const uint16_t* k, int H, int T, int
                          float* scratch, float* a_out, dymoe_stream_t stream);
 
 /* Look-ahead prediction of the next layer's experts (PAPER.md "Phase-Adaptive
- * Prefetcher", Eqs. 6-8).  Eq. 6: logits = h · W_g^(l+1)^T (fp32 in the order of
- * reading P1: 32 lane partial sums over 8-element chunks, then an xor butterfly), g_hat = softmax.  PREFILL (Eq. 7): c_e = #{tokens whose top-k_route
+ * Prefetcher", Eqs. 6-8).  Eq. 6: logits = h · W_g^(l+1)^T evaluated in fp32 with the
+ * accuracy of dymoe_gate_logits (below), g_hat = softmax.  PREFILL (Eq. 7): c_e = #{tokens whose top-k_route
  * predicted experts contain e}; requests = the t experts with the largest c_e (> 0), priority =
  * c_e.  DECODE (Eq. 8): requests = top-t of the predicted decode importance (B = 1: the predicted
  * logit row; B > 1: sum over the batch of g_hat), priority = that value.  Order: (value desc,
@@ -277,10 +277,14 @@ int dymoe_predict_next(int phase, const uint16_t* h, const uint16_t* w_gate_next
 
 /* Router / gate logits (P:111 router; the gate product of Eq. 6, reading P1):
  *   logits[t][e] = h[t] · w_gate[e] + bias[e],
- * the dot product in fp32 in the order of reading P1 (32 lane partial sums over 8-element chunks,
- * sequential within a lane, one rounding per multiply-add -- bf16 products are exact -- then an
- * xor butterfly), then one fp32 add of bias[e] (bias nullable = 0).  Used to route each layer of a
- * stack from its own hidden state on the device.
+ * the dot product accumulated in fp32 (bf16 x bf16 products are exact in fp32) so that every
+ * partial sum passes through at most Hd/32 + 5 roundings, then one fp32 add of bias[e] (bias
+ * nullable = 0).  Accuracy contract (reading P1: Eq. 6 fixes the value, not an order):
+ *   |logits - exact| <= gamma_(Hd/32+5) · sum_k |h[t][k] w[e][k]|  (+ 2^-24 |logit| with a bias),
+ *   gamma_n = n 2^-24 / (1 - n 2^-24); a top-k taken from these logits is therefore the exact
+ * top-k wherever the margin exceeds twice that bound.  Deterministic: the same inputs give the
+ * same bits on every call.  Used to route each layer of a stack from its own
+ * hidden state on the device.
  *   h [T][Hd] bf16, w_gate [M][Hd] bf16 (Hd multiple of 8, 16-byte aligned), bias [M] f32,
  *   logits [T][M] f32 out; all device.
  * Errors: T < 0, M outside [1, 256], Hd not a positive multiple of 8, NULL or misaligned

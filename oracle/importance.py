@@ -65,7 +65,9 @@ def decode_importance(logits, probs):
 
     B > 1: I[j] = sum_b g[b][j] with g the full softmax (float64 here).
     """
-    logits = np.asarray(logits, dtype=np.float32)
+    logits = np.asarray(logits)
+    if logits.dtype != np.float64:        # float64 = exact gate-product logits (reading P1)
+        logits = logits.astype(np.float32)
     B = logits.shape[0]
     if B == 1:
         return logits[0].astype(np.float64)

@@ -29,11 +29,14 @@ def topk_order(row, k):
 def route(logits, k):
     """Route every token.
 
-    logits: float32 [T, M].  Returns (topk_idx int32 [T,k], topk_w float64 [T,k],
+    logits: float32 [T, M] (float64 is taken as is: the exact router logits of a gate product,
+    reading P1).  Returns (topk_idx int32 [T,k], topk_w float64 [T,k],
     probs float64 [T,M]).  Softmaxes are evaluated in float64 with the max
     subtracted (mathematically identical to the plain definition).
     """
-    logits = np.asarray(logits, dtype=np.float32)
+    logits = np.asarray(logits)
+    if logits.dtype != np.float64:
+        logits = logits.astype(np.float32)
     T, M = logits.shape
     if not (1 <= k <= M):
         raise ValueError("k: must satisfy 1 <= k <= M")

@@ -7,8 +7,8 @@ Per layer l = 0 .. L-1 (attention omitted; a synthetic attention
 a Mixtral block's MoE half on the bf16 residual stream (pre-norm, unit RMSNorm weight):
   u_l      = RNE_bf16(x_l / sqrt(mean(x_l^2) + eps))     RMSNorm (fp64, one rounding);
   logits_l = u_l W_g^(l)T + beta^(l)   the router on the layer's own hidden state: the
-                                       Eq. 6 gate product in the fp32 order of reading P1
-                                       (prefetch.gate_logits), then one fp32 add of the bias;
+                                       Eq. 6 gate product evaluated exactly (prefetch.gate_logits,
+                                       reading P1) plus the bias, in fp64;
   y_l      = moe.moe_forward(u_l, logits_l, experts_l, l, L, ...)   (fp64, the whole layer with
                                        the depth-aware bits of Eq. 4-5 at depth l);
   x_{l+1}  = RNE_bf16(x_l + y_l)       (the residual stream is bf16; x_l + y_l in fp64, one
@@ -28,10 +28,11 @@ from . import prefetch as _prefetch
 
 
 def router_logits(x, w_gate, bias=None):
-    """fp32 [T, M]: prefetch.gate_logits(x, w_gate) (+ bias, one fp32 add per element)."""
+    """float64 [T, M]: the exact router logits x W_g^T + bias (prefetch.gate_logits + bias, fp64;
+    the bias add of two such values is within 2^-53 relative of exact)."""
     lg = _prefetch.gate_logits(x, w_gate)
     if bias is not None:
-        lg = (lg + np.asarray(bias, dtype=np.float32)[None, :]).astype(np.float32)
+        lg = lg + np.asarray(bias, dtype=np.float64)[None, :]
     return lg
 
 
@@ -50,14 +51,15 @@ def residual(x, y):
 
 
 def stack_layer(x, w_gate, bias, experts, l, L, ladder, k_route, phase="decode", attn_mass=None,
-                k_tokens=None, u=None):
+                k_tokens=None, u=None, forced_bits=None):
     """One layer of the stack: returns (x_next float64 [T, Hd] of bf16 values, logits, the
     moe_forward result dict with 'u' added).  u: the normed input to use instead of rmsnorm(x)
-    (teacher forcing in parity tests: the GPU's u, checked separately against rmsnorm(x))."""
+    (teacher forcing in parity tests: the GPU's u, checked separately against rmsnorm(x)).
+    forced_bits: widths to use instead of the schedule's (moe.moe_forward's option)."""
     u = rmsnorm(x) if u is None else np.asarray(u, dtype=np.float64)
-    lg = router_logits(u.astype(np.float32), w_gate, bias)
+    lg = router_logits(u, w_gate, bias)
     out = _moe.moe_forward(u.astype(np.float32), lg, experts, l, L, ladder, k_route, phase=phase,
-                           attn_mass=attn_mass, k_tokens=k_tokens)
+                           attn_mass=attn_mass, k_tokens=k_tokens, forced_bits=forced_bits)
     out["u"] = u
     return residual(x, out["y"]), lg, out
 

@@ -181,7 +181,7 @@ cudaError_t launch_combine(const float* y_perm, int n_parts, int part_rows, cons
                            void* y, cudaStream_t s, const uint16_t* residual = nullptr);
 // u[t] = bf16(x[t] / sqrt(mean(x[t]^2) + eps))  (stack RMSNorm, Hd multiple of 8)
 cudaError_t launch_rmsnorm(const uint16_t* x, int T, int Hd, float eps, uint16_t* u, cudaStream_t s);
-// logits[t][e] = h[t] . wg[e] (fp32, reading P1 order) + bias[e] (nullable)
+// logits[t][e] = h[t] . wg[e] (fp32, accumulation depth <= Hd/32 + 5) + bias[e] (nullable)
 cudaError_t launch_gate_logits(const uint16_t* h, const uint16_t* wg, const float* bias, int T,
                                int Hd, int M, float* logits, cudaStream_t s);
 

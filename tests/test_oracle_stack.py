@@ -2,7 +2,7 @@
 import numpy as np
 import torch
 
-from oracle import stack, prefetch, schedule as sc
+from oracle import stack, schedule as sc
 from oracle.bf16 import round_bf16
 import synthetic
 
@@ -22,16 +22,20 @@ def _gates(cfg, L):
     return out
 
 
-def test_router_bias_is_one_fp32_add():
+def test_router_is_the_exact_affine_map():
     rng = np.random.default_rng(0)
     x = round_bf16(rng.standard_normal((3, 64))).astype(np.float32)
     w = round_bf16(rng.standard_normal((5, 64)) / 8).astype(np.float32)
     b = np.array([0.5, -1.25, 0.0, 3.0, -0.0], np.float32)
-    base = prefetch.gate_logits(x, w)
-    assert np.array_equal(stack.router_logits(x, w, None), base)
+    base = stack.router_logits(x, w, None)
+    assert base.dtype == np.float64
     assert np.array_equal(stack.router_logits(x, w, np.zeros(5, np.float32)), base)
-    assert np.array_equal(stack.router_logits(x, w, b), (base + b).astype(np.float32))
-    # hand case: one nonzero product per entry, exact in fp32, plus the bias
+    # independent: torch fp64 x @ w^T + b (bf16 products exact in fp64, 64 terms: exact sums at
+    # these magnitudes up to 64 * 2^-53 relative)
+    ref = (torch.from_numpy(x).double() @ torch.from_numpy(w).double().T
+           + torch.from_numpy(b).double()).numpy()
+    assert np.allclose(stack.router_logits(x, w, b), ref, rtol=0, atol=1e-13)
+    # hand case: one nonzero product per entry, plus the bias
     xh = np.zeros((1, 64), np.float32)
     xh[0, 3] = 2.0
     wh = np.zeros((2, 64), np.float32)
@@ -99,16 +103,15 @@ def test_dense_bf16_stack_equals_torch_chain():
     for l in range(L):
         ut = torch.from_numpy(round_bf16((xt / torch.sqrt((xt * xt).mean(dim=1, keepdim=True)
                                                            + 1e-5)).numpy()))
-        lg = torch.from_numpy(prefetch.gate_logits(ut.numpy().astype(np.float32), gates[l][0])
-                              + gates[l][1][None, :].astype(np.float32)).double()
+        lg = ut @ torch.from_numpy(gates[l][0]).double().T + torch.from_numpy(gates[l][1]).double()
         p = torch.softmax(lg, dim=1)
         y = torch.zeros_like(xt)
         for e in range(cfg.M):
             W = [torch.from_numpy(ex[l][e][n]).double() for n in ("w1", "w3", "w2")]
             y += p[:, e:e + 1] * _torch_swiglu(ut, *W)
         xt = torch.from_numpy(round_bf16((xt + y).numpy()))
-    # the oracle's router adds the bias in fp32 (one rounding), the chain above in fp32 too; the
-    # mixtures differ only by fp64 summation order -> identical bf16 streams but for rare ties
+    # router logits and mixtures differ from the oracle's only by fp64 summation order ->
+    # identical bf16 streams but for rare rounding ties
     diff = np.abs(xL - xt.numpy())
     ulp = np.abs(xt.numpy()) * 2.0 ** -7 + 1e-30
     assert (diff <= ulp).all() and (diff > 0).mean() < 0.01
