@@ -129,10 +129,10 @@ def build_layer_copies(d, cfg, copies, device):
     return layers
 
 
-def step_inputs(cfg, n, device):
+def step_inputs(cfg, n, device, seed=1000):
     out = []
     for i in range(n):
-        x, lg, a = synthetic.layer_inputs(cfg, 1000 + i, device)
+        x, lg, a = synthetic.layer_inputs(cfg, seed + i, device)
         out.append((x.contiguous(), lg.contiguous(), a.contiguous()))
     return out
 
@@ -168,137 +168,159 @@ def workload_cfg(args):
     return base.with_tokens(T), decode, name
 
 
-def run_ours(args, rank, world, device):
-    import paper_2603_19172_b200.dymoe as d
-    d.lib()
-    torch.cuda.set_device(device)
-    peaks = load_peaks()
-    cfg, is_decode, wname = workload_cfg(args)
-    T = cfg.T
-    phase = d.DYMOE_DECODE if is_decode else d.DYMOE_PREFILL
-    layers = build_layer_copies(d, cfg, args.copies, device)
-    n_inputs = 8
-    inputs = step_inputs(cfg, n_inputs, device)
-    ladder = d.make_ladder(LADDER_BITS, LADDER_LAMBDAS)
-    ws = [L.workspace(T, device) for L, _ in layers]
-    out = torch.empty(T, cfg.hidden, dtype=torch.float32, device=device)
-    stream = torch.cuda.current_stream()
+class LayerTimer:
+    """Times one layer workload on one GPU through dymoe_moe_forward: census of the algorithmic
+    work of every distinct step, W untimed warm-up steps, then K steps captured once as a CUDA
+    graph (per-kernel events included) and replayed between two device events; optional
+    end-to-end run with pinned-host inputs and outputs inside the timed region."""
 
-    def plan(i):
-        return i % len(layers), i % NUM_LAYERS, i % n_inputs
+    def __init__(self, d, layers, cfg, phase, ladder, device, ladder_desc=None, forced=None,
+                 n_inputs=8, input_seed=1000):
+        self.d, self.layers, self.cfg, self.phase, self.ladder = d, layers, cfg, phase, ladder
+        self.device = device
+        self.ladder_desc = ladder_desc or {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS}
+        self.forced = forced
+        self.T = cfg.T
+        self.n_inputs = n_inputs
+        self.inputs = step_inputs(cfg, n_inputs, device, input_seed)
+        self.ws = [L.workspace(self.T, device) for L, _ in layers]
+        self.out = torch.empty(self.T, cfg.hidden, dtype=torch.float32, device=device)
 
-    events = None
-    ffn_mode = d.DYMOE_FFN_PREFILL_TS if (phase == d.DYMOE_PREFILL and args.prefill_kernel == "ts") else -1
+    def plan(self, i):
+        return i % len(self.layers), i % NUM_LAYERS, i % self.n_inputs
 
-    def one_step(i, ev=None):
-        c, l, j = plan(i)
-        L = layers[c][0]
-        x, lg, a = inputs[j]
-        L.forward(x, lg, ladder, l, NUM_LAYERS, phase=phase, attn_mass=a, ws=ws[c], out=out,
-                  prof_events=ev, ffn_mode=ffn_mode)
+    def step(self, i, ev=None, x=None, lg=None, a=None, out=None):
+        c, l, j = self.plan(i)
+        if x is None:
+            x, lg, a = self.inputs[j]
+        self.layers[c][0].forward(x, lg, self.ladder, l, NUM_LAYERS, phase=self.phase, attn_mass=a,
+                                  ws=self.ws[c], out=self.out if out is None else out,
+                                  prof_events=ev, forced_bits=self.forced)
 
-    # census: algorithmic bytes / flops of every distinct step (bits are data-dependent)
-    census = {}
-    period = math.lcm(len(layers), NUM_LAYERS, n_inputs)
-    for i in range(period):
-        one_step(i)
-        c = plan(i)[0]
-        v = layers[c][0].views(T, ws[c])
-        bits = v["bits"].cpu().numpy()
-        off = v["expert_off"].cpu().numpy()
-        census[plan(i)] = (algorithmic_bytes(cfg, bits, off), algorithmic_flops(cfg, off, bits),
-                           int((np.diff(off) > 0).sum()))
-        rc, word = layers[c][0].check_status(T, ws[c])
-        assert rc == 0, "device status word %x" % word
-    for i in range(args.warmup):
-        one_step(i)
-    torch.cuda.synchronize()
+    def census(self):
+        """algorithmic bytes / flops of every distinct step (bits are data-dependent)"""
+        cen = {}
+        period = math.lcm(len(self.layers), NUM_LAYERS, self.n_inputs)
+        for i in range(period):
+            self.step(i)
+            c = self.plan(i)[0]
+            v = self.layers[c][0].views(self.T, self.ws[c])
+            bits = v["bits"].cpu().numpy() if self.forced is None else self.forced.cpu().numpy()
+            off = v["expert_off"].cpu().numpy()
+            cen[self.plan(i)] = (algorithmic_bytes(self.cfg, bits, off),
+                                 algorithmic_flops(self.cfg, off, bits), bits.copy(), np.diff(off))
+            rc, word = self.layers[c][0].check_status(self.T, self.ws[c])
+            assert rc == 0, "device status word %x" % word
+        self.cen = cen
+        return cen
 
-    # ---------------- timed region (device events, max over ranks)
-    K = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
-    for row in ev:
-        for e_ in row:
-            e_.record(stream)   # creates the CUDA event so its handle can be passed down
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # the K steps (4 launches each in decode, no host synchronisation inside dymoe_moe_forward)
-    # are captured once as a CUDA graph -- per-kernel events included -- and replayed in the timed
-    # region, as a serving loop would: launch gaps and host-side marshalling leave the step
-    graph = None
-    if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream(device=device)
-        side.wait_stream(stream)
-        with torch.cuda.stream(side):
-            with torch.cuda.graph(graph, stream=side):
+    def run(self, K, W, graph=True, world=1):
+        d, stream = self.d, torch.cuda.current_stream()
+        self.census()
+        for i in range(W):
+            self.step(i)
+        torch.cuda.synchronize()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+        for row in ev:
+            for e_ in row:
+                e_.record(stream)   # creates the CUDA event so its handle can be passed down
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g = None
+        if graph:
+            # the K steps (no host synchronisation inside dymoe_moe_forward) captured once as a
+            # CUDA graph -- per-kernel events included -- and replayed, as a serving loop would
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(device=self.device)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side):
+                    for i in range(K):
+                        self.step(W + i, ev[i])
+            stream.wait_stream(side)
+            g.replay()          # one untimed replay (the warm-up steps above ran call by call)
+            torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            t0.record(stream)
+            if g is not None:
+                g.replay()
+            else:
                 for i in range(K):
-                    one_step(args.warmup + i, ev[i])
-        stream.wait_stream(side)
-        graph.replay()          # one untimed replay (the warm-up steps above ran call by call)
-        torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        t0.record(stream)
-        if graph is not None:
-            graph.replay()
-        else:
-            for i in range(K):
-                one_step(args.warmup + i, ev[i])
-        t1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    ms = t0.elapsed_time(t1)
-    if world > 1:
-        tt = torch.tensor([ms], device=device)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
-    ms_per_step = ms / K
-    tokens = T * K * world
-    value = tokens / (ms / 1e3)
+                    self.step(W + i, ev[i])
+            t1.record(stream)
+            torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+        w13_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(K)]
+        w2_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
+        steps = [self.plan(W + i) for i in range(K)]
+        b13 = sum(self.cen[p][0][0] for p in steps)
+        b2 = sum(self.cen[p][0][1] for p in steps)
+        fl = sum(self.cen[p][1] for p in steps)
+        self.res = dict(ms=ms, K=K, W=W, w13_ms=sum(w13_ms), w2_ms=sum(w2_ms), b13=b13, b2=b2,
+                        fl=fl, clocks=clk.summary(), graph=g is not None)
+        return self.res
 
-    w13_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(K)]
-    w2_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
-    b13 = sum(census[plan(args.warmup + i)][0][0] for i in range(K))
-    b2 = sum(census[plan(args.warmup + i)][0][1] for i in range(K))
-    fl = sum(census[plan(args.warmup + i)][1] for i in range(K))
-    ffn_ms = sum(w13_ms) + sum(w2_ms)
-    achieved_w13 = b13 / (sum(w13_ms) / 1e3) / 1e9
-    achieved_ffn = (b13 + b2) / (ffn_ms / 1e3) / 1e9
-    # the committed ncu capture is of the Mixtral layer's kernels
-    tr = load_traffic("k_decode_gemv<W13>" if phase == d.DYMOE_DECODE else "k_prefill_gemm<W13>") \
-        if wname.startswith("mixtral") else None
-    traffic = tr["traffic"] if tr else None
+    def roofline(self, peaks, tr=None):
+        r = self.res
+        ms, K = r["ms"], r["K"]
+        ffn_ms = r["w13_ms"] + r["w2_ms"]
+        if self.phase == self.d.DYMOE_DECODE:
+            # dominant kernel: the W1/W3 fused-dequant SwiGLU GEMV (HBM-bound); per launch the
+            # algorithmic bytes are the packed W1+W3 bytes of the active experts (+ x, h)
+            ach = r["b13"] / (r["w13_ms"] / 1e3) / 1e9
+            ach2 = r["b2"] / (r["w2_ms"] / 1e3) / 1e9
+            return {"bound": "hbm", "kernel": "k_decode_gemv<W13> (fused-dequant SwiGLU GEMV)",
+                    "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s",
+                    "frac": ach / peaks["hbm"], "traffic": tr["traffic"] if tr else None,
+                    "traffic_capture": tr, "peak_src": peaks["src"], "frac_of_8TBs": ach / 8000.0,
+                    "w2_GBs": ach2, "w2_frac": ach2 / peaks["hbm"],
+                    "ffn_w13_plus_w2_GBs": (r["b13"] + r["b2"]) / (ffn_ms / 1e3) / 1e9,
+                    "ffn_share_of_step": ffn_ms / ms,
+                    "algorithmic_bytes_per_step": (r["b13"] + r["b2"]) / K,
+                    "w13_us_per_step": r["w13_ms"] / K * 1e3, "w2_us_per_step": r["w2_ms"] / K * 1e3}
+        # dominant kernel: the tcgen05 fused-dequant grouped GEMMs (tensor-bound); algorithmic
+        # flops per step = 6 * Hd * F per executed (token, expert) pair
+        tfl = r["fl"] / (ffn_ms / 1e3) / 1e12
+        pk = peaks["bf16_sus"] or peaks["bf16"]
+        return {"bound": "tensor", "kernel": "k_prefill_gemm<W13> + <W2> (tcgen05 fused-dequant grouped GEMM)",
+                "achieved": tfl, "peak": pk, "unit": "TFLOP/s", "frac": tfl / pk,
+                "traffic": tr["traffic"] if tr else None, "traffic_capture": tr,
+                "peak_src": peaks["src"] + " bf16 sustained", "frac_of_2250": tfl / 2250.0,
+                "w13_tflops": (r["fl"] * 2 / 3) / (r["w13_ms"] / 1e3) / 1e12,
+                "w2_tflops": (r["fl"] / 3) / (r["w2_ms"] / 1e3) / 1e12,
+                "ffn_share_of_step": ffn_ms / ms, "algorithmic_flops_per_step": r["fl"] / K,
+                "hbm_GBs_ffn": (r["b13"] + r["b2"]) / (ffn_ms / 1e3) / 1e9}
 
-    # ---------------- end-to-end through the public API with host buffers
-    e2e = None
-    if rank == 0 or world > 1:
-        hx = [inp[0].cpu().pin_memory() for inp in inputs]
-        hl = [inp[1].cpu().pin_memory() for inp in inputs]
-        ha = [inp[2].cpu().pin_memory() for inp in inputs]
-        # double-buffered device inputs / outputs; the copies run on a side stream so that step
-        # i+1's inputs and step i-1's output move while step i computes (what a serving loop does)
-        dbuf = [tuple(torch.empty_like(t) for t in inputs[0]) for _ in range(2)]
-        obuf = [torch.empty(T, cfg.hidden, dtype=torch.float32, device=device) for _ in range(2)]
+    def e2e(self, K, W):
+        """The same steps through the public API with the step's inputs copied in from pinned
+        host memory and its output copied out, inside the timed region (double-buffered on a side
+        stream: step i+1's inputs and step i-1's output move while step i computes)."""
+        d, stream, T, cfg = self.d, torch.cuda.current_stream(), self.T, self.cfg
+        pre = self.phase == d.DYMOE_PREFILL
+        hx = [inp[0].cpu().pin_memory() for inp in self.inputs]
+        hl = [inp[1].cpu().pin_memory() for inp in self.inputs]
+        ha = [inp[2].cpu().pin_memory() for inp in self.inputs]
+        dbuf = [tuple(torch.empty_like(t) for t in self.inputs[0]) for _ in range(2)]
+        obuf = [torch.empty(T, cfg.hidden, dtype=torch.float32, device=self.device) for _ in range(2)]
         hy = [torch.empty(T, cfg.hidden, dtype=torch.float32).pin_memory() for _ in range(2)]
-        h2d = hx[0].numel() * 2 + hl[0].numel() * 4 + (ha[0].numel() * 4 if phase == d.DYMOE_PREFILL else 0)
+        h2d = hx[0].numel() * 2 + hl[0].numel() * 4 + (ha[0].numel() * 4 if pre else 0)
         d2h = hy[0].numel() * 4
-        cstream = torch.cuda.Stream(device=device)
+        cstream = torch.cuda.Stream(device=self.device)
         in_ready = [torch.cuda.Event() for _ in range(2)]
         out_ready = [torch.cuda.Event() for _ in range(2)]
         buf_free = [torch.cuda.Event() for _ in range(2)]
         out_free = [torch.cuda.Event() for _ in range(2)]
 
         def stage_in(i):
-            _, _, j = plan(args.warmup + i)
+            j = self.plan(W + i)[2]
             b = i & 1
             with torch.cuda.stream(cstream):
                 cstream.wait_event(buf_free[b])
                 dbuf[b][0].copy_(hx[j], non_blocking=True)
                 dbuf[b][1].copy_(hl[j], non_blocking=True)
-                if phase == d.DYMOE_PREFILL:
+                if pre:
                     dbuf[b][2].copy_(ha[j], non_blocking=True)
                 in_ready[b].record(cstream)
 
@@ -310,15 +332,13 @@ def run_ours(args, rank, world, device):
         cstream.wait_event(e0)          # no copy starts before the timed region
         stage_in(0)
         for i in range(K):
-            c, l, j = plan(args.warmup + i)
             b = i & 1
             if i + 1 < K:
                 stage_in(i + 1)
             stream.wait_event(in_ready[b])
             stream.wait_event(out_free[b])          # step i-2's output has left the device
             dx, dl, da = dbuf[b]
-            layers[c][0].forward(dx, dl, ladder, l, NUM_LAYERS, phase=phase, attn_mass=da,
-                                 ws=ws[c], out=obuf[b])
+            self.step(W + i, x=dx, lg=dl, a=da, out=obuf[b])
             buf_free[b].record(stream)
             out_ready[b].record(stream)
             with torch.cuda.stream(cstream):
@@ -328,78 +348,130 @@ def run_ours(args, rank, world, device):
         e1.record(cstream)                            # after the last output copy
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1)
-        if world > 1:
-            tt = torch.tensor([e_ms], device=device)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            e_ms = float(tt.item())
-        e2e = {"value": T * K * world / (e_ms / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        return {"value": T * K / (e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)}
 
-    # ---------------- quantize kernel (row a4), alone: one Mixtral expert per width
-    quant = measure_quantize(d, layers[0][1], cfg, peaks)
-    extras = measure_extras(d, cfg, phase, device, peaks)
+    def widths_seen(self):
+        out = {}
+        for p, (_, _, bits, rows) in self.cen.items():
+            for b, n in zip(bits.tolist(), rows.tolist()):
+                if n > 0:
+                    out[str(b)] = out.get(str(b), 0) + 1
+        return dict(sorted(out.items()))
 
-    if phase == d.DYMOE_DECODE:
-        # dominant kernel: the W1/W3 fused-dequant SwiGLU GEMV (HBM-bound); per launch the
-        # algorithmic bytes are the packed W1+W3 bytes of the active experts (+ x, h)
-        roofline = {"bound": "hbm", "kernel": "k_decode_gemv<W13> (fused-dequant SwiGLU GEMV)",
-                    "achieved": achieved_w13, "peak": peaks["hbm"], "unit": "GB/s",
-                    "frac": achieved_w13 / peaks["hbm"], "traffic": traffic,
-                    "traffic_capture": tr, "peak_src": peaks["src"], "frac_of_8TBs": achieved_w13 / 8000.0,
-                    "ffn_w13_plus_w2_GBs": achieved_ffn,
-                    "ffn_share_of_step": ffn_ms / ms if world == 1 else None,
-                    "algorithmic_bytes_per_step": (b13 + b2) / K}
-    else:
-        # dominant kernel: the tcgen05 fused-dequant grouped GEMMs (tensor-bound); algorithmic
-        # flops per step = 6 * Hd * F per executed (token, expert) pair
-        tfl = fl / (ffn_ms / 1e3) / 1e12
-        tfl13 = (fl * 2 / 3) / (sum(w13_ms) / 1e3) / 1e12
-        pk = peaks["bf16_sus"] or peaks["bf16"]
-        roofline = {"bound": "tensor", "kernel": "k_prefill_gemm<W13> + <W2> (tcgen05 fused-dequant grouped GEMM)",
-                    "achieved": tfl, "peak": pk, "unit": "TFLOP/s", "frac": tfl / pk,
-                    "traffic": traffic, "traffic_capture": tr, "peak_src": peaks["src"] + " bf16 sustained",
-                    "frac_of_2250": tfl / 2250.0, "w13_tflops": tfl13,
-                    "w2_tflops": (fl / 3) / (sum(w2_ms) / 1e3) / 1e12,
-                    "ffn_share_of_step": ffn_ms / ms if world == 1 else None,
-                    "algorithmic_flops_per_step": fl / K, "hbm_GBs_ffn": achieved_ffn}
-    res = None
-    if rank == 0:
+    def launches_per_step(self):
         # decode: fused front (route+score+assign+permute), W13, W2, combine; prefill: route, score,
-        # assign, permute, gather into expert order, W13, W2, combine
-        launches_per_step = 4 if phase == d.DYMOE_DECODE else 8
-        res = {
-            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
-            "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
-            "config": {"workload": wname, "hidden": cfg.hidden, "ffn": cfg.ffn,
-                       "experts": cfg.M, "top_k": cfg.k, "tokens_per_step": T,
-                       "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
-                       "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
-                       "weight_copies": args.copies,
-                       "l2": "inputs larger than L2: %d rotating weight copies of %.1f GB each (L2 126 MB)" % (
-                           args.copies, cfg.M * 3 * cfg.hidden * cfg.ffn * sum(
-                               bytes_per_weight(b) for b in (16, 8, 4, 2)) / 1e9),
-                       "parallelism": "replicas" if world > 1 else "single GPU"},
-            "roofline": roofline,
-            "clocks": clk.summary(),
-            "e2e": e2e,
-            "gpu_launches": launches_per_step * K,
-            "cuda_graph": graph is not None,
-            "prefill_kernel": args.prefill_kernel if phase == d.DYMOE_PREFILL else None,
-            "quantize": quant,
-            "next_rows": extras,
-            "tensor_tflops_ffn": fl / (ffn_ms / 1e3) / 1e12,
-        }
-        if not args.no_cpu_baseline and world == 1:
-            res["cpu_baseline"] = cpu_baseline(cfg, args, phase == d.DYMOE_PREFILL)
+        # assign, permute, active list, gather into expert order, W13, zero rows, W2, combine
+        return 4 if self.phase == self.d.DYMOE_DECODE else 9
+
+
+def sub_line(t, K, W, peaks, e2e=True, extra=None):
+    """A compact JSON object for one extra layer workload (BASELINE.json metric, same clock)."""
+    r = t.run(K, W)
+    roof = t.roofline(peaks)
+    out = {"value": t.T * K / (r["ms"] / 1e3), "unit": "tokens/s", "ms_per_step": r["ms"] / K,
+           "steps": K, "tokens_per_step": t.T, "ladder": t.ladder_desc,
+           "roofline": {k: roof[k] for k in roof if k not in ("traffic_capture",)},
+           "clocks": r["clocks"], "widths_active": t.widths_seen(), "cuda_graph": r["graph"],
+           "gpu_launches": t.launches_per_step() * K}
+    if e2e:
+        out["e2e"] = t.e2e(K, W)
+    if extra:
+        out.update(extra)
+    return out
+
+
+def run_ours(args, rank, world, device):
+    import paper_2603_19172_b200.dymoe as d
+    d.lib()
+    torch.cuda.set_device(device)
+    peaks = load_peaks()
+    cfg, is_decode, wname = workload_cfg(args)
+    phase = d.DYMOE_DECODE if is_decode else d.DYMOE_PREFILL
+    layers = build_layer_copies(d, cfg, args.copies, device)
+    ladder = d.make_ladder(LADDER_BITS, LADDER_LAMBDAS)
+    K, W = args.steps, args.warmup
+    main = LayerTimer(d, layers, cfg, phase, ladder, device)
+    r = main.run(K, W, graph=not args.no_graph)
+    ms = r["ms"]
+    # the committed ncu capture is of the Mixtral layer's kernels
+    tr = load_traffic("k_decode_gemv<W13>" if phase == d.DYMOE_DECODE else "k_prefill_gemm<W13>") \
+        if wname.startswith("mixtral") else None
+    roofline = main.roofline(peaks, tr)
+    e2e = main.e2e(K, W)
+    res = {
+        "metric": METRIC, "value": cfg.T * K / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
+        "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
+        "config": {"workload": wname, "hidden": cfg.hidden, "ffn": cfg.ffn,
+                   "experts": cfg.M, "top_k": cfg.k, "tokens_per_step": cfg.T,
+                   "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
+                   "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
+                   "weight_copies": args.copies,
+                   "l2": "inputs larger than L2: %d rotating weight copies of %.1f GB each (L2 126 MB)" % (
+                       args.copies, cfg.M * 3 * cfg.hidden * cfg.ffn * sum(
+                           bytes_per_weight(b) for b in (16, 8, 4, 2)) / 1e9),
+                   "parallelism": "single GPU"},
+        "roofline": roofline,
+        "clocks": r["clocks"],
+        "e2e": e2e,
+        "gpu_launches": main.launches_per_step() * K,
+        "cuda_graph": r["graph"],
+        "widths_active": main.widths_seen(),
+    }
+    # ---------------- the rest of the metric on the same weights and clock (default run):
+    # prefill (configs[2]), decode at B = 1 (configs[1] "batch 1-8"; the paper's batch, P:336), the
+    # paper's own 4/2 and 4/0 ladders (P:312), and every width forced alone (per-width fractions)
+    if wname == "mixtral_decode" and not args.main_only:
+        Ks, Kp = min(K, 128), min(K, 32)
+        subs = {}
+        pf = LayerTimer(d, layers, cfg.with_tokens(args.tokens), d.DYMOE_PREFILL, ladder, device)
+        subs["prefill"] = sub_line(pf, Kp, W, peaks, extra={"config": "BASELINE.json configs[2]: "
+                                   "Mixtral-8x7B layer prefill %d tokens" % args.tokens})
+        del pf
+        torch.cuda.empty_cache()
+        b1 = LayerTimer(d, layers, cfg.with_tokens(1), d.DYMOE_DECODE, ladder, device)
+        subs["decode_b1"] = sub_line(b1, Ks, W, peaks)
+        for name, (bits, lams) in PAPER_LADDERS.items():
+            lad = d.make_ladder(bits, lams)
+            desc = {"bits": bits, "lambdas": lams, "paper": "P:312 %s, r_mean = %.2f (D6)" % (
+                name, (1 + lams[0]) / 2)}
+            for B in (1, args.batch):
+                t = LayerTimer(d, layers, cfg.with_tokens(B), d.DYMOE_DECODE, lad, device, ladder_desc=desc)
+                subs["decode_b%d_ladder_%s" % (B, name.replace("/", "_"))] = sub_line(t, Ks, W, peaks, e2e=False)
+        sweep = {}
+        for b in (16, 8, 4, 2):
+            forced = torch.full((cfg.M,), b, dtype=torch.uint8, device=device)
+            t = LayerTimer(d, layers, cfg, d.DYMOE_DECODE, ladder, device, forced=forced,
+                           ladder_desc={"forced_bits": b})
+            t.run(min(K, 64), W)
+            rf = t.roofline(peaks)
+            sweep["int%d" % b if b != 16 else "bf16"] = {
+                "w13_GBs": rf["achieved"], "w13_frac": rf["frac"], "w2_GBs": rf["w2_GBs"],
+                "w2_frac": rf["w2_frac"], "tokens_per_s": t.T * t.res["K"] / (t.res["ms"] / 1e3)}
+        subs["decode_width_sweep"] = dict(sweep, note="B = %d, every expert forced to one width "
+                                          "(forced_bits), fractions of measured HBM" % cfg.T)
+        res["sub_lines"] = subs
+    res["quantize"] = measure_quantize(d, layers[0][1], cfg, peaks)
+    res["next_rows"] = measure_extras(d, cfg, phase, device, peaks)
+    if not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(cfg, args, phase == d.DYMOE_PREFILL)
     return res
 
 
+PAPER_LADDERS = {"4/2": ((4, 2), (0.5,)), "4/0": ((4, 0), (0.5,))}
+
+
 def run_ep(args, rank, world, device):
-    """N > 1: expert-parallel layer (experts sharded in contiguous blocks over the ranks, NCCL
-    all-to-all dispatch/combine via paper_2603_19172_b200.ep); every rank brings its own batch
-    (weak scaling).  Timed exactly like the single-GPU run; max over ranks."""
+    """N > 1: the expert-parallel layer through the C ABI (dymoe_moe_forward_ep): experts sharded
+    in contiguous blocks over the ranks, every rank its own batch (weak scaling).  Both transports
+    are timed -- the handle's own NCCL communicator (grouped send/recv of the (source, expert)
+    chunks) and the peer-memory windows (fused dispatch / combine kernels, device flag barriers,
+    no host synchronisation); the main line is the peer-memory path when its first steps run clean
+    on every rank.  Decode also times the replicated-batch placement (strong scaling of one
+    batch).  Timing: W warm-up steps, K steps between a barrier + synchronize on both sides,
+    CUDA events on the launching stream, max over ranks."""
     import paper_2603_19172_b200.dymoe as d
     from paper_2603_19172_b200 import ep
     d.lib()
@@ -408,119 +480,122 @@ def run_ep(args, rank, world, device):
     cfg, is_decode, wname = workload_cfg(args)
     T = cfg.T
     phase = d.DYMOE_DECODE if is_decode else d.DYMOE_PREFILL
-    comm = ep.TorchComm(stage_cpu=torch.distributed.get_backend() != "nccl")
-
-    class TimedOps(ep.CudaOps):
-        """CudaOps recording CUDA events around the local expert FFN (roofline numerator)."""
-
-        def __init__(self):
-            super().__init__()
-            self.events, self.rows = [], []
-
-        def expert_ffn(self, layer, x_rows, bits, expert_off, perm_token, mode):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            y = super().expert_ffn(layer, x_rows, bits, expert_off, perm_token, mode)
-            e1.record()
-            self.events.append((e0, e1, bits, expert_off))
-            return y
-
-    ops = TimedOps()
+    gloo = torch.distributed.get_backend() != "nccl"
+    # gloo: the test hook of several ranks time-sharing ONE GPU -- NCCL refuses two ranks on one
+    # device, so only the peer-memory transport (windows over CUDA IPC) runs there
+    transports = d.DYMOE_EP_PEER if gloo else (d.DYMOE_EP_NCCL | d.DYMOE_EP_PEER)
+    uid = None if gloo else ep.broadcast_unique_id()
     first, last = ep.owned_range(rank, cfg.M, world)
-    shards = []
+    layers = []
     for c in range(args.copies):
-        ex = [{n: t.to(device) for n, t in e.items()}
-              for e in synthetic.expert_weights(cfg, 100 + c, device, experts=list(range(first, last)))]
-        ex = ex[first:last] if len(ex) > last - first else ex
+        ex = synthetic.expert_weights(cfg, 100 + c, device, experts=list(range(first, last)))
+        ex = [{n: t.to(device) for n, t in e.items()} for e in ex]
         d.quantize_experts(ex, (8, 4, 2))
-        shards.append(ep.EPMoELayer(comm, ops, ex, cfg.M, cfg.k, cfg.hidden, cfg.ffn,
-                                    make_local_layer=lambda e_: d.MoELayer(e_, 1, cfg.hidden, cfg.ffn)))
+        layers.append(ep.EPLayer(rank, world, cfg.M, cfg.k, cfg.hidden, cfg.ffn, T, ex,
+                                 transports=transports, nccl_uid=uid))
+        if gloo:
+            opened = ep.connect_processes(layers[-1])
+            layers[-1]._opened = opened
+    torch.cuda.synchronize()
     n_inputs = 8
     inputs = []
     for i in range(n_inputs):
         x, lg, a = synthetic.layer_inputs(cfg, 1000 + i * 97 + rank, device)
         inputs.append((x.contiguous(), lg.contiguous(), a.contiguous()))
     ladder = d.make_ladder(LADDER_BITS, LADDER_LAMBDAS)
+    K, W = args.steps, args.warmup
+    ws = [L.workspace(T) for L in layers]
+    out = torch.empty(T, cfg.hidden, dtype=torch.float32, device=device)
 
-    def one_step(i):
-        x, lg, a = inputs[i % n_inputs]
-        return shards[i % len(shards)].forward(x, lg, ladder, i % NUM_LAYERS, NUM_LAYERS, phase,
-                                               attn_mass=a)
+    def step(i, transport, placement=d.DYMOE_EP_ALL_TO_ALL, ev=None, x=None, lg=None, a=None, y=None):
+        c = i % len(layers)
+        if x is None:
+            x, lg, a = inputs[i % n_inputs] if placement == d.DYMOE_EP_ALL_TO_ALL else rep_in
+        layers[c].forward(x, lg, ladder, i % NUM_LAYERS, NUM_LAYERS, phase, transport=transport,
+                          placement=placement, attn_mass=a, prof_events=ev,
+                          ws=ws[c] if placement == d.DYMOE_EP_ALL_TO_ALL else wsr[c],
+                          out=out if y is None else y)
 
-    for i in range(args.warmup):
-        one_step(i)
-    torch.cuda.synchronize()
-    K = args.steps
-    ops.events.clear()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        t0.record()
-        for i in range(K):
-            one_step(args.warmup + i)
-        t1.record()
+    def status_all(placement=d.DYMOE_EP_ALL_TO_ALL):
+        word = 0
+        for c, L in enumerate(layers):
+            word |= L.check_status(T, ws[c] if placement == d.DYMOE_EP_ALL_TO_ALL else wsr[c],
+                                   placement=placement)[1]
+        return int(_max_over_ranks(float(word), device))
+
+    def census():
+        """local algorithmic work of every distinct step: the rows this rank's experts receive
+        (all ranks' per-expert counts, gathered untimed) at the widths the step assigned"""
+        cen = {}
+        for i in range(math.lcm(len(layers), NUM_LAYERS, n_inputs)):
+            step(i, transports & d.DYMOE_EP_PEER or d.DYMOE_EP_NCCL)
+            c = i % len(layers)
+            v = layers[c].views(T, ws[c])
+            cnt = torch.diff(v["expert_off"]).to(torch.int64)
+            allc = _all_gather(cnt, device)
+            rows = allc.sum(0).cpu().numpy()[first:last]
+            bits = v["bits"].cpu().numpy()[first:last]
+            sub = synthetic.MoEConfig("loc", M=last - first, k=1, hidden=cfg.hidden, ffn=cfg.ffn, T=T)
+            off = np.concatenate([[0], np.cumsum(rows)])
+            cen[(c, i % NUM_LAYERS, i % n_inputs)] = (algorithmic_bytes(sub, bits, off),
+                                                      algorithmic_flops(sub, off, bits))
+        return cen
+
+    def timed(transport, placement=d.DYMOE_EP_ALL_TO_ALL):
+        for i in range(W):
+            step(i, transport, placement)
         torch.cuda.synchronize()
-    torch.distributed.barrier()
-    ms = t0.elapsed_time(t1)
-    ms = _max_over_ranks(ms, device)
-    value = T * K * world / (ms / 1e3)
-    ffn_events = list(ops.events)
-
-    # ---------------- the same weak-scaling steps with dispatch / combine over peer memory
-    # (forward_p2p: fused gather+store and pull+combine kernels, flag barriers; SURVEY §8e).  It
-    # is the main line when it runs clean on every rank; the NCCL all-to-all line is kept beside it
-    p2p, win = None, None
-    nccl_ms = ms
-    try:
-        gloo = torch.distributed.get_backend() != "nccl"
-        win = ep.PeerWindows(comm, cfg.M, cfg.hidden, T * cfg.k * world,
-                             barrier="host" if gloo else "device", device=device)
-
-        def p2p_step(i, x=None, lg=None, a=None):
-            if x is None:
-                x, lg, a = inputs[i % n_inputs]
-            return shards[i % len(shards)].forward_p2p(win, x, lg, ladder, i % NUM_LAYERS, NUM_LAYERS,
-                                                       phase, attn_mass=a)
-
-        p2p_step(0)   # one step, then check every rank's status before timing anything
-        torch.cuda.synchronize()
-        st = torch.tensor([float(win.status.item())], device=device if not gloo else "cpu",
-                          dtype=torch.float64)
-        torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.MAX)
-        if st.item() != 0:
-            raise RuntimeError("peer-memory step reported status %d" % int(st.item()))
-        for i in range(1, args.warmup):
-            p2p_step(i)
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+        for row in ev:
+            for e_ in row:
+                e_.record()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.distributed.barrier()
         torch.cuda.synchronize()
-        with ClockSampler(torch.cuda.current_device()) as clk_p2p:
-            q0.record()
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            t0.record()
             for i in range(K):
-                p2p_step(args.warmup + i)
-            q1.record()
+                step(W + i, transport, placement, ev=ev[i])
+            t1.record()
             torch.cuda.synchronize()
         torch.distributed.barrier()
-        qms = _max_over_ranks(q0.elapsed_time(q1), device)
-        st = torch.tensor([float(win.status.item())], device=device if not gloo else "cpu",
-                          dtype=torch.float64)
-        torch.distributed.all_reduce(st, op=torch.distributed.ReduceOp.MAX)
-        p2p = {"value": T * K * world / (qms / 1e3), "unit": "tokens/s", "ms_per_step": qms / K,
-               "scaling": "weak", "barrier": win.barrier_mode, "status": int(st.item()),
-               "note": "dymoe_ep_dispatch / dymoe_ep_combine over peer windows (CUDA IPC), "
-                       "no NCCL on the data path; 3 flag barriers + 1 count read per step"}
-    except Exception as ex:   # reported, never fatal for the NCCL line
-        p2p = {"error": "%s: %s" % (type(ex).__name__, str(ex)[:300])}
-    use_p2p = p2p is not None and "error" not in p2p and p2p["status"] == 0 and \
-        args.ep_main != "nccl" and (torch.distributed.get_backend() == "nccl" or args.ep_main == "p2p")
-    nccl_line = {"value": value, "unit": "tokens/s", "ms_per_step": nccl_ms / K, "scaling": "weak",
-                 "note": "NCCL all_to_all_single dispatch / combine (counts exchanged first)"}
-    if use_p2p:
-        ms, value, clk = qms, p2p["value"], clk_p2p
+        ms = _max_over_ranks(t0.elapsed_time(t1), device)
+        w13 = sum(ev[i][0].elapsed_time(ev[i][1]) for i in range(K))
+        w2 = sum(ev[i][1].elapsed_time(ev[i][2]) for i in range(K))
+        return ms, w13, w2, clk.summary()
 
-    # ---------------- end-to-end: per step the rank's inputs come from pinned host memory and
-    # its output goes back to the host, inside the timed region
+    lines, errors = {}, {}
+    cen = census()
+    for name, tp in (("peer", d.DYMOE_EP_PEER), ("nccl", d.DYMOE_EP_NCCL)):
+        if not (transports & tp):
+            continue
+        try:
+            step(0, tp)                       # one step, then every rank's status, before timing
+            torch.cuda.synchronize()
+            if status_all():
+                raise RuntimeError("status word after the first step")
+            ms, w13, w2, clk = timed(tp)
+            st = status_all()
+            steps = [((W + i) % len(layers), (W + i) % NUM_LAYERS, (W + i) % n_inputs) for i in range(K)]
+            b13 = sum(cen[p][0][0] for p in steps)
+            b2 = sum(cen[p][0][1] for p in steps)
+            fl = sum(cen[p][1] for p in steps)
+            lines[name] = {"value": T * K * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms / K,
+                           "status": st, "clocks": clk, "w13_ms": w13, "w2_ms": w2, "b13": b13, "b2": b2,
+                           "fl": fl}
+        except Exception as ex:   # reported, never fatal for the other transport
+            errors[name] = "%s: %s" % (type(ex).__name__, str(ex)[:300])
+    main = "peer" if ("peer" in lines and lines["peer"]["status"] == 0 and args.ep_main != "nccl") \
+        else ("nccl" if "nccl" in lines else None)
+    if args.ep_main == "nccl" and "nccl" in lines:
+        main = "nccl"
+    if main is None:
+        raise SystemExit("no expert-parallel transport ran: %s" % errors)
+    L0 = lines[main]
+    main_tp = d.DYMOE_EP_PEER if main == "peer" else d.DYMOE_EP_NCCL
+
+    # ---------------- end-to-end through the main line: the rank's inputs from pinned host memory
+    # and its output back to the host, every step, inside the timed region
     hx = [inp[0].cpu().pin_memory() for inp in inputs]
     hl = [inp[1].cpu().pin_memory() for inp in inputs]
     ha = [inp[2].cpu().pin_memory() for inp in inputs]
@@ -533,96 +608,96 @@ def run_ep(args, rank, world, device):
     torch.cuda.synchronize()
     e0.record()
     for i in range(K):
-        j = (args.warmup + i) % n_inputs
+        j = (W + i) % n_inputs
         dx.copy_(hx[j], non_blocking=True)
         dl.copy_(hl[j], non_blocking=True)
         if phase == d.DYMOE_PREFILL:
             da.copy_(ha[j], non_blocking=True)
-        if use_p2p:
-            y, _ = p2p_step(args.warmup + i, dx, dl, da)
-        else:
-            y, _ = shards[(args.warmup + i) % len(shards)].forward(
-                dx, dl, ladder, (args.warmup + i) % NUM_LAYERS, NUM_LAYERS, phase, attn_mass=da)
-        hy.copy_(y, non_blocking=True)
+        step(W + i, main_tp, x=dx, lg=dl, a=da)
+        hy.copy_(out, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
     torch.distributed.barrier()
-    e2e = {"value": T * K * world / (_max_over_ranks(e0.elapsed_time(e1), device) / 1e3), "unit": "tokens/s",
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+    e2e = {"value": T * K * world / (_max_over_ranks(e0.elapsed_time(e1), device) / 1e3),
+           "unit": "tokens/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
-    if win is not None:
-        torch.distributed.barrier()
-        win.close()
+    # ---------------- decode, the same batch replicated on every rank (SURVEY §8e latency
+    # variant): local experts, the partial outputs summed over the ranks; strong scaling
+    rep = {}
+    if phase == d.DYMOE_DECODE and T <= 64:
+        rep_in = tuple(t.clone() for t in inputs[0])
+        _broadcast(rep_in[0])
+        _broadcast(rep_in[1])
+        wsr = [L.workspace(T, placement=d.DYMOE_EP_REPLICATED) for L in layers]
+        for name, tp in (("peer", d.DYMOE_EP_PEER), ("nccl", d.DYMOE_EP_NCCL)):
+            if not (transports & tp):
+                continue
+            try:
+                ms, _, _, clk = timed(tp, d.DYMOE_EP_REPLICATED)
+                rep[name] = {"value": T * K / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms / K,
+                             "scaling": "strong", "global_batch": T,
+                             "status": status_all(d.DYMOE_EP_REPLICATED)}
+            except Exception as ex:
+                rep[name] = {"error": "%s: %s" % (type(ex).__name__, str(ex)[:300])}
 
-    # ---------------- decode, batch replicated on every rank (SURVEY §8e latency variant):
-    # the same B tokens everywhere, local experts, one all-reduce of y; strong scaling of one batch
-    rep = None
+    # local FFN roofline of the main line (rank 0's experts: algorithmic bytes or flops / FFN time)
+    ffn_ms = L0["w13_ms"] + L0["w2_ms"]
     if phase == d.DYMOE_DECODE:
-        xr, lgr, _ = inputs[0]
-        _broadcast(xr)
-        _broadcast(lgr)
-        for i in range(args.warmup):
-            shards[i % len(shards)].forward_replicated(xr, lgr, ladder, i % NUM_LAYERS, NUM_LAYERS)
-        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.distributed.barrier()
-        torch.cuda.synchronize()
-        r0.record()
-        for i in range(K):
-            shards[(args.warmup + i) % len(shards)].forward_replicated(
-                xr, lgr, ladder, (args.warmup + i) % NUM_LAYERS, NUM_LAYERS)
-        r1.record()
-        torch.cuda.synchronize()
-        torch.distributed.barrier()
-        rms = _max_over_ranks(r0.elapsed_time(r1), device)
-        rep = {"value": T * K / (rms / 1e3), "unit": "tokens/s", "ms_per_step": rms / K,
-               "scaling": "strong", "global_batch": T,
-               "note": "the same %d-token batch on every rank; local experts + all-reduce(sum) of y" % T}
-
-    # local FFN roofline (bytes of the local experts actually streamed / FFN time)
-    ffn_ms, ffn_bytes, ffn_flops = 0.0, 0.0, 0.0
-    for e0, e1, bits, off in ffn_events:
-        ffn_ms += e0.elapsed_time(e1)
-        b = bits.cpu().numpy()
-        o = off.cpu().numpy()
-        for e in range(len(o) - 1):
-            n = int(o[e + 1] - o[e])
-            if n:
-                chunks = (n + 7) // 8 if phase == d.DYMOE_DECODE else max(1, (n + 255) // 256)
-                ffn_bytes += 3 * cfg.hidden * cfg.ffn * bytes_per_weight(int(b[e])) * chunks
-                ffn_flops += 6.0 * cfg.hidden * cfg.ffn * n
-    res = None
-    if phase == d.DYMOE_DECODE:
-        ach = ffn_bytes / max(ffn_ms / 1e3, 1e-12) / 1e9
-        roof = {"bound": "hbm", "kernel": "local fused-dequant FFN (k_decode_gemv W13 + W2), rank 0",
+        ach = L0["b13"] / max(L0["w13_ms"] / 1e3, 1e-12) / 1e9
+        roof = {"bound": "hbm", "kernel": "k_decode_gemv<W13> on the rows rank 0 received",
                 "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
-                "traffic": None, "peak_src": peaks["src"]}
+                "traffic": None, "peak_src": peaks["src"],
+                "ffn_w13_plus_w2_GBs": (L0["b13"] + L0["b2"]) / max(ffn_ms / 1e3, 1e-12) / 1e9,
+                "ffn_share_of_step": ffn_ms / (L0["ms_per_step"] * K)}
     else:
-        ach = ffn_flops / max(ffn_ms / 1e3, 1e-12) / 1e12
+        ach = L0["fl"] / max(ffn_ms / 1e3, 1e-12) / 1e12
         pk = peaks["bf16_sus"] or peaks["bf16"]
-        roof = {"bound": "tensor", "kernel": "local tcgen05 fused-dequant grouped GEMM, rank 0",
+        roof = {"bound": "tensor", "kernel": "k_prefill_gemm<W13> + <W2> on the rows rank 0 received",
                 "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
-                "peak_src": peaks["src"] + " bf16 sustained"}
-    if rank == 0:
-        res = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K,
-               "warmup": args.warmup, "ms_per_step": ms / K, "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
-               "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
-               "config": {"workload": wname, "hidden": cfg.hidden, "ffn": cfg.ffn,
-                          "experts": cfg.M, "top_k": cfg.k, "tokens_per_step_per_rank": T,
-                          "global_batch": T * world,
-                          "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
-                          "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
-                          "weight_copies": args.copies, "l2": "inputs larger than L2 (rotating weight copies)",
-                          "parallelism": ("ep%d (experts sharded, peer-memory dispatch/combine kernels)" % world)
-                          if use_p2p else ("ep%d (experts sharded, NCCL all-to-all dispatch/combine)" % world)},
-               "roofline": roof, "clocks": clk.summary(), "e2e": e2e,
-               # libdymoe launches per step and rank: route, score, assign, permute, ep_plan,
-               # gather_rows, local permute, active list, W13, W2, reduce / prefill gather,
-               # unit-weight reorder, weighted combine (NCCL collectives not counted)
-               "gpu_launches": (15 if use_p2p else 13) * K,
-               "ep_path": "p2p" if use_p2p else "nccl_all_to_all",
-               "ep_replicated_decode": rep, "ep_p2p": p2p, "ep_nccl_all_to_all": nccl_line}
-    return res
+                "peak_src": peaks["src"] + " bf16 sustained",
+                "ffn_share_of_step": ffn_ms / (L0["ms_per_step"] * K)}
+    for l in layers:
+        for b in getattr(l, "_opened", []):
+            d.dymoe_ep_window_close(b)
+    torch.distributed.barrier()
+    for l in layers:
+        l.close()
+    if rank != 0:
+        return None
+    pub = lambda v: {k: v[k] for k in ("value", "unit", "ms_per_step", "status")}
+    return {"metric": METRIC, "value": L0["value"], "unit": "tokens/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": L0["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
+            "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts, Zipf-skewed router logits)",
+            "config": {"workload": wname, "hidden": cfg.hidden, "ffn": cfg.ffn,
+                       "experts": cfg.M, "top_k": cfg.k, "tokens_per_step_per_rank": T,
+                       "global_batch": T * world,
+                       "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
+                       "schedule": "layer l = step mod 32 of a 32-layer depth schedule",
+                       "weight_copies": args.copies, "l2": "inputs larger than L2 (rotating weight copies)",
+                       "parallelism": "ep%d: experts sharded, dymoe_moe_forward_ep over %s" % (
+                           world, "peer-memory windows (fused dispatch/combine kernels)" if main == "peer"
+                           else "the library's NCCL communicator (grouped send/recv)")},
+            "roofline": roof, "clocks": L0["clocks"], "e2e": e2e,
+            # libdymoe launches per step and rank (peer: route, score, publish, barrier, reduce,
+            # assign, permute, dispatch, barrier, active list, W13, W2, reduce/zero, barrier,
+            # combine; NCCL: route, score, assign, permute, counts, gather, active, W13, W2,
+            # reduce/zero, combine -- NCCL's own kernels not counted)
+            "gpu_launches": (15 if main == "peer" else 11) * K,
+            "ep_path": main, "ep_transports": {k: pub(v) for k, v in lines.items()},
+            "ep_errors": errors or None, "ep_replicated_decode": rep or None}
+
+
+def _all_gather(t, device):
+    ws = torch.distributed.get_world_size()
+    if torch.distributed.get_backend() == "nccl":
+        out = [torch.empty_like(t) for _ in range(ws)]
+        torch.distributed.all_gather(out, t)
+    else:
+        c = t.cpu()
+        out = [torch.empty_like(c) for _ in range(ws)]
+        torch.distributed.all_gather(out, c)
+    return torch.stack(out)
 
 
 def _max_over_ranks(v, device):
@@ -949,14 +1024,14 @@ def main():
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prefill-kernel", default="ss", choices=["ss", "ts"],
-                    help="prefill expert GEMM: ss = dequantized weights through shared memory "
-                         "(default), ts = the experimental operand-swapped kernel (weights in TMEM)")
+    ap.add_argument("--main-only", action="store_true",
+                    help="decode workload: skip the sub-lines (prefill, B = 1, the paper's ladders, "
+                         "the per-width sweep) that the default line carries")
     ap.add_argument("--no-graph", action="store_true", help="time the steps call by call instead "
                     "of replaying their CUDA graph (single-GPU decode / prefill / stack workloads)")
-    ap.add_argument("--ep-main", default="auto", choices=["auto", "nccl", "p2p"],
-                    help="N > 1: the main line's dispatch/combine path (auto: the peer-memory path "
-                         "when it runs clean under NCCL, else the NCCL all-to-all)")
+    ap.add_argument("--ep-main", default="auto", choices=["auto", "nccl", "peer"],
+                    help="N > 1: the main line's transport (auto: the peer-memory windows when they "
+                         "run clean on every rank, else the library's NCCL communicator)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: test hook for several ranks sharing one GPU (collectives staged "
                          "through host memory); never used for reported numbers")
@@ -966,6 +1041,20 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched as `python bench.py --gpus N`: become the launcher of N ranks (one process per
+        # GPU, torch.distributed.run on 127.0.0.1), relay their output and exit code
+        import socket
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit("bench.py: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
     if args.impl == "reference":
         if rank != 0:
             return

@@ -42,10 +42,6 @@ enum {
 };
 
 enum { DYMOE_PREFILL = 0, DYMOE_DECODE = 1 };
-/* Expert-FFN kernel selector only (dymoe_expert_ffn mode, dymoe_fwd_opts.ffn_mode): the
- * experimental operand-swapped tcgen05 prefill GEMM (dequantized weights as the A operand in
- * TMEM, tokens as B).  Same function as DYMOE_PREFILL; measured slower. */
-enum { DYMOE_FFN_PREFILL_TS = 2 };
 enum { DYMOE_M_TOTAL = 0, DYMOE_M_ACTIVE = 1 };  /* reading D5: meaning of M in Eq. 5 */
 enum { DYMOE_OUT_F32 = 0, DYMOE_OUT_BF16 = 1 };
 
@@ -186,10 +182,14 @@ int dymoe_layer_destroy(dymoe_layer* layer);
  *   topk_idx [T][k] i32; bits [M] u8 device
  *   expert_off [M+1] i32 out: rows of expert e are [expert_off[e], expert_off[e+1])
  *   perm_token, perm_slot [T*k] i32 out (first expert_off[M] valid)
- *   inv_row [T][k] i32 out: row of pair (t, slot) or -1 if dropped                           */
+ *   inv_row [T][k] i32 out: row of pair (t, slot) or -1 if dropped
+ *   scratch: caller-owned device buffer of dymoe_permute_scratch_bytes(T, k, M) bytes (the
+ *   active-expert list and the multi-CTA count/scan arrays); no allocation inside the call.
+ * Errors: WORKSPACE if scratch_bytes is too small.                                            */
+size_t dymoe_permute_scratch_bytes(int T, int k, int M);
 int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
                   int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot, int32_t* inv_row,
-                  dymoe_stream_t stream);
+                  void* scratch, size_t scratch_bytes, dymoe_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Expert FFN on the permuted rows (P:203 step 4 "the Model Executor operates on a unified
@@ -199,12 +199,17 @@ int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* b
  * deq = RNE_bf16((q - z)·RNE_bf16(s)) (D17) or the bf16 master for bits == 16.
  *   x [T][Hd] bf16; h_ws [T*k][F] bf16 scratch (intermediate); y_perm [T*k][Hd] f32 out.
  * mode: DYMOE_DECODE = fused-dequant GEMV kernels (intended for <= 8 rows per expert),
- *       DYMOE_PREFILL = fused-dequant tcgen05 grouped GEMM, DYMOE_FFN_PREFILL_TS = its
- *       operand-swapped experimental variant.  All compute the same function.
- * status: device u32 word (nullable) receiving DYMOE_STATUS_* bits.                           */
+ *       DYMOE_PREFILL = fused-dequant tcgen05 grouped GEMM.  Both compute the same function.
+ * status: device u32 word (nullable) receiving DYMOE_STATUS_* bits.
+ * ws: caller-owned device scratch of dymoe_expert_ffn_ws_bytes(layer, T) bytes (256-byte
+ *   aligned): the active-expert lists and the decode kernels' W2 K-slice partials / the prefill
+ *   kernel's expert-ordered token rows.  No allocation happens inside the call.
+ * Errors: WORKSPACE if ws_bytes is too small.                                                  */
+size_t dymoe_expert_ffn_ws_bytes(const dymoe_layer* layer, int T);
 int dymoe_expert_ffn(const dymoe_layer* layer, int mode, const uint16_t* x, int T,
                      const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,
-                     uint16_t* h_ws, float* y_perm, uint32_t* status, dymoe_stream_t stream);
+                     uint16_t* h_ws, float* y_perm, uint32_t* status, void* ws, size_t ws_bytes,
+                     dymoe_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Combine ("0-bit" experts; reading D12): E_t = {slots with inv_row >= 0};
@@ -331,6 +336,8 @@ int dymoe_gather_rows(const uint16_t* x, int Hd, const int32_t* rows, int n, uin
  *   cnt    i32[2][P][M]    cnt[parity][src][e] = rows rank src routes to expert e (double-
  *                          buffered by step parity so a step's publish never races a peer's
  *                          previous combine)
+ *   imp    f32[2][P][M]    rank src's local importance (used by dymoe_moe_forward_ep)
+ *   red    f32[2][64][Hd]  this rank's partial output (dymoe_moe_forward_ep, replicated decode)
  *   recv_x bf16[cap][Hd]   rows received by this rank, EXPERT-MAJOR: local expert e's rows are
  *                          [Σ_{e'<e} Σ_src cnt[src][e'], ...) and within an expert by source rank,
  *                          then in the source's (token, slot) order -- i.e. exactly the order
@@ -391,10 +398,12 @@ int dymoe_ep_dispatch(const dymoe_ep_window* w, const uint16_t* x, int T,
                       const int32_t* expert_off, const int32_t* perm_token, int32_t* recv_off,
                       uint32_t* status, dymoe_stream_t stream);
 /* inv_row [T][k], topk_w [T][k], expert_off [M+1] of this rank's dymoe_permute; y [T][Hd]
- * (out_dtype) out.  Same result as dymoe_combine on the unsharded layer.                      */
+ * (out_dtype) out.  Same result as dymoe_combine on the unsharded layer.  A live slot whose row
+ * lies past cap_rows (it was never stored by the dispatch) contributes nothing and sets
+ * DYMOE_STATUS_EP_OVERFLOW in *status (nullable).                                             */
 int dymoe_ep_combine(const dymoe_ep_window* w, const int32_t* inv_row, const float* topk_w,
                      int T, int k, const int32_t* expert_off, int renorm, int out_dtype, void* y,
-                     dymoe_stream_t stream);
+                     uint32_t* status, dymoe_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
 /* The whole layer, one step: route -> score -> assign -> permute -> FFN
@@ -454,6 +463,103 @@ int dymoe_moe_forward(const dymoe_layer* layer, const uint16_t* x, const float* 
  * workspace's status word (*bits_out receives the word, nullable); clears the word.           */
 int dymoe_check_status(const dymoe_layer* layer, int T, void* workspace, uint32_t* bits_out,
                        dymoe_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* The expert-parallel layer (BASELINE.json north_star "expert-parallel partitioning across 2, 4
+ * and 8 GPUs"; PAPER.md P:203 steps ③-④ with the experts spread over P
+ * GPUs).  Expert e lives on rank floor(e P / M) (contiguous blocks); each rank holds a
+ * dymoe_layer of its own experts only (k_route = 1) and calls dymoe_moe_forward_ep with its own
+ * tokens.  One step, every part inside the library:
+ *   route + score the local tokens; make the importance GLOBAL (sum over ranks: exact counts in
+ *   prefill, gate sums in decode; identical on every rank, so every rank assigns identical bits,
+ *   Eq. 4-5); permute by expert (= by destination rank); send every routed row to its owner;
+ *   the owner runs its experts' fused-dequant FFN on the rows it received (expert-major order:
+ *   expert, source rank, source order); the rows come back and are combined with the routing
+ *   weights (reading D12) -- the same result as dymoe_moe_forward on the unsharded layer.
+ * Transports (dymoe_ep_config.transports, a mask; the call picks one):
+ *   DYMOE_EP_NCCL  a communicator the handle owns (ncclCommInitRank on the caller's unique id;
+ *                  libnccl.so.2 is loaded at dymoe_ep_create): importance all-reduce, count
+ *                  all-gather, then grouped send/recv of exactly the rows each (source, expert)
+ *                  pair exchanges -- straight into the expert-major receive rows and back into
+ *                  the source's permuted order.  One host synchronisation per step (the count
+ *                  matrix sizes the sends).
+ *   DYMOE_EP_PEER  the symmetric windows above, mapped into every rank (dymoe_ep_connect): the
+ *                  importance and per-expert counts go into every window, dispatch is the row
+ *                  gather fused with the store into the owner's window, combine is the remote
+ *                  load fused with the weighted combine; 3 device flag barriers, NO host
+ *                  synchronisation (CUDA-graph capturable).  Needs peer access (NVLink /
+ *                  NVSwitch) or one device.
+ * Placements (the call's `placement`):
+ *   DYMOE_EP_ALL_TO_ALL   every rank brings its own tokens (weak scaling), as above;
+ *   DYMOE_EP_REPLICATED   decode with the SAME batch x on every rank (T <= 64): every rank
+ *                  routes / scores / assigns the batch (identical, no exchange), runs its own
+ *                  experts on the pairs routed to them, combines them with weights renormalised
+ *                  over the global live set (D12), and the partial outputs are summed over the
+ *                  ranks in rank order (NCCL all-reduce, or each rank's partial in its window
+ *                  read by every rank after one barrier).
+ * Requirements: every rank calls dymoe_moe_forward_ep the same number of times with the same
+ * opts (phase, layer, ladder), placement and transport; T <= max_tokens; T_peer_max >= every
+ * rank's T this step (0 = T); the ladder's m_mode may be ACTIVE (an expert is active if any rank
+ * routes a token to it).  Device faults (barrier timeout, window overflow, a width not resident
+ * on its owner) set bits of the step's status word (dymoe_ep_check_status).
+ * Errors: INVALID (names the field), NCCL (communicator creation or a collective failed, message
+ * has NCCL's error string; also when libnccl.so.2 cannot be loaded), CUDA, WORKSPACE.          */
+typedef struct dymoe_ep dymoe_ep;
+enum { DYMOE_EP_NCCL = 1, DYMOE_EP_PEER = 2 };
+enum { DYMOE_EP_ALL_TO_ALL = 0, DYMOE_EP_REPLICATED = 1 };
+#define DYMOE_EP_UID_BYTES 128
+#define DYMOE_EP_IPC_BYTES 64
+typedef struct dymoe_ep_config {
+  int M, k_route, hidden, ffn;   /* the whole layer's shape (M experts over the ranks) */
+  int max_tokens;                /* upper bound of T on any rank in any step */
+  int transports;                /* DYMOE_EP_NCCL | DYMOE_EP_PEER */
+} dymoe_ep_config;
+/* An NCCL unique id (DYMOE_EP_UID_BYTES bytes, host) to broadcast from rank 0 to the others. */
+int dymoe_ep_unique_id(void* uid);
+/* Collective over the P ranks when nccl_uid != NULL (ncclCommInitRank on the current device).
+ * Allocates this rank's window (cap = max_tokens * k_route * P rows).  With DYMOE_EP_PEER and a
+ * communicator, the windows are exchanged over it (CUDA IPC handles all-gathered) and opened:
+ * the handle is ready.  Without a communicator (nccl_uid = NULL, PEER only) the caller exchanges
+ * the bases itself (dymoe_ep_window_base) and calls dymoe_ep_connect.                         */
+int dymoe_ep_create(int rank, int world, const void* nccl_uid, const dymoe_ep_config* cfg,
+                    dymoe_ep** out);
+/* This rank's window base (device pointer) and its CUDA IPC handle (DYMOE_EP_IPC_BYTES, nullable). */
+int dymoe_ep_window_base(const dymoe_ep* ep, void** base, void* ipc_handle);
+/* peer_bases: host array [P] of every rank's window base valid in this process (the same
+ * pointers for ranks that are threads of one process; dymoe_ep_window_open results otherwise). */
+int dymoe_ep_connect(dymoe_ep* ep, void* const* peer_bases);
+/* Workspace of one dymoe_moe_forward_ep call (device, 256-byte aligned). */
+size_t dymoe_ep_workspace_size(const dymoe_ep* ep, int T, int T_peer_max, int placement);
+/* Pointers into the workspace (as dymoe_workspace_views; `importance` is the global vector,
+ * `expert_off` / `perm_*` / `inv_row` this rank's permutation, h / y_perm NULL). */
+int dymoe_ep_workspace_views(const dymoe_ep* ep, int T, int T_peer_max, int placement,
+                             void* workspace, dymoe_ws_views* views);
+/* local: this rank's experts (dymoe_layer with M_loc = its block, k_route = 1, same hidden /
+ * ffn).  x [T][Hd] bf16, logits [T][M] f32 device; y [T][Hd] (opts->out_dtype) out; opts as for
+ * dymoe_moe_forward (forced_bits, prof_events and ffn_mode included; residual allowed).       */
+int dymoe_moe_forward_ep(dymoe_ep* ep, const dymoe_layer* local, int transport, int placement,
+                         const uint16_t* x, const float* logits, int T, int T_peer_max,
+                         const dymoe_fwd_opts* opts, void* y, void* workspace, size_t ws_bytes,
+                         dymoe_stream_t stream);
+/* Host-side exchange plan of one all-to-all step -- exactly what the NCCL transport sends and
+ * receives (exported so that the plan is checked without a GPU, tests/test_ep_gloo.py).
+ *   counts [P][M] i32 host: rows rank src routes to expert e this step (after skips);
+ *   send_off [M+1] i64 out: this rank's permuted rows of expert e are [send_off[e], send_off[e+1])
+ *     and go to owner(e) as ONE message;
+ *   recv_base [M_loc][P] i64 out: first receive row of (local expert el, source src): the rows
+ *     are expert-major (local expert, then source rank, then the source's order);
+ *   recv_off [M_loc+1] i32 out: local expert el's receive rows [recv_off[el], recv_off[el+1]).
+ * Message order between a pair of ranks (NCCL matches sends and receives in order): the sender
+ * walks the receiver's experts ascending, the receiver walks its own experts ascending; empty
+ * messages are skipped on both sides.  The outputs return along the same chunks reversed.
+ * Errors: INVALID (P, M, rank, negative counts, > 2^31 received rows).                        */
+int dymoe_ep_plan_host(int P, int M, int rank, const int32_t* counts, int64_t* send_off,
+                       int64_t* recv_base, int32_t* recv_off);
+/* Synchronises `stream`; DYMOE_ERR_DEVICE if the step's status word (workspace) has a bit set
+ * (*bits_out receives it, nullable); clears it. */
+int dymoe_ep_check_status(const dymoe_ep* ep, int T, int T_peer_max, int placement,
+                          void* workspace, uint32_t* bits_out, dymoe_stream_t stream);
+int dymoe_ep_destroy(dymoe_ep* ep);
 
 /* Last error message of the calling thread ("" if none). */
 const char* dymoe_last_error(void);

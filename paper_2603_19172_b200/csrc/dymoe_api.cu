@@ -16,13 +16,6 @@
 
 using namespace dymoe;
 
-struct dymoe_layer {
-  int M, k, Hd, F;
-  std::vector<DevExpert> host;
-  DevExpert* dev = nullptr;
-  uint32_t* meta_pool = nullptr;   // derived dequant metadata of every resident quantized matrix
-  CUtensorMap* tmap_pool = nullptr;   // TMA descriptors of every resident matrix (device)
-};
 
 namespace {
 
@@ -207,8 +200,10 @@ int dymoe_tier_counts(int layer, int num_layers, const dymoe_ladder* ladder, int
   return ok();
 }
 
-static int fill_assign_params(const dymoe_ladder* ladder, int M, int k_route, int layer,
-                              int num_layers, AssignParams& p) {
+}  // extern "C"
+
+int dymoe::assign_params(const dymoe_ladder* ladder, int M, int k_route, int layer,
+                         int num_layers, AssignParams& p) {
   int rc = check_ladder(ladder);
   if (rc) return rc;
   CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
@@ -227,11 +222,13 @@ static int fill_assign_params(const dymoe_ladder* ladder, int M, int k_route, in
   return DYMOE_OK;
 }
 
+extern "C" {
+
 int dymoe_assign_bits(const float* importance, int M, int layer, int num_layers,
                       const dymoe_ladder* ladder, int k_route, const uint8_t* active_mask,
                       uint8_t* bits, int32_t* tier_counts, dymoe_stream_t stream) {
   AssignParams p{};
-  int rc = fill_assign_params(ladder, M, k_route, layer, num_layers, p);
+  int rc = assign_params(ladder, M, k_route, layer, num_layers, p);
   if (rc) return rc;
   CHECK_ARG(importance != nullptr, "importance: must not be NULL");
   CHECK_ARG(bits != nullptr, "bits: must not be NULL");
@@ -525,9 +522,14 @@ int dymoe_layer_destroy(dymoe_layer* L) {
 }
 
 // ------------------------------------------------------------------------------------------
+size_t dymoe_permute_scratch_bytes(int T, int k, int M) {
+  if (T < 0 || k < 1 || M < 1) return 0;
+  return align_up((size_t)(M + 1) * sizeof(int32_t)) + align_up(permute_scratch_bytes(T, k, M));
+}
+
 int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* bits,
                   int32_t* expert_off, int32_t* perm_token, int32_t* perm_slot, int32_t* inv_row,
-                  dymoe_stream_t stream) {
+                  void* scratch_ws, size_t scratch_bytes, dymoe_stream_t stream) {
   CHECK_ARG(T >= 0, "T: must be >= 0");
   CHECK_ARG(M >= 1 && M <= DYMOE_MAX_EXPERTS, "M: must be in [1, %d]", DYMOE_MAX_EXPERTS);
   CHECK_ARG(k >= 1 && k <= M, "k: must satisfy 1 <= k <= M");
@@ -537,18 +539,20 @@ int dymoe_permute(const int32_t* topk_idx, int T, int k, int M, const uint8_t* b
     CHECK_ARG(topk_idx != nullptr, "topk_idx: must not be NULL");
     CHECK_ARG(perm_token && perm_slot && inv_row, "perm_token/perm_slot/inv_row: must not be NULL");
   }
-  // the active list is an internal by-product; use a small temporary
-  int32_t* active = nullptr;
-  int32_t* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&active, (M + 1) * sizeof(int32_t), S(stream));
-  if (e == cudaSuccess && T > 0)
-    e = cudaMallocAsync(&scratch, permute_scratch_bytes(T, k, M), S(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "dymoe_permute");
-  e = launch_permute(topk_idx, T, k, M, bits, expert_off, perm_token, perm_slot, inv_row, active,
-                     S(stream), scratch);
-  if (scratch) cudaFreeAsync(scratch, S(stream));
-  cudaFreeAsync(active, S(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "dymoe_permute");
+  const size_t need = dymoe_permute_scratch_bytes(T, k, M);
+  CHECK_ARG(scratch_ws != nullptr, "scratch: must not be NULL");
+  if (scratch_bytes < need)
+    return fail(DYMOE_ERR_WORKSPACE, "scratch_bytes: %zu < dymoe_permute_scratch_bytes = %zu",
+                scratch_bytes, need);
+  int rc = check_ptr_align(scratch_ws, 256, "scratch");
+  if (rc) return rc;
+  // the active list is an internal by-product (first section of the scratch)
+  int32_t* active = reinterpret_cast<int32_t*>(scratch_ws);
+  int32_t* scratch = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(scratch_ws) +
+                                                align_up((size_t)(M + 1) * sizeof(int32_t)));
+  CHECK_LAUNCH(launch_permute(topk_idx, T, k, M, bits, expert_off, perm_token, perm_slot, inv_row,
+                              active, S(stream), scratch),
+               "dymoe_permute");
   return ok();
 }
 
@@ -765,7 +769,7 @@ static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, con
     FfnArgs al = a;
     al.active_list = large_list;
     void* ev2[3] = {ev ? ev[0] : nullptr, ev ? ev[1] : nullptr, nullptr};
-    e = launch_ffn_prefill(al, s, ev ? ev2 : nullptr, false);
+    e = launch_ffn_prefill(al, s, ev ? ev2 : nullptr);
     if (e == cudaSuccess) {
       FfnArgs as = a;
       as.active_list = small_list;
@@ -774,8 +778,7 @@ static int run_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T, con
     }
     if (e == cudaSuccess && ev) record_ev(ev, 2, s);
   } else {
-    e = mode == DYMOE_DECODE ? launch_ffn_decode(a, s, ev)
-                             : launch_ffn_prefill(a, s, ev, mode == DYMOE_FFN_PREFILL_TS);
+    e = mode == DYMOE_DECODE ? launch_ffn_decode(a, s, ev) : launch_ffn_prefill(a, s, ev);
   }
   if (e != cudaSuccess) return cuda_fail(e, "expert ffn");
   return DYMOE_OK;
@@ -796,36 +799,68 @@ __global__ void k_active_from_off(const int32_t* __restrict__ off, int M, int32_
   if (lane == 0) list[0] = n;
 }
 
+}  // extern "C"
+
+// dymoe_expert_ffn scratch: active lists (3 x (M + 1)), then the W2 K-slice partials (decode) or
+// the expert-ordered token rows (prefill) -- the larger of the two.
+size_t dymoe::ffn_ws_parts_bytes(const dymoe_layer* L, int rows) {
+  const size_t dec = (size_t)decode_w2_slices(L->F) * rows * L->Hd * sizeof(float);
+  const size_t pre = (size_t)rows * L->Hd * 2;
+  return dec > pre ? dec : pre;
+}
+
+extern "C" size_t dymoe_expert_ffn_ws_bytes(const dymoe_layer* L, int T) {
+  if (!L || T < 0) return 0;
+  return align_up((size_t)3 * (L->M + 1) * sizeof(int32_t)) +
+         align_up(ffn_ws_parts_bytes(L, (T > 0 ? T : 1) * L->k));
+}
+
+// The expert FFN on expert-ordered rows whose count lives on the device (expert_off[M]):
+// `cap_rows` bounds it (workspace, descriptors); the kernels read the real count.  Shared by
+// dymoe_expert_ffn and the expert-parallel layer (rows received from peers).
+int dymoe::expert_ffn_rows(const dymoe_layer* L, int mode, const uint16_t* x, int cap_rows,
+                    const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,
+                    uint16_t* h_ws, float* y_perm, uint32_t* status, void* ws, cudaStream_t s,
+                    void* const* ev) {
+  int32_t* active = reinterpret_cast<int32_t*>(ws);
+  float* parts = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) +
+                                          align_up((size_t)3 * (L->M + 1) * sizeof(int32_t)));
+  k_active_from_off<<<1, 32, 0, s>>>(expert_off, L->M, active);
+  int n_parts = 0;
+  // run_ffn's rows = T * k: pass the capacity as T with the layer's k folded in
+  int rc = run_ffn(L, mode, x, cap_rows / L->k, bits, expert_off, perm_token, active, h_ws,
+                   y_perm, parts, cap_rows, &n_parts, status, s, ev);
+  if (rc == DYMOE_OK && n_parts > 0) {
+    cudaError_t e = launch_reduce_parts(parts, n_parts, cap_rows, cap_rows, L->Hd, y_perm, s,
+                                        expert_off + L->M);
+    if (e != cudaSuccess) rc = cuda_fail(e, "expert ffn");
+  }
+  return rc;
+}
+
+extern "C" {
+
 int dymoe_expert_ffn(const dymoe_layer* L, int mode, const uint16_t* x, int T,
                      const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,
-                     uint16_t* h_ws, float* y_perm, uint32_t* status, dymoe_stream_t stream) {
+                     uint16_t* h_ws, float* y_perm, uint32_t* status, void* ws, size_t ws_bytes,
+                     dymoe_stream_t stream) {
   CHECK_ARG(L != nullptr, "layer: must not be NULL");
-  CHECK_ARG(mode == DYMOE_PREFILL || mode == DYMOE_DECODE || mode == DYMOE_FFN_PREFILL_TS,
-            "mode: must be DYMOE_PREFILL, DYMOE_DECODE or DYMOE_FFN_PREFILL_TS");
+  CHECK_ARG(mode == DYMOE_PREFILL || mode == DYMOE_DECODE,
+            "mode: must be DYMOE_PREFILL or DYMOE_DECODE");
   CHECK_ARG(T >= 0, "T: must be >= 0");
   if (T == 0) return ok();
   CHECK_ARG(x && bits && expert_off && perm_token && h_ws && y_perm,
             "x/bits/expert_off/perm_token/h_ws/y_perm: must not be NULL");
+  CHECK_ARG(ws != nullptr, "ws: must not be NULL");
   int rc = check_ptr_align(x, 16, "x");
   if (rc) return rc;
-  const int rows = T * L->k;
-  const int SK = decode_w2_slices(L->F);
-  int32_t* active = nullptr;
-  float* parts = nullptr;
-  cudaError_t e = cudaMallocAsync(&active, 3 * (L->M + 1) * sizeof(int32_t), S(stream));
-  if (e == cudaSuccess)
-    e = cudaMallocAsync(&parts, (size_t)SK * rows * L->Hd * sizeof(float), S(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "dymoe_expert_ffn");
-  k_active_from_off<<<1, 32, 0, S(stream)>>>(expert_off, L->M, active);
-  int n_parts = 0;
-  rc = run_ffn(L, mode, x, T, bits, expert_off, perm_token, active, h_ws, y_perm, parts, rows,
-               &n_parts, status, S(stream));
-  if (rc == DYMOE_OK && n_parts > 0) {
-    e = launch_reduce_parts(parts, n_parts, rows, rows, L->Hd, y_perm, S(stream));
-    if (e != cudaSuccess) rc = cuda_fail(e, "dymoe_expert_ffn");
-  }
-  cudaFreeAsync(parts, S(stream));
-  cudaFreeAsync(active, S(stream));
+  rc = check_ptr_align(ws, 256, "ws");
+  if (rc) return rc;
+  const size_t need = dymoe_expert_ffn_ws_bytes(L, T);
+  if (ws_bytes < need)
+    return fail(DYMOE_ERR_WORKSPACE, "ws_bytes: %zu < dymoe_expert_ffn_ws_bytes = %zu", ws_bytes, need);
+  rc = expert_ffn_rows(L, mode, x, T * L->k, bits, expert_off, perm_token, h_ws, y_perm, status,
+                       ws, S(stream), nullptr);
   if (rc) return rc;
   return ok();
 }
@@ -869,11 +904,10 @@ int dymoe_moe_forward(const dymoe_layer* L, const uint16_t* x, const float* logi
   CHECK_ARG(T >= 0, "T: must be >= 0");
   CHECK_ARG(o->phase == DYMOE_PREFILL || o->phase == DYMOE_DECODE, "opts.phase: must be DYMOE_PREFILL or DYMOE_DECODE");
   CHECK_ARG(o->out_dtype == DYMOE_OUT_F32 || o->out_dtype == DYMOE_OUT_BF16, "opts.out_dtype: must be DYMOE_OUT_F32 or DYMOE_OUT_BF16");
-  CHECK_ARG(o->ffn_mode == -1 || o->ffn_mode == DYMOE_PREFILL || o->ffn_mode == DYMOE_DECODE ||
-                o->ffn_mode == DYMOE_FFN_PREFILL_TS,
-            "opts.ffn_mode: must be -1, DYMOE_PREFILL, DYMOE_DECODE or DYMOE_FFN_PREFILL_TS");
+  CHECK_ARG(o->ffn_mode == -1 || o->ffn_mode == DYMOE_PREFILL || o->ffn_mode == DYMOE_DECODE,
+            "opts.ffn_mode: must be -1, DYMOE_PREFILL or DYMOE_DECODE");
   AssignParams ap{};
-  int rc = fill_assign_params(&o->ladder, L->M, L->k, o->layer, o->num_layers, ap);
+  int rc = assign_params(&o->ladder, L->M, L->k, o->layer, o->num_layers, ap);
   if (rc) {
     g_err = "opts." + g_err;
     return rc;

@@ -7,7 +7,20 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/dymoe.h"
+
+namespace dymoe {
+struct DevExpert;
+}
+struct dymoe_layer {
+  int M, k, Hd, F;
+  std::vector<dymoe::DevExpert> host;
+  dymoe::DevExpert* dev = nullptr;
+  uint32_t* meta_pool = nullptr;   // derived dequant metadata of every resident quantized matrix
+  CUtensorMap* tmap_pool = nullptr;   // TMA descriptors of every resident matrix (device)
+};
 
 namespace dymoe {
 
@@ -135,13 +148,14 @@ struct FfnArgs {
 // Number of K-slices (and slice length) the decode W2 kernel splits F into.
 int decode_w2_slices(int F);
 int decode_w2_slice_k(int F);
-// y_perm[r][n] = sum_s y_part[s][r][n] (slice order)
+// y_perm[r][n] = sum_s y_part[s][r][n] (slice order), r < rows (and < *rows_dev when non-null)
 cudaError_t launch_reduce_parts(const float* y_part, int n_parts, int part_rows, int rows, int Hd,
-                                float* y_perm, cudaStream_t s);
+                                float* y_perm, cudaStream_t s, const int32_t* rows_dev = nullptr);
+// y[r][:] = 0 for r < min(cap_rows, *rows_dev) (the routed rows of a capacity-sized buffer)
+cudaError_t launch_zero_rows(float* y, int Hd, int cap_rows, const int32_t* rows_dev, cudaStream_t s);
 // ev (nullable, 3 entries, each nullable): recorded before W13, between W13 and W2, after W2.
 cudaError_t launch_ffn_decode(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
-cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr,
-                               bool operand_swapped = false);
+cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev = nullptr);
 // 2-D tiled TMA descriptor over a row-major [d1][d0] tensor (stride1 bytes between rows), box
 // b0 x b1, CUtensorMapDataType dt, swizzle swz (host; false if the driver rejects it)
 bool encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t d0,
@@ -184,6 +198,73 @@ cudaError_t launch_rmsnorm(const uint16_t* x, int T, int Hd, float eps, uint16_t
 // logits[t][e] = h[t] . wg[e] (fp32, accumulation depth <= Hd/32 + 5) + bias[e] (nullable)
 cudaError_t launch_gate_logits(const uint16_t* h, const uint16_t* wg, const float* bias, int T,
                                int Hd, int M, float* logits, cudaStream_t s);
+
+// ------------------------------------------------------------------------------------------
+// Expert-parallel windows (ep_p2p.cu; include/dymoe.h "Expert-parallel dispatch and combine over
+// peer memory").  One symmetric window per rank, mapped into every rank:
+//   flags  u32[P]            barrier counters
+//   cnt    i32[2][P][M]      cnt[parity][src][e]: rows rank src routes to expert e
+//   imp    f32[2][P][M]      imp[parity][src][e]: rank src's local importance (global Eq. 2 / 3)
+//   red    f32[2][R][Hd]     replicated decode: this rank's partial output (R = kEpRedRows)
+//   recv_x bf16[cap][Hd]     received rows, expert-major (local expert, source, source order)
+//   y_out  f32[cap][Hd]      the local experts' outputs, row-aligned with recv_x
+constexpr int kEpMaxP = 64;
+constexpr int kEpRedRows = 64;
+struct EpWinLayout {
+  size_t flags, cnt, imp, red, recv_x, y_out, total;
+};
+__host__ __device__ inline size_t ep_align256(size_t v) { return (v + 255) & ~size_t(255); }
+__host__ __device__ inline EpWinLayout ep_win_layout(int P, int M, int Hd, int cap) {
+  EpWinLayout L;
+  L.flags = 0;
+  L.cnt = ep_align256((size_t)P * 4);
+  L.imp = L.cnt + ep_align256((size_t)2 * P * M * 4);
+  L.red = L.imp + ep_align256((size_t)2 * P * M * 4);
+  L.recv_x = L.red + ep_align256((size_t)2 * kEpRedRows * Hd * 4);
+  L.y_out = L.recv_x + ep_align256((size_t)cap * Hd * 2);
+  L.total = L.y_out + ep_align256((size_t)cap * Hd * 4);
+  return L;
+}
+struct EpWin {
+  int P, rank, M, Hd, cap, parity;
+  char* const* peers;      // device array [P] of window bases as mapped in this process
+  const uint8_t* bits;     // device [M], nullable: counts of experts with bits == 0 read as 0
+  EpWinLayout L;
+};
+__host__ __device__ inline int ep_owner_of(int e, int M, int P) { return (int)(((long long)e * P) / M); }
+__host__ __device__ inline int ep_first_of_owner(int o, int M, int P) {
+  return (int)(((long long)o * M + P - 1) / P);
+}
+// cnt[parity][rank][e] = off[e+1] - off[e] into every window (dymoe_ep_publish_counts)
+cudaError_t launch_ep_publish(const EpWin& w, const int32_t* off, cudaStream_t s);
+// imp[parity][rank][*] = importance, cnt[parity][rank][e] = #(t, slot) with topk_idx == e (before
+// any skip: readers mask by bits) into every window
+cudaError_t launch_ep_publish_pre(const EpWin& w, const float* importance, const int32_t* topk_idx,
+                                  int T, int k, cudaStream_t s);
+// importance[e] = sum_src imp[parity][src][e] (src order, fp32: identical on every rank);
+// active[e] = (sum_src cnt[parity][src][e] > 0) (nullable)
+cudaError_t launch_ep_reduce_imp(const EpWin& w, float* importance, uint8_t* active, cudaStream_t s);
+cudaError_t launch_ep_barrier(const EpWin& w, uint32_t epoch, uint32_t* status, cudaStream_t s);
+cudaError_t launch_ep_dispatch(const EpWin& w, const uint16_t* x, const int32_t* off,
+                               const int32_t* perm_token, int32_t* recv_off, uint32_t* status,
+                               cudaStream_t s);
+cudaError_t launch_ep_combine(const EpWin& w, const int32_t* inv_row, const float* topk_w, int T,
+                              int k, const int32_t* off, int renorm, int out_dtype, void* y,
+                              const uint16_t* residual, uint32_t* status, cudaStream_t s);
+// y[t] = out_dtype(residual[t] + sum_src red[parity][t] of window src), src order, t < B
+cudaError_t launch_ep_reduce_red(const EpWin& w, int B, int out_dtype, void* y,
+                                 const uint16_t* residual, cudaStream_t s);
+cudaError_t preload_ep();
+cudaError_t preload_ep_layer();
+// The expert FFN on expert-ordered rows whose count is on the device (expert_off[M] of `L`);
+// cap_rows bounds it.  ws: dymoe_expert_ffn's scratch for cap_rows rows (dymoe_api.cu).
+size_t ffn_ws_parts_bytes(const dymoe_layer* L, int rows);
+int expert_ffn_rows(const dymoe_layer* L, int mode, const uint16_t* x, int cap_rows,
+                    const uint8_t* bits, const int32_t* expert_off, const int32_t* perm_token,
+                    uint16_t* h_ws, float* y_perm, uint32_t* status, void* ws, cudaStream_t s,
+                    void* const* ev);
+int assign_params(const dymoe_ladder* ladder, int M, int k_route, int layer, int num_layers,
+                  AssignParams& p);
 
 // ------------------------------------------------------------------------------------------
 // Small device helpers.

@@ -386,7 +386,28 @@ struct Sched {
 // ntiles_n.  Lanes take contiguous blocks of the list and load them in parallel; two warp scans
 // (kept count, tiles) place every entry -- one dependent round trip instead of a serial walk
 // over the experts by one thread (tens of microseconds at 64 active experts).
-__device__ void build_sched_warp(const FfnArgs& a, int tok, int ntiles_n, Sched& S, int* n_tiles) {
+// An expert whose assigned width is not resident (codes / bf16 master or their TMA descriptors
+// missing, e.g. a pool slot not yet filled) is left out of the schedule and flagged in the status
+// word (include/dymoe.h DYMOE_STATUS_WIDTH_NOT_RESIDENT): its h rows are not written and its
+// y_perm rows keep the zeros of the pre-GEMM-2 memset, so the combine adds nothing for it.
+__device__ __forceinline__ bool prefill_resident(const FfnArgs& a, int e, bool w13) {
+  const int be = a.bits[e];
+  const DevExpert& E = a.experts[e];
+  bool ok = true;
+  for (int m = w13 ? 0 : 2; m < (w13 ? 2 : 3); ++m) {
+    if (be == 16) {
+      ok &= E.w[m] != nullptr && E.tm_wp[m] != nullptr;
+    } else {
+      const int wi = width_index(be);
+      ok &= wi >= 0 && E.q[wi][m].codes != nullptr && E.q[wi][m].tm_raw != nullptr &&
+            E.q[wi][m].tm_rawmeta != nullptr;
+    }
+  }
+  return ok;
+}
+
+__device__ void build_sched_warp(const FfnArgs& a, int tok, int ntiles_n, Sched& S, int* n_tiles,
+                                 bool w13) {
   const int lane = threadIdx.x & 31;
   const int n = a.active_list[0];
   const int per = (n + 31) / 32;
@@ -396,6 +417,11 @@ __device__ void build_sched_warp(const FfnArgs& a, int tok, int ntiles_n, Sched&
     const int e = a.active_list[1 + i];
     const int n_e = a.expert_off[e + 1] - a.expert_off[e];
     if (a.bits[e] == 0 || n_e == 0) continue;
+    if (!prefill_resident(a, e, w13)) {
+      if (a.status && blockIdx.x == 0)
+        atomicOr(a.status, (unsigned)DYMOE_STATUS_WIDTH_NOT_RESIDENT);
+      continue;
+    }
     ++kept;
     tiles += ((n_e + tok - 1) / tok) * ntiles_n;
   }
@@ -409,7 +435,7 @@ __device__ void build_sched_warp(const FfnArgs& a, int tok, int ntiles_n, Sched&
   for (int i = i0; i < i1; ++i) {   // second pass: the loads hit L1 / L2
     const int e = a.active_list[1 + i];
     const int n_e = a.expert_off[e + 1] - a.expert_off[e];
-    if (a.bits[e] == 0 || n_e == 0) continue;
+    if (a.bits[e] == 0 || n_e == 0 || !prefill_resident(a, e, w13)) continue;
     S.expert[na] = e;
     S.first[na] = acc;
     acc += ((n_e + tok - 1) / tok) * ntiles_n;
@@ -479,7 +505,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
   const uint32_t full_cl = mapa(full0, 0);                     // the leader's full barriers
   const uint32_t tempty_cl = mapa(smem_u32(&tempty_bar[0]), 0);
 
-  if (threadIdx.x < 32) build_sched_warp(a, TOK, ntiles_n, S, &n_tiles_sh);
+  if (threadIdx.x < 32) build_sched_warp(a, TOK, ntiles_n, S, &n_tiles_sh, W13);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full_bar[s]), 2 + 2 * kBWarps);   // leader's: both CTAs arrive
@@ -662,368 +688,24 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
   }
 }
 
-// ======================================================================================== TS
-// Operand-swapped variant (profiles/r01_micro_decode_design.md): the dequantized
-// WEIGHTS are the A operand, written by the producer warps straight into TMEM (tcgen05.st), and
-// the expert-ordered TOKENS are B (N <= 192 per pair tile, by TMA into shared memory), with
-// tcgen05.mma.cta_group::2 (M = 256 weight rows: 128 per CTA in its own TMEM).  Shared memory
-// then only carries the token tiles and the raw codes -- no dequantized tile is stored to it or
-// read back by the tensor core -- and an expert's last tile shrinks N to its token count rounded
-// up to 32.  D (fp32, TMEM): lanes = the CTA's weight rows, columns = the tile's tokens.
-//   W13: CTA r's 128 A rows = W1 rows [f0 + 64 r, +64) then W3 rows of the same features, so gate
-//        (lanes 0-63) and up (lanes 64-127) of a feature meet in one CTA; the epilogue pairs them
-//        through shared memory (TMEM lane quarters belong to different warps).
-//   W2:  CTA r's 128 A rows = W2 rows [n0 + 128 r, +128); K split in two halves as in the SS kernel
-//        (fp32 red.add of exactly two partials into the zeroed y_perm).
-// TMEM: two accumulators of NT columns + SA A stages of 32 columns (64 k of bf16 pairs) = 512.
-namespace ts {
-constexpr int NT = 192;                          // max tokens per pair tile (MMA N)
-constexpr int SA = 4;                            // pipeline stages (B in smem, A in TMEM)
-constexpr int B_STAGE = (NT / 2) * BK * 2;       // 12 KB: this CTA's token rows of one stage
-constexpr int RAW_SLOT_T = 2 * RAW_SLOT;         // W13: the W1 and the W3 128-row boxes
-constexpr int PF_T = 6;
-constexpr int XBUF = 32 * 64 * 4;                // epilogue gate/up exchange: [32 tokens][64]
-constexpr int kSmemT = SA * B_STAGE + PF_T * RAW_SLOT_T + XBUF + 1024;
-constexpr uint32_t A_COL0 = 2 * NT;              // 384
-constexpr uint32_t TMEM_T = 512;
-static_assert(A_COL0 + SA * 32 <= TMEM_T, "TMEM budget");
-}  // namespace ts
-
-__device__ __forceinline__ void tc_mma_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                               uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
-      ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
-      "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
-      "r"(r[15]) : "memory");
-}
-
-// 32 k of one A row in natural k order (16 bf16 pairs) from this thread's raw codes
-template <int BE>
-__device__ __forceinline__ void deq_row32(const RawStage<BE>& r, uint32_t (&o)[16]) {
-  const DQP d = dqp_from_meta(r.m);
-  if constexpr (BE == 4) {
-    const uint32_t wv[4] = {r.v[0].x, r.v[0].y, r.v[0].z, r.v[0].w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 x = deq_int4_word(wv[q], d);
-      o[4 * q] = x.x; o[4 * q + 1] = x.y; o[4 * q + 2] = x.z; o[4 * q + 3] = x.w;
-    }
-  } else if constexpr (BE == 2) {
-    const uint32_t wv[2] = {r.v[0].x, r.v[0].y};
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      uint4 lo, hi;
-      deq_int2_word(wv[q], d, lo, hi);
-      o[8 * q] = lo.x; o[8 * q + 1] = lo.y; o[8 * q + 2] = lo.z; o[8 * q + 3] = lo.w;
-      o[8 * q + 4] = hi.x; o[8 * q + 5] = hi.y; o[8 * q + 6] = hi.z; o[8 * q + 7] = hi.w;
-    }
-  } else {  // 8
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const uint4 v = r.v[i];
-      o[8 * i] = deq_int8_pair(v.x, 0, d); o[8 * i + 1] = deq_int8_pair(v.x, 2, d);
-      o[8 * i + 2] = deq_int8_pair(v.y, 0, d); o[8 * i + 3] = deq_int8_pair(v.y, 2, d);
-      o[8 * i + 4] = deq_int8_pair(v.z, 0, d); o[8 * i + 5] = deq_int8_pair(v.z, 2, d);
-      o[8 * i + 6] = deq_int8_pair(v.w, 0, d); o[8 * i + 7] = deq_int8_pair(v.w, 2, d);
-    }
-  }
-}
-
-struct TileT {
-  int e, m0, f0, rows, ncol;   // expert, first token (relative), first weight row of the pair,
-                               // valid tokens, MMA N (rows rounded up to 32)
-  int kb0, kb1;
-};
-__device__ __forceinline__ TileT tile_at_ts(const Sched& S, const FfnArgs& a, int t, int ntiles_n,
-                                            int fstep, int nk, int ksplit) {
-  int i = 0;
-  while (S.first[i + 1] <= t) ++i;
-  TileT r;
-  r.e = S.expert[i];
-  const int local = t - S.first[i];
-  const int mt = local / ntiles_n, ntk = local - mt * ntiles_n;
-  const int nt = ntk / ksplit, kh = ntk - nt * ksplit;
-  r.kb0 = (int)((long long)kh * nk / ksplit);
-  r.kb1 = (int)((long long)(kh + 1) * nk / ksplit);
-  const int n_e = a.expert_off[r.e + 1] - a.expert_off[r.e];
-  r.m0 = mt * ts::NT;
-  r.f0 = nt * fstep;
-  r.rows = min(ts::NT, n_e - r.m0);
-  r.ncol = (r.rows + 31) / 32 * 32;
-  return r;
-}
-
-template <bool W13>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-k_prefill_ts(const FfnArgs a, const __grid_constant__ CUtensorMap tmB, int ksplit_w2) {
-  using namespace ts;
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ Sched S;
-  __shared__ __align__(8) uint64_t full_bar[SA], empty_bar[SA], tfull_bar[2], tempty_bar[2];
-  __shared__ __align__(8) uint64_t raw_full[PF_T], raw_empty[PF_T];
-  __shared__ uint32_t tmem_base_sh;
-  __shared__ int n_tiles_sh;
-  const int K = W13 ? a.Hd : a.F;
-  const int NWR = W13 ? a.F : a.Hd;
-  const int fstep = W13 ? 128 : 256;                 // weight rows (features) per pair tile
-  const int KSPLIT = W13 ? 1 : ksplit_w2;
-  const int ntiles_n = (NWR + fstep - 1) / fstep * KSPLIT;
-  const int nk = K / BK;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cta_rank();
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-
-  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t sbase = smem_u32(smem);
-  auto sB = [&](int st) { return sbase + st * B_STAGE; };
-  const uint32_t raw_base = sbase + SA * B_STAGE;          // 1 KB aligned slots
-  float* xbuf = reinterpret_cast<float*>(smem + SA * B_STAGE + PF_T * RAW_SLOT_T);
-  const uint32_t full0 = smem_u32(&full_bar[0]), empty0 = smem_u32(&empty_bar[0]);
-  const uint32_t raw_full0 = smem_u32(&raw_full[0]), raw_empty0 = smem_u32(&raw_empty[0]);
-  const uint32_t full_cl = mapa(full0, 0);
-  const uint32_t tempty_cl = mapa(smem_u32(&tempty_bar[0]), 0);
-
-  if (threadIdx.x < 32) build_sched_warp(a, NT, ntiles_n, S, &n_tiles_sh);
-  if (threadIdx.x == 0) {
-    for (int st = 0; st < SA; ++st) {
-      mbar_init(smem_u32(&full_bar[st]), 2 + 2 * kBWarps);
-      mbar_init(smem_u32(&empty_bar[st]), 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&tfull_bar[b]), 1);
-      mbar_init(smem_u32(&tempty_bar[b]), 2 * kEpiWarps);
-    }
-    for (int r = 0; r < PF_T; ++r) {
-      mbar_init(smem_u32(&raw_full[r]), 1);
-      mbar_init(smem_u32(&raw_empty[r]), kBWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base_sh)), "r"(TMEM_T));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem = tmem_base_sh;
-  const int n_tiles = n_tiles_sh;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------------------ B (token rows) TMA
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = pair; t < n_tiles; t += npairs) {
-        const TileT T = tile_at_ts(S, a, t, ntiles_n, fstep, nk, KSPLIT);
-        // D column j <-> token m0 + j: CTA r's B rows are tokens [m0 + r ncol/2, + ncol/2)
-        const int row0 = a.expert_off[T.e] + T.m0 + (int)rank * (T.ncol / 2);
-        for (int kb = T.kb0; kb < T.kb1; ++kb) {
-          mbar_wait(empty0 + stage * 8, phase ^ 1);
-          mbar_expect_tx_cl(full_cl + stage * 8, B_STAGE);
-          tma2d_pair(sB(stage), &tmB, kb * BK, row0, full_cl + stage * 8);
-          if (++stage == SA) { stage = 0; phase ^= 1; }
-        }
-      }
-    } else if (lane == 1) {
-      // ------------------------------------------------------------ raw codes of the A rows
-      int rslot = 0;
-      uint32_t rphase = 0;
-      for (int t = pair; t < n_tiles; t += npairs) {
-        const TileT T = tile_at_ts(S, a, t, ntiles_n, fstep, nk, KSPLIT);
-        const int be = a.bits[T.e];
-        if (be == 16) continue;
-        const int wi = width_index(be);
-        const DevExpert& E = a.experts[T.e];
-        const int rb = BK * be / 8;
-        for (int kb = T.kb0; kb < T.kb1; ++kb) {
-          mbar_wait(raw_empty0 + rslot * 8, rphase ^ 1);
-          const uint32_t slot = raw_base + rslot * RAW_SLOT_T;
-          const uint32_t bar = raw_full0 + rslot * 8;
-          if (W13) {
-            const int row0 = T.f0 + 64 * (int)rank;   // W1 rows and W3 rows of 64 features
-            mbar_expect_tx_local(bar, 2 * (128 * rb + 128 * 4));
-#pragma unroll
-            for (int m = 0; m < 2; ++m) {
-              const DevQMat& q = E.q[wi][m];
-              tma2d_local(slot + m * RAW_SLOT, q.tm_raw, kb * rb, row0, bar);
-              tma2d_local(slot + m * RAW_SLOT + RAW_CODES, q.tm_rawmeta, row0, kb * BK / DYMOE_GROUP, bar);
-            }
-          } else {
-            const int row0 = T.f0 + 128 * (int)rank;
-            const DevQMat& q = E.q[wi][2];
-            mbar_expect_tx_local(bar, 128 * rb + 128 * 4);
-            tma2d_local(slot, q.tm_raw, kb * rb, row0, bar);
-            tma2d_local(slot + RAW_CODES, q.tm_rawmeta, row0, kb * BK / DYMOE_GROUP, bar);
-          }
-          if (++rslot == PF_T) { rslot = 0; rphase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer (leader)
-    if (rank == 0 && lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      int i = 0;
-      for (int t = pair; t < n_tiles; t += npairs, ++i) {
-        const TileT T = tile_at_ts(S, a, t, ntiles_n, fstep, nk, KSPLIT);
-        const int b = i & 1;
-        const uint32_t idesc = make_idesc(256, T.ncol);
-        mbar_wait(smem_u32(&tempty_bar[b]), ((i >> 1) & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = T.kb0; kb < T.kb1; ++kb) {
-          mbar_wait(full0 + stage * 8, phase);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            tc_mma_pair_ts(tmem + b * NT, tmem + A_COL0 + stage * 32 + kk * 8,
-                           sw_desc(sB(stage) + kk * 32), idesc, ((kb - T.kb0) | kk) != 0);
-          tc_commit_pair(empty0 + stage * 8);
-          if (++stage == SA) { stage = 0; phase ^= 1; }
-        }
-        tc_commit_pair(smem_u32(&tfull_bar[b]));
-      }
-    }
-  } else if (warp < kEpiWarp0) {
-    // ------------------------------------------------------------------ A producers -> TMEM
-    const int q = warp & 3;                       // TMEM lane quarter this warp may access
-    const int row = 32 * q + lane;                // A row within this CTA's 128
-    const int khalf = (warp - kBWarp0) >> 2;      // k half of each 64-k stage
-    const int box = W13 ? (row >> 6) : 0;         // W13: W1 box / W3 box
-    const int wr = W13 ? (row & 63) : row;        // row within the box
-    const uint32_t tlane = tmem + ((uint32_t)(32 * q) << 16) + A_COL0 + khalf * 16;
-    int stage = 0, rslot = 0;
-    uint32_t phase = 0, rphase = 0;
-    for (int t = pair; t < n_tiles; t += npairs) {
-      const TileT T = tile_at_ts(S, a, t, ntiles_n, fstep, nk, KSPLIT);
-      const int be = a.bits[T.e];
-      // BF16 experts: the master row straight from global memory
-      const uint16_t* wrow = nullptr;
-      if (be == 16) {
-        const int mi = W13 ? box : 2;
-        const int grow = W13 ? T.f0 + 64 * (int)rank + wr : T.f0 + 128 * (int)rank + row;
-        wrow = grow < NWR ? a.experts[T.e].w[mi] + (size_t)grow * K : nullptr;
-      }
-      for (int kb = T.kb0; kb < T.kb1; ++kb) {
-        uint32_t o[16];
-        if (be == 16) {
-          if (wrow != nullptr) {
-            const uint4* src = reinterpret_cast<const uint4*>(wrow + kb * BK + khalf * 32);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const uint4 v = __ldg(src + i);
-              o[4 * i] = v.x; o[4 * i + 1] = v.y; o[4 * i + 2] = v.z; o[4 * i + 3] = v.w;
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = 0;
-          }
-        } else {
-          mbar_wait(raw_full0 + rslot * 8, rphase);
-          const uint32_t slot = raw_base + rslot * RAW_SLOT_T + box * RAW_SLOT;
-          switch (be) {
-            case 2: { RawStage<2> r; read_raw<2>(r, slot, wr, khalf); deq_row32<2>(r, o); break; }
-            case 4: { RawStage<4> r; read_raw<4>(r, slot, wr, khalf); deq_row32<4>(r, o); break; }
-            default: { RawStage<8> r; read_raw<8>(r, slot, wr, khalf); deq_row32<8>(r, o); break; }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive_local(raw_empty0 + rslot * 8);
-          if (++rslot == PF_T) { rslot = 0; rphase ^= 1; }
-        }
-        mbar_wait(empty0 + stage * 8, phase ^ 1);   // the MMAs are done with this A stage
-        tc_fence_after();
-        tmem_st16(tlane + stage * 32, o);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cl(full_cl + stage * 8);
-        if (++stage == SA) { stage = 0; phase ^= 1; }
-      }
-    }
-  } else {
-    // ------------------------------------------------------------------ epilogue (TMEM -> global)
-    const int q = warp & 3;
-    int i = 0;
-    for (int t = pair; t < n_tiles; t += npairs, ++i) {
-      const TileT T = tile_at_ts(S, a, t, ntiles_n, fstep, nk, KSPLIT);
-      const int b = i & 1;
-      mbar_wait_sleep(smem_u32(&tfull_bar[b]), (i >> 1) & 1, 256);
-      tc_fence_after();
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * NT);
-      const size_t grow0 = (size_t)(a.expert_off[T.e] + T.m0);
-#pragma unroll 1
-      for (int cc = 0; cc < T.ncol / 32; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tbase + cc * 32, v);
-        tmem_ld_wait();
-        const int jmax = min(32, T.rows - cc * 32);   // valid tokens in this chunk
-        if (W13) {
-          const int fi = 32 * (q & 1) + lane;          // feature within the CTA's 64
-          if (q >= 2) {                                // up rows: hand them to the gate warps
-#pragma unroll
-            for (int j = 0; j < 32; ++j) xbuf[j * 64 + fi] = __uint_as_float(v[j]);
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (q < 2) {
-            const int f = T.f0 + 64 * (int)rank + fi;
-            if (f < NWR) {
-              for (int j = 0; j < jmax; ++j) {
-                const float A = __uint_as_float(v[j]), B = xbuf[j * 64 + fi];
-                const float hv = __fmul_rn(__fdividef(A, 1.f + __expf(-A)), B);
-                a.h[(grow0 + cc * 32 + j) * a.F + f] = __bfloat16_as_ushort(__float2bfloat16_rn(hv));
-              }
-            }
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-        } else {
-          const int n = T.f0 + 128 * (int)rank + 32 * q + lane;
-          if (n < NWR) {
-            for (int j = 0; j < jmax; ++j)
-              asm volatile("red.global.add.f32 [%0], %1;" ::"l"(a.y_perm + (grow0 + cc * 32 + j) * a.Hd + n),
-                           "f"(__uint_as_float(v[j])) : "memory");
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cl(tempty_cl + b * 8);
-    }
-  }
-  tc_fence_before();
-  cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ts::TMEM_T));
-  }
-}
-
 }  // namespace pf
 
-// GEMM 1's A operand in expert order: xp[r] = x[perm_token[r]] for r < expert_off[M] (rows past
-// the routed count are zeroed), 16-byte vectors.
+// GEMM 1's A operand in expert order: xp[r] = x[perm_token[r]] for r < expert_off[M] (the one
+// partial pair tile past the routed count is zeroed; `rows` is only the capacity), 16-byte vectors.
 __global__ void __launch_bounds__(256) k_gather_perm(const uint4* __restrict__ x, int vpr,
                                                      const int32_t* __restrict__ perm_token,
                                                      const int32_t* __restrict__ count, int rows,
                                                      uint4* __restrict__ xp) {
   const int n = *count;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (size_t)rows * vpr;
+  const size_t lim = (size_t)min(rows, n + pf::TOK) * vpr;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < lim;
        i += (size_t)gridDim.x * blockDim.x) {
     const int r = (int)(i / vpr), c = (int)(i - (size_t)r * vpr);
     xp[i] = r < n ? __ldg(x + (size_t)perm_token[r] * vpr + c) : make_uint4(0, 0, 0, 0);
   }
 }
 
-cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev, bool operand_swapped) {
+cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev) {
   using namespace pf;
   if (a.Hd % BNH || a.F % BNH || a.Hd % BK || a.F % BK) return cudaErrorInvalidValue;
   static const int sms = [] {   // one-time setup, thread-safe (magic static)
@@ -1032,8 +714,6 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_prefill_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     cudaFuncSetAttribute(k_prefill_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    cudaFuncSetAttribute(k_prefill_ts<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts::kSmemT);
-    cudaFuncSetAttribute(k_prefill_ts<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ts::kSmemT);
     return n;
   }();
   const int rows = a.T * a.k;
@@ -1058,31 +738,12 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
   // tiles (W2 269 -> 334 TFLOP/s).  DYMOE_PREFILL_W2_KSPLIT overrides (measurement knob).
   static const int ks_env = getenv("DYMOE_PREFILL_W2_KSPLIT") ? atoi(getenv("DYMOE_PREFILL_W2_KSPLIT")) : 0;
   const int ksplit = ks_env > 0 ? ks_env : (a.F / BK >= 64 ? 2 : 1);
-  if (operand_swapped) {
-    // token tiles: this CTA's ts::NT / 2 rows of 64 k per TMA box
-    CUtensorMap tb13, tb2;
-    if (!encode_tmap_2d(&tb13, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, xp, a.Hd, rows, (uint64_t)a.Hd * 2,
-                        BK, ts::NT / 2, CU_TENSOR_MAP_SWIZZLE_128B) ||
-        !encode_tmap_2d(&tb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, a.h, a.F, rows, (uint64_t)a.F * 2,
-                        BK, ts::NT / 2, CU_TENSOR_MAP_SWIZZLE_128B))
-      return cudaErrorInvalidValue;
-    k_prefill_ts<true><<<grid, kThreads, ts::kSmemT, s>>>(a, tb13, 1);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    record_ev(ev, 1, s);
-    e = cudaMemsetAsync(a.y_perm, 0, (size_t)rows * a.Hd * sizeof(float), s);
-    if (e != cudaSuccess) return e;
-    k_prefill_ts<false><<<grid, kThreads, ts::kSmemT, s>>>(a, tb2, ksplit == 1 ? 1 : 2);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    record_ev(ev, 2, s);
-    return cudaSuccess;
-  }
   k_prefill_gemm<true><<<grid, kThreads, kSmem, s>>>(a, tm13, 1);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   record_ev(ev, 1, s);
-  e = cudaMemsetAsync(a.y_perm, 0, (size_t)rows * a.Hd * sizeof(float), s);   // split-K target
+  // split-K target: the routed rows (device count) zeroed, not the whole capacity
+  e = launch_zero_rows(a.y_perm, a.Hd, rows, a.expert_off + a.M, s);
   if (e != cudaSuccess) return e;
   k_prefill_gemm<false><<<grid, kThreads, kSmem, s>>>(a, tm2, ksplit == 1 ? 1 : 2);
   e = cudaGetLastError();
@@ -1092,8 +753,7 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
 }
 
 cudaError_t preload_ffn_prefill() {
-  return preload_kernels(k_gather_perm, pf::k_prefill_gemm<true>, pf::k_prefill_gemm<false>,
-                         pf::k_prefill_ts<true>, pf::k_prefill_ts<false>);
+  return preload_kernels(k_gather_perm, pf::k_prefill_gemm<true>, pf::k_prefill_gemm<false>);
 }
 
 }  // namespace dymoe

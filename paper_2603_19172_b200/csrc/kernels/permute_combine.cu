@@ -210,7 +210,9 @@ __device__ __forceinline__ float4 load_row(const float* __restrict__ y_perm, int
 
 __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ y_part, int n_parts,
                                                       int part_rows, int rows, int Hd,
-                                                      float* __restrict__ y_perm) {
+                                                      float* __restrict__ y_perm,
+                                                      const int32_t* __restrict__ rows_dev) {
+  if (rows_dev != nullptr) rows = min(rows, *rows_dev);
   const size_t stride = (size_t)part_rows * Hd;
   const size_t total4 = (size_t)rows * Hd / 4;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total4;
@@ -222,11 +224,28 @@ __global__ void __launch_bounds__(256) k_reduce_parts(const float* __restrict__ 
 }
 
 cudaError_t launch_reduce_parts(const float* y_part, int n_parts, int part_rows, int rows, int Hd,
-                                float* y_perm, cudaStream_t s) {
+                                float* y_perm, cudaStream_t s, const int32_t* rows_dev) {
   if (rows == 0) return cudaSuccess;
   const size_t total4 = (size_t)rows * Hd / 4;
   const int blocks = (int)((total4 + 255) / 256 < 4096 ? (total4 + 255) / 256 : 4096);
-  k_reduce_parts<<<blocks, 256, 0, s>>>(y_part, n_parts, part_rows, rows, Hd, y_perm);
+  k_reduce_parts<<<blocks, 256, 0, s>>>(y_part, n_parts, part_rows, rows, Hd, y_perm, rows_dev);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) k_zero_rows(float4* __restrict__ y, int Hd, int cap_rows,
+                                                   const int32_t* __restrict__ rows_dev) {
+  const int rows = rows_dev != nullptr ? min(cap_rows, *rows_dev) : cap_rows;
+  const size_t n4 = (size_t)rows * Hd / 4;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x)
+    y[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+cudaError_t launch_zero_rows(float* y, int Hd, int cap_rows, const int32_t* rows_dev, cudaStream_t s) {
+  if (cap_rows == 0) return cudaSuccess;
+  const size_t n4 = (size_t)cap_rows * Hd / 4;
+  const int blocks = (int)((n4 + 255) / 256 < 2 * 148 * 4 ? (n4 + 255) / 256 : 2 * 148 * 4);
+  k_zero_rows<<<blocks, 256, 0, s>>>(reinterpret_cast<float4*>(y), Hd, cap_rows, rows_dev);
   return cudaGetLastError();
 }
 
@@ -341,7 +360,7 @@ cudaError_t launch_renorm_weights(const int32_t* topk_idx, const float* topk_w, 
 }
 
 cudaError_t preload_permute_combine() {
-  return preload_kernels(k_permute, k_perm_count, k_perm_scan, k_perm_place, k_ep_plan, k_gather_rows, k_reduce_parts, k_combine,
+  return preload_kernels(k_permute, k_perm_count, k_perm_scan, k_perm_place, k_ep_plan, k_gather_rows, k_reduce_parts, k_zero_rows, k_combine,
                          k_renorm_weights);
 }
 

@@ -14,7 +14,6 @@ LIB_PATH = os.path.join(_HERE, "libdymoe.so")
 
 DYMOE_OK = 0
 DYMOE_PREFILL, DYMOE_DECODE = 0, 1
-DYMOE_FFN_PREFILL_TS = 2   # expert-FFN kernel selector: the operand-swapped prefill GEMM (experimental)
 DYMOE_M_TOTAL, DYMOE_M_ACTIVE = 0, 1
 DYMOE_OUT_F32, DYMOE_OUT_BF16 = 0, 1
 MAX_TIERS = 5
@@ -33,8 +32,14 @@ EXPORTED = [
     "dymoe_layer_set_expert", "dymoe_attention_mass", "dymoe_gate_logits",
     "dymoe_rmsnorm", "dymoe_ep_window_bytes", "dymoe_ep_window_alloc", "dymoe_ep_window_open",
     "dymoe_ep_window_close", "dymoe_ep_window_free", "dymoe_ep_publish_counts", "dymoe_ep_barrier",
-    "dymoe_ep_dispatch", "dymoe_ep_combine", "dymoe_preload",
+    "dymoe_ep_dispatch", "dymoe_ep_combine", "dymoe_preload", "dymoe_permute_scratch_bytes",
+    "dymoe_expert_ffn_ws_bytes", "dymoe_ep_unique_id", "dymoe_ep_create", "dymoe_ep_window_base",
+    "dymoe_ep_connect", "dymoe_ep_workspace_size", "dymoe_ep_workspace_views",
+    "dymoe_moe_forward_ep", "dymoe_ep_check_status", "dymoe_ep_destroy", "dymoe_ep_plan_host",
 ]
+DYMOE_EP_NCCL, DYMOE_EP_PEER = 1, 2
+DYMOE_EP_ALL_TO_ALL, DYMOE_EP_REPLICATED = 0, 1
+EP_UID_BYTES, EP_IPC_BYTES = 128, 64
 DYMOE_STATUS_EP_TIMEOUT, DYMOE_STATUS_EP_OVERFLOW = 2, 4
 
 
@@ -88,6 +93,11 @@ class WsViews(ctypes.Structure):
 _lib = None
 
 
+class EpConfig(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int), ("k_route", ctypes.c_int), ("hidden", ctypes.c_int),
+                ("ffn", ctypes.c_int), ("max_tokens", ctypes.c_int), ("transports", ctypes.c_int)]
+
+
 class EpWindow(ctypes.Structure):
     _fields_ = [("P", ctypes.c_int), ("rank", ctypes.c_int), ("M", ctypes.c_int), ("Hd", ctypes.c_int),
                 ("cap_rows", ctypes.c_int), ("parity", ctypes.c_int), ("peers", ctypes.c_void_p)]
@@ -113,8 +123,10 @@ def lib():
             "dymoe_layer_create": [ctypes.POINTER(LayerDesc), ctypes.POINTER(vp)],
             "dymoe_layer_destroy": [vp],
             "dymoe_layer_refresh": [vp, vp],
-            "dymoe_permute": [vp, ci, ci, ci, vp, vp, vp, vp, vp, vp],
-            "dymoe_expert_ffn": [vp, ci, vp, ci, vp, vp, vp, vp, vp, vp, vp],
+            "dymoe_permute": [vp, ci, ci, ci, vp, vp, vp, vp, vp, vp, cz, vp],
+            "dymoe_permute_scratch_bytes": [ci, ci, ci],
+            "dymoe_expert_ffn": [vp, ci, vp, ci, vp, vp, vp, vp, vp, vp, vp, cz, vp],
+            "dymoe_expert_ffn_ws_bytes": [vp, ci],
             "dymoe_combine": [vp, vp, vp, ci, ci, ci, ci, ci, vp, vp],
             "dymoe_workspace_size": [vp, ci],
             "dymoe_workspace_views": [vp, ci, vp, ctypes.POINTER(WsViews)],
@@ -149,7 +161,18 @@ def lib():
             "dymoe_ep_publish_counts": [ctypes.POINTER(EpWindow), vp, vp],
             "dymoe_ep_barrier": [ctypes.POINTER(EpWindow), ctypes.c_uint32, vp, vp],
             "dymoe_ep_dispatch": [ctypes.POINTER(EpWindow), vp, ci, vp, vp, vp, vp, vp],
-            "dymoe_ep_combine": [ctypes.POINTER(EpWindow), vp, vp, ci, ci, vp, ci, ci, vp, vp],
+            "dymoe_ep_combine": [ctypes.POINTER(EpWindow), vp, vp, ci, ci, vp, ci, ci, vp, vp, vp],
+            "dymoe_ep_unique_id": [vp],
+            "dymoe_ep_create": [ci, ci, vp, ctypes.POINTER(EpConfig), ctypes.POINTER(vp)],
+            "dymoe_ep_window_base": [vp, ctypes.POINTER(vp), vp],
+            "dymoe_ep_connect": [vp, vp],
+            "dymoe_ep_workspace_size": [vp, ci, ci, ci],
+            "dymoe_ep_workspace_views": [vp, ci, ci, ci, vp, ctypes.POINTER(WsViews)],
+            "dymoe_moe_forward_ep": [vp, vp, ci, ci, vp, vp, ci, ci, ctypes.POINTER(FwdOpts), vp, vp,
+                                     cz, vp],
+            "dymoe_ep_check_status": [vp, ci, ci, ci, vp, vp, vp],
+            "dymoe_ep_destroy": [vp],
+            "dymoe_ep_plan_host": [ci, ci, ci, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -161,6 +184,9 @@ def lib():
         L.dymoe_predict_ws_bytes.restype = cz
         L.dymoe_pool_used.restype = cz
         L.dymoe_ep_window_bytes.restype = cz
+        L.dymoe_permute_scratch_bytes.restype = cz
+        L.dymoe_expert_ffn_ws_bytes.restype = cz
+        L.dymoe_ep_workspace_size.restype = cz
         L.dymoe_last_error.restype = ctypes.c_char_p
         L.dymoe_version.restype = ctypes.c_char_p
         _lib = L
@@ -288,8 +314,10 @@ def dymoe_permute(topk_idx, M, bits, stream=None):
     pt = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev)
     ps = torch.empty(max(T * k, 1), dtype=torch.int32, device=dev)
     inv = torch.empty(T, k, dtype=torch.int32, device=dev)
+    nb = lib().dymoe_permute_scratch_bytes(T, k, M)
+    scratch = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
     _check(lib().dymoe_permute(_p(topk_idx), T, k, M, _p(bits), _p(off), _p(pt), _p(ps), _p(inv),
-                               _stream(stream)))
+                               _p(scratch), scratch.numel(), _stream(stream)))
     return off, pt, ps, inv
 
 
@@ -352,13 +380,29 @@ def dymoe_ep_dispatch(win, x, expert_off, perm_token, recv_off, status=None, str
 
 
 def dymoe_ep_combine(win, inv_row, topk_w, expert_off, renorm=True, out_dtype=DYMOE_OUT_F32,
-                     stream=None):
+                     status=None, stream=None):
     T, k = inv_row.shape
     y = torch.empty(T, win.Hd, dtype=torch.float32 if out_dtype == DYMOE_OUT_F32 else torch.bfloat16,
                     device=inv_row.device)
     _check(lib().dymoe_ep_combine(ctypes.byref(win), _p(inv_row), _p(topk_w), T, k, _p(expert_off),
-                                  int(renorm), out_dtype, _p(y) if T else None, _stream(stream)))
+                                  int(renorm), out_dtype, _p(y) if T else None, _p(status),
+                                  _stream(stream)))
     return y
+
+
+def dymoe_ep_plan_host(P, M, rank, counts):
+    """Host-side all-to-all plan (include/dymoe.h): counts int32 [P][M] (CPU) ->
+    (send_off int64 [M+1], recv_base int64 [M_loc][P], recv_off int32 [M_loc+1]).  No GPU."""
+    counts = torch.as_tensor(counts, dtype=torch.int32).contiguous()
+    first = -(-rank * M // P)
+    last = -(-(rank + 1) * M // P)
+    m_loc = last - first
+    so = torch.empty(M + 1, dtype=torch.int64)
+    rb = torch.empty(max(m_loc * P, 1), dtype=torch.int64)
+    ro = torch.empty(m_loc + 1, dtype=torch.int32)
+    _check(lib().dymoe_ep_plan_host(P, M, rank, counts.data_ptr(), so.data_ptr(), rb.data_ptr(),
+                                    ro.data_ptr()))
+    return so, rb[:m_loc * P].view(m_loc, P), ro
 
 
 def dymoe_combine(y_perm, inv_row, topk_w, renorm=True, out_dtype=DYMOE_OUT_F32, stream=None):
@@ -495,6 +539,27 @@ class Pool:
         return lib().dymoe_pool_used(self.handle)
 
 
+def make_opts(phase, layer, num_layers, ladder, attn_mass=None, k_tokens=0, ffn_mode=-1,
+              out_dtype=DYMOE_OUT_F32, forced_bits=None, residual=None, prof_events=None):
+    """dymoe_fwd_opts (include/dymoe.h) from tensors; prof_events: 3 torch.cuda.Events or None."""
+    o = FwdOpts()
+    o.phase = phase
+    o.layer = layer
+    o.num_layers = num_layers
+    o.ladder = ladder
+    o.attn_mass = _p(attn_mass)
+    o.heads = attn_mass.shape[0] if attn_mass is not None else 0
+    o.k_tokens = k_tokens
+    o.ffn_mode = ffn_mode
+    o.out_dtype = out_dtype
+    o.forced_bits = _p(forced_bits)
+    o.residual = _p(_u16(residual)) if residual is not None else None
+    if prof_events is not None:
+        for i, ev in enumerate(prof_events):
+            o.prof_events[i] = ev.cuda_event
+    return o
+
+
 # ---------------------------------------------------------------------------------------------
 class MoELayer:
     """An expert table (dymoe_layer handle).  `experts` is a list of dicts with bf16 masters
@@ -561,21 +626,28 @@ class MoELayer:
             inv_row=view("inv_row", (T, k), torch.int32), h=view("h", (T * k, F), torch.bfloat16),
             y_perm=view("y_perm", (T * k, Hd), torch.float32), status=view("status", (1,), torch.int32))
 
+    def ffn_workspace(self, T, device="cuda"):
+        n = lib().dymoe_expert_ffn_ws_bytes(self.handle, T)
+        return torch.empty(max(n, 256), dtype=torch.uint8, device=device)
+
     def expert_ffn_into(self, x_ptr, T, bits, expert_off, perm_token, mode, y_ptr, h, status,
-                        stream=None):
+                        ws=None, stream=None):
         """dymoe_expert_ffn on raw device rows (x_ptr [T][Hd] bf16) writing y_perm to y_ptr
         ([T*k][Hd] f32), e.g. an expert-parallel peer window; h [T*k][F] bf16 scratch."""
+        ws = self.ffn_workspace(T, h.device) if ws is None else ws
         _check(lib().dymoe_expert_ffn(self.handle, mode, ctypes.c_void_p(x_ptr), T, _p(bits),
                                       _p(expert_off), _p(perm_token), _p(h), ctypes.c_void_p(y_ptr),
-                                      _p(status), _stream(stream)))
+                                      _p(status), _p(ws), ws.numel(), _stream(stream)))
 
-    def expert_ffn(self, x, bits, expert_off, perm_token, mode, stream=None):
+    def expert_ffn(self, x, bits, expert_off, perm_token, mode, ws=None, stream=None):
         T = x.shape[0]
         h = torch.empty(max(T * self.k, 1), self.ffn, dtype=torch.bfloat16, device=x.device)
         y = torch.empty(max(T * self.k, 1), self.hidden, dtype=torch.float32, device=x.device)
         status = torch.zeros(1, dtype=torch.int32, device=x.device)
+        ws = self.ffn_workspace(T, x.device) if ws is None else ws
         _check(lib().dymoe_expert_ffn(self.handle, mode, _p(_u16(x)), T, _p(bits), _p(expert_off),
-                                      _p(perm_token), _p(h), _p(y), _p(status), _stream(stream)))
+                                      _p(perm_token), _p(h), _p(y), _p(status), _p(ws), ws.numel(),
+                                      _stream(stream)))
         return h, y, status
 
     def forward(self, x, logits, ladder, layer, num_layers, phase=DYMOE_DECODE, attn_mass=None,
@@ -589,21 +661,8 @@ class MoELayer:
         if out is None:
             out = torch.empty(T, self.hidden, device=x.device,
                               dtype=torch.float32 if out_dtype == DYMOE_OUT_F32 else torch.bfloat16)
-        o = FwdOpts()
-        o.phase = phase
-        o.layer = layer
-        o.num_layers = num_layers
-        o.ladder = ladder
-        o.attn_mass = _p(attn_mass)
-        o.heads = attn_mass.shape[0] if attn_mass is not None else 0
-        o.k_tokens = k_tokens
-        o.ffn_mode = ffn_mode
-        o.out_dtype = out_dtype
-        o.forced_bits = _p(forced_bits)
-        o.residual = _p(_u16(residual)) if residual is not None else None
-        if prof_events is not None:
-            for i, ev in enumerate(prof_events):
-                o.prof_events[i] = ev.cuda_event
+        o = make_opts(phase, layer, num_layers, ladder, attn_mass, k_tokens, ffn_mode, out_dtype,
+                      forced_bits, residual, prof_events)
         _check(lib().dymoe_moe_forward(self.handle, _p(_u16(x)), _p(logits), T, ctypes.byref(o),
                                        _p(out), _p(ws), ws.numel(), _stream(stream)))
         return out, ws

@@ -36,6 +36,8 @@ class MoEConfig:
 # BASELINE.json configs[0..4]
 CONFIGS = {
     "tiny": MoEConfig("tiny", M=8, k=2, hidden=256, ffn=512, T=16),
+    # a small fine-grained-style layer (many experts, top-4) for multi-rank parity tests
+    "ep_small": MoEConfig("ep_small", M=16, k=4, hidden=256, ffn=384, T=40),
     "mixtral_decode": MoEConfig("mixtral_decode", M=8, k=2, hidden=4096, ffn=14336, T=8),
     "mixtral_prefill": MoEConfig("mixtral_prefill", M=8, k=2, hidden=4096, ffn=14336, T=2048),
     "finegrained": MoEConfig("finegrained", M=64, k=6, hidden=2048, ffn=1408, T=2048),

@@ -1,6 +1,8 @@
-"""Worker of tests/test_gpu_ep.py::test_ep_p2p_ipc_processes (launched by torchrun, several
-processes on one GPU): peer windows opened through CUDA IPC, host barriers (processes time-share
-one GPU), forward_p2p compared bit for bit with the all-to-all forward over gloo."""
+"""Worker of tests/test_gpu_ep.py::test_ep_peer_ipc_processes (launched by torchrun, two processes
+on one GPU): each process creates its dymoe_ep handle (peer-memory transport), the windows are
+exchanged as CUDA IPC handles over a gloo group and opened, and three layer steps run through
+dymoe_moe_forward_ep with device flag barriers across the processes.  Each rank checks its output
+against the unsharded oracle layer with the global importance (oracle = test infrastructure)."""
 import json
 import os
 import sys
@@ -10,9 +12,12 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import synthetic  # noqa: E402
 import paper_2603_19172_b200.dymoe as d  # noqa: E402
 from paper_2603_19172_b200 import ep  # noqa: E402
+from oracle import moe as o_moe, route as o_route, importance as o_imp, schedule as o_sched  # noqa: E402
+from validity import check_bits, decode_importance_tol  # noqa: E402
 
 
 def main():
@@ -23,25 +28,38 @@ def main():
     cfg = synthetic.CONFIGS["tiny"].with_tokens(48)
     ex_all = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
     d.quantize_experts(ex_all, (8, 4, 2))
-    comm = ep.TorchComm(stage_cpu=True)
     first, last = ep.owned_range(rank, cfg.M, P)
-    shard = ep.EPMoELayer(comm, ep.CudaOps(), ex_all[first:last], cfg.M, cfg.k, cfg.hidden, cfg.ffn,
-                          make_local_layer=lambda ex: d.MoELayer(ex, 1, cfg.hidden, cfg.ffn))
-    win = ep.PeerWindows(comm, cfg.M, cfg.hidden, cfg.T * cfg.k * P, barrier="host")
+    layer = ep.EPLayer(rank, P, cfg.M, cfg.k, cfg.hidden, cfg.ffn, cfg.T, ex_all[first:last],
+                       transports=d.DYMOE_EP_PEER)
+    opened = ep.connect_processes(layer)
     lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
-    ok, worst = True, 0.0
+    lad_o = o_sched.Ladder((8, 4, 2), (0.25, 0.5))
+    experts = [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+    ok, worst, status = True, 0.0, 0
     for s in range(3):
-        x, lg, a = synthetic.layer_inputs(cfg, 700 + 10 * s + rank)
         phase = s % 2
-        y2, _ = shard.forward_p2p(win, x.cuda(), lg.cuda(), lad, 9 + s, 32, phase, attn_mass=a.cuda())
-        y1, _ = shard.forward(x.cuda(), lg.cuda(), lad, 9 + s, 32, phase, attn_mass=a.cuda())
-        torch.cuda.synchronize()
-        y1, y2 = y1.cpu().numpy(), y2.cpu().numpy()
-        ok = ok and bool(np.array_equal(y1, y2))
-        worst = max(worst, float(np.abs(y1 - y2).max()))
-    status = int(win.status.item())
+        x, lg, a = synthetic.layer_inputs(cfg, 700 + 10 * s + rank)
+        y, ws = layer.forward(x.cuda(), lg.cuda(), lad, 9 + s, 32, phase, attn_mass=a.cuda())
+        bits = layer.views(cfg.T, ws)["bits"].cpu().numpy()
+        rc, word = layer.check_status(cfg.T, ws)
+        status |= word
+        I = np.zeros(cfg.M)
+        for r in range(P):
+            xr, lgr, ar = synthetic.layer_inputs(cfg, 700 + 10 * s + r)
+            idx, _, p = o_route.route(lgr.numpy(), cfg.k)
+            I = I + (o_imp.score_prefill(ar.numpy(), idx, cfg.M)[0] if phase == 0
+                     else o_imp.decode_importance(lgr.numpy(), p))
+        ref_bits, _ = o_sched.assign_bits(I, 9 + s, 32, lad_o, cfg.k)
+        check_bits(bits, ref_bits, I, 0 if phase == 0 else decode_importance_tol(cfg.T * P))
+        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, 9 + s, 32, lad_o, cfg.k,
+                                forced_bits=bits)["y"]
+        err = float(np.abs(y.cpu().numpy() - ref).max() / np.abs(ref).max())
+        worst = max(worst, err)
+        ok = ok and err <= 2e-3
+    torch.cuda.synchronize()
     dist.barrier()
-    win.close()
+    ep.disconnect(opened)
+    layer.close()
     with open("%s.%d" % (out_path, rank), "w") as f:
         json.dump({"ok": ok, "worst": worst, "status": status}, f)
     dist.destroy_process_group()

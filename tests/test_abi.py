@@ -104,10 +104,12 @@ def test_no_cpu_fallback(d):
 
 def test_ep_window_layout_and_validation(d):
     """Host-side parts of the peer-memory EP calls: the window size formula (flags, cnt[2][P][M],
-    recv_x bf16 and y_out f32 sections, each 256-byte aligned) and field-naming validation."""
+    imp[2][P][M], red f32[2][64][Hd], recv_x bf16 and y_out f32 sections, each 256-byte aligned)
+    and field-naming validation."""
     a = lambda v: (v + 255) // 256 * 256
     for P, M, Hd, cap in [(2, 8, 256, 64), (8, 64, 2048, 98304), (1, 1, 8, 0), (3, 7, 24, 5)]:
-        want = a(P * 4) + a(2 * P * M * 4) + a(cap * Hd * 2) + a(cap * Hd * 4)
+        want = (a(P * 4) + 2 * a(2 * P * M * 4) + a(2 * 64 * Hd * 4) + a(cap * Hd * 2)
+                + a(cap * Hd * 4))
         assert d.dymoe_ep_window_bytes(P, M, Hd, cap) == want
     assert d.dymoe_ep_window_bytes(0, 8, 256, 4) == 0
     L = d.lib()
@@ -121,8 +123,38 @@ def test_ep_window_layout_and_validation(d):
     rc, msg = _err(d, L.dymoe_ep_dispatch(ctypes.byref(w), FAKE, 4, FAKE, FAKE, FAKE, None, None))
     assert rc == 1 and msg.startswith("window.Hd:")
     w = d.EpWindow(2, 0, 8, 256, 16, 2, 0x100000)
-    rc, msg = _err(d, L.dymoe_ep_combine(ctypes.byref(w), FAKE, FAKE, 4, 2, FAKE, 1, 0, FAKE, None))
+    rc, msg = _err(d, L.dymoe_ep_combine(ctypes.byref(w), FAKE, FAKE, 4, 2, FAKE, 1, 0, FAKE, None, None))
     assert rc == 1 and msg.startswith("window.parity:")
     w = d.EpWindow(2, 0, 8, 256, 16, 0, None)
-    rc, msg = _err(d, L.dymoe_ep_combine(ctypes.byref(w), FAKE, FAKE, 4, 2, FAKE, 1, 0, FAKE, None))
+    rc, msg = _err(d, L.dymoe_ep_combine(ctypes.byref(w), FAKE, FAKE, 4, 2, FAKE, 1, 0, FAKE, None, None))
     assert rc == 1 and msg.startswith("window.peers:")
+
+
+def test_ep_handle_validation(d):
+    """dymoe_ep_create validates its configuration without touching the device (field named)."""
+    L = d.lib()
+    h = ctypes.c_void_p()
+    cfg = d.EpConfig(8, 2, 256, 512, 16, d.DYMOE_EP_PEER)
+    rc, msg = _err(d, L.dymoe_ep_create(0, 9, None, ctypes.byref(cfg), ctypes.byref(h)))
+    assert rc == 1 and msg.startswith("world:")
+    rc, msg = _err(d, L.dymoe_ep_create(2, 2, None, ctypes.byref(cfg), ctypes.byref(h)))
+    assert rc == 1 and msg.startswith("rank:")
+    bad = d.EpConfig(8, 2, 200, 512, 16, d.DYMOE_EP_PEER)
+    rc, msg = _err(d, L.dymoe_ep_create(0, 2, None, ctypes.byref(bad), ctypes.byref(h)))
+    assert rc == 1 and msg.startswith("cfg.hidden:")
+    bad = d.EpConfig(8, 2, 256, 512, 16, 0)
+    rc, msg = _err(d, L.dymoe_ep_create(0, 2, None, ctypes.byref(bad), ctypes.byref(h)))
+    assert rc == 1 and msg.startswith("cfg.transports:")
+    nccl = d.EpConfig(8, 2, 256, 512, 16, d.DYMOE_EP_NCCL)
+    rc, msg = _err(d, L.dymoe_ep_create(0, 2, None, ctypes.byref(nccl), ctypes.byref(h)))
+    assert rc == 1 and msg.startswith("nccl_uid:")
+    rc, msg = _err(d, L.dymoe_moe_forward_ep(None, None, 1, 0, None, None, 0, 0, None, None, None, 0, None))
+    assert rc == 1 and msg.startswith("ep:")
+    assert L.dymoe_ep_workspace_size(None, 4, 0, 0) == 0
+
+
+def test_ep_unique_id_is_ncclish(d):
+    """The NCCL unique id comes from the NCCL library the process loads (no device needed)."""
+    import paper_2603_19172_b200.ep as ep
+    a, b = ep.unique_id(), ep.unique_id()
+    assert len(a) == d.EP_UID_BYTES and a != b

@@ -1,5 +1,8 @@
-"""Expert-parallel layer on the CUDA path with P ranks simulated by P threads on one GPU
-(ThreadComm): real kernels for every step, compared with the unsharded oracle."""
+"""The expert-parallel layer through the C ABI (dymoe_ep_create / dymoe_moe_forward_ep,
+include/dymoe.h) on one GPU: P ranks simulated by P threads (each with its own CUDA stream,
+windows connected by pointer, device flag barriers) for the peer-memory transport, P = 1 for the
+library-owned NCCL communicator, and two processes over CUDA IPC.  Every rank's output is checked
+against the unsharded oracle layer with the GLOBAL importance (sum over the ranks)."""
 import threading
 
 import numpy as np
@@ -11,216 +14,262 @@ from oracle import moe as o_moe, route as o_route, importance as o_imp, schedule
 from validity import check_bits, decode_importance_tol
 
 pytestmark = pytest.mark.gpu
+FFN_TOL = 2e-3
 
 
-def _run(P, phase, bits_t, lams, layer_idx, T, cfg, ffn_mode=None):
+def D():
     import paper_2603_19172_b200.dymoe as d
+    d.lib()
+    return d
+
+
+def _experts(cfg, widths=(8, 4, 2)):
+    d = D()
+    ex = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+    d.quantize_experts(ex, widths)
+    return ex
+
+
+def _np_experts(cfg):
+    return [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+
+
+def _inputs(cfg, r, s):
+    return synthetic.layer_inputs(cfg, 500 + 10 * s + r)
+
+
+def _make_layers(P, cfg, ex_all, transports, max_tokens, nccl_uid=None):
     from paper_2603_19172_b200 import ep
-    ex_all = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
-    d.quantize_experts(ex_all, (8, 4, 2))
-    comm = ep.ThreadComm(P)
-    ops = ep.CudaOps()
+    layers = []
+    for r in range(P):
+        first, last = ep.owned_range(r, cfg.M, P)
+        layers.append(ep.EPLayer(r, P, cfg.M, cfg.k, cfg.hidden, cfg.ffn, max_tokens,
+                                 ex_all[first:last], transports=transports, nccl_uid=nccl_uid))
+    if P > 1:
+        ep.connect_threads(layers)
+    return layers
+
+
+def _run_threads(P, cfg, phase, lad, layer_idx, steps=3, placement=0, transport=None,
+                 same_batch=False, **kw):
+    """Each simulated rank runs `steps` layer steps on its own stream."""
+    d = D()
+    transport = d.DYMOE_EP_PEER if transport is None else transport
+    ex_all = _experts(cfg)
+    layers = _make_layers(P, cfg, ex_all, d.DYMOE_EP_PEER, cfg.T)
     results, errors = {}, []
 
     def worker(r):
         try:
-            comm.bind(r)
-            first, last = ep.owned_range(r, cfg.M, P)
-            shard = ep.EPMoELayer(comm, ops, ex_all[first:last], cfg.M, cfg.k, cfg.hidden, cfg.ffn,
-                                  make_local_layer=lambda ex: d.MoELayer(ex, 1, cfg.hidden, cfg.ffn))
-            x, lg, a = synthetic.layer_inputs(cfg, 500 + r)
-            y, info = shard.forward(x.cuda(), lg.cuda(), d.make_ladder(bits_t, lams), layer_idx, 32,
-                                    phase, attn_mass=a.cuda(), ffn_mode=ffn_mode)
-            torch.cuda.synchronize()
-            results[r] = (y.cpu().numpy(), info["bits"].cpu().numpy())
+            torch.cuda.set_device(0)
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out = []
+                for s in range(steps):
+                    x, lg, a = _inputs(cfg, 0 if same_batch else r, s)
+                    y, ws = layers[r].forward(x.cuda(), lg.cuda(), lad, (layer_idx + s) % 32, 32, phase,
+                                              transport=transport, placement=placement,
+                                              attn_mass=a.cuda(), **kw)
+                    v = layers[r].views(x.shape[0], ws, placement=placement)
+                    rc, word = layers[r].check_status(x.shape[0], ws, placement=placement)
+                    out.append((y.float().cpu().numpy(), v["bits"].cpu().numpy(),
+                                v["importance"].cpu().numpy(), word))
+                results[r] = out
         except Exception as e:   # pragma: no cover
             errors.append(e)
-            comm.barrier.abort()
 
     th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
     for t in th:
         t.start()
     for t in th:
         t.join()
+    for l in layers:
+        l.close()
     assert not errors, errors
     return results
 
 
-@pytest.mark.parametrize("P,phase,bits_t,lams,layer_idx,T", [
-    (2, 0, (8, 4, 2), (0.25, 0.5), 20, 40), (4, 0, (4, 0), (0.5,), 31, 24),
-    (2, 1, (8, 4, 2), (0.25, 0.5), 25, 8), (8, 0, (8, 4, 2), (0.25, 0.5), 10, 300)])
-def test_ep_threads_match_unsharded(P, phase, bits_t, lams, layer_idx, T):
-    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
-    res = _run(P, phase, bits_t, lams, layer_idx, T, cfg)
-    experts = [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
+def _oracle_global(cfg, P, phase, s, same_batch=False):
+    """Global importance of step s (sum over the ranks' local importances, oracle)."""
     I = np.zeros(cfg.M)
-    ins = []
     for r in range(P):
-        x, lg, a = synthetic.layer_inputs(cfg, 500 + r)
+        x, lg, a = _inputs(cfg, 0 if same_batch else r, s)
         idx, w, p = o_route.route(lg.numpy(), cfg.k)
-        I = I + (o_imp.score_prefill(a.numpy(), idx, cfg.M)[0] if phase == 0
-                 else o_imp.decode_importance(lg.numpy(), p))
-        ins.append((x, lg))
-    bits, _ = o_sched.assign_bits(I, layer_idx, 32, o_sched.Ladder(bits_t, lams), cfg.k)
-    tol = 0 if phase == 0 else decode_importance_tol(T * P)
+        if phase == 0:
+            I = I + o_imp.score_prefill(a.numpy(), idx, cfg.M)[0].astype(np.float64)
+        else:
+            I = I + (p[0] if (x.shape[0] == 1 and P > 1) else o_imp.decode_importance(lg.numpy(), p))
+    return I
+
+
+def _check_a2a(res, cfg, P, phase, bits_t, lams, layer_idx, renorm=True):
+    experts = _np_experts(cfg)
+    lad_o = o_sched.Ladder(bits_t, lams, renorm_on_skip=renorm)
+    for s in range(len(res[0])):
+        I = _oracle_global(cfg, P, phase, s)
+        l = (layer_idx + s) % 32
+        bits, _ = o_sched.assign_bits(I, l, 32, lad_o, cfg.k)
+        tol = 0 if phase == 0 else decode_importance_tol(cfg.T * P)
+        for r in range(P):
+            y, gbits, gI, status = res[r][s]
+            assert status == 0, (r, s, status)
+            assert np.array_equal(gbits, res[0][s][1])           # identical widths on every rank
+            if phase == 0:
+                assert np.array_equal(gI, I.astype(np.float32))  # exact global counts
+            else:
+                assert np.allclose(gI, I, rtol=0, atol=decode_importance_tol(cfg.T * P) / 2)
+            check_bits(gbits, bits, I, tol)
+            x, lg, a = _inputs(cfg, r, s)
+            ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, l, 32, lad_o, cfg.k,
+                                    forced_bits=gbits)["y"]
+            err = np.abs(y - ref).max() / max(np.abs(ref).max(), 1e-30)
+            assert err <= FFN_TOL, (r, s, err)
+
+
+@pytest.mark.parametrize("P,phase,bits_t,lams,layer_idx,T,cfg_name", [
+    (2, 0, (8, 4, 2), (0.25, 0.5), 20, 40, "tiny"), (4, 0, (4, 0), (0.5,), 29, 24, "tiny"),
+    (2, 1, (8, 4, 2), (0.25, 0.5), 25, 8, "tiny"), (8, 0, (8, 4, 2), (0.25, 0.5), 10, 300, "tiny"),
+    (8, 1, (4, 0), (0.5,), 30, 3, "tiny"), (4, 1, (8, 4, 2), (0.25, 0.5), 7, 1, "tiny"),
+    (4, 0, (16, 8, 4, 2), (0.2, 0.5, 0.8), 12, 64, "ep_small")])
+def test_ep_peer_threads_match_unsharded(P, phase, bits_t, lams, layer_idx, T, cfg_name):
+    """Peer-memory transport, every rank its own tokens, 3 consecutive steps (window parity and
+    barrier epochs advance); prefill at T = 300 runs the tcgen05 GEMM on received rows."""
+    d = D()
+    cfg = synthetic.CONFIGS[cfg_name].with_tokens(T)
+    res = _run_threads(P, cfg, phase, d.make_ladder(bits_t, lams), layer_idx)
+    _check_a2a(res, cfg, P, phase, bits_t, lams, layer_idx)
+
+
+@pytest.mark.parametrize("phase,T", [(0, 256), (1, 8)])
+def test_ep_peer_finegrained_p8(phase, T):
+    """BASELINE.json configs[3]'s layer (64 experts, top-6, hidden 2048, ffn 1408) over 8 ranks
+    (threads, 8 experts each)."""
+    d = D()
+    cfg = synthetic.CONFIGS["finegrained"].with_tokens(T)
+    res = _run_threads(8, cfg, phase, d.make_ladder((8, 4, 2), (0.25, 0.5)), 17, steps=2)
+    _check_a2a(res, cfg, 8, phase, (8, 4, 2), (0.25, 0.5), 17)
+
+
+def test_ep_peer_bf16_output_and_residual():
+    """out_dtype bf16 with a residual: y = bf16(residual + sum) per element."""
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(16)
+    lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
+    P = 2
+    ex_all = _experts(cfg)
+    layers = _make_layers(P, cfg, ex_all, d.DYMOE_EP_PEER, cfg.T)
+    outs, errors = {}, []
+
+    def worker(r):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                x, lg, a = _inputs(cfg, r, 0)
+                xc = x.cuda()
+                y32, _ = layers[r].forward(xc, lg.cuda(), lad, 3, 32, 0, attn_mass=a.cuda())
+                yb, _ = layers[r].forward(xc, lg.cuda(), lad, 3, 32, 0, attn_mass=a.cuda(),
+                                          out_dtype=d.DYMOE_OUT_BF16, residual=xc)
+                torch.cuda.current_stream().synchronize()
+                outs[r] = (y32, yb, xc)
+        except Exception as e:   # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    [l.close() for l in layers]
+    assert not errors, errors
     for r in range(P):
-        y, gbits = res[r]
-        assert np.array_equal(gbits, res[0][1])          # every rank assigns the same widths
-        check_bits(gbits, bits, I, tol)                  # = the oracle's, or valid on a near-tie
-        x, lg = ins[r]
-        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, layer_idx, 32,
-                                o_sched.Ladder(bits_t, lams), cfg.k, forced_bits=gbits)
-        err = np.abs(y - ref["y"]).max() / np.abs(ref["y"]).max()
-        assert err <= 2e-3, (r, err)
+        y32, yb, xc = outs[r]
+        assert torch.equal(yb, (xc.float() + y32).to(torch.bfloat16))
 
 
 @pytest.mark.parametrize("P,bits_t,lams,layer_idx,T", [
-    (2, (8, 4, 2), (0.25, 0.5), 25, 8), (4, (8, 4, 2), (0.25, 0.5), 3, 8), (8, (4, 0), (0.5,), 31, 5)])
-def test_ep_replicated_decode_threads(P, bits_t, lams, layer_idx, T):
-    """Decode, batch replicated on P ranks (threads on one GPU): local experts + all-reduce(sum)
-    equals the unsharded single-GPU layer and the oracle."""
-    import paper_2603_19172_b200.dymoe as d
-    from paper_2603_19172_b200 import ep
+    (2, (8, 4, 2), (0.25, 0.5), 25, 8), (4, (8, 4, 2), (0.25, 0.5), 3, 8), (8, (4, 0), (0.5,), 31, 5),
+    (2, (4, 2), (0.5,), 6, 1)])
+def test_ep_replicated_decode_peer_threads(P, bits_t, lams, layer_idx, T):
+    """Decode with the batch replicated on P ranks: local experts + the sum of the partial outputs
+    over the windows equals the unsharded single-GPU layer (<= 1e-6: top-2 gives at most two
+    nonzero terms per element, exact in any order) and the oracle."""
+    d = D()
     cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
-    ex_all = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
-    d.quantize_experts(ex_all, (8, 4, 2))
-    x, lg, _ = synthetic.layer_inputs(cfg, 77)
     lad = d.make_ladder(bits_t, lams)
+    res = _run_threads(P, cfg, 1, lad, layer_idx, steps=2, placement=d.DYMOE_EP_REPLICATED,
+                       same_batch=True)
+    ex_all = _experts(cfg)
     full = d.MoELayer(ex_all, cfg.k, cfg.hidden, cfg.ffn)
-    y_one, _ = full.forward(x.cuda(), lg.cuda(), lad, layer_idx, 32, phase=d.DYMOE_DECODE)
-    torch.cuda.synchronize()
-    comm = ep.ThreadComm(P)
-    ops = ep.CudaOps()
-    results, errors = {}, []
-
-    def worker(r):
-        try:
-            comm.bind(r)
-            first, last = ep.owned_range(r, cfg.M, P)
-            shard = ep.EPMoELayer(comm, ops, ex_all[first:last], cfg.M, cfg.k, cfg.hidden, cfg.ffn,
-                                  make_local_layer=lambda ex: d.MoELayer(ex, 1, cfg.hidden, cfg.ffn))
-            y, info = shard.forward_replicated(x.cuda(), lg.cuda(), lad, layer_idx, 32)
-            torch.cuda.synchronize()
-            results[r] = y.cpu().numpy()
-        except Exception as e:   # pragma: no cover
-            errors.append(e)
-            comm.barrier.abort()
-
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    assert not errors, errors
-    experts = [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
-    ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, layer_idx, 32,
-                            o_sched.Ladder(bits_t, lams), cfg.k)
-    y1 = y_one.cpu().numpy()
-    for r in range(P):
-        assert np.abs(results[r] - y1).max() <= 1e-6 * np.abs(y1).max(), r
-        err = np.abs(results[r] - ref["y"]).max() / np.abs(ref["y"]).max()
-        assert err <= 2e-3, (r, err)
+    experts = _np_experts(cfg)
+    for s in range(2):
+        x, lg, _ = _inputs(cfg, 0, s)
+        l = (layer_idx + s) % 32
+        y_one, _ = full.forward(x.cuda(), lg.cuda(), lad, l, 32, phase=d.DYMOE_DECODE)
+        y1 = y_one.cpu().numpy()
+        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, l, 32,
+                                o_sched.Ladder(bits_t, lams), cfg.k)
+        for r in range(P):
+            y, gbits, _, status = res[r][s]
+            assert status == 0
+            assert np.abs(y - y1).max() <= 1e-6 * np.abs(y1).max(), (r, s)
+            check_bits(gbits, ref["bits"], ref["importance"], 0 if T == 1 else decode_importance_tol(T))
+            err = np.abs(y - ref["y"]).max() / np.abs(ref["y"]).max()
+            assert err <= FFN_TOL, (r, err)
 
 
-def _run_p2p(P, phase, bits_t, lams, layer_idx, cfg, steps=3, barrier="device", ffn_mode=None):
-    """Each simulated rank runs `steps` layer steps through forward_p2p (peer windows, device flag
-    barriers, one CUDA stream per rank) and through forward (all-to-all through ThreadComm)."""
-    import paper_2603_19172_b200.dymoe as d
+@pytest.mark.parametrize("phase,placement,T", [(0, 0, 40), (1, 0, 8), (1, 1, 8), (0, 0, 300)])
+def test_ep_nccl_single_rank(phase, placement, T):
+    """The library-owned NCCL communicator (one rank: every collective and send/recv runs, to
+    itself) gives the peer-memory transport's output bit for bit, and the oracle's."""
+    d = D()
     from paper_2603_19172_b200 import ep
-    ex_all = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
-    d.quantize_experts(ex_all, (8, 4, 2))
-    comm = ep.ThreadComm(P)
-    ops = ep.CudaOps()
-    results, errors = {}, []
-    lad = d.make_ladder(bits_t, lams)
-
-    def worker(r):
-        try:
-            comm.bind(r)
-            with torch.cuda.stream(torch.cuda.Stream()):
-                first, last = ep.owned_range(r, cfg.M, P)
-                shard = ep.EPMoELayer(comm, ops, ex_all[first:last], cfg.M, cfg.k, cfg.hidden,
-                                      cfg.ffn, make_local_layer=lambda ex: d.MoELayer(ex, 1, cfg.hidden, cfg.ffn))
-                win = ep.PeerWindows(comm, cfg.M, cfg.hidden, cfg.T * cfg.k * P, barrier=barrier)
-                out = []
-                for s in range(steps):
-                    x, lg, a = synthetic.layer_inputs(cfg, 500 + 10 * s + r)
-                    y2, i2 = shard.forward_p2p(win, x.cuda(), lg.cuda(), lad, (layer_idx + s) % 32, 32,
-                                               phase, attn_mass=a.cuda(), ffn_mode=ffn_mode)
-                    y1, i1 = shard.forward(x.cuda(), lg.cuda(), lad, (layer_idx + s) % 32, 32, phase,
-                                           attn_mass=a.cuda(), ffn_mode=ffn_mode)
-                    torch.cuda.current_stream().synchronize()
-                    out.append((y1.cpu().numpy(), y2.cpu().numpy(), i2["recv"], sum(i1["recv"]),
-                                int(win.status.item())))
-                results[r] = out
-                comm._exchange(None)
-                win.close()
-        except Exception as e:   # pragma: no cover
-            errors.append(e)
-            comm.barrier.abort()
-
-    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
-    for t in th:
-        t.start()
-    for t in th:
-        t.join()
-    assert not errors, errors
-    return results
-
-
-@pytest.mark.parametrize("P,phase,bits_t,lams,layer_idx,T", [
-    (2, 0, (8, 4, 2), (0.25, 0.5), 20, 40), (4, 0, (4, 0), (0.5,), 29, 24),
-    (2, 1, (8, 4, 2), (0.25, 0.5), 25, 8), (8, 0, (8, 4, 2), (0.25, 0.5), 10, 300),
-    (8, 1, (4, 0), (0.5,), 30, 3)])
-def test_ep_p2p_equals_all_to_all(P, phase, bits_t, lams, layer_idx, T):
-    """Peer-memory dispatch/combine (fused kernels, device flag barriers) gives the all-to-all
-    path's output bit for bit, step after step (window parity and barrier epochs advance)."""
     cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
-    res = _run_p2p(P, phase, bits_t, lams, layer_idx, cfg)
-    for r in range(P):
-        for s, (y1, y2, n2, n1, status) in enumerate(res[r]):
-            assert status == 0, (r, s, status)
-            assert n1 == n2, (r, s)
-            assert np.array_equal(y1, y2), (r, s, np.abs(y1 - y2).max())
+    lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
+    ex_all = _experts(cfg)
+    both = ep.EPLayer(0, 1, cfg.M, cfg.k, cfg.hidden, cfg.ffn, T, ex_all,
+                      transports=d.DYMOE_EP_NCCL | d.DYMOE_EP_PEER, nccl_uid=ep.unique_id())
+    experts = _np_experts(cfg)
+    for s in range(2):
+        x, lg, a = _inputs(cfg, 0, s)
+        args = (x.cuda(), lg.cuda(), lad, 9 + s, 32, phase)
+        y_n, ws = both.forward(*args, transport=d.DYMOE_EP_NCCL, placement=placement, attn_mass=a.cuda())
+        assert both.check_status(T, ws, placement=placement) == (0, 0)
+        bits = both.views(T, ws, placement=placement)["bits"].cpu().numpy()
+        y_p, _ = both.forward(*args, transport=d.DYMOE_EP_PEER, placement=placement, attn_mass=a.cuda())
+        torch.cuda.synchronize()
+        assert torch.equal(y_n, y_p)
+        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, 9 + s, 32,
+                                o_sched.Ladder((8, 4, 2), (0.25, 0.5)), cfg.k,
+                                phase="prefill" if phase == 0 else "decode", attn_mass=a.numpy(),
+                                forced_bits=bits)
+        err = np.abs(y_n.cpu().numpy() - ref["y"]).max() / np.abs(ref["y"]).max()
+        assert err <= FFN_TOL
+    both.close()
 
 
-def test_ep_p2p_host_barrier_threads():
-    cfg = synthetic.CONFIGS["tiny"].with_tokens(16)
-    res = _run_p2p(4, 0, (8, 4, 2), (0.25, 0.5), 12, cfg, steps=2, barrier="host")
-    for r in range(4):
-        for y1, y2, n2, n1, status in res[r]:
-            assert status == 0 and n1 == n2 and np.array_equal(y1, y2)
+def test_ep_validation_names_the_field():
+    d = D()
+    from paper_2603_19172_b200 import ep
+    cfg = synthetic.CONFIGS["tiny"]
+    ex_all = _experts(cfg)
+    with pytest.raises(d.DymoeError, match="nccl_uid"):
+        ep.EPLayer(0, 1, cfg.M, cfg.k, cfg.hidden, cfg.ffn, 16, ex_all, transports=d.DYMOE_EP_NCCL)
+    L = ep.EPLayer(0, 1, cfg.M, cfg.k, cfg.hidden, cfg.ffn, 16, ex_all)
+    x, lg, a = _inputs(cfg, 0, 0)
+    lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
+    with pytest.raises(d.DymoeError, match="transport: not enabled"):
+        L.forward(x.cuda(), lg.cuda(), lad, 1, 32, 1, transport=d.DYMOE_EP_NCCL)
+    x2, lg2, _ = synthetic.layer_inputs(cfg.with_tokens(17), 1)
+    with pytest.raises(d.DymoeError, match="T: must satisfy"):
+        L.forward(x2.cuda(), lg2.cuda(), lad, 1, 32, 1)
+    with pytest.raises(d.DymoeError, match="opts.phase: DYMOE_EP_REPLICATED"):
+        L.forward(x.cuda(), lg.cuda(), lad, 1, 32, 0, placement=d.DYMOE_EP_REPLICATED,
+                  attn_mass=a.cuda())
+    L.close()
+    with pytest.raises(d.DymoeError, match="world"):
+        ep.EPLayer(0, 9, cfg.M, cfg.k, cfg.hidden, cfg.ffn, 16, ex_all[:0])
 
 
-def test_ep_p2p_prefill_mode_matches_oracle():
-    """Large enough that every owner runs the tcgen05 prefill kernel on received rows; against the
-    unsharded oracle at the FFN bar."""
-    P, T, layer_idx = 2, 200, 7
-    bits_t, lams = (8, 4, 2), (0.25, 0.5)
-    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
-    res = _run_p2p(P, 0, bits_t, lams, layer_idx, cfg, steps=1)
-    experts = [{n: t.float().numpy() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 9)]
-    I = np.zeros(cfg.M)
-    ins = []
-    for r in range(P):
-        x, lg, a = synthetic.layer_inputs(cfg, 500 + r)
-        idx, w, p = o_route.route(lg.numpy(), cfg.k)
-        I = I + o_imp.score_prefill(a.numpy(), idx, cfg.M)[0]
-        ins.append((x, lg))
-    bits, _ = o_sched.assign_bits(I, layer_idx, 32, o_sched.Ladder(bits_t, lams), cfg.k)
-    for r in range(P):
-        x, lg = ins[r]
-        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), experts, layer_idx, 32,
-                                o_sched.Ladder(bits_t, lams), cfg.k, forced_bits=bits)
-        y = res[r][0][1]
-        assert res[r][0][2] > 64
-        err = np.abs(y - ref["y"]).max() / np.abs(ref["y"]).max()
-        assert err <= 2e-3, (r, err)
-
-
-def test_ep_p2p_ipc_processes(tmp_path):
-    """Two processes on one GPU: windows exchanged as CUDA IPC handles and opened in the other
-    process; forward_p2p equals the all-to-all forward bit for bit."""
+def test_ep_peer_ipc_processes(tmp_path):
+    """Two processes on one GPU: windows exchanged as CUDA IPC handles over a gloo group and
+    opened in the other process; device barriers across the processes; each rank's output
+    against the unsharded oracle with the global importance (3 steps, prefill and decode)."""
     import json
     import os
     import subprocess
@@ -235,15 +284,3 @@ def test_ep_p2p_ipc_processes(tmp_path):
     for rank in range(2):
         res = json.load(open("%s.%d" % (out, rank)))
         assert res["ok"] and res["status"] == 0, res
-
-
-@pytest.mark.parametrize("phase,T", [(0, 256), (1, 8)])
-def test_ep_p2p_finegrained_p8(phase, T):
-    """BASELINE.json configs[3]'s layer (64 experts, top-6, hidden 2048, ffn 1408) over 8 ranks
-    (threads, 8 experts each): peer-memory dispatch/combine equals the all-to-all path."""
-    cfg = synthetic.CONFIGS["finegrained"].with_tokens(T)
-    res = _run_p2p(8, phase, (8, 4, 2), (0.25, 0.5), 17, cfg, steps=2)
-    for r in range(8):
-        for y1, y2, n2, n1, status in res[r]:
-            assert status == 0 and n1 == n2 and n2 > 0
-            assert np.array_equal(y1, y2), (r, np.abs(y1 - y2).max())

@@ -205,7 +205,7 @@ FFN_CFGS = [synthetic.CONFIGS["tiny"],
 
 
 @pytest.mark.parametrize("cfg", FFN_CFGS, ids=lambda c: c.name)
-@pytest.mark.parametrize("mode", ["decode", "prefill", "prefill_ts"])
+@pytest.mark.parametrize("mode", ["decode", "prefill"])
 def test_expert_ffn_all_widths(cfg, mode):
     d = D()
     ex = gpu_experts(cfg, 1)
@@ -216,7 +216,7 @@ def test_expert_ffn_all_widths(cfg, mode):
     x, lg, _ = synthetic.layer_inputs(cfg, 1)
     r_idx, _, _ = o_route.route(lg.numpy(), cfg.k)
     perm = o_moe.permute(r_idx, bits, cfg.M)
-    m = {"decode": d.DYMOE_DECODE, "prefill": d.DYMOE_PREFILL, "prefill_ts": d.DYMOE_FFN_PREFILL_TS}[mode]
+    m = {"decode": d.DYMOE_DECODE, "prefill": d.DYMOE_PREFILL}[mode]
     h, y, status = layer.expert_ffn(x.cuda(), torch.from_numpy(bits).cuda(),
                                     torch.from_numpy(perm["expert_off"]).cuda(),
                                     torch.from_numpy(perm["perm_token"]).cuda(), m)
@@ -247,6 +247,37 @@ def test_ffn_width_not_resident_sets_status():
     assert rc == 6 and word == 1
     rc, word = layer.check_status(cfg.T, ws)
     assert rc == 0 and word == 0
+
+
+def test_prefill_width_not_resident_sets_status():
+    """Prefill grouped GEMM: an expert assigned a width that is not resident is left
+    out of the tile schedule with the status bit set -- no TMA on a null descriptor -- and every
+    token not routed to it is still the oracle's."""
+    d = D()
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(200)
+    ex = gpu_experts(cfg, 2, widths=(4,))
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    x, lg, a = synthetic.layer_inputs(cfg, 2)
+    idx, _, _ = o_route.route(lg.numpy(), cfg.k)
+    counts = np.bincount(idx.ravel(), minlength=cfg.M)
+    bad = int(np.argmax(counts))               # > 16 rows: runs on the grouped GEMM
+    assert counts[bad] > 16
+    forced = np.full(cfg.M, 4, np.uint8)
+    forced[bad] = 2                            # Int2 was never quantized
+    y, ws = layer.forward(x.cuda(), lg.cuda(), d.make_ladder((4, 2), (0.5,)), 0, 32,
+                          phase=d.DYMOE_PREFILL, attn_mass=a.cuda(),
+                          forced_bits=torch.from_numpy(forced).cuda())
+    torch.cuda.synchronize()
+    rc, word = layer.check_status(cfg.T, ws)
+    assert rc == 6 and word == 1
+    forced[bad] = 4
+    ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), np_experts(cfg, 2), 0, 32,
+                            o_sched.Ladder((4, 2), (0.5,)), cfg.k, phase="prefill",
+                            attn_mass=a.numpy(), forced_bits=forced)["y"]
+    keep = ~(idx == bad).any(axis=1)
+    yn = y.cpu().numpy()
+    assert np.isfinite(yn).all()
+    assert rel_err(yn[keep], ref[keep]) <= FFN_TOL
 
 
 # ------------------------------------------------------------------------------------ whole layer
@@ -429,24 +460,3 @@ def test_decode_combine_paths(T, out_dtype):
                 assert (np.abs(yg - full) <= bound).all()
 
 
-@pytest.mark.parametrize("T", [600, 1000])
-def test_prefill_operand_swapped_multi_tile(T):
-    """The operand-swapped prefill kernel (DYMOE_FFN_PREFILL_TS) on enough tokens that experts span
-    several 192-token tiles plus a ragged tail (N rounded up to 32): the whole layer equals the
-    oracle (bits exact, y within the FFN bar)."""
-    d = D()
-    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
-    ex = gpu_experts(cfg, 8)
-    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
-    x, lg, a = synthetic.layer_inputs(cfg, 8)
-    y, ws = layer.forward(x.cuda(), lg.cuda(), d.make_ladder((16, 8, 4, 2), (0.2, 0.5, 0.8)), 9, 32,
-                          phase=d.DYMOE_PREFILL, attn_mass=a.cuda(), ffn_mode=d.DYMOE_FFN_PREFILL_TS)
-    torch.cuda.synchronize()
-    ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), np_experts(cfg, 8), 9, 32,
-                            o_sched.Ladder((16, 8, 4, 2), (0.2, 0.5, 0.8)), cfg.k, phase="prefill",
-                            attn_mass=a.numpy())
-    v = layer.views(T, ws)
-    assert np.array_equal(v["bits"].cpu().numpy(), ref["bits"])
-    counts = np.diff(ref["expert_off"])
-    assert counts.max() > 192            # at least one expert spans several tiles
-    assert rel_err(y.cpu().numpy(), ref["y"]) <= FFN_TOL

@@ -13,7 +13,6 @@ import torch  # noqa: E402
 
 import synthetic  # noqa: E402
 import paper_2603_19172_b200.dymoe as d  # noqa: E402
-from paper_2603_19172_b200 import ep  # noqa: E402
 
 
 def main():
@@ -29,11 +28,13 @@ def main():
         bits = torch.full((cfg.M,), 4, dtype=torch.uint8, device=dev)
         off, pt, ps, inv = d.dymoe_permute(idx, cfg.M, bits)
         rows = int(off[-1].item())
-        comm = ep.ThreadComm(1).bind(0)
-        win = ep.PeerWindows(comm, cfg.M, cfg.hidden, rows, barrier="device", device=dev)
+        base, _ = d.dymoe_ep_window_alloc(d.dymoe_ep_window_bytes(1, cfg.M, cfg.hidden, rows))
+        peers = torch.tensor([base], dtype=torch.int64, device=dev)
+        win = d.EpWindow(1, 0, cfg.M, cfg.hidden, rows, 0, peers.data_ptr())
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
         recv_off = torch.empty(cfg.M + 1, dtype=torch.int32, device=dev)
-        d.dymoe_ep_publish_counts(win.win, off)
-        d.dymoe_ep_barrier(win.win, 1, win.status)
+        d.dymoe_ep_publish_counts(win, off)
+        d.dymoe_ep_barrier(win, 1, status)
 
         def timed(fn, reps=50):
             for _ in range(5):
@@ -47,14 +48,15 @@ def main():
             torch.cuda.synchronize()
             return e0.elapsed_time(e1) / reps * 1e3   # us
 
-        t_disp = timed(lambda: d.dymoe_ep_dispatch(win.win, x, off, pt, recv_off, win.status))
-        t_comb = timed(lambda: d.dymoe_ep_combine(win.win, inv, w, off))
+        t_disp = timed(lambda: d.dymoe_ep_dispatch(win, x, off, pt, recv_off, status))
+        t_comb = timed(lambda: d.dymoe_ep_combine(win, inv, w, off, status=status))
         b_disp = rows * cfg.hidden * 2 * 2
         b_comb = rows * cfg.hidden * 4 + cfg.T * cfg.hidden * 4
         out.append({"config": name, "rows": rows, "dispatch_us": round(t_disp, 2),
                     "dispatch_GBs": round(b_disp / t_disp / 1e3, 1), "combine_us": round(t_comb, 2),
-                    "combine_GBs": round(b_comb / t_comb / 1e3, 1), "status": int(win.status.item())})
-        win.close()
+                    "combine_GBs": round(b_comb / t_comb / 1e3, 1), "status": int(status.item())})
+        torch.cuda.synchronize()
+        d.dymoe_ep_window_free(base)
     print(json.dumps({"ep_kernels_one_gpu": out, "hbm_peak": peak.get("hbm_gbs")}))
 
 

@@ -25,7 +25,6 @@ def main():
     ap.add_argument("--layer", type=int, default=20)
     ap.add_argument("--input", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=2)
-    ap.add_argument("--ffn-mode", default="auto", choices=["auto", "ts"])
     args = ap.parse_args()
     import paper_2603_19172_b200.dymoe as d
     dev = torch.device("cuda", 0)
@@ -39,7 +38,7 @@ def main():
     lad = d.make_ladder(bench.LADDER_BITS, bench.LADDER_LAMBDAS)
     for _ in range(args.warmup + 1):
         y, _ = layer.forward(x, lg, lad, args.layer, bench.NUM_LAYERS, phase=phase, attn_mass=a, ws=ws,
-                             ffn_mode=d.DYMOE_FFN_PREFILL_TS if args.ffn_mode == "ts" else -1)
+                             ffn_mode=-1)
     torch.cuda.synchronize()
     v = layer.views(cfg.T, ws)
     bits = v["bits"].cpu().numpy()
