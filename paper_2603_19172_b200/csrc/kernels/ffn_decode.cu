@@ -283,11 +283,13 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
     if (++j_iss == cmax) { j_iss = 0; tile_iss += NSG; }
     const uint32_t sq = seq + q;
     const int p = warp + WPT * j;
+    const uint32_t slot = sq % S;
+    // every phase is waited on, including the empty items' (arrive-only) phases: no mbarrier
+    // phase completes unobserved (compute-sanitizer synccheck), at no cost (already complete)
+    mbar_wait(bars + slot * 8, (sq / S) & 1);
     if (p < npr) {
-      const uint32_t slot = sq % S;
       const uint32_t cs = cring + slot * C::CODES;
       const uint32_t ms = mring + slot * C::META;
-      mbar_wait(bars + slot * 8, (sq / S) & 1);
 #pragma unroll
       for (int sub = 0; sub < NSUB; ++sub) {
         const int ci = NSUB * p + sub;

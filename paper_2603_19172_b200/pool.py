@@ -17,8 +17,15 @@ One step of layer l (`forward`):
      the expert (dymoe_layer_set_expert).  BF16 requests are served by the masters (outside the
      budget).  Every expert of the step is pinned while the step is prepared;
   3. dymoe_moe_forward with the SERVED widths as forced bits.
-`prefetch(l, bits)` runs step 2 ahead of time (e.g. for the widths dymoe_predict_next predicts
-for the next layer), on the caller's stream.
+`prefetch(l, bits, stream, after)` runs step 2 ahead of time on a SIDE stream (SURVEY §8f f1;
+PAPER.md "Phase-Adaptive Prefetcher"): the look-ahead predictor dymoe_predict_next
+(Eqs. 6-8) names layer l+1's likely critical experts from layer l's hidden state, and their
+high-precision formats are quantized into the arena while layer l's FFN runs on the main stream
+(`PrefetchingStack` below).  Ordering: the side stream first waits for `after` (an event the main
+stream recorded once every kernel of earlier layers was queued before it), so an eviction never
+overwrites a slot an in-flight kernel still reads; the experts of the running layer are pinned
+while the prefetch decides its evictions; layer l+1's step waits for the prefetch's completion
+event before it touches the pool.
 
 Host-offload variant (the paper's own setting): with masters in (pinned)
 host memory, BF16 becomes a pool format like the packed ones (the arena holds a bf16 copy), and a
@@ -60,7 +67,10 @@ class ExpertStore:
         else:
             self.layers = [d.MoELayer([dict(e) for e in ml], k_route, hidden, ffn) for ml in masters]
         self.bound = [[None] * self.M for _ in range(self.L)]   # (bits, offset) of the bound format
-        self.stats = dict(hits=0, misses=0, promotions=0, evictions=0, quantized_bytes=0)
+        self.stats = dict(hits=0, misses=0, promotions=0, evictions=0, quantized_bytes=0,
+                          prefetched=0, prefetch_hits=0)
+        self.ready = {}            # layer -> event: its prefetch has finished on the side stream
+        self.prefetched = set()    # (layer, expert) inserted by a prefetch, not yet used by a step
 
     # ------------------------------------------------------------------ arena layout
     def _shapes(self):
@@ -104,10 +114,14 @@ class ExpertStore:
         self.bound[l][e] = (bits, off) if bits is not None else None
 
     # ------------------------------------------------------------------ policy
-    def prepare(self, l, bits, stream=None):
-        """Make every requested width of layer l resident; returns the served widths (list)."""
+    def prepare(self, l, bits, stream=None, keep_pinned=(), prefetch=False):
+        """Make every requested width of layer l resident; returns the served widths (list).
+        keep_pinned: (layer, expert) keys held pinned while this call decides evictions."""
         served = [0] * self.M
         pinned = []
+        for key in keep_pinned:
+            self.pool.pin(*key)
+            pinned.append(key)
         try:
             for e, b in enumerate(bits):
                 b = int(b)
@@ -116,14 +130,23 @@ class ExpertStore:
                     continue
                 out, sb, off = self.pool.lookup(l, e, b)
                 if out == d.POOL_HIT:
-                    self.stats["hits"] += 1
+                    if not prefetch:
+                        self.stats["hits"] += 1
+                        if (l, e) in self.prefetched:
+                            self.stats["prefetch_hits"] += 1
+                            self.prefetched.discard((l, e))
                     if self.bound[l][e] != (sb, off):
                         self._bind(l, e, sb, off, stream)
                 else:
-                    self.stats["misses" if out == d.POOL_MISS else "promotions"] += 1
+                    if prefetch:
+                        self.stats["prefetched"] += 1
+                        self.prefetched.add((l, e))
+                    else:
+                        self.stats["misses" if out == d.POOL_MISS else "promotions"] += 1
                     off, evicted = self.pool.insert(l, e, b, self.entry_bytes(b))
                     for (l2, e2) in evicted:
                         self.stats["evictions"] += 1
+                        self.prefetched.discard((l2, e2))
                         self._bind(l2, e2, None, None, stream)
                     views = self._views(off, b)
                     src = self._source(l, e, stream)
@@ -145,7 +168,21 @@ class ExpertStore:
                 self.pool.unpin(pl, pe)
         return served
 
-    prefetch = prepare
+    def prefetch(self, l, bits, stream, after=None, keep_pinned=()):
+        """prepare(l, bits) on the side `stream` (after the main stream's event `after`); the
+        completion event is what layer l's step waits for (`ready[l]`)."""
+        if after is not None:
+            stream.wait_event(after)
+        self.prepare(l, bits, stream, keep_pinned=keep_pinned, prefetch=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.ready[l] = ev
+        return ev
+
+    def wait_ready(self, l, stream=None):
+        ev = self.ready.pop(l, None)
+        if ev is not None:
+            (stream or torch.cuda.current_stream()).wait_event(ev)
 
     def _source(self, l, e, stream):
         """The expert's bf16 master on the device (host-offload: copied into the staging buffer)."""
@@ -169,9 +206,10 @@ class ExpertStore:
         return (bits * active.to(bits.dtype)).cpu().tolist(), bits
 
     def forward(self, l, x, logits, ladder, num_layers, phase=d.DYMOE_DECODE, attn_mass=None,
-                k_tokens=0, stream=None):
+                k_tokens=0, stream=None, out=None, out_dtype=d.DYMOE_OUT_F32, residual=None):
         """One pooled layer step; returns (y, served widths, requested widths, forced widths the
         forward ran with: served for routed experts, assigned for the others)."""
+        self.wait_ready(l, stream)          # a prefetch of this layer has finished writing
         want, bits_dev = self.assigned_bits(l, x, logits, ladder, num_layers, phase, attn_mass, k_tokens)
         served = self.prepare(l, want, stream)
         # experts not routed this step keep their assigned width (they run no rows)
@@ -179,5 +217,60 @@ class ExpertStore:
         forced_t = torch.tensor(forced, dtype=torch.uint8, device=x.device)
         y, _ = self.layers[l].forward(x, logits, ladder, l, num_layers, phase=phase,
                                       attn_mass=attn_mass, k_tokens=k_tokens, forced_bits=forced_t,
-                                      stream=stream)
+                                      stream=stream, out=out, out_dtype=out_dtype, residual=residual)
         return y, served, want, forced
+
+
+class PrefetchingStack:
+    """A layer stack (stack.MoEStack's block: RMSNorm -> router -> MoE -> residual) over an
+    ExpertStore whose arena is smaller than the packed formats of the whole stack, with the
+    paper's look-ahead prefetcher (Eqs. 6-8, steps 5-6 of
+    P:203): at layer l, dymoe_predict_next on l's normed hidden state with layer l+1's gate names
+    the top-t experts of l+1 (prefill: token frequency, Eq. 7; decode: the predicted gate, Eq. 8),
+    t = layer l+1's high-tier count (Eq. 5); their top-tier formats are quantized into the arena on
+    a side stream while layer l's FFN runs on the main stream.  prefetch=False: every format is
+    loaded on demand (the baseline the overlap is measured against)."""
+
+    def __init__(self, store, gates):
+        self.store = store
+        self.gates = gates
+        self.L, self.M, self.k = store.L, store.M, store.k
+        self.side = torch.cuda.Stream(device=store.device)
+
+    def forward(self, x, ladder, phase=d.DYMOE_DECODE, attn_masses=None, prefetch=True, eps=1e-5,
+                trace=False):
+        s = self.store
+        main = torch.cuda.current_stream()
+        T = x.shape[0]
+        u = torch.empty_like(x)
+        bufs = (torch.empty_like(x), torch.empty_like(x))
+        logits = torch.empty(T, self.M, dtype=torch.float32, device=x.device)
+        cur, out_trace = x, [] if trace else None
+        for l in range(self.L):
+            start = torch.cuda.Event()
+            start.record(main)                   # every kernel of layers < l is queued before it
+            wg, beta = self.gates[l]
+            d.dymoe_rmsnorm(cur, eps, out=u)
+            d.dymoe_gate_logits(u, wg, beta, out=logits)
+            nxt = bufs[l & 1]
+            a = attn_masses[l] if attn_masses is not None else None
+            req = None
+            if prefetch and l + 1 < self.L:
+                # Eqs. 6-8 on the device; the requests are read back before this layer's FFN is
+                # queued (the step synchronises for its own bits anyway), so nothing waits for it
+                t_hi = d.dymoe_tier_counts(l + 1, self.L, ladder, self.M, self.k)
+                t = max(1, t_hi[0] if t_hi else self.M)
+                ex, _, _ = d.dymoe_predict_next(phase, u, self.gates[l + 1][0], self.k, t)
+                req = [0] * self.M
+                for e in ex.cpu().tolist():
+                    req[e] = ladder.bits[0]
+            y, served, want, forced = s.forward(l, u, logits, ladder, self.L, phase=phase,
+                                                attn_mass=a, out=nxt, out_dtype=d.DYMOE_OUT_BF16,
+                                                residual=cur)
+            if req is not None:
+                keep = [(l, e) for e in range(self.M) if want[e]]
+                s.prefetch(l + 1, req, self.side, after=start, keep_pinned=keep)
+            if trace:
+                out_trace.append((cur.clone(), u.clone(), logits.clone(), list(forced), list(served)))
+            cur = nxt
+        return cur, out_trace

@@ -58,17 +58,25 @@ def _run_threads(P, cfg, phase, lad, layer_idx, steps=3, placement=0, transport=
     ex_all = _experts(cfg)
     layers = _make_layers(P, cfg, ex_all, d.DYMOE_EP_PEER, cfg.T)
     results, errors = {}, []
+    # every allocation and host->device copy before the ranks start: a cudaMalloc / pageable copy
+    # in one thread while another rank's flag barrier spins can wait for the device to idle
+    ins = {(r, s): tuple(t.cuda() for t in _inputs(cfg, 0 if same_batch else r, s))
+           for r in range(P) for s in range(steps)}
+    wss = [l.workspace(cfg.T, placement=placement) for l in layers]
+    outs = [torch.empty(cfg.T, cfg.hidden, device="cuda") for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    torch.cuda.synchronize()
 
     def worker(r):
         try:
             torch.cuda.set_device(0)
-            with torch.cuda.stream(torch.cuda.Stream()):
+            with torch.cuda.stream(streams[r]):
                 out = []
                 for s in range(steps):
-                    x, lg, a = _inputs(cfg, 0 if same_batch else r, s)
-                    y, ws = layers[r].forward(x.cuda(), lg.cuda(), lad, (layer_idx + s) % 32, 32, phase,
+                    x, lg, a = ins[(r, s)]
+                    y, ws = layers[r].forward(x, lg, lad, (layer_idx + s) % 32, 32, phase,
                                               transport=transport, placement=placement,
-                                              attn_mass=a.cuda(), **kw)
+                                              attn_mass=a, ws=wss[r], out=outs[r], **kw)
                     v = layers[r].views(x.shape[0], ws, placement=placement)
                     rc, word = layers[r].check_status(x.shape[0], ws, placement=placement)
                     out.append((y.float().cpu().numpy(), v["bits"].cpu().numpy(),
@@ -158,14 +166,19 @@ def test_ep_peer_bf16_output_and_residual():
     ex_all = _experts(cfg)
     layers = _make_layers(P, cfg, ex_all, d.DYMOE_EP_PEER, cfg.T)
     outs, errors = {}, []
+    ins = [tuple(t.cuda() for t in _inputs(cfg, r, 0)) for r in range(P)]
+    wss = [l.workspace(cfg.T) for l in layers]
+    o32 = [torch.empty(cfg.T, cfg.hidden, device="cuda") for _ in range(P)]
+    o16 = [torch.empty(cfg.T, cfg.hidden, device="cuda", dtype=torch.bfloat16) for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    torch.cuda.synchronize()
 
     def worker(r):
         try:
-            with torch.cuda.stream(torch.cuda.Stream()):
-                x, lg, a = _inputs(cfg, r, 0)
-                xc = x.cuda()
-                y32, _ = layers[r].forward(xc, lg.cuda(), lad, 3, 32, 0, attn_mass=a.cuda())
-                yb, _ = layers[r].forward(xc, lg.cuda(), lad, 3, 32, 0, attn_mass=a.cuda(),
+            with torch.cuda.stream(streams[r]):
+                xc, lg, a = ins[r]
+                y32, _ = layers[r].forward(xc, lg, lad, 3, 32, 0, attn_mass=a, ws=wss[r], out=o32[r])
+                yb, _ = layers[r].forward(xc, lg, lad, 3, 32, 0, attn_mass=a, ws=wss[r], out=o16[r],
                                           out_dtype=d.DYMOE_OUT_BF16, residual=xc)
                 torch.cuda.current_stream().synchronize()
                 outs[r] = (y32, yb, xc)

@@ -84,3 +84,57 @@ def test_host_offload_stack_matches_oracle():
         err = np.abs(y.cpu().numpy() - ref["y"]).max() / max(np.abs(ref["y"]).max(), 1e-30)
         assert err <= FFN_TOL, (step, err)
     assert store.stats["h2d_bytes"] > 0 and store.stats["evictions"] > 0, store.stats
+
+
+@pytest.mark.parametrize("phase,T", [("decode", 8), ("prefill", 64)])
+def test_prefetching_stack_matches_oracle(phase, T):
+    """f1 (Eqs. 6-8): a 4-layer stack over a pooled arena at 40 % of its packed formats,
+    the next layer's predicted critical experts quantized on a side stream while the current
+    layer runs.  Teacher-forced layer by layer: every layer equals the oracle stack layer run with
+    the widths the step served; prefetches happen and some of them serve the next step."""
+    import paper_2603_19172_b200.dymoe as d
+    from paper_2603_19172_b200.pool import ExpertStore, PrefetchingStack
+    from oracle import stack as o_stack
+    from validity import check_logits, check_topk, gate_logit_bound
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+    L = 4
+    masters = [[{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 80 + l)]
+               for l in range(L)]
+    gates = [synthetic.stack_gate(cfg, l, 3) for l in range(L)]
+    probe = ExpertStore(masters[:1], cfg.k, cfg.hidden, cfg.ffn, 1 << 20)
+    full = L * cfg.M * sum(probe.entry_bytes(b) for b in (8, 4, 2))
+    del probe
+    np_masters = [[{n: t.float().cpu().numpy() for n, t in e.items()} for e in ml] for ml in masters]
+    lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
+    o_lad = o_sched.Ladder((8, 4, 2), (0.25, 0.5))
+    ph = d.DYMOE_PREFILL if phase == "prefill" else d.DYMOE_DECODE
+    for prefetch in (True, False):
+        store = ExpertStore(masters, cfg.k, cfg.hidden, cfg.ffn, int(full * 0.4))
+        st = PrefetchingStack(store, [(w.cuda(), b.cuda()) for w, b in gates])
+        attn = [synthetic.attention_mass(cfg, 300 + l).cuda() for l in range(L)] if ph == d.DYMOE_PREFILL else None
+        for rep in range(3):
+            x0 = synthetic.hidden_states(cfg, 50 + rep).cuda()
+            xL, tr = st.forward(x0, lad, phase=ph, attn_masses=attn, prefetch=prefetch, trace=True)
+            torch.cuda.synchronize()
+            for l in range(L):
+                x_in = tr[l][0].float().cpu().numpy().astype(np.float64)
+                u = tr[l][1].float().cpu().numpy().astype(np.float64)
+                wg, beta = gates[l]
+                lg_ref = o_stack.router_logits(u, wg.float().numpy(), beta.numpy())
+                bound = gate_logit_bound(u, wg.float().numpy(), lg_ref)
+                check_logits(tr[l][2].cpu().numpy(), lg_ref, bound)
+                from oracle import route as o_route
+                assert not check_topk(o_route.route(tr[l][2].cpu().numpy(), cfg.k)[0], lg_ref, bound).any()
+                ref = o_moe.moe_forward(u.astype(np.float32), lg_ref, np_masters[l], l, L, o_lad, cfg.k,
+                                        phase=phase, attn_mass=attn[l].cpu().numpy() if attn else None,
+                                        forced_bits=np.array(tr[l][3], np.uint8))["y"]
+                full_ref = o_stack.residual(x_in, ref)
+                x_out = (tr[l + 1][0] if l + 1 < L else xL).float().cpu().numpy().astype(np.float64)
+                bound = FFN_TOL * np.abs(ref).max() + np.abs(full_ref) * 2.0 ** -7
+                assert (np.abs(x_out - full_ref) <= bound).all(), (prefetch, rep, l)
+        s = store.stats
+        assert store.pool.used() <= store.pool.capacity
+        if prefetch:
+            assert s["prefetched"] > 0 and s["prefetch_hits"] > 0, s
+        else:
+            assert s["prefetched"] == 0, s
