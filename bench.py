@@ -771,8 +771,11 @@ def measure_extras(d, cfg, phase, device, peaks, reps=10):
         k = torch.randn(H, T, 128, generator=g, device=device).to(torch.bfloat16)
         us = timed(lambda: d.dymoe_attention_mass(q, k))
         fl = 2 * 2 * T * T * 128 * H / 2
-        out["attention_mass"] = {"us": us, "TFLOP/s": fl / (us * 1e-6) / 1e12, "H": H, "d": 128,
-                                 "note": "two causal Q.K^T passes (row stats, column sums), mma.sync"}
+        tf = fl / (us * 1e-6) / 1e12
+        out["attention_mass"] = {"us": us, "TFLOP/s": tf, "frac_bf16_burst": tf / peaks["bf16"],
+                                 "H": H, "d": 128, "T": T,
+                                 "note": "two causal Q.K^T passes on tcgen05 (row stats, column sums "
+                                         "of P from TMEM), 2 x 2 T^2 d H / 2 flops; timed alone"}
     return out
 
 
@@ -1008,6 +1011,113 @@ def run_stack(args, device):
             "gpu_launches": per_layer * L * K}
 
 
+def run_stack_ep(args, rank, world, device):
+    """SURVEY §8d C5 / BASELINE.json configs[4] as named: the 32-layer Mixtral-8x7B-shaped stack
+    expert-parallel over the ranks (paper_2603_19172_b200.stack.EPStack: per layer RMSNorm and
+    router on the rank's own tokens, then dymoe_moe_forward_ep -- global importance, exchange,
+    owners' fused-dequant FFN, combine with the residual).  Each rank holds its block of every
+    layer's experts (packed widths only) and brings its own batch (weak scaling).  value = tokens
+    of all ranks through all 32 layers per second (max over ranks)."""
+    import paper_2603_19172_b200.dymoe as d
+    from paper_2603_19172_b200 import ep
+    from paper_2603_19172_b200.stack import EPStack
+    d.lib()
+    torch.cuda.set_device(device)
+    peaks = load_peaks()
+    prefill = args.workload == "stack_prefill"
+    T = args.tokens if prefill else args.batch
+    cfg = synthetic.CONFIGS["stack"].with_tokens(T)
+    L = cfg.layers
+    phase = d.DYMOE_PREFILL if prefill else d.DYMOE_DECODE
+    gloo = torch.distributed.get_backend() != "nccl"
+    transports = d.DYMOE_EP_PEER if gloo else (d.DYMOE_EP_NCCL | d.DYMOE_EP_PEER)
+    uid = None if gloo else ep.broadcast_unique_id()
+    first, last = ep.owned_range(rank, cfg.M, world)
+    local = []
+    for l in range(L):
+        ex = synthetic.expert_weights(cfg, 3000 + l, device, experts=list(range(first, last)))
+        ex = [{n: t for n, t in e.items()} for e in ex]
+        d.quantize_experts(ex, (8, 4, 2))
+        torch.cuda.synchronize()
+        for e in ex:          # the ladder has no BF16 tier: keep only the packed widths
+            for n in ("w1", "w3", "w2"):
+                del e[n]
+        local.append(ex)
+    torch.cuda.empty_cache()
+    h = ep.EPLayer(rank, world, cfg.M, cfg.k, cfg.hidden, cfg.ffn, T, local[0],
+                   transports=transports, nccl_uid=uid)
+    opened = ep.connect_processes(h) if gloo else []
+    gates = [synthetic.stack_gate(cfg, l, 7, device) for l in range(L)]
+    st = EPStack(h, local, gates)
+    x = synthetic.hidden_states(cfg, 8 + rank, device)
+    attn = [synthetic.attention_mass(cfg, 400 + l, device) for l in range(L)] if prefill else None
+    ladder = d.make_ladder(LADDER_BITS, LADDER_LAMBDAS)
+    ws = h.workspace(T)
+    bufs = (torch.empty_like(x), torch.empty_like(x), torch.empty_like(x))
+    logits = torch.empty(T, cfg.M, dtype=torch.float32, device=device)
+    K, W = args.steps, args.warmup
+    lines = {}
+    for name, tp in (("peer", d.DYMOE_EP_PEER), ("nccl", d.DYMOE_EP_NCCL)):
+        if not (transports & tp):
+            continue
+        for _ in range(W):
+            st.forward(x, ladder, phase, tp, attn, ws=ws, bufs=bufs, logits=logits)
+        torch.cuda.synchronize()
+        torch.distributed.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            t0.record()
+            for _ in range(K):
+                st.forward(x, ladder, phase, tp, attn, ws=ws, bufs=bufs, logits=logits)
+            t1.record()
+            torch.cuda.synchronize()
+        torch.distributed.barrier()
+        ms = _max_over_ranks(t0.elapsed_time(t1), device)
+        word = int(_max_over_ranks(float(h.check_status(T, ws)[1]), device))
+        lines[name] = {"value": T * world * K / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms / K,
+                       "status": word, "clocks": clk.summary()}
+    main = "peer" if "peer" in lines and lines["peer"]["status"] == 0 else "nccl"
+    tp_main = d.DYMOE_EP_PEER if main == "peer" else d.DYMOE_EP_NCCL
+    L0 = lines[main]
+    # e2e: the rank's x from pinned host memory in, its final stream out, every pass
+    hx = x.cpu().pin_memory()
+    hy = torch.empty_like(hx).pin_memory()
+    dx = torch.empty_like(x)
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        dx.copy_(hx, non_blocking=True)
+        y, _ = st.forward(dx, ladder, phase, tp_main, attn, ws=ws, bufs=bufs, logits=logits)
+        hy.copy_(y, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e_ms = _max_over_ranks(e0.elapsed_time(e1), device)
+    torch.distributed.barrier()
+    ep.disconnect(opened)
+    h.close()
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": L0["value"], "unit": "tokens/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": L0["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 x int8/int4/int2 (fp32 accum)",
+            "data": "synthetic (seeded random-init Mixtral-8x7B-shaped experts and routers per layer)",
+            "config": {"workload": "mixtral_stack32_%s" % ("prefill" if prefill else "decode"),
+                       "layers": L, "hidden": cfg.hidden, "ffn": cfg.ffn, "experts": cfg.M, "top_k": cfg.k,
+                       "tokens_per_step_per_rank": T, "global_batch": T * world,
+                       "ladder": {"bits": LADDER_BITS, "lambdas": LADDER_LAMBDAS},
+                       "l2": "inputs larger than L2 (32 distinct layers of packed weights)",
+                       "parallelism": "ep%d: every layer's experts sharded, dymoe_moe_forward_ep over %s" % (
+                           world, "peer-memory windows" if main == "peer" else "the library's NCCL communicator")},
+            "ms_per_layer": L0["ms_per_step"] / L, "roofline": None, "clocks": L0["clocks"],
+            "e2e": {"value": T * world * K / (e_ms / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int(hx.numel() * 2), "d2h_bytes_per_step": int(hy.numel() * 2)},
+            "gpu_launches": (17 if main == "peer" else 13) * L * K,
+            "ep_path": main, "ep_transports": {k: {kk: v[kk] for kk in ("value", "ms_per_step", "status")}
+                                               for k, v in lines.items()}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1069,8 +1179,9 @@ def main():
             torch.distributed.init_process_group("gloo")
     if args.workload.startswith("stack"):
         if world > 1:
-            raise SystemExit("--workload stack runs on one GPU (the EP stack needs 8 GPUs)")
-        res = run_stack(args, torch.device("cuda", local))
+            res = run_stack_ep(args, rank, world, torch.device("cuda", local))
+        else:
+            res = run_stack(args, torch.device("cuda", local))
     elif world > 1:
         res = run_ep(args, rank, world, torch.device("cuda", local))
     else:

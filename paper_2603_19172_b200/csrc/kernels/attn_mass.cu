@@ -1,193 +1,302 @@
 // Heavy-hitter attention mass without materializing P (Eq. 1 input,
 // P:216-221, reading R1): a[h][j] = sum_{i >= j} softmax_{j' <= i}(scale q_i . k_j')[j].
 //
-// Two passes over causal 64 x 64 blocks of S = Q K^T on the tensor cores (mma.sync m16n8k16,
-// bf16 -> fp32; the score tiles stay in registers):
-//   pass 1 (row statistics): per query row i, m_i = max_j s_ij and l_i = sum_j exp(s_ij - m_i)
-//            (online over key blocks, as in flash attention);
-//   pass 2 (column sums): each warp owns 16 keys and walks every query block at or below the
-//            diagonal, computing S^T = K Q^T so that the column sums of P are row sums of its
-//            accumulator tile, adds exp(s_ij - m_i) / l_i, and writes its 16 a[h][j] once.
-// Sums run in a fixed order (deterministic).  Roofline: tensor (2 x T^2 d H flops, causal half).
+// Two passes over causal 128 x 128 blocks of the score matrix on the 5th-generation tensor cores
+// (tcgen05.mma.cta_group::1.kind::f16, M = N = 128, K = d = 128, bf16 -> fp32 in TMEM):
+//   pass 1 (row statistics): one work item = (head, 128-query block); S = Q_blk K_blk^T for every
+//            key block at or below the diagonal; each epilogue thread owns one query row (one TMEM
+//            lane) and keeps m_i = max_j s_ij, l_i = sum_j exp(s_ij - m_i) online;
+//   pass 2 (column sums): one work item = (head, 128-key block); S^T = K_blk Q_blk^T for every
+//            query block at or after the diagonal, so that a TMEM lane holds one KEY and its
+//            row of 128 queries: each epilogue thread adds exp(s_ij - m_i) / l_i over the
+//            queries (ascending, one fp32 chain per key -- deterministic) and writes a[h][j].
+// Per CTA (persistent, one per SM): warp 0 lane 0 streams the tiles by TMA (the work item's A
+// tile once into one of two buffers, B tiles through a 3-stage ring; 128B-swizzled K-major, two 64-column boxes per
+// 128 x 128 tile), warp 1 owns TMEM (two 128-column accumulators) and one lane issues the MMAs,
+// warps 2-5 drain TMEM (tcgen05.ld 32x32b) and do the softmax arithmetic -- the MMA of block
+// n + 1 overlaps the exponentials of block n.  Work items are handed out longest first.
+// Roofline: tensor (2 passes x 2 T^2 d H / 2 causal flops) with the SFU's exp2 alongside.
 #include "../dymoe_internal.cuh"
 
 namespace dymoe {
 namespace attn {
 
-constexpr int D = 128;        // head dim
-constexpr int BQ = 64;        // rows per block (4 warps x 16)
-constexpr int RS = D / 2 + 4; // padded smem row stride in 32-bit words (conflict-free fragments)
+constexpr int D = 128;            // head dim (= MMA K)
+constexpr int BT = 128;           // rows / columns per block (MMA M = N)
+constexpr int NST = 3;            // B-tile ring stages
+constexpr int CHUNK = BT * 128;   // one 64-column box: 128 rows x 128 bytes
+constexpr int TILE = 2 * CHUNK;   // 32 KB
+constexpr int kSmem = (2 + NST) * TILE + 1024;   // A double-buffered by item, B ring
+constexpr int kThreads = 192;     // warps 0 (TMA), 1 (TMEM + MMA), 2-5 (epilogue)
+constexpr uint32_t TMEM_COLS = 2 * BT;
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BT >> 3) << 17) |
+                           ((uint32_t)(BT >> 4) << 24);   // kind::f16: bf16 x bf16 -> f32, K-major
 
-__device__ __forceinline__ void mma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                    uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, int x, int y, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(IDESC), "r"(acc)
+      : "memory");
+}
+// K-major, 128-byte swizzle, 8-row atoms 1024 B apart (rows of 128 bytes)
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  d |= (uint64_t)2u << 61;
+  return d;
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t (&r)[32] = reinterpret_cast<uint32_t(&)[32]>(v);
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void epi_sync() {   // the 128 epilogue threads only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
-// rows [r0, r0 + 64) of a [T][D] bf16 matrix into smem (words, stride RS); rows >= T zero-filled
-__device__ __forceinline__ void load_block(uint32_t* dst, const uint16_t* src, int r0, int T) {
-  for (int i = threadIdx.x; i < BQ * (D / 8); i += blockDim.x) {
-    const int r = i / (D / 8), c = i - r * (D / 8);
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r0 + r < T) v = *reinterpret_cast<const uint4*>(src + (size_t)(r0 + r) * D + c * 8);
-    *reinterpret_cast<uint4*>(dst + r * RS + c * 4) = v;
-  }
+// Work item n (longest first) -> (head, block of the A operand, first and end B block).
+// Pass 1: A = query block qb, B = key blocks 0 .. qb.  Pass 2: A = key block kb, B = query
+// blocks kb .. nb - 1.
+template <bool COLS>
+__device__ __forceinline__ void item_at(int n, int H, int nb, int& h, int& a, int& b0, int& b1) {
+  const int r = n / H;   // rank in the cost order
+  h = n - r * H;
+  if (COLS) { a = r; b0 = r; b1 = nb; }
+  else { a = nb - 1 - r; b0 = 0; b1 = a + 1; }
 }
 
-// A fragments of 16 rows (r0 .. r0+15 of the smem block) over all D: 8 k-steps x 4 words
-__device__ __forceinline__ void a_frags(const uint32_t* s, int r0, uint32_t (&a)[D / 16][4]) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
-#pragma unroll
-  for (int ks = 0; ks < D / 16; ++ks) {
-    a[ks][0] = s[(r0 + g) * RS + ks * 8 + c];
-    a[ks][1] = s[(r0 + g + 8) * RS + ks * 8 + c];
-    a[ks][2] = s[(r0 + g) * RS + ks * 8 + 4 + c];
-    a[ks][3] = s[(r0 + g + 8) * RS + ks * 8 + 4 + c];
-  }
-}
+template <bool COLS>
+__global__ void __launch_bounds__(kThreads, 1)
+k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+            int H, int T, float scale_log2, float* __restrict__ m_io, float* __restrict__ l_io,
+            float* __restrict__ a_out) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], tfull_bar[2], tempty_bar[2];
+  __shared__ __align__(8) uint64_t a_full[2], a_empty[2];
+  __shared__ uint32_t tmem_base_sh;
+  __shared__ __align__(16) float s_m[2][BT], s_il[2][BT];   // pass 2: the query block's m, 1/l
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t sA0 = smem_u32(smem);
+  auto sA = [&](int it) { return sA0 + (uint32_t)(it & 1) * TILE; };
+  auto sB = [&](int s) { return sA0 + (uint32_t)(2 + s) * TILE; };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = (T + BT - 1) / BT;
+  const int n_items = H * nb;
+  const CUtensorMap* tmA = COLS ? &tmK : &tmQ;
+  const CUtensorMap* tmB = COLS ? &tmQ : &tmK;
 
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                        uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
-}
-
-// acc[n][.] = (rows of A) x (rows n*8.. of the smem block B)^T, 8 n-tiles of 8 columns.
-// B fragments by ldmatrix.x4: matrices (k 0-7, k 8-15) x (n-tiles 2p, 2p+1) of each k16 step.
-__device__ __forceinline__ void tile_product(const uint32_t (&a)[D / 16][4], const uint32_t* sb,
-                                             float (&acc)[8][4]) {
-  const int lane = threadIdx.x & 31;
-  // lane l supplies the row address of matrix l / 8: n-tile 2p + (l / 16), k half (l / 8) & 1
-  const uint32_t base = (uint32_t)__cvta_generic_to_shared(sb) +
-                        (uint32_t)(((lane >> 4) * 8 + (lane & 7)) * RS * 4 + ((lane >> 3) & 1) * 16);
-#pragma unroll
-  for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-#pragma unroll
-  for (int ks = 0; ks < D / 16; ++ks)
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      uint32_t b00, b01, b10, b11;
-      ldsm_x4(base + p * 16 * RS * 4 + ks * 32, b00, b01, b10, b11);
-      mma(acc[2 * p], a[ks][0], a[ks][1], a[ks][2], a[ks][3], b00, b01);
-      mma(acc[2 * p + 1], a[ks][0], a[ks][1], a[ks][2], a[ks][3], b10, b11);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
     }
-}
-
-// Pass 1: one CTA per (head, 64-query block); warp w owns queries q0 + 16w ..
-__global__ void __launch_bounds__(128) k_row_stats(const uint16_t* __restrict__ Q,
-                                                   const uint16_t* __restrict__ K, int T,
-                                                   float scale_log2, float* __restrict__ m_out,
-                                                   float* __restrict__ l_out) {
-  __shared__ __align__(16) uint32_t sq[BQ * RS], sk[BQ * RS];
-  const int h = blockIdx.y, qb = blockIdx.x, q0 = qb * BQ;
-  const uint16_t* Qh = Q + (size_t)h * T * D;
-  const uint16_t* Kh = K + (size_t)h * T * D;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
-  load_block(sq, Qh, q0, T);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull_bar[b]), 1);
+      mbar_init(smem_u32(&tempty_bar[b]), 4);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&a_full[b]), 1);
+      mbar_init(smem_u32(&a_empty[b]), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)), "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
   __syncthreads();
-  uint32_t a[D / 16][4];
-  a_frags(sq, warp * 16, a);
-  const int i0 = q0 + warp * 16 + g, i1 = i0 + 8;   // this thread's two query rows
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-  for (int kb = 0; kb <= qb; ++kb) {
-    __syncthreads();
-    load_block(sk, Kh, kb * BQ, T);
-    __syncthreads();
-    float acc[8][4];
-    tile_product(a, sk, acc);
-    // scores in log2 units; causal / tail mask
-    float bm0 = -INFINITY, bm1 = -INFINITY;
-#pragma unroll
-    for (int n = 0; n < 8; ++n)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = kb * BQ + n * 8 + 2 * c + (e & 1);
-        const int i = e < 2 ? i0 : i1;
-        const float s = (j <= i && j < T) ? acc[n][e] * scale_log2 : -INFINITY;
-        acc[n][e] = s;
-        if (e < 2) bm0 = fmaxf(bm0, s);
-        else bm1 = fmaxf(bm1, s);
-      }
-#pragma unroll
-    for (int off = 1; off < 4; off <<= 1) {
-      bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, off));
-      bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, off));
-    }
-    const float n0 = fmaxf(m0, bm0), n1 = fmaxf(m1, bm1);
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      s0 += exp2f(acc[n][0] - n0) + exp2f(acc[n][1] - n0);
-      s1 += exp2f(acc[n][2] - n1) + exp2f(acc[n][3] - n1);
-    }
-#pragma unroll
-    for (int off = 1; off < 4; off <<= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, off);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, off);
-    }
-    l0 = (m0 == -INFINITY ? 0.f : l0 * exp2f(m0 - n0)) + s0;
-    l1 = (m1 == -INFINITY ? 0.f : l1 * exp2f(m1 - n1)) + s1;
-    m0 = n0;
-    m1 = n1;
-  }
-  if (c == 0) {
-    if (i0 < T) { m_out[(size_t)h * T + i0] = m0; l_out[(size_t)h * T + i0] = l0; }
-    if (i1 < T) { m_out[(size_t)h * T + i1] = m1; l_out[(size_t)h * T + i1] = l1; }
-  }
-}
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
 
-// Pass 2: one CTA per (head, 64-key block); warp w owns keys k0 + 16w ..; S^T = K Q^T
-__global__ void __launch_bounds__(128) k_col_sums(const uint16_t* __restrict__ Q,
-                                                  const uint16_t* __restrict__ K, int T,
-                                                  float scale_log2, const float* __restrict__ m_in,
-                                                  const float* __restrict__ l_in,
-                                                  float* __restrict__ a_out) {
-  __shared__ __align__(16) uint32_t sk[BQ * RS], sq[BQ * RS];
-  __shared__ float sm[BQ], sl[BQ];   // row max (log2 units) and 1 / row sum of the query block
-  const int h = blockIdx.y, kb = blockIdx.x, k0 = kb * BQ;
-  const uint16_t* Qh = Q + (size_t)h * T * D;
-  const uint16_t* Kh = K + (size_t)h * T * D;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, c = lane & 3;
-  load_block(sk, Kh, k0, T);
-  __syncthreads();
-  uint32_t a[D / 16][4];
-  a_frags(sk, warp * 16, a);
-  const int j0 = k0 + warp * 16 + g, j1 = j0 + 8;   // this thread's two keys
-  float col0 = 0.f, col1 = 0.f;
-  const int nqb = (T + BQ - 1) / BQ;
-  for (int qb = kb; qb < nqb; ++qb) {
-    __syncthreads();
-    load_block(sq, Qh, qb * BQ, T);
-    if (threadIdx.x < BQ) {
-      const int i = qb * BQ + threadIdx.x;
-      sm[threadIdx.x] = i < T ? m_in[(size_t)h * T + i] : 0.f;
-      sl[threadIdx.x] = i < T ? 1.f / l_in[(size_t)h * T + i] : 1.f;
-    }
-    __syncthreads();
-    float acc[8][4];
-    tile_product(a, sq, acc);    // acc[n][e]: key (e < 2 ? j0 : j1), query qb*64 + 8n + 2c + (e & 1)
-#pragma unroll
-    for (int n = 0; n < 8; ++n)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int qi = n * 8 + 2 * c + (e & 1);
-        const int i = qb * BQ + qi;
-        const int j = e < 2 ? j0 : j1;
-        const float p = (j <= i && i < T) ? exp2f(acc[n][e] * scale_log2 - sm[qi]) * sl[qi] : 0.f;
-        if (e < 2) col0 += p;
-        else col1 += p;
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0, it = 0;
+      uint32_t phase = 0;
+      for (int n = blockIdx.x; n < n_items; n += gridDim.x, ++it) {
+        int h, ab, b0, b1;
+        item_at<COLS>(n, H, nb, h, ab, b0, b1);
+        const uint32_t af = smem_u32(&a_full[it & 1]);
+        mbar_wait(smem_u32(&a_empty[it & 1]), ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(af, TILE);
+        tma2d(sA(it), tmA, 0, h * T + ab * BT, af);
+        tma2d(sA(it) + CHUNK, tmA, 64, h * T + ab * BT, af);
+        for (int bb = b0; bb < b1; ++bb) {
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          mbar_expect_tx(smem_u32(&full_bar[stage]), TILE);
+          tma2d(sB(stage), tmB, 0, h * T + bb * BT, smem_u32(&full_bar[stage]));
+          tma2d(sB(stage) + CHUNK, tmB, 64, h * T + bb * BT, smem_u32(&full_bar[stage]));
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+        }
       }
-  }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      int stage = 0, it = 0, blk = 0;
+      uint32_t phase = 0;
+      for (int n = blockIdx.x; n < n_items; n += gridDim.x, ++it) {
+        int h, ab, b0, b1;
+        item_at<COLS>(n, H, nb, h, ab, b0, b1);
+        mbar_wait(smem_u32(&a_full[it & 1]), (it >> 1) & 1);
+        tc_fence_after();
+        for (int bb = b0; bb < b1; ++bb, ++blk) {
+          const int b = blk & 1;
+          mbar_wait(smem_u32(&tempty_bar[b]), ((blk >> 1) & 1) ^ 1);
+          mbar_wait(smem_u32(&full_bar[stage]), phase);
+          tc_fence_after();
 #pragma unroll
-  for (int off = 1; off < 4; off <<= 1) {
-    col0 += __shfl_xor_sync(0xffffffffu, col0, off);
-    col1 += __shfl_xor_sync(0xffffffffu, col1, off);
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (uint32_t)(kk >> 2) * CHUNK + (uint32_t)(kk & 3) * 32;
+            tc_mma(tmem + (uint32_t)(b * BT), sw_desc(sA(it) + off), sw_desc(sB(stage) + off), kk != 0);
+          }
+          tc_commit(smem_u32(&empty_bar[stage]));
+          tc_commit(smem_u32(&tfull_bar[b]));
+          if (++stage == NST) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(smem_u32(&a_empty[it & 1]));   // every MMA reading this A buffer has completed
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2-5)
+    const int q = warp & 3;                   // TMEM lane quarter this warp may access
+    const int r = q * 32 + lane;              // A row = TMEM lane owned by this thread
+    const int et = (warp - 2) * 32 + lane;    // 0..127 among the epilogue threads
+    int blk = 0, nbuf = 0;
+    for (int n = blockIdx.x; n < n_items; n += gridDim.x) {
+      int h, ab, b0, b1;
+      item_at<COLS>(n, H, nb, h, ab, b0, b1);
+      const int row = ab * BT + r;            // query (pass 1) / key (pass 2) of this thread
+      float m = -INFINITY, l = 0.f, acc = 0.f;
+      for (int bb = b0; bb < b1; ++bb, ++blk) {
+        const int b = blk & 1;
+        if (COLS) {
+          // the query block's row statistics, double-buffered (one barrier per block)
+          const int i = bb * BT + et;
+          const int sb = nbuf++ & 1;
+          s_m[sb][et] = i < T ? m_io[(size_t)h * T + i] : 0.f;
+          s_il[sb][et] = i < T ? 1.f / l_io[(size_t)h * T + i] : 0.f;
+          epi_sync();
+          mbar_wait(smem_u32(&tfull_bar[b]), (blk >> 1) & 1);
+          tc_fence_after();
+          float s[BT];
+          const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BT);
+#pragma unroll
+          for (int c = 0; c < BT / 32; ++c)
+            tmem_ld32(tb + c * 32, reinterpret_cast<float(&)[32]>(s[c * 32]));
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[b]));
+          // queries i = bb*128 + c in ascending order; valid when i >= row (causal) and i < T
+          const int cmin = row - bb * BT;      // first valid column (may be <= 0)
+          const int cmax = T - bb * BT;        // columns >= cmax are past the sequence
+#pragma unroll
+          for (int c = 0; c < BT; c += 4) {
+            const float4 mm = *reinterpret_cast<const float4*>(&s_m[sb][c]);
+            const float4 il = *reinterpret_cast<const float4*>(&s_il[sb][c]);
+            const float mv[4] = {mm.x, mm.y, mm.z, mm.w}, iv[4] = {il.x, il.y, il.z, il.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float p = exp2f(__fmaf_rn(s[c + e], scale_log2, -mv[e])) * iv[e];
+              acc += (c + e >= cmin && c + e < cmax) ? p : 0.f;
+            }
+          }
+        } else {
+          mbar_wait(smem_u32(&tfull_bar[b]), (blk >> 1) & 1);
+          tc_fence_after();
+          float s[BT];
+          const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BT);
+#pragma unroll
+          for (int c = 0; c < BT / 32; ++c)
+            tmem_ld32(tb + c * 32, reinterpret_cast<float(&)[32]>(s[c * 32]));
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[b]));
+          // keys j = bb*128 + c, valid when j <= row (causal) and j < T; scores in log2 units
+          const int cmax = min(row - bb * BT + 1, T - bb * BT);
+          float bm = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < BT; ++c) {
+            s[c] = c < cmax ? s[c] * scale_log2 : -INFINITY;
+            bm = fmaxf(bm, s[c]);
+          }
+          const float nm = fmaxf(m, bm);
+          float sum = 0.f;
+          if (nm != -INFINITY) {
+#pragma unroll
+            for (int c = 0; c < BT; ++c) sum += exp2f(s[c] - nm);
+          }
+          l = (m == -INFINITY ? 0.f : l * exp2f(m - nm)) + sum;
+          m = nm;
+        }
+      }
+      if (row < T) {
+        if (COLS) {
+          a_out[(size_t)h * T + row] = acc;
+        } else {
+          m_io[(size_t)h * T + row] = m;
+          l_io[(size_t)h * T + row] = l;
+        }
+      }
+    }
   }
-  if (c == 0) {
-    if (j0 < T) a_out[(size_t)h * T + j0] = col0;
-    if (j1 < T) a_out[(size_t)h * T + j1] = col1;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
   }
 }
 
@@ -199,15 +308,35 @@ cudaError_t launch_attention_mass(const uint16_t* Q, const uint16_t* K, int H, i
   using namespace attn;
   if (d != D) return cudaErrorInvalidValue;
   if (T == 0 || H == 0) return cudaSuccess;
+  static const int sms = [] {   // one-time setup, thread-safe (magic static)
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_attn_mass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(k_attn_mass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    return n;
+  }();
+  // Q, K as 2-D [H*T][128] bf16 tensors; boxes of 64 columns x 128 rows, 128-byte swizzle (rows
+  // of a block past T read the next head's rows or TMA's zero fill: masked in the epilogue)
+  CUtensorMap tq, tk;
+  const uint64_t rows = (uint64_t)H * T;
+  if (!encode_tmap_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, Q, D, rows, D * 2, 64, BT,
+                      CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !encode_tmap_2d(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, K, D, rows, D * 2, 64, BT,
+                      CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
   const float sl2 = scale * 1.4426950408889634f;
-  const dim3 grid((T + BQ - 1) / BQ, H);
-  k_row_stats<<<grid, 128, 0, s>>>(Q, K, T, sl2, m_scratch, l_scratch);
+  const int items = H * ((T + BT - 1) / BT);
+  const int grid = items < sms ? items : sms;
+  k_attn_mass<false><<<grid, kThreads, kSmem, s>>>(tq, tk, H, T, sl2, m_scratch, l_scratch, a_out);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_col_sums<<<grid, 128, 0, s>>>(Q, K, T, sl2, m_scratch, l_scratch, a_out);
+  k_attn_mass<true><<<grid, kThreads, kSmem, s>>>(tq, tk, H, T, sl2, m_scratch, l_scratch, a_out);
   return cudaGetLastError();
 }
 
-cudaError_t preload_attn_mass() { return preload_kernels(attn::k_row_stats, attn::k_col_sums); }
+cudaError_t preload_attn_mass() {
+  return preload_kernels(attn::k_attn_mass<false>, attn::k_attn_mass<true>);
+}
 
 }  // namespace dymoe

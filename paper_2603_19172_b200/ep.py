@@ -87,8 +87,11 @@ class EPLayer:
     def forward(self, x, logits, ladder, layer, num_layers, phase, transport=d.DYMOE_EP_PEER,
                 placement=d.DYMOE_EP_ALL_TO_ALL, attn_mass=None, k_tokens=0, T_peer_max=0,
                 out_dtype=d.DYMOE_OUT_F32, forced_bits=None, ffn_mode=-1, residual=None,
-                prof_events=None, ws=None, out=None, stream=None):
-        """dymoe_moe_forward_ep.  Returns (y, ws)."""
+                prof_events=None, ws=None, out=None, stream=None, local=None):
+        """dymoe_moe_forward_ep.  Returns (y, ws).  local: another dymoe.MoELayer of this rank's
+        experts (same shapes) to run instead of the one given at construction -- one handle (one
+        window) serves every layer of a stack."""
+        local = self.local if local is None else local
         T = x.shape[0]
         if ws is None:
             ws = self.workspace(T, T_peer_max, placement, x.device)
@@ -98,7 +101,7 @@ class EPLayer:
         o = d.make_opts(phase, layer, num_layers, ladder, attn_mass, k_tokens, ffn_mode, out_dtype,
                         forced_bits, residual, prof_events)
         d._check(d.lib().dymoe_moe_forward_ep(
-            self.handle, self.local.handle, transport, placement, d._p(d._u16(x)), d._p(logits), T,
+            self.handle, local.handle, transport, placement, d._p(d._u16(x)), d._p(logits), T,
             T_peer_max, ctypes.byref(o), d._p(out) if T else None, d._p(ws), ws.numel(),
             d._stream(stream)))
         return out, ws

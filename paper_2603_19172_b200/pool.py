@@ -60,9 +60,10 @@ class ExpertStore:
         self.arena = torch.empty(capacity, dtype=torch.uint8, device=device)
         self.pool = d.Pool(capacity)
         if self.host:
-            # one staging buffer for an expert's three bf16 matrices (reused, stream-ordered)
-            self.stage = {n: torch.empty(N, K, dtype=torch.bfloat16, device=device)
-                          for n, N, K in self._shapes()}
+            # staging buffers for an expert's three bf16 matrices, one set per stream that loads
+            # (the main stream's demand misses and the prefetch side stream run concurrently);
+            # reuse within a stream is stream-ordered
+            self.stages = {}
             self.layers = [d.MoELayer([{} for _ in ml], k_route, hidden, ffn) for ml in masters]
         else:
             self.layers = [d.MoELayer([dict(e) for e in ml], k_route, hidden, ffn) for ml in masters]
@@ -188,11 +189,16 @@ class ExpertStore:
         """The expert's bf16 master on the device (host-offload: copied into the staging buffer)."""
         if not self.host:
             return self.masters[l][e]
+        key = (stream or torch.cuda.current_stream()).cuda_stream
+        if key not in self.stages:
+            self.stages[key] = {n: torch.empty(N, K, dtype=torch.bfloat16, device=self.device)
+                                for n, N, K in self._shapes()}
+        stage = self.stages[key]
         with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
             for n in ("w1", "w3", "w2"):
-                self.stage[n].copy_(self.masters[l][e][n], non_blocking=True)
-        self.stats["h2d_bytes"] = self.stats.get("h2d_bytes", 0) + sum(t.numel() * 2 for t in self.stage.values())
-        return self.stage
+                stage[n].copy_(self.masters[l][e][n], non_blocking=True)
+        self.stats["h2d_bytes"] = self.stats.get("h2d_bytes", 0) + sum(t.numel() * 2 for t in stage.values())
+        return stage
 
     def assigned_bits(self, l, x, logits, ladder, num_layers, phase, attn_mass=None, k_tokens=0):
         """Steps route -> score -> assign of dymoe_moe_forward (libdymoe kernels); returns the
@@ -209,8 +215,10 @@ class ExpertStore:
                 k_tokens=0, stream=None, out=None, out_dtype=d.DYMOE_OUT_F32, residual=None):
         """One pooled layer step; returns (y, served widths, requested widths, forced widths the
         forward ran with: served for routed experts, assigned for the others)."""
-        self.wait_ready(l, stream)          # a prefetch of this layer has finished writing
         want, bits_dev = self.assigned_bits(l, x, logits, ladder, num_layers, phase, attn_mass, k_tokens)
+        # a prefetch of this layer must have finished writing before this stream touches the
+        # arena (its own loads may evict and overwrite, its FFN reads); the routing above did not
+        self.wait_ready(l, stream)
         served = self.prepare(l, want, stream)
         # experts not routed this step keep their assigned width (they run no rows)
         forced = [s if w else int(b) for s, w, b in zip(served, want, bits_dev.cpu().tolist())]

@@ -1,6 +1,12 @@
 import os
 import sys
 
+# Ranks simulated by threads (tests/test_gpu_ep.py, test_gpu_stack.py) each launch on their own
+# stream, and a rank's device flag barrier spins until every peer arrives: with the default 8
+# hardware work queues two ranks' streams can share one queue, so a peer's kernels wait behind a
+# spinning barrier (a false dependency that ends in the barrier's timeout).  One queue per stream.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

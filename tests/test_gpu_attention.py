@@ -16,7 +16,7 @@ def D():
     return d
 
 
-@pytest.mark.parametrize("H,T", [(2, 64), (3, 200), (1, 1), (4, 517)])
+@pytest.mark.parametrize("H,T", [(2, 64), (3, 200), (1, 1), (4, 517), (2, 2048), (5, 1300)])
 def test_attention_mass_matches_oracle(H, T):
     d = D()
     g = torch.Generator().manual_seed(H * 1000 + T)

@@ -180,10 +180,10 @@ def test_mixtral_decode_full(B):
 
 
 def test_mixtral_prefill_full():
-    """configs[2]: Mixtral-8x7B layer, prefill T = 2048 (bench's prefill line), layer 3 (all three
-    ladder tiers present): every pair tile of every expert sampled at its first / middle / last
-    row (multi-tile experts, ragged tails, the split-K W2 GEMM)."""
-    bits, perm, n = run_case("mixtral_prefill", 2048, "prefill", 3, tile_rows)
+    """configs[2]: Mixtral-8x7B layer, prefill T = 2048 (bench's prefill line), layer 24 (Eq. 4-5:
+    3 x Int8, 2 x Int4, 3 x Int2): every pair tile of every expert sampled at its first / middle /
+    last row (multi-tile experts, ragged tails, the split-K W2 GEMM)."""
+    bits, perm, n = run_case("mixtral_prefill", 2048, "prefill", 24, tile_rows)
     rows = np.diff(perm["expert_off"])
     assert (rows > 256).any() and len(set(int(b) for b in bits[rows > 0])) >= 2
 

@@ -113,8 +113,117 @@ def test_gate_logits_bias_and_residual_args():
     x = synthetic.hidden_states(cfg, 2)
     lg = d.dymoe_gate_logits(x.cuda(), wg.cuda(), beta.cuda()).cpu().numpy()
     ref = o_stack.router_logits(x.float().numpy(), wg.float().numpy(), beta.numpy())
-    assert np.array_equal(lg, ref)
+    check_logits(lg, ref, gate_logit_bound(x.float().numpy(), wg.float().numpy(), ref))
     lg0 = d.dymoe_gate_logits(x.cuda(), wg.cuda()).cpu().numpy()
-    assert np.array_equal(lg0, o_stack.router_logits(x.float().numpy(), wg.float().numpy()))
+    ref0 = o_stack.router_logits(x.float().numpy(), wg.float().numpy())
+    check_logits(lg0, ref0, gate_logit_bound(x.float().numpy(), wg.float().numpy()))
+    # the bias is one fp32 add of the kernel's own product (beta = 0 leaves it unchanged)
+    assert np.array_equal(lg, (lg0 + beta.numpy()).astype(np.float32))
     with pytest.raises(d.DymoeError):
         d.dymoe_gate_logits(x.cuda()[:, :100].contiguous(), wg.cuda()[:, :100].contiguous())   # Hd % 8 != 0
+
+
+@pytest.mark.parametrize("phase,T", [("decode", 8), ("prefill", 40)])
+def test_ep_stack_single_rank_equals_stack(phase, T):
+    """EPStack (one dymoe_ep handle serving every layer) on one rank, over the peer windows and
+    over the library's NCCL communicator, gives MoEStack's stream bit for bit (same kernels, same
+    arithmetic, one rank owning every expert)."""
+    d = D()
+    from paper_2603_19172_b200 import ep
+    from paper_2603_19172_b200.stack import EPStack, MoEStack
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(T)
+    L = 4
+    layers = []
+    for l in range(L):
+        ex = [{n: t.cuda() for n, t in e.items()} for e in synthetic.expert_weights(cfg, 140 + l)]
+        d.quantize_experts(ex, (8, 4, 2))
+        layers.append(ex)
+    gates = [tuple(t.cuda() for t in synthetic.stack_gate(cfg, l, 4)) for l in range(L)]
+    attn = [synthetic.attention_mass(cfg, 220 + l).cuda() for l in range(L)] if phase == "prefill" else None
+    ph = d.DYMOE_PREFILL if phase == "prefill" else d.DYMOE_DECODE
+    lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
+    x0 = synthetic.hidden_states(cfg, 7).cuda()
+    ref, _ = MoEStack(layers, gates, cfg.k, cfg.hidden, cfg.ffn).forward(x0, lad, phase=ph, attn_masses=attn)
+    h = ep.EPLayer(0, 1, cfg.M, cfg.k, cfg.hidden, cfg.ffn, T, layers[0],
+                   transports=d.DYMOE_EP_NCCL | d.DYMOE_EP_PEER, nccl_uid=ep.unique_id())
+    st = EPStack(h, layers, gates)
+    for tp in (d.DYMOE_EP_PEER, d.DYMOE_EP_NCCL):
+        y, _ = st.forward(x0, lad, phase=ph, transport=tp, attn_masses=attn)
+        torch.cuda.synchronize()
+        assert torch.equal(y, ref), tp
+    h.close()
+
+
+def test_ep_stack_two_ranks_teacher_forced():
+    """EPStack over 2 ranks (threads, peer windows), 4 layers, decode: every layer of every rank
+    against the oracle stack layer with the GLOBAL bits (both ranks' gate sums), teacher-forced."""
+    import threading
+    d = D()
+    from paper_2603_19172_b200 import ep
+    from paper_2603_19172_b200.stack import EPStack
+    from oracle import importance as o_imp, route as o_route, moe as o_moe
+    cfg = synthetic.CONFIGS["tiny"].with_tokens(8)
+    L, P = 4, 2
+    masters = [synthetic.expert_weights(cfg, 160 + l) for l in range(L)]
+    layers = []
+    for l in range(L):
+        ex = [{n: t.cuda() for n, t in e.items()} for e in masters[l]]
+        d.quantize_experts(ex, (8, 4, 2))
+        layers.append(ex)
+    gates = [synthetic.stack_gate(cfg, l, 4) for l in range(L)]
+    gates_d = [tuple(t.cuda() for t in g) for g in gates]
+    lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
+    hs, stacks = [], []
+    for r in range(P):
+        first, last = ep.owned_range(r, cfg.M, P)
+        h = ep.EPLayer(r, P, cfg.M, cfg.k, cfg.hidden, cfg.ffn, cfg.T, layers[0][first:last])
+        hs.append(h)
+        stacks.append(EPStack(h, [lay[first:last] for lay in layers], gates_d))
+    ep.connect_threads(hs)
+    xs = [synthetic.hidden_states(cfg, 30 + r).cuda() for r in range(P)]
+    wss = [h.workspace(cfg.T) for h in hs]
+    bufs = [(torch.empty_like(x), torch.empty_like(x), torch.empty_like(x)) for x in xs]
+    lgs = [torch.empty(cfg.T, cfg.M, device="cuda") for _ in range(P)]
+    streams = [torch.cuda.Stream() for _ in range(P)]
+    torch.cuda.synchronize()
+    res, errors = {}, []
+
+    def worker(r):
+        try:
+            with torch.cuda.stream(streams[r]):
+                y, tr = stacks[r].forward(xs[r], lad, d.DYMOE_DECODE, ws=wss[r], bufs=bufs[r],
+                                          logits=lgs[r], trace=True)
+                torch.cuda.current_stream().synchronize()
+                res[r] = (y.float().cpu().numpy(), [tuple(t.cpu() for t in e) for e in tr])
+        except Exception as e:   # pragma: no cover
+            errors.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    [h.close() for h in hs]
+    assert not errors, errors
+    lad_o = o_sched.Ladder((8, 4, 2), (0.25, 0.5))
+    np_ex = [[{n: t.float().numpy() for n, t in e.items()} for e in masters[l]] for l in range(L)]
+    for l in range(L):
+        wg, beta = gates[l]
+        I = np.zeros(cfg.M)
+        lg_ref = {}
+        for r in range(P):
+            u = res[r][1][l][1].float().numpy().astype(np.float64)
+            lg_ref[r] = o_stack.router_logits(u, wg.float().numpy(), beta.numpy())
+            _, _, p = o_route.route(lg_ref[r], cfg.k)
+            I = I + o_imp.decode_importance(lg_ref[r], p)
+        bits_ref, _ = o_sched.assign_bits(I, l, L, lad_o, cfg.k)
+        for r in range(P):
+            x_in, u, _, bits, idx = res[r][1][l]
+            assert np.array_equal(bits.numpy(), res[0][1][l][3].numpy())
+            check_bits(bits.numpy(), bits_ref, I, decode_importance_tol(cfg.T * P))
+            assert np.array_equal(idx.numpy(), o_route.route(lg_ref[r], cfg.k)[0])
+            y_ref = o_moe.moe_forward(u.float().numpy(), lg_ref[r], np_ex[l], l, L, lad_o, cfg.k,
+                                      forced_bits=bits.numpy())["y"]
+            xin = x_in.float().numpy().astype(np.float64)
+            full = o_stack.residual(xin, y_ref)
+            x_out = (res[r][1][l + 1][0].float().numpy() if l + 1 < L else res[r][0]).astype(np.float64)
+            bound = 2e-3 * np.abs(y_ref).max() + _ulp_bf16(full)
+            assert (np.abs(x_out - full) <= bound).all(), (r, l)

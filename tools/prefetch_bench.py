@@ -21,10 +21,10 @@ import paper_2603_19172_b200.dymoe as d  # noqa: E402
 from paper_2603_19172_b200.pool import ExpertStore, PrefetchingStack  # noqa: E402
 
 
-def intervals(trace, pred):
+def intervals(trace, pred, cat="kernel"):
     out = []
     for ev in trace.get("traceEvents", []):
-        if ev.get("cat") == "kernel" and pred(ev.get("name", "")):
+        if ev.get("cat") == cat and pred(ev.get("name", "")):
             out.append((ev["ts"], ev["ts"] + ev["dur"], ev.get("args", {}).get("stream")))
     return sorted(out)
 
@@ -47,6 +47,9 @@ def main():
     ap.add_argument("--budget", type=float, default=0.45)
     ap.add_argument("--passes", type=int, default=4)
     ap.add_argument("--prefill", action="store_true")
+    ap.add_argument("--offload", action="store_true",
+                    help="host-offload variant (f4, the paper's setting): bf16 masters in pinned host "
+                         "memory, every format a pool entry, a miss = H2D copy + quantize")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
@@ -57,12 +60,16 @@ def main():
     gates = [synthetic.stack_gate(cfg, l, 9, dev) for l in range(L)]
     probe = ExpertStore(masters[:1], cfg.k, cfg.hidden, cfg.ffn, 1 << 20)
     full = L * cfg.M * sum(probe.entry_bytes(b) for b in (8, 4, 2))
+    if args.offload:
+        masters = [[{n: t.cpu().pin_memory() for n, t in e.items()} for e in ml] for ml in masters]
+        torch.cuda.empty_cache()
     del probe
     lad = d.make_ladder((8, 4, 2), (0.25, 0.5))
     ph = d.DYMOE_PREFILL if args.prefill else d.DYMOE_DECODE
     attn = [synthetic.attention_mass(cfg, 40 + l, dev) for l in range(L)] if args.prefill else None
     xs = [synthetic.hidden_states(cfg, 70 + i, dev) for i in range(args.passes)]
     res = {"layers": L, "tokens": T, "phase": "prefill" if args.prefill else "decode",
+           "offload": args.offload,
            "arena_GB": round(full * args.budget / 1e9, 2), "all_packed_GB": round(full / 1e9, 2),
            "budget": args.budget}
     for prefetch in (False, True):
@@ -99,6 +106,14 @@ def main():
                                  "kernels": len(qq), "quantize_us": us,
                                  "overlapped_by_ffn_us": overlap(qq, f),
                                  "frac_hidden": overlap(qq, f) / us if us else None}
+            h2d = intervals(tr, lambda n: "HtoD" in n, cat="gpu_memcpy")
+            h2d_side = [iv for iv in h2d if iv[2] not in fstreams]
+            hs = sum(e - s for s, e, _ in h2d_side)
+            ffn_us = sum(e - s for s, e, _ in f)
+            res["overlap_h2d"] = {
+                "side_stream_h2d_us": hs, "overlapped_by_ffn_us": overlap(h2d_side, f),
+                "ffn_us": ffn_us, "ffn_us_overlapped_by_side_h2d": overlap(f, h2d_side),
+                "frac_of_ffn_time_with_a_prefetch_copy_in_flight": overlap(f, h2d_side) / ffn_us if ffn_us else None}
             res["overlap"] = {
                 "quantize_kernels": len(q), "quantize_us": qs, "per_stream": per,
                 "frac_hidden_all": overlap(q, f) / qs if qs else None,
