@@ -9,7 +9,8 @@
 //   pass 2 (column sums): one work item = (head, 128-key block); S^T = K_blk Q_blk^T for every
 //            query block at or after the diagonal, so that a TMEM lane holds one KEY and its
 //            row of 128 queries: each epilogue thread adds exp(s_ij - m_i) / l_i over the
-//            queries (ascending, one fp32 chain per key -- deterministic) and writes a[h][j].
+//            queries (ascending, four interleaved fp32 chains per key combined in a fixed order --
+//            deterministic) and writes a[h][j].
 // Per CTA (persistent, one per SM): warp 0 lane 0 streams the tiles by TMA (the work item's A
 // tile once into one of two buffers, B tiles through a 3-stage ring; 128B-swizzled K-major, two 64-column boxes per
 // 128 x 128 tile), warp 1 owns TMEM (two 128-column accumulators) and one lane issues the MMAs,
@@ -97,6 +98,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ex2(float x) {   // 2^x on the SFU (ex2(-inf) = +0)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 __device__ __forceinline__ void epi_sync() {   // the 128 epilogue threads only
   asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -209,6 +215,8 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     }
   } else {
     // ------------------------------------------------------------------ epilogue (warps 2-5)
+    // One warp per SM sub-partition: the per-row reductions run as 4 independent chains (ILP
+    // instead of warps to hide the FMA / SFU latency), combined in a fixed order at the end.
     const int q = warp & 3;                   // TMEM lane quarter this warp may access
     const int r = q * 32 + lane;              // A row = TMEM lane owned by this thread
     const int et = (warp - 2) * 32 + lane;    // 0..127 among the epilogue threads
@@ -217,20 +225,33 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
       int h, ab, b0, b1;
       item_at<COLS>(n, H, nb, h, ab, b0, b1);
       const int row = ab * BT + r;            // query (pass 1) / key (pass 2) of this thread
-      float m = -INFINITY, l = 0.f, acc = 0.f;
+      float m = -INFINITY, l = 0.f;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      // pass 2: the first query block's statistics, loaded ahead (their latency overlaps the
+      // previous block's arithmetic from then on)
+      float m_nx = 0.f, il_nx = 0.f;
+      if (COLS) {
+        const int i = b0 * BT + et;
+        m_nx = i < T ? m_io[(size_t)h * T + i] : 0.f;
+        il_nx = i < T ? l_io[(size_t)h * T + i] : 1.f;
+      }
       for (int bb = b0; bb < b1; ++bb, ++blk) {
         const int b = blk & 1;
+        float s[BT];
+        const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BT);
         if (COLS) {
           // the query block's row statistics, double-buffered (one barrier per block)
-          const int i = bb * BT + et;
           const int sb = nbuf++ & 1;
-          s_m[sb][et] = i < T ? m_io[(size_t)h * T + i] : 0.f;
-          s_il[sb][et] = i < T ? 1.f / l_io[(size_t)h * T + i] : 0.f;
+          s_m[sb][et] = m_nx;
+          s_il[sb][et] = 1.f / il_nx;
           epi_sync();
+          if (bb + 1 < b1) {
+            const int i = (bb + 1) * BT + et;
+            m_nx = i < T ? m_io[(size_t)h * T + i] : 0.f;
+            il_nx = i < T ? l_io[(size_t)h * T + i] : 1.f;
+          }
           mbar_wait(smem_u32(&tfull_bar[b]), (blk >> 1) & 1);
           tc_fence_after();
-          float s[BT];
-          const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BT);
 #pragma unroll
           for (int c = 0; c < BT / 32; ++c)
             tmem_ld32(tb + c * 32, reinterpret_cast<float(&)[32]>(s[c * 32]));
@@ -238,7 +259,7 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[b]));
-          // queries i = bb*128 + c in ascending order; valid when i >= row (causal) and i < T
+          // queries i = bb*128 + c; valid when i >= row (causal) and i < T
           const int cmin = row - bb * BT;      // first valid column (may be <= 0)
           const int cmax = T - bb * BT;        // columns >= cmax are past the sequence
 #pragma unroll
@@ -248,15 +269,13 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
             const float mv[4] = {mm.x, mm.y, mm.z, mm.w}, iv[4] = {il.x, il.y, il.z, il.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const float p = exp2f(__fmaf_rn(s[c + e], scale_log2, -mv[e])) * iv[e];
-              acc += (c + e >= cmin && c + e < cmax) ? p : 0.f;
+              const float p = ex2(__fmaf_rn(s[c + e], scale_log2, -mv[e])) * iv[e];
+              acc[e] += (c + e >= cmin && c + e < cmax) ? p : 0.f;
             }
           }
         } else {
           mbar_wait(smem_u32(&tfull_bar[b]), (blk >> 1) & 1);
           tc_fence_after();
-          float s[BT];
-          const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BT);
 #pragma unroll
           for (int c = 0; c < BT / 32; ++c)
             tmem_ld32(tb + c * 32, reinterpret_cast<float(&)[32]>(s[c * 32]));
@@ -266,25 +285,25 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
           if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[b]));
           // keys j = bb*128 + c, valid when j <= row (causal) and j < T; scores in log2 units
           const int cmax = min(row - bb * BT + 1, T - bb * BT);
-          float bm = -INFINITY;
+          float bm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
           for (int c = 0; c < BT; ++c) {
             s[c] = c < cmax ? s[c] * scale_log2 : -INFINITY;
-            bm = fmaxf(bm, s[c]);
+            bm[c & 3] = fmaxf(bm[c & 3], s[c]);
           }
-          const float nm = fmaxf(m, bm);
-          float sum = 0.f;
+          const float nm = fmaxf(fmaxf(m, fmaxf(bm[0], bm[1])), fmaxf(bm[2], bm[3]));
+          float sum[4] = {0.f, 0.f, 0.f, 0.f};
           if (nm != -INFINITY) {
 #pragma unroll
-            for (int c = 0; c < BT; ++c) sum += exp2f(s[c] - nm);
+            for (int c = 0; c < BT; ++c) sum[c & 3] += ex2(s[c] - nm);
           }
-          l = (m == -INFINITY ? 0.f : l * exp2f(m - nm)) + sum;
+          l = (m == -INFINITY ? 0.f : l * ex2(m - nm)) + ((sum[0] + sum[1]) + (sum[2] + sum[3]));
           m = nm;
         }
       }
       if (row < T) {
         if (COLS) {
-          a_out[(size_t)h * T + row] = acc;
+          a_out[(size_t)h * T + row] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         } else {
           m_io[(size_t)h * T + row] = m;
           l_io[(size_t)h * T + row] = l;

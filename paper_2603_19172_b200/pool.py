@@ -189,10 +189,16 @@ class ExpertStore:
         """The expert's bf16 master on the device (host-offload: copied into the staging buffer)."""
         if not self.host:
             return self.masters[l][e]
-        key = (stream or torch.cuda.current_stream()).cuda_stream
+        st = stream or torch.cuda.current_stream()
+        key = st.cuda_stream
         if key not in self.stages:
-            self.stages[key] = {n: torch.empty(N, K, dtype=torch.bfloat16, device=self.device)
-                                for n, N, K in self._shapes()}
+            # allocated on the stream that uses it: the caching allocator may hand a block freed
+            # on stream S to a new allocation made on S while S's queued kernels still read it
+            # (safe only for work ordered on S) -- a side-stream staging buffer carved from a
+            # main-stream block would be overwritten by H2D copies that race those kernels
+            with torch.cuda.stream(st):
+                self.stages[key] = {n: torch.empty(N, K, dtype=torch.bfloat16, device=self.device)
+                                    for n, N, K in self._shapes()}
         stage = self.stages[key]
         with (torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()):
             for n in ("w1", "w3", "w2"):
@@ -233,10 +239,11 @@ class PrefetchingStack:
     """A layer stack (stack.MoEStack's block: RMSNorm -> router -> MoE -> residual) over an
     ExpertStore whose arena is smaller than the packed formats of the whole stack, with the
     paper's look-ahead prefetcher (Eqs. 6-8, steps 5-6 of
-    P:203): at layer l, dymoe_predict_next on l's normed hidden state with layer l+1's gate names
-    the top-t experts of l+1 (prefill: token frequency, Eq. 7; decode: the predicted gate, Eq. 8),
-    t = layer l+1's high-tier count (Eq. 5); their top-tier formats are quantized into the arena on
-    a side stream while layer l's FFN runs on the main stream.  prefetch=False: every format is
+    P:203): at layer l, dymoe_predict_next on l's normed hidden state with layer l+1's gate ranks
+    the experts of l+1 (prefill: token frequency, Eq. 7; decode: the predicted gate, Eq. 8); the
+    predicted experts' formats at the widths layer l+1's schedule gives their ranks (Eq. 5 tier
+    counts: the top t_1 -- the paper's critical experts -- at the top tier) are quantized into
+    the arena on a side stream while layer l's FFN runs on the main stream.  prefetch=False: every format is
     loaded on demand (the baseline the overlap is measured against)."""
 
     def __init__(self, store, gates):
@@ -265,13 +272,19 @@ class PrefetchingStack:
             req = None
             if prefetch and l + 1 < self.L:
                 # Eqs. 6-8 on the device; the requests are read back before this layer's FFN is
-                # queued (the step synchronises for its own bits anyway), so nothing waits for it
-                t_hi = d.dymoe_tier_counts(l + 1, self.L, ladder, self.M, self.k)
-                t = max(1, t_hi[0] if t_hi else self.M)
+                # queued (the step synchronises for its own bits anyway), so nothing waits for it.
+                # Every predicted expert is requested at the width layer l+1's schedule gives its
+                # predicted rank (Eq. 5 tier counts at depth l+1): the critical ones at the top
+                # tier as in the paper, the rest at theirs -- prefetching everything
+                # at the top width would overfill the byte budget and evict the next layers
+                tiers = d.dymoe_tier_counts(l + 1, self.L, ladder, self.M, self.k)
+                # decode: at most T k experts can be active (B = 1: the top-k of Eq. 8)
+                t = self.M if phase == d.DYMOE_PREFILL else min(self.M, T * self.k)
                 ex, _, _ = d.dymoe_predict_next(phase, u, self.gates[l + 1][0], self.k, t)
                 req = [0] * self.M
-                for e in ex.cpu().tolist():
-                    req[e] = ladder.bits[0]
+                for rank, e in enumerate(ex.cpu().tolist()):
+                    tier = sum(1 for t in tiers if rank >= t)
+                    req[e] = ladder.bits[tier]
             y, served, want, forced = s.forward(l, u, logits, ladder, self.L, phase=phase,
                                                 attn_mass=a, out=nxt, out_dtype=d.DYMOE_OUT_BF16,
                                                 residual=cur)
