@@ -255,9 +255,9 @@ size_t dymoe_pool_used(const dymoe_pool* pool);
 
 /* Heavy-hitter attention mass (the input of Eq. 1, reading R1) without
  * materializing the attention matrix: a[h][j] = sum_{i >= j} softmax_{j' <= i}(scale *
- * q[h][i] . k[h][j'])[j] (causal).  Two passes of tensor-core Q K^T tiles (row max / sum, then
- * column sums of P), fixed summation order.
- *   q, k [H][T][d] bf16 device (d == 128, 16-byte aligned); scratch [2*H*T] f32 device;
+ * q[h][i] . k[h][j'])[j] (causal).  Two persistent passes of tcgen05 128 x 128 score tiles in
+ * TMEM (row max / sum, then column sums of P from K Q^T), fixed summation order.
+ *   q, k [H][T][d] bf16 device (d == 128, 16-byte aligned); scale > 0; scratch [2*H*T] f32 device;
  *   a_out [H][T] f32 device (the attn_mass argument of dymoe_score / dymoe_fwd_opts).          */
 int dymoe_attention_mass(const uint16_t* q, const uint16_t* k, int H, int T, int d, float scale,
                          float* scratch, float* a_out, dymoe_stream_t stream);

@@ -603,6 +603,7 @@ int dymoe_attention_mass(const uint16_t* q, const uint16_t* k, int H, int T, int
                          float* scratch, float* a_out, dymoe_stream_t stream) {
   CHECK_ARG(H >= 0 && T >= 0, "H/T: must be >= 0");
   CHECK_ARG(d == 128, "d: only head dim 128 is implemented");
+  CHECK_ARG(scale > 0.f, "scale: must be > 0");
   if (H == 0 || T == 0) return ok();
   CHECK_ARG(q && k && scratch && a_out, "q/k/scratch/a_out: must not be NULL");
   int rc = check_ptr_align(q, 16, "q");

@@ -5,17 +5,21 @@
 // (tcgen05.mma.cta_group::1.kind::f16, M = N = 128, K = d = 128, bf16 -> fp32 in TMEM):
 //   pass 1 (row statistics): one work item = (head, 128-query block); S = Q_blk K_blk^T for every
 //            key block at or below the diagonal; each epilogue thread owns one query row (one TMEM
-//            lane) and keeps m_i = max_j s_ij, l_i = sum_j exp(s_ij - m_i) online;
+//            lane) and keeps m_i = max_j s_ij, l_i = sum_j exp(s_ij - m_i) online; it stores
+//            n_i = m_i + log2 l_i (log2 units), so that p_ij = 2^(s_ij - n_i);
 //   pass 2 (column sums): one work item = (head, 128-key block); S^T = K_blk Q_blk^T for every
 //            query block at or after the diagonal, so that a TMEM lane holds one KEY and its
-//            row of 128 queries: each epilogue thread adds exp(s_ij - m_i) / l_i over the
+//            row of 128 queries: each epilogue thread adds 2^(s_ij - n_i) over the
 //            queries (ascending, four interleaved fp32 chains per key combined in a fixed order --
 //            deterministic) and writes a[h][j].
 // Per CTA (persistent, one per SM): warp 0 lane 0 streams the tiles by TMA (the work item's A
 // tile once into one of two buffers, B tiles through a 3-stage ring; 128B-swizzled K-major, two 64-column boxes per
 // 128 x 128 tile), warp 1 owns TMEM (two 128-column accumulators) and one lane issues the MMAs,
-// warps 2-5 drain TMEM (tcgen05.ld 32x32b) and do the softmax arithmetic -- the MMA of block
-// n + 1 overlaps the exponentials of block n.  Work items are handed out longest first.
+// warps 2-9 drain TMEM (tcgen05.ld 32x32b, two warps per lane quarter, 64 columns each) and do
+// the softmax arithmetic -- the MMA of block n + 1 overlaps the exponentials of block n.  Work
+// items are ordered longest first and dealt out in alternating directions.  (Taking every 4th
+// exponential on the FMA pipe with a degree-6 polynomial unloaded the SFU but raised the
+// instruction count 70 % and cost 20 %: the epilogue is issue-bound, not SFU-bound.)
 // Roofline: tensor (2 passes x 2 T^2 d H / 2 causal flops) with the SFU's exp2 alongside.
 #include "../dymoe_internal.cuh"
 
@@ -28,7 +32,10 @@ constexpr int NST = 3;            // B-tile ring stages
 constexpr int CHUNK = BT * 128;   // one 64-column box: 128 rows x 128 bytes
 constexpr int TILE = 2 * CHUNK;   // 32 KB
 constexpr int kSmem = (2 + NST) * TILE + 1024;   // A double-buffered by item, B ring
-constexpr int kThreads = 192;     // warps 0 (TMA), 1 (TMEM + MMA), 2-5 (epilogue)
+constexpr int kEpi = 16;          // epilogue warps: four per TMEM lane quarter, 32 columns each
+constexpr int NQ = kEpi / 4;      // column parts per block (warps sharing a lane quarter)
+constexpr int HC = BT / NQ;       // columns per part
+constexpr int kThreads = (2 + kEpi) * 32;   // warps 0 (TMA), 1 (TMEM + MMA), 2.. (epilogue)
 constexpr uint32_t TMEM_COLS = 2 * BT;
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BT >> 3) << 17) |
                            ((uint32_t)(BT >> 4) << 24);   // kind::f16: bf16 x bf16 -> f32, K-major
@@ -104,8 +111,8 @@ __device__ __forceinline__ float ex2(float x) {   // 2^x on the SFU (ex2(-inf) =
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ void epi_sync() {   // the 128 epilogue threads only
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+__device__ __forceinline__ void epi_sync() {   // the epilogue threads only
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpi * 32) : "memory");
 }
 
 // Work item n (longest first) -> (head, block of the A operand, first and end B block).
@@ -119,6 +126,11 @@ __device__ __forceinline__ void item_at(int n, int H, int nb, int& h, int& a, in
   else { a = nb - 1 - r; b0 = 0; b1 = a + 1; }
 }
 
+// The work item of round j for CTA c of G: the rounds alternate direction (round 0: c, round 1:
+// 2G-1-c, ...), so a CTA that took a long item in one round takes a short one in the next
+// (items are ordered longest first).
+__device__ __forceinline__ int snake(int j, int c, int G) { return j * G + ((j & 1) ? G - 1 - c : c); }
+
 template <bool COLS>
 __global__ void __launch_bounds__(kThreads, 1)
 k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -128,7 +140,7 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
   __shared__ __align__(8) uint64_t full_bar[NST], empty_bar[NST], tfull_bar[2], tempty_bar[2];
   __shared__ __align__(8) uint64_t a_full[2], a_empty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ __align__(16) float s_m[2][BT], s_il[2][BT];   // pass 2: the query block's m, 1/l
+  __shared__ float x_m[NQ][BT], x_l[NQ][BT];                 // the column parts' partials
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t sA0 = smem_u32(smem);
   auto sA = [&](int it) { return sA0 + (uint32_t)(it & 1) * TILE; };
@@ -146,7 +158,7 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&tfull_bar[b]), 1);
-      mbar_init(smem_u32(&tempty_bar[b]), 4);
+      mbar_init(smem_u32(&tempty_bar[b]), kEpi);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&a_full[b]), 1);
@@ -169,7 +181,9 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     if (lane == 0) {
       int stage = 0, it = 0;
       uint32_t phase = 0;
-      for (int n = blockIdx.x; n < n_items; n += gridDim.x, ++it) {
+      for (int j = 0;; ++j, ++it) {
+        const int n = snake(j, blockIdx.x, gridDim.x);
+        if (n >= n_items) break;
         int h, ab, b0, b1;
         item_at<COLS>(n, H, nb, h, ab, b0, b1);
         const uint32_t af = smem_u32(&a_full[it & 1]);
@@ -191,7 +205,9 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
     if (lane == 0) {
       int stage = 0, it = 0, blk = 0;
       uint32_t phase = 0;
-      for (int n = blockIdx.x; n < n_items; n += gridDim.x, ++it) {
+      for (int j = 0;; ++j, ++it) {
+        const int n = snake(j, blockIdx.x, gridDim.x);
+        if (n >= n_items) break;
         int h, ab, b0, b1;
         item_at<COLS>(n, H, nb, h, ab, b0, b1);
         mbar_wait(smem_u32(&a_full[it & 1]), (it >> 1) & 1);
@@ -214,101 +230,139 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
       }
     }
   } else {
-    // ------------------------------------------------------------------ epilogue (warps 2-5)
-    // One warp per SM sub-partition: the per-row reductions run as 4 independent chains (ILP
-    // instead of warps to hide the FMA / SFU latency), combined in a fixed order at the end.
-    const int q = warp & 3;                   // TMEM lane quarter this warp may access
-    const int r = q * 32 + lane;              // A row = TMEM lane owned by this thread
-    const int et = (warp - 2) * 32 + lane;    // 0..127 among the epilogue threads
-    int blk = 0, nbuf = 0;
-    for (int n = blockIdx.x; n < n_items; n += gridDim.x) {
+    // ------------------------------------------------------------------ epilogue (warps 2..)
+    // NQ warps per TMEM lane quarter (one per HC-column part of the block), so every SM
+    // sub-partition runs NQ epilogue warps -- the epilogue is latency-bound, not issue-bound; each
+    // row's reductions run as 4 interleaved chains per part, combined in a fixed order (chains,
+    // then parts 0, 1, ...) at the end of the item.  Blocks strictly off the diagonal and inside
+    // the sequence take a mask-free path.
+    const int q = warp & 3;                    // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;          // column part 0 .. NQ-1
+    const int r = q * 32 + lane;               // A row = TMEM lane owned by this thread
+    int blk = 0;
+    for (int j = 0;; ++j) {
+      const int n = snake(j, blockIdx.x, gridDim.x);
+      if (n >= n_items) break;
       int h, ab, b0, b1;
       item_at<COLS>(n, H, nb, h, ab, b0, b1);
       const int row = ab * BT + r;            // query (pass 1) / key (pass 2) of this thread
       float m = -INFINITY, l = 0.f;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
-      // pass 2: the first query block's statistics, loaded ahead (their latency overlaps the
-      // previous block's arithmetic from then on)
-      float m_nx = 0.f, il_nx = 0.f;
-      if (COLS) {
-        const int i = b0 * BT + et;
-        m_nx = i < T ? m_io[(size_t)h * T + i] : 0.f;
-        il_nx = i < T ? l_io[(size_t)h * T + i] : 1.f;
-      }
       for (int bb = b0; bb < b1; ++bb, ++blk) {
         const int b = blk & 1;
-        float s[BT];
-        const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BT);
+        float s[HC];
+        const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BT + half * HC);
+        const bool full = bb != ab && (bb + 1) * BT <= T;   // no causal / tail mask (uniform)
+        const int c0 = half * HC;
         if (COLS) {
-          // the query block's row statistics, double-buffered (one barrier per block)
-          const int sb = nbuf++ & 1;
-          s_m[sb][et] = m_nx;
-          s_il[sb][et] = 1.f / il_nx;
-          epi_sync();
-          if (bb + 1 < b1) {
-            const int i = (bb + 1) * BT + et;
-            m_nx = i < T ? m_io[(size_t)h * T + i] : 0.f;
-            il_nx = i < T ? l_io[(size_t)h * T + i] : 1.f;
+          // n_i of this part's 32 queries (pass 1): one address per load across the warp (a
+          // broadcast from L1), issued before the wait for the MMA so that their latency
+          // overlaps it -- no shared memory, no barrier
+          const float* mq = m_io + (size_t)h * T + bb * BT + c0;
+          float4 mm4[HC / 4];
+          if (full) {
+#pragma unroll
+            for (int c = 0; c < HC / 4; ++c) mm4[c] = __ldg(reinterpret_cast<const float4*>(mq) + c);
+          } else {
+            const int nv = T - bb * BT - c0;      // queries of this part inside the sequence
+#pragma unroll
+            for (int c = 0; c < HC / 4; ++c) {
+              float t0[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) t0[e] = 4 * c + e < nv ? __ldg(mq + 4 * c + e) : 0.f;
+              mm4[c] = make_float4(t0[0], t0[1], t0[2], t0[3]);
+            }
           }
           mbar_wait(smem_u32(&tfull_bar[b]), (blk >> 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < BT / 32; ++c)
+          for (int c = 0; c < HC / 32; ++c)
             tmem_ld32(tb + c * 32, reinterpret_cast<float(&)[32]>(s[c * 32]));
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[b]));
-          // queries i = bb*128 + c; valid when i >= row (causal) and i < T
-          const int cmin = row - bb * BT;      // first valid column (may be <= 0)
-          const int cmax = T - bb * BT;        // columns >= cmax are past the sequence
+          // queries i = bb*128 + c0 + c; valid when i >= row (causal) and i < T
+          if (full) {
 #pragma unroll
-          for (int c = 0; c < BT; c += 4) {
-            const float4 mm = *reinterpret_cast<const float4*>(&s_m[sb][c]);
-            const float4 il = *reinterpret_cast<const float4*>(&s_il[sb][c]);
-            const float mv[4] = {mm.x, mm.y, mm.z, mm.w}, iv[4] = {il.x, il.y, il.z, il.w};
+            for (int c = 0; c < HC; c += 4) {
+              const float4 mm = mm4[c / 4];
+              acc[0] += ex2(__fmaf_rn(s[c], scale_log2, -mm.x));
+              acc[1] += ex2(__fmaf_rn(s[c + 1], scale_log2, -mm.y));
+              acc[2] += ex2(__fmaf_rn(s[c + 2], scale_log2, -mm.z));
+              acc[3] += ex2(__fmaf_rn(s[c + 3], scale_log2, -mm.w));
+            }
+          } else {
+            const int cmin = row - bb * BT - c0;   // first valid column of this half
+            const int cmax = T - bb * BT - c0;     // columns >= cmax are past the sequence
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float p = ex2(__fmaf_rn(s[c + e], scale_log2, -mv[e])) * iv[e];
-              acc[e] += (c + e >= cmin && c + e < cmax) ? p : 0.f;
+            for (int c = 0; c < HC; c += 4) {
+              const float4 mm = mm4[c / 4];
+              const float mv[4] = {mm.x, mm.y, mm.z, mm.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const bool ok = c + e >= cmin && c + e < cmax;
+                const float p = ex2(__fmaf_rn(s[c + e], scale_log2, -mv[e]));
+                acc[e] += ok ? p : 0.f;
+              }
             }
           }
         } else {
           mbar_wait(smem_u32(&tfull_bar[b]), (blk >> 1) & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < BT / 32; ++c)
+          for (int c = 0; c < HC / 32; ++c)
             tmem_ld32(tb + c * 32, reinterpret_cast<float(&)[32]>(s[c * 32]));
           tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(smem_u32(&tempty_bar[b]));
-          // keys j = bb*128 + c, valid when j <= row (causal) and j < T; scores in log2 units
-          const int cmax = min(row - bb * BT + 1, T - bb * BT);
+          // keys j = bb*128 + c0 + c, valid when j <= row (causal) and j < T; the max is taken on
+          // the raw scores (scale > 0), the exponent is fma(s, scale_log2, -max * scale_log2)
+          if (!full) {
+            const int cmax = min(row - bb * BT + 1, T - bb * BT) - c0;
+#pragma unroll
+            for (int c = 0; c < HC; ++c) s[c] = c < cmax ? s[c] : -INFINITY;
+          }
           float bm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-          for (int c = 0; c < BT; ++c) {
-            s[c] = c < cmax ? s[c] * scale_log2 : -INFINITY;
-            bm[c & 3] = fmaxf(bm[c & 3], s[c]);
-          }
-          const float nm = fmaxf(fmaxf(m, fmaxf(bm[0], bm[1])), fmaxf(bm[2], bm[3]));
+          for (int c = 0; c < HC; ++c) bm[c & 3] = fmaxf(bm[c & 3], s[c]);
+          const float nm = fmaxf(m, fmaxf(fmaxf(bm[0], bm[1]), fmaxf(bm[2], bm[3])));
           float sum[4] = {0.f, 0.f, 0.f, 0.f};
           if (nm != -INFINITY) {
+            const float nms = -nm * scale_log2;
 #pragma unroll
-            for (int c = 0; c < BT; ++c) sum[c & 3] += ex2(s[c] - nm);
+            for (int c = 0; c < HC; ++c) sum[c & 3] += ex2(__fmaf_rn(s[c], scale_log2, nms));
           }
-          l = (m == -INFINITY ? 0.f : l * ex2(m - nm)) + ((sum[0] + sum[1]) + (sum[2] + sum[3]));
+          l = (m == -INFINITY ? 0.f : l * ex2((m - nm) * scale_log2)) +
+              ((sum[0] + sum[1]) + (sum[2] + sum[3]));
           m = nm;
         }
       }
-      if (row < T) {
+      // combine the column parts of each row: parts 1.. hand their partials to part 0
+      x_m[half][r] = COLS ? (acc[0] + acc[1]) + (acc[2] + acc[3]) : m;
+      x_l[half][r] = l;
+      epi_sync();
+      if (half == 0 && row < T) {
         if (COLS) {
-          a_out[(size_t)h * T + row] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+          float a = x_m[0][r];
+#pragma unroll
+          for (int p = 1; p < NQ; ++p) a += x_m[p][r];
+          a_out[(size_t)h * T + row] = a;
         } else {
-          m_io[(size_t)h * T + row] = m;
-          l_io[(size_t)h * T + row] = l;
+          float mt = x_m[0][r];   // raw-score maxima; m, l in the scaled log2 domain
+#pragma unroll
+          for (int p = 1; p < NQ; ++p) mt = fmaxf(mt, x_m[p][r]);
+          float lt = 0.f;
+#pragma unroll
+          for (int p = 0; p < NQ; ++p)
+            lt += x_m[p][r] == -INFINITY ? 0.f : x_l[p][r] * ex2((x_m[p][r] - mt) * scale_log2);
+          // p_ij = 2^(s_ij c - m_i) / l_i = 2^(s_ij c - (m_i + log2 l_i)): pass 2 needs one value
+          m_io[(size_t)h * T + row] = __fadd_rn(mt * scale_log2, log2f(lt));
+          l_io[(size_t)h * T + row] = lt;
         }
       }
+      epi_sync();   // x_m / x_l are rewritten by the next item
     }
   }
   tc_fence_before();

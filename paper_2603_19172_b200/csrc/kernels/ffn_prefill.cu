@@ -460,11 +460,16 @@ __device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t,
   Tile r;
   r.e = S.expert[i];
   const int local = t - S.first[i];
-  const int mt = local / ntiles_n, ntk = local - mt * ntiles_n;
+  const int n_e = a.expert_off[r.e + 1] - a.expert_off[r.e];
+  // column-tile major: consecutive tiles (run concurrently by consecutive clusters) are the
+  // expert's token tiles of the SAME weight columns, so a weight tile is streamed from HBM once
+  // and served to the other token tiles from L2 (token-tile major re-read every column of the
+  // expert's packed weights once per token tile: 2.2x the packed bytes at the Zipf loads)
+  const int nmt = (n_e + TOK - 1) / TOK;
+  const int ntk = local / nmt, mt = local - ntk * nmt;
   const int nt = ntk / ksplit, kh = ntk - nt * ksplit;
   r.kb0 = (int)((long long)kh * nk / ksplit);
   r.kb1 = (int)((long long)(kh + 1) * nk / ksplit);
-  const int n_e = a.expert_off[r.e + 1] - a.expert_off[r.e];
   r.m0 = mt * TOK;
   r.n0 = nt * nstep;
   r.rows = min(TOK, n_e - r.m0);

@@ -244,11 +244,15 @@ class PrefetchingStack:
     predicted experts' formats at the widths layer l+1's schedule gives their ranks (Eq. 5 tier
     counts: the top t_1 -- the paper's critical experts -- at the top tier) are quantized into
     the arena on a side stream while layer l's FFN runs on the main stream.  prefetch=False: every format is
-    loaded on demand (the baseline the overlap is measured against)."""
+    loaded on demand (the baseline the overlap is measured against).  policy "critical": only the
+    top t_1 predicted experts, at the top tier (the paper's prefetch of the critical experts);
+    "tiered": every predicted expert at its predicted tier."""
 
-    def __init__(self, store, gates):
+    def __init__(self, store, gates, policy="critical"):
+        assert policy in ("critical", "tiered")
         self.store = store
         self.gates = gates
+        self.policy = policy
         self.L, self.M, self.k = store.L, store.M, store.k
         self.side = torch.cuda.Stream(device=store.device)
 
@@ -280,6 +284,8 @@ class PrefetchingStack:
                 tiers = d.dymoe_tier_counts(l + 1, self.L, ladder, self.M, self.k)
                 # decode: at most T k experts can be active (B = 1: the top-k of Eq. 8)
                 t = self.M if phase == d.DYMOE_PREFILL else min(self.M, T * self.k)
+                if self.policy == "critical":
+                    t = max(1, min(t, tiers[0] if tiers else self.M))
                 ex, _, _ = d.dymoe_predict_next(phase, u, self.gates[l + 1][0], self.k, t)
                 req = [0] * self.M
                 for rank, e in enumerate(ex.cpu().tolist()):

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--budget", type=float, default=0.45)
     ap.add_argument("--passes", type=int, default=4)
     ap.add_argument("--prefill", action="store_true")
+    ap.add_argument("--policy", default="critical", choices=["critical", "tiered"])
     ap.add_argument("--offload", action="store_true",
                     help="host-offload variant (f4, the paper's setting): bf16 masters in pinned host "
                          "memory, every format a pool entry, a miss = H2D copy + quantize")
@@ -69,12 +70,12 @@ def main():
     attn = [synthetic.attention_mass(cfg, 40 + l, dev) for l in range(L)] if args.prefill else None
     xs = [synthetic.hidden_states(cfg, 70 + i, dev) for i in range(args.passes)]
     res = {"layers": L, "tokens": T, "phase": "prefill" if args.prefill else "decode",
-           "offload": args.offload,
+           "offload": args.offload, "policy": args.policy,
            "arena_GB": round(full * args.budget / 1e9, 2), "all_packed_GB": round(full / 1e9, 2),
            "budget": args.budget}
     for prefetch in (False, True):
         store = ExpertStore(masters, cfg.k, cfg.hidden, cfg.ffn, int(full * args.budget))
-        st = PrefetchingStack(store, gates)
+        st = PrefetchingStack(store, gates, policy=args.policy)
         st.forward(xs[0], lad, ph, attn, prefetch=prefetch)     # warm the pool
         torch.cuda.synchronize()
         t0 = time.perf_counter()
