@@ -260,11 +260,11 @@ k_attn_mass(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUt
           // overlaps it -- no shared memory, no barrier
           const float* mq = m_io + (size_t)h * T + bb * BT + c0;
           float4 mm4[HC / 4];
-          if (full) {
+          if (full && (T & 3) == 0) {           // 16-byte aligned rows of the scratch
 #pragma unroll
             for (int c = 0; c < HC / 4; ++c) mm4[c] = __ldg(reinterpret_cast<const float4*>(mq) + c);
           } else {
-            const int nv = T - bb * BT - c0;      // queries of this part inside the sequence
+            const int nv = min(HC, T - bb * BT - c0);   // queries of this part inside the sequence
 #pragma unroll
             for (int c = 0; c < HC / 4; ++c) {
               float t0[4];
