@@ -365,10 +365,10 @@ class LayerTimer:
         return 4 if self.phase == self.d.DYMOE_DECODE else 9
 
 
-def sub_line(t, K, W, peaks, e2e=True, extra=None):
+def sub_line(t, K, W, peaks, e2e=True, extra=None, tr=None):
     """A compact JSON object for one extra layer workload (BASELINE.json metric, same clock)."""
     r = t.run(K, W)
-    roof = t.roofline(peaks)
+    roof = t.roofline(peaks, tr)
     out = {"value": t.T * K / (r["ms"] / 1e3), "unit": "tokens/s", "ms_per_step": r["ms"] / K,
            "steps": K, "tokens_per_step": t.T, "ladder": t.ladder_desc,
            "roofline": {k: roof[k] for k in roof if k not in ("traffic_capture",)},
@@ -428,7 +428,8 @@ def run_ours(args, rank, world, device):
         subs = {}
         pf = LayerTimer(d, layers, cfg.with_tokens(args.tokens), d.DYMOE_PREFILL, ladder, device)
         subs["prefill"] = sub_line(pf, Kp, W, peaks, extra={"config": "BASELINE.json configs[2]: "
-                                   "Mixtral-8x7B layer prefill %d tokens" % args.tokens})
+                                   "Mixtral-8x7B layer prefill %d tokens" % args.tokens},
+                                   tr=load_traffic("k_prefill_gemm<W13>"))
         del pf
         torch.cuda.empty_cache()
         b1 = LayerTimer(d, layers, cfg.with_tokens(1), d.DYMOE_DECODE, ladder, device)
