@@ -488,12 +488,29 @@ def run_ep(args, rank, world, device):
     uid = None if gloo else ep.broadcast_unique_id()
     first, last = ep.owned_range(rank, cfg.M, world)
     layers = []
+    setup_errors = {}
     for c in range(args.copies):
         ex = synthetic.expert_weights(cfg, 100 + c, device, experts=list(range(first, last)))
         ex = [{n: t.to(device) for n, t in e.items()} for e in ex]
         d.quantize_experts(ex, (8, 4, 2))
-        layers.append(ep.EPLayer(rank, world, cfg.M, cfg.k, cfg.hidden, cfg.ffn, T, ex,
-                                 transports=transports, nccl_uid=uid))
+        try:
+            L_ = ep.EPLayer(rank, world, cfg.M, cfg.k, cfg.hidden, cfg.ffn, T, ex,
+                            transports=transports, nccl_uid=uid)
+            ok = 1.0
+        except d.DymoeError as err:   # e.g. no peer access between the GPUs: NCCL only
+            setup_errors["peer"] = str(err)[:300]
+            L_, ok = None, 0.0
+        # every rank must agree on the transports (the window exchange is collective)
+        if _max_over_ranks(1.0 - ok, device) > 0:
+            if L_ is not None:
+                L_.close()
+            if gloo:
+                raise SystemExit("expert-parallel handle creation failed: %s" % setup_errors)
+            transports = d.DYMOE_EP_NCCL
+            uid = ep.broadcast_unique_id()
+            L_ = ep.EPLayer(rank, world, cfg.M, cfg.k, cfg.hidden, cfg.ffn, T, ex,
+                            transports=transports, nccl_uid=uid)
+        layers.append(L_)
         if gloo:
             opened = ep.connect_processes(layers[-1])
             layers[-1]._opened = opened
@@ -529,7 +546,7 @@ def run_ep(args, rank, world, device):
         (all ranks' per-expert counts, gathered untimed) at the widths the step assigned"""
         cen = {}
         for i in range(math.lcm(len(layers), NUM_LAYERS, n_inputs)):
-            step(i, transports & d.DYMOE_EP_PEER or d.DYMOE_EP_NCCL)
+            step(i, d.DYMOE_EP_NCCL if transports & d.DYMOE_EP_NCCL else d.DYMOE_EP_PEER)
             c = i % len(layers)
             v = layers[c].views(T, ws[c])
             cnt = torch.diff(v["expert_off"]).to(torch.int64)
@@ -686,7 +703,7 @@ def run_ep(args, rank, world, device):
             # reduce/zero, combine -- NCCL's own kernels not counted)
             "gpu_launches": (15 if main == "peer" else 11) * K,
             "ep_path": main, "ep_transports": {k: pub(v) for k, v in lines.items()},
-            "ep_errors": errors or None, "ep_replicated_decode": rep or None}
+            "ep_errors": dict(errors, **setup_errors) or None, "ep_replicated_decode": rep or None}
 
 
 def _all_gather(t, device):
