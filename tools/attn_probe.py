@@ -11,6 +11,9 @@ import torch  # noqa: E402
 
 import paper_2603_19172_b200.dymoe as d  # noqa: E402
 
+if os.environ.get("ATTN_LIB"):   # a variant library built by tools/attn_trace.py --build NAME ...
+    d.LIB_PATH = os.environ["ATTN_LIB"]
+
 
 def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(

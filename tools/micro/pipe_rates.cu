@@ -57,6 +57,16 @@ __global__ void k(uint32_t* out, int iters, uint32_t seed, long long* cyc) {
         __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&c1);
         a = __hmul2(__hsub2(a, b), b);
         r[i] ^= *reinterpret_cast<uint32_t*>(&a);
+      } else if (OP == 20) {  // MUFU.EX2 (ex2.approx.ftz.f32)
+        float y;   // a pure chain: 2^x of the previous result (the value does not matter)
+        asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(__uint_as_float(r[i])));
+        r[i] = __float_as_uint(y);
+      } else if (OP == 21) {  // FFMA2 (fma.rn.f32x2)
+        uint64_t a, y;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "r"(r[i]), "r"(r[(i + 1) & 7]));
+        const uint64_t b = ((uint64_t)c1 << 32) | c1, c = ((uint64_t)c2 << 32) | c2;
+        asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(y) : "l"(a), "l"(b), "l"(c));
+        r[i] = (uint32_t)y ^ (uint32_t)(y >> 32);
       } else if (OP == 10) {  // mma.sync m16n8k16 bf16, 2 independent accumulators per chain pair
         if (i < 2) {
           float* d = &acc[i].x;
@@ -159,5 +169,7 @@ int main() {
   run<13>("mma + 8 FMUL", out, cyc);
   run<14>("mma + 8 LOP3", out, cyc);
   run<15>("mma + 8 IMAD", out, cyc);
+  run<20>("MUFU.EX2", out, cyc);
+  run<21>("FFMA2 (+MOV +XOR)", out, cyc);
   return 0;
 }

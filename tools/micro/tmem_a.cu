@@ -318,6 +318,8 @@ int main() {
     mr(k_mma_rate<128, 16, false>, 128, 16, "SS");
     mr(k_mma_rate<128, 64, false>, 128, 64, "SS");
     mr(k_mma_rate<128, 256, false>, 128, 256, "SS");
+    mr(k_mma_rate<128, 128, false>, 128, 128, "SS");
+    mr(k_mma_rate<128, 192, false>, 128, 192, "SS");
     mr(k_mma_rate<64, 8, true>, 64, 8, "TS");
     mr(k_mma_rate<64, 8, false>, 64, 8, "SS");
   }
