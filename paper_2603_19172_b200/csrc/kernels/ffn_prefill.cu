@@ -138,17 +138,20 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
-// commit this thread's prior MMAs to the barrier at the same offset in both CTAs of the pair
-__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+// MMA issue and commit to the barrier at the same offset in both CTAs of the pair, warp-collective:
+// every lane executes them with warp-uniform operands and one elected lane issues (no
+// per-instruction R2UR / elect loop around a lane-0-only branch)
+__device__ __forceinline__ void tc_commit_pair_elect(uint32_t bar) {
   asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}"
       ::"r"(bar), "h"((uint16_t)0x3) : "memory");
 }
-__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
+__device__ __forceinline__ void tc_mma_pair_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                  uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -407,7 +410,7 @@ __device__ __forceinline__ bool prefill_resident(const FfnArgs& a, int e, bool w
 }
 
 __device__ void build_sched_warp(const FfnArgs& a, int tok, int ntiles_n, Sched& S, int* n_tiles,
-                                 bool w13) {
+                                 bool w13, int* nr_list, int* nr_count) {
   const int lane = threadIdx.x & 31;
   const int n = a.active_list[0];
   const int per = (n + 31) / 32;
@@ -420,6 +423,7 @@ __device__ void build_sched_warp(const FfnArgs& a, int tok, int ntiles_n, Sched&
     if (!prefill_resident(a, e, w13)) {
       if (a.status && blockIdx.x == 0)
         atomicOr(a.status, (unsigned)DYMOE_STATUS_WIDTH_NOT_RESIDENT);
+      nr_list[atomicAdd(nr_count, 1)] = e;   // rows left out of the schedule (shared memory)
       continue;
     }
     ++kept;
@@ -453,10 +457,14 @@ struct Tile {
   int kb0, kb1;          // k-block range of this tile (GEMM 2: one of two K halves)
 };
 // ntiles_n counts (n tile, k half) pairs when ksplit == 2
+// ei: the caller's cursor into the schedule's expert table -- every role walks its tiles in
+// increasing t, so the lookup resumes where the previous one stopped (a scan from 0 cost up to
+// M shared-memory round trips per tile and role at 64 active experts).
 __device__ __forceinline__ Tile tile_at(const Sched& S, const FfnArgs& a, int t, int ntiles_n,
-                                        int nstep, int nk, int ksplit) {
-  int i = 0;
+                                        int nstep, int nk, int ksplit, int& ei) {
+  int i = ei;
   while (S.first[i + 1] <= t) ++i;
+  ei = i;
   Tile r;
   r.e = S.expert[i];
   const int local = t - S.first[i];
@@ -485,6 +493,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
   __shared__ __align__(8) uint64_t raw_full[PF], raw_empty[PF];
   __shared__ uint32_t tmem_base_sh;
   __shared__ int n_tiles_sh;
+  __shared__ int nr_list[DYMOE_MAX_EXPERTS], nr_count;   // experts left out (width not resident)
   constexpr uint32_t IDESC = make_idesc(2 * BM, NCOL);
   const int K = W13 ? a.Hd : a.F;
   const int NWR = W13 ? a.F : a.Hd;                  // weight rows per matrix
@@ -510,7 +519,9 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
   const uint32_t full_cl = mapa(full0, 0);                     // the leader's full barriers
   const uint32_t tempty_cl = mapa(smem_u32(&tempty_bar[0]), 0);
 
-  if (threadIdx.x < 32) build_sched_warp(a, TOK, ntiles_n, S, &n_tiles_sh, W13);
+  if (threadIdx.x == 0) nr_count = 0;
+  __syncwarp();
+  if (threadIdx.x < 32) build_sched_warp(a, TOK, ntiles_n, S, &n_tiles_sh, W13, nr_list, &nr_count);
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full_bar[s]), 2 + 2 * kBWarps);   // leader's: both CTAs arrive
@@ -537,6 +548,16 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
   tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const int n_tiles = n_tiles_sh;
+  int ei = 0;   // this thread's schedule cursor (tile_at)
+  if (!W13 && KSPLIT == 1 && blockIdx.x == 0 && nr_count > 0) {
+    // whole-K tiles store y_perm without a pre-zeroed target: the rows of experts left out of
+    // the schedule are zeroed here instead, so the combine adds nothing for them (rare path)
+    for (int x = 0; x < nr_count; ++x) {
+      const int e = nr_list[x];
+      const size_t r0 = a.expert_off[e], r1 = a.expert_off[e + 1];
+      for (size_t i = r0 * a.Hd + threadIdx.x; i < r1 * a.Hd; i += blockDim.x) a.y_perm[i] = 0.f;
+    }
+  }
 
   if (warp == 0) {
     // ------------------------------------------------------------------ A (and BF16 B) TMA
@@ -544,7 +565,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
       int stage = 0;
       uint32_t phase = 0;
       for (int t = pair; t < n_tiles; t += npairs) {
-        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
+        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
         const int row0 = a.expert_off[T.e] + T.m0 + (int)rank * BM;
         const bool bf = a.bits[T.e] == 16;
         const CUtensorMap* tmB = nullptr;
@@ -567,7 +588,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
       int rslot = 0;
       uint32_t rphase = 0;
       for (int t = pair; t < n_tiles; t += npairs) {
-        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
+        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
         const int be = a.bits[T.e];
         if (be == 16) continue;
         const DevQMat& q = a.experts[T.e].q[width_index(be)][W13 ? (int)rank : 2];
@@ -585,26 +606,58 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (leader)
-    if (rank == 0 && lane == 0) {
-      int stage = 0;
+    // The whole warp runs the loop (warp-uniform control flow and descriptors), one elected lane
+    // issues.  The waits for the next k-block's stage (and, at a tile change, the next tile's
+    // accumulator and schedule lookup) sit before the k-block's last MMA, so that they overlap
+    // the MMAs still queued in the tensor core instead of leaving it idle between k-blocks.
+    if (rank == 0) {
+      int stage = 0, i = 0;
       uint32_t phase = 0;
-      int i = 0;
-      for (int t = pair; t < n_tiles; t += npairs, ++i) {
-        const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
-        const int b = i & 1;
-        mbar_wait(smem_u32(&tempty_bar[b]), ((i >> 1) & 1) ^ 1);
+      int t = pair;
+      Tile T{};
+      if (t < n_tiles) {
+        T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
+        mbar_wait(smem_u32(&tempty_bar[0]), 1);
+        mbar_wait(full0, 0);
         tc_fence_after();
-        for (int kb = T.kb0; kb < T.kb1; ++kb) {
-          mbar_wait(full0 + stage * 8, phase);
-          tc_fence_after();
+      }
+      int kb = T.kb0;
+      while (t < n_tiles) {
+        const int b = i & 1;
+        const uint64_t ad = sw_desc(sA(stage)), bd = sw_desc(sB(stage));
+        const uint32_t d_tmem = tmem + b * NCOL;
+        const uint32_t acc0 = kb != T.kb0;
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            tc_mma_pair(tmem + b * NCOL, sw_desc(sA(stage) + kk * 32), sw_desc(sB(stage) + kk * 32),
-                        IDESC, ((kb - T.kb0) | kk) != 0);
-          tc_commit_pair(empty0 + stage * 8);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        for (int kk = 0; kk < BK / 16 - 1; ++kk)   // + kk * 32 bytes = + 2 kk in the start field
+          tc_mma_pair_elect(d_tmem, ad + 2 * kk, bd + 2 * kk, IDESC, acc0 | (uint32_t)(kk != 0));
+        // the next k-block: this tile's, or the first of the next tile
+        int nkb = kb + 1, nt = t, ni = i;
+        Tile NT = T;
+        const bool tile_end = nkb >= T.kb1;
+        if (tile_end) {
+          nt = t + npairs;
+          ni = i + 1;
+          if (nt < n_tiles) {
+            NT = tile_at(S, a, nt, ntiles_n, nstep, nk, KSPLIT, ei);
+            nkb = NT.kb0;
+          }
         }
-        tc_commit_pair(smem_u32(&tfull_bar[b]));
+        const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
+        const uint32_t nphase = stage + 1 == STAGES ? phase ^ 1 : phase;
+        if (nt < n_tiles) {
+          if (tile_end) mbar_wait(smem_u32(&tempty_bar[ni & 1]), ((ni >> 1) & 1) ^ 1);
+          mbar_wait(full0 + nstage * 8, nphase);
+        }
+        tc_mma_pair_elect(d_tmem, ad + 2 * (BK / 16 - 1), bd + 2 * (BK / 16 - 1), IDESC, 1);
+        tc_commit_pair_elect(empty0 + stage * 8);
+        if (tile_end) tc_commit_pair_elect(smem_u32(&tfull_bar[b]));
+        tc_fence_after();   // the next k-block's MMAs are ordered after the waits above
+        stage = nstage;
+        phase = nphase;
+        kb = nkb;
+        t = nt;
+        i = ni;
+        T = NT;
       }
     }
   } else if (warp < kEpiWarp0) {
@@ -615,7 +668,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     int stage = 0, rslot = 0;
     uint32_t phase = 0, rphase = 0;
     for (int t = pair; t < n_tiles; t += npairs) {
-      const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
+      const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
       const int be = a.bits[T.e];
 #define DYMOE_PRODUCE(B) produce<B>(khalf, wr, T.kb0, T.kb1, sbase, raw_base, raw_full0, raw_empty0, \
                                     full_cl, empty0, stage, phase, rslot, rphase)
@@ -633,7 +686,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     const int trow = q * 32 + lane;               // token row within this CTA's half
     int i = 0;
     for (int t = pair; t < n_tiles; t += npairs, ++i) {
-      const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT);
+      const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
       const int b = i & 1;
       mbar_wait_sleep(smem_u32(&tfull_bar[b]), (i >> 1) & 1, 256);
       tc_fence_after();
@@ -669,14 +722,22 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
           tmem_ld32(tbase + cc * 32, v);
           tmem_ld_wait();
           if (live && T.n0 + cc * 32 < NWR) {   // last W2 tile may overhang Hd (clamped rows)
-            // one of the two K halves: add into the zeroed output (two addends per element)
             float* dstp = a.y_perm + grow * a.Hd + T.n0 + cc * 32;
+            if (KSPLIT == 1) {   // the whole K: the element's only write
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dstp + 4 * j),
-                           "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
-                           "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
-                           : "memory");
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<float4*>(dstp + 4 * j) =
+                    make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+            } else {
+              // one of the two K halves: add into the zeroed output (two addends per element)
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dstp + 4 * j),
+                             "f"(__uint_as_float(v[4 * j])), "f"(__uint_as_float(v[4 * j + 1])),
+                             "f"(__uint_as_float(v[4 * j + 2])), "f"(__uint_as_float(v[4 * j + 3]))
+                             : "memory");
+            }
           }
         }
       }
@@ -747,9 +808,12 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   record_ev(ev, 1, s);
-  // split-K target: the routed rows (device count) zeroed, not the whole capacity
-  e = launch_zero_rows(a.y_perm, a.Hd, rows, a.expert_off + a.M, s);
-  if (e != cudaSuccess) return e;
+  // split-K target: the routed rows (device count) zeroed, not the whole capacity; whole-K
+  // tiles store their rows (and zero those of experts left out) themselves
+  if (ksplit != 1) {
+    e = launch_zero_rows(a.y_perm, a.Hd, rows, a.expert_off + a.M, s);
+    if (e != cudaSuccess) return e;
+  }
   k_prefill_gemm<false><<<grid, kThreads, kSmem, s>>>(a, tm2, ksplit == 1 ? 1 : 2);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
