@@ -57,6 +57,31 @@ constexpr int RAW_BYTES = PF * RAW_SLOT;
 constexpr int kSmem = STAGES * STAGE_BYTES + RAW_BYTES + 1024;   // + alignment slack
 constexpr uint32_t TMEM_COLS = 2 * NCOL;                // two accumulators
 
+// Optional timeline of CTA 0 (tools/pf_trace.py builds a separate library with -DDYMOE_PF_TRACE;
+// the product build has no trace code): (event, clock64) pairs per role -- 0 MMA issuer,
+// 1 producer warp 2 lane 0, 2 A-tile TMA thread -- for the W13 (pass 0) and W2 (pass 1) GEMMs.
+#ifdef DYMOE_PF_TRACE
+__device__ unsigned long long g_pf_tr[2][3][8192];
+__device__ int g_pf_trn[2][3];
+#define PF_TR_BEGIN int tr_i = 0
+#define PF_TR(role, ev)                                                  \
+  do {                                                                   \
+    if (blockIdx.x == 0 && tr_i < 4096) {                                \
+      g_pf_tr[W13 ? 0 : 1][role][2 * tr_i] = (ev);                       \
+      g_pf_tr[W13 ? 0 : 1][role][2 * tr_i + 1] = clock64();              \
+      ++tr_i;                                                            \
+    }                                                                    \
+  } while (0)
+#define PF_TR_END(role) \
+  do {                  \
+    if (blockIdx.x == 0) g_pf_trn[W13 ? 0 : 1][role] = tr_i; \
+  } while (0)
+#else
+#define PF_TR_BEGIN do {} while (0)
+#define PF_TR(role, ev) do {} while (0)
+#define PF_TR_END(role) do {} while (0)
+#endif
+
 // ---------------------------------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -351,22 +376,29 @@ __device__ __forceinline__ void store_stage(const RawStage<BE>& r, uint32_t dst,
 
 // One tile's k-blocks [kb0, kb1).  full_cl: shared::cluster address of the leader's full_bar[0]
 // (stage s at + 8 s); raw ring position (rslot, rphase) shared with the issuer's order.
-template <int BE>
+template <int BE, bool W13>
 __device__ __forceinline__ void produce(int khalf, int wr, int kb0, int kb1, uint32_t sbase,
                                         uint32_t raw_base, uint32_t raw_full0, uint32_t raw_empty0,
                                         uint32_t full_cl, uint32_t empty_bar, int& stage,
-                                        uint32_t& phase, int& rslot, uint32_t& rphase) {
+                                        uint32_t& phase, int& rslot, uint32_t& rphase, int& tr_i) {
   const int j0 = khalf * (KPER / 8);
   const bool lane0 = (threadIdx.x & 31) == 0;
+  const bool tr = threadIdx.x == 64;   // producer warp 2, lane 0
+  (void)tr;
+  (void)tr_i;
   for (int kb = kb0; kb < kb1; ++kb) {
     if constexpr (BE != 16) {
       RawStage<BE> r;
+      if (tr) PF_TR(1, 11);
       mbar_wait(raw_full0 + rslot * 8, rphase);
+      if (tr) PF_TR(1, 12);
       read_raw<BE>(r, raw_base + rslot * RAW_SLOT, wr, khalf);
       __syncwarp();
       if (lane0) mbar_arrive_local(raw_empty0 + rslot * 8);
       if (++rslot == PF) { rslot = 0; rphase ^= 1; }
+      if (tr) PF_TR(1, 13);
       mbar_wait(empty_bar + stage * 8, phase ^ 1);
+      if (tr) PF_TR(1, 14);
       store_stage<BE>(r, sbase + stage * STAGE_BYTES + A_BYTES, wr, j0);
       fence_proxy_async();
     } else {
@@ -374,6 +406,7 @@ __device__ __forceinline__ void produce(int khalf, int wr, int kb0, int kb1, uin
     }
     __syncwarp();   // one release-arrive per warp (the whole warp's writes are fenced)
     if (lane0) mbar_arrive_cl(full_cl + stage * 8);
+    if (tr) PF_TR(1, 15);
     if (++stage == STAGES) { stage = 0; phase ^= 1; }
   }
 }
@@ -564,6 +597,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      PF_TR_BEGIN;
       for (int t = pair; t < n_tiles; t += npairs) {
         const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
         const int row0 = a.expert_off[T.e] + T.m0 + (int)rank * BM;
@@ -576,13 +610,16 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
           brow0 = T.n0 + (W13 ? 0 : (int)rank * BNH);
         }
         for (int kb = T.kb0; kb < T.kb1; ++kb) {
+          PF_TR(2, 21);
           mbar_wait(empty0 + stage * 8, phase ^ 1);
+          PF_TR(2, 22);
           mbar_expect_tx_cl(full_cl + stage * 8, A_BYTES + (bf ? B_BYTES : 0));
           tma2d_pair(sA(stage), &tmA, kb * BK, row0, full_cl + stage * 8);
           if (bf) tma2d_pair(sB(stage), tmB, kb * BK, brow0, full_cl + stage * 8);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+      PF_TR_END(2);
     } else if (lane == 1) {
       // packed codes + dequant words of this CTA's 128 B rows, PF stages ahead of the producers
       int rslot = 0;
@@ -614,6 +651,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
       int stage = 0, i = 0;
       uint32_t phase = 0;
       int t = pair;
+      PF_TR_BEGIN;
       Tile T{};
       if (t < n_tiles) {
         T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
@@ -644,10 +682,13 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
         }
         const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
         const uint32_t nphase = stage + 1 == STAGES ? phase ^ 1 : phase;
+        if (lane == 0) PF_TR(0, tile_end ? 5 : 1);
         if (nt < n_tiles) {
           if (tile_end) mbar_wait(smem_u32(&tempty_bar[ni & 1]), ((ni >> 1) & 1) ^ 1);
+          if (lane == 0) PF_TR(0, 2);
           mbar_wait(full0 + nstage * 8, nphase);
         }
+        if (lane == 0) PF_TR(0, 3);
         tc_mma_pair_elect(d_tmem, ad + 2 * (BK / 16 - 1), bd + 2 * (BK / 16 - 1), IDESC, 1);
         tc_commit_pair_elect(empty0 + stage * 8);
         if (tile_end) tc_commit_pair_elect(smem_u32(&tfull_bar[b]));
@@ -659,6 +700,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
         i = ni;
         T = NT;
       }
+      if (lane == 0) PF_TR_END(0);
     }
   } else if (warp < kEpiWarp0) {
     // ------------------------------------------------------------------ B producer (dequant)
@@ -667,11 +709,12 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
     const int khalf = tb >> 7;
     int stage = 0, rslot = 0;
     uint32_t phase = 0, rphase = 0;
+    int tr_i = 0;
     for (int t = pair; t < n_tiles; t += npairs) {
       const Tile T = tile_at(S, a, t, ntiles_n, nstep, nk, KSPLIT, ei);
       const int be = a.bits[T.e];
-#define DYMOE_PRODUCE(B) produce<B>(khalf, wr, T.kb0, T.kb1, sbase, raw_base, raw_full0, raw_empty0, \
-                                    full_cl, empty0, stage, phase, rslot, rphase)
+#define DYMOE_PRODUCE(B) produce<B, W13>(khalf, wr, T.kb0, T.kb1, sbase, raw_base, raw_full0, \
+                                         raw_empty0, full_cl, empty0, stage, phase, rslot, rphase, tr_i)
       switch (be) {
         case 2: DYMOE_PRODUCE(2); break;
         case 4: DYMOE_PRODUCE(4); break;
@@ -680,6 +723,7 @@ k_prefill_gemm(const FfnArgs a, const __grid_constant__ CUtensorMap tmA, int ksp
       }
 #undef DYMOE_PRODUCE
     }
+    if (threadIdx.x == 64) PF_TR_END(1);
   } else {
     // ------------------------------------------------------------------ epilogue (TMEM -> global)
     const int q = warp & 3;                       // TMEM lane quarter this warp may access
@@ -820,6 +864,17 @@ cudaError_t launch_ffn_prefill(const FfnArgs& a, cudaStream_t s, void* const* ev
   record_ev(ev, 2, s);
   return cudaSuccess;
 }
+
+#ifdef DYMOE_PF_TRACE
+extern "C" int dymoe_pf_trace_read(unsigned long long* host, int* counts) {
+  int zero[6] = {0, 0, 0, 0, 0, 0};
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(counts, pf::g_pf_trn, sizeof(zero));
+  cudaMemcpyFromSymbol(host, pf::g_pf_tr, sizeof(pf::g_pf_tr));
+  cudaMemcpyToSymbol(pf::g_pf_trn, zero, sizeof(zero));
+  return (int)cudaGetLastError();
+}
+#endif
 
 cudaError_t preload_ffn_prefill() {
   return preload_kernels(k_gather_perm, pf::k_prefill_gemm<true>, pf::k_prefill_gemm<false>);
