@@ -45,6 +45,8 @@ import synthetic  # noqa: E402
 
 LADDER_BITS, LADDER_LAMBDAS = (8, 4, 2), (0.25, 0.5)
 NUM_LAYERS = 32
+PROF_EVERY = 17  # --prof-every: per-kernel profiling events on every n-th timed step (17: coprime
+                 # with the 32-step period of (copy, layer, input), so the sample covers all of them)
 METRIC = "MoE-layer tokens/s (prefill, decode) + achieved HBM GB/s / tensor-pipe %"
 
 
@@ -214,8 +216,15 @@ class LayerTimer:
         self.cen = cen
         return cen
 
-    def run(self, K, W, graph=True, world=1):
+    def run(self, K, W, graph=True, world=1, prof_every=None):
+        """prof_every: per-kernel events on steps i % prof_every == 0 only (None: the
+        --prof-every option).  The events are external event-record nodes of the captured graph;
+        on every step they added ~14 us to the 214 us decode step (7 %), so the throughput is
+        taken over all K steps with events on a sample, and the kernel roofline from that
+        sample."""
         d, stream = self.d, torch.cuda.current_stream()
+        pe = max(1, PROF_EVERY if prof_every is None else prof_every)
+        prof = [i for i in range(K) if i % pe == 0]
         self.census()
         for i in range(W):
             self.step(i)
@@ -235,7 +244,7 @@ class LayerTimer:
             with torch.cuda.stream(side):
                 with torch.cuda.graph(g, stream=side):
                     for i in range(K):
-                        self.step(W + i, ev[i])
+                        self.step(W + i, ev[i] if i % pe == 0 else None)
             stream.wait_stream(side)
             g.replay()          # one untimed replay (the warm-up steps above ran call by call)
             torch.cuda.synchronize()
@@ -248,23 +257,25 @@ class LayerTimer:
                 g.replay()
             else:
                 for i in range(K):
-                    self.step(W + i, ev[i])
+                    self.step(W + i, ev[i] if i % pe == 0 else None)
             t1.record(stream)
             torch.cuda.synchronize()
         ms = t0.elapsed_time(t1)
-        w13_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in range(K)]
-        w2_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in range(K)]
-        steps = [self.plan(W + i) for i in range(K)]
+        w13_ms = [ev[i][0].elapsed_time(ev[i][1]) for i in prof]
+        w2_ms = [ev[i][1].elapsed_time(ev[i][2]) for i in prof]
+        steps = [self.plan(W + i) for i in prof]
         b13 = sum(self.cen[p][0][0] for p in steps)
         b2 = sum(self.cen[p][0][1] for p in steps)
         fl = sum(self.cen[p][1] for p in steps)
         self.res = dict(ms=ms, K=K, W=W, w13_ms=sum(w13_ms), w2_ms=sum(w2_ms), b13=b13, b2=b2,
-                        fl=fl, clocks=clk.summary(), graph=g is not None)
+                        fl=fl, clocks=clk.summary(), graph=g is not None, K_prof=len(prof),
+                        prof_every=pe)
         return self.res
 
     def roofline(self, peaks, tr=None):
         r = self.res
-        ms, K = r["ms"], r["K"]
+        # the kernel times and algorithmic work of the profiled steps; ms / K the whole run's
+        ms, K = r["ms"] * r["K_prof"] / r["K"], r["K_prof"]
         ffn_ms = r["w13_ms"] + r["w2_ms"]
         if self.phase == self.d.DYMOE_DECODE:
             # dominant kernel: the W1/W3 fused-dequant SwiGLU GEMV (HBM-bound); per launch the
@@ -279,7 +290,8 @@ class LayerTimer:
                     "ffn_w13_plus_w2_GBs": (r["b13"] + r["b2"]) / (ffn_ms / 1e3) / 1e9,
                     "ffn_share_of_step": ffn_ms / ms,
                     "algorithmic_bytes_per_step": (r["b13"] + r["b2"]) / K,
-                    "w13_us_per_step": r["w13_ms"] / K * 1e3, "w2_us_per_step": r["w2_ms"] / K * 1e3}
+                    "w13_us_per_step": r["w13_ms"] / K * 1e3, "w2_us_per_step": r["w2_ms"] / K * 1e3,
+                    "profiled_steps": r["K_prof"], "prof_every": r["prof_every"]}
         # dominant kernel: the tcgen05 fused-dequant grouped GEMMs (tensor-bound); algorithmic
         # flops per step = 6 * Hd * F per executed (token, expert) pair
         tfl = r["fl"] / (ffn_ms / 1e3) / 1e12
@@ -291,7 +303,8 @@ class LayerTimer:
                 "w13_tflops": (r["fl"] * 2 / 3) / (r["w13_ms"] / 1e3) / 1e12,
                 "w2_tflops": (r["fl"] / 3) / (r["w2_ms"] / 1e3) / 1e12,
                 "ffn_share_of_step": ffn_ms / ms, "algorithmic_flops_per_step": r["fl"] / K,
-                "hbm_GBs_ffn": (r["b13"] + r["b2"]) / (ffn_ms / 1e3) / 1e9}
+                "hbm_GBs_ffn": (r["b13"] + r["b2"]) / (ffn_ms / 1e3) / 1e9,
+                "profiled_steps": r["K_prof"], "prof_every": r["prof_every"]}
 
     def e2e(self, K, W):
         """The same steps through the public API with the step's inputs copied in from pinned
@@ -570,17 +583,18 @@ def run_ep(args, rank, world, device):
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.distributed.barrier()
         torch.cuda.synchronize()
+        prof = [i for i in range(K) if i % PROF_EVERY == 0]   # per-kernel events: a sample
         with ClockSampler(torch.cuda.current_device()) as clk:
             t0.record()
             for i in range(K):
-                step(W + i, transport, placement, ev=ev[i])
+                step(W + i, transport, placement, ev=ev[i] if i % PROF_EVERY == 0 else None)
             t1.record()
             torch.cuda.synchronize()
         torch.distributed.barrier()
         ms = _max_over_ranks(t0.elapsed_time(t1), device)
-        w13 = sum(ev[i][0].elapsed_time(ev[i][1]) for i in range(K))
-        w2 = sum(ev[i][1].elapsed_time(ev[i][2]) for i in range(K))
-        return ms, w13, w2, clk.summary()
+        w13 = sum(ev[i][0].elapsed_time(ev[i][1]) for i in prof)
+        w2 = sum(ev[i][1].elapsed_time(ev[i][2]) for i in prof)
+        return ms, w13, w2, clk.summary(), prof
 
     lines, errors = {}, {}
     cen = census()
@@ -592,15 +606,15 @@ def run_ep(args, rank, world, device):
             torch.cuda.synchronize()
             if status_all():
                 raise RuntimeError("status word after the first step")
-            ms, w13, w2, clk = timed(tp)
+            ms, w13, w2, clk, prof = timed(tp)
             st = status_all()
-            steps = [((W + i) % len(layers), (W + i) % NUM_LAYERS, (W + i) % n_inputs) for i in range(K)]
+            steps = [((W + i) % len(layers), (W + i) % NUM_LAYERS, (W + i) % n_inputs) for i in prof]
             b13 = sum(cen[p][0][0] for p in steps)
             b2 = sum(cen[p][0][1] for p in steps)
             fl = sum(cen[p][1] for p in steps)
             lines[name] = {"value": T * K * world / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms / K,
                            "status": st, "clocks": clk, "w13_ms": w13, "w2_ms": w2, "b13": b13, "b2": b2,
-                           "fl": fl}
+                           "fl": fl, "K_prof": len(prof)}
         except Exception as ex:   # reported, never fatal for the other transport
             errors[name] = "%s: %s" % (type(ex).__name__, str(ex)[:300])
     main = "peer" if ("peer" in lines and lines["peer"]["status"] == 0 and args.ep_main != "nccl") \
@@ -651,7 +665,7 @@ def run_ep(args, rank, world, device):
             if not (transports & tp):
                 continue
             try:
-                ms, _, _, clk = timed(tp, d.DYMOE_EP_REPLICATED)
+                ms, _, _, clk, _ = timed(tp, d.DYMOE_EP_REPLICATED)
                 rep[name] = {"value": T * K / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms / K,
                              "scaling": "strong", "global_batch": T,
                              "status": status_all(d.DYMOE_EP_REPLICATED)}
@@ -666,14 +680,16 @@ def run_ep(args, rank, world, device):
                 "achieved": ach, "peak": peaks["hbm"], "unit": "GB/s", "frac": ach / peaks["hbm"],
                 "traffic": None, "peak_src": peaks["src"],
                 "ffn_w13_plus_w2_GBs": (L0["b13"] + L0["b2"]) / max(ffn_ms / 1e3, 1e-12) / 1e9,
-                "ffn_share_of_step": ffn_ms / (L0["ms_per_step"] * K)}
+                "ffn_share_of_step": ffn_ms / (L0["ms_per_step"] * L0["K_prof"]),
+                "profiled_steps": L0["K_prof"], "prof_every": PROF_EVERY}
     else:
         ach = L0["fl"] / max(ffn_ms / 1e3, 1e-12) / 1e12
         pk = peaks["bf16_sus"] or peaks["bf16"]
         roof = {"bound": "tensor", "kernel": "k_prefill_gemm<W13> + <W2> on the rows rank 0 received",
                 "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk, "traffic": None,
                 "peak_src": peaks["src"] + " bf16 sustained",
-                "ffn_share_of_step": ffn_ms / (L0["ms_per_step"] * K)}
+                "ffn_share_of_step": ffn_ms / (L0["ms_per_step"] * L0["K_prof"]),
+                "profiled_steps": L0["K_prof"], "prof_every": PROF_EVERY}
     for l in layers:
         for b in getattr(l, "_opened", []):
             d.dymoe_ep_window_close(b)
@@ -1149,6 +1165,10 @@ def main():
                          "finegrained_decode: the 64-expert top-6 layer of configs[3]; stack / "
                          "stack_prefill: the 32-layer stack of configs[4] on one GPU")
     ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--prof-every", type=int, default=17,
+                    help="per-kernel CUDA events on every n-th timed step only: the kernel "
+                         "roofline comes from those steps; each event is a node in the step's "
+                         "CUDA graph and, on every step, cost the decode step ~14 us of its 214")
     ap.add_argument("--tokens", type=int, default=2048)
     ap.add_argument("--copies", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -1165,6 +1185,8 @@ def main():
                          "through host memory); never used for reported numbers")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    global PROF_EVERY
+    PROF_EVERY = max(1, args.prof_every)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
