@@ -42,6 +42,38 @@ namespace dec {
 // partial-tile reduction buffer per warp and matrix: [tok 8][row 16] floats
 constexpr int kRedTile = 8 * 16;
 
+// Optional per-CTA timeline (tools/dec_trace.py builds a separate library with -DDYMOE_DEC_TRACE;
+// the product build has no trace code): (event, globaltimer ns) pairs per CTA for the W13 (0) and
+// W2 (1) kernels -- 0 start, 1 allocation done, 2 x slice staged, 3 unit's tiles done, 4 end.
+#ifdef DYMOE_DEC_TRACE
+constexpr int kTrEv = 32;
+__device__ unsigned long long g_dec_tr[2][256][2 * kTrEv];
+__device__ int g_dec_trn[2][256];
+__device__ __forceinline__ void dec_tr(bool w13, int& n, int ev) {
+  if (threadIdx.x == 0 && n < kTrEv && blockIdx.x < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dec_tr[w13 ? 0 : 1][blockIdx.x][2 * n] = ev;
+    g_dec_tr[w13 ? 0 : 1][blockIdx.x][2 * n + 1] = t;
+    ++n;
+    g_dec_trn[w13 ? 0 : 1][blockIdx.x] = n;
+  }
+}
+#define DEC_TR(ev) dec_tr(W13, tr_n, ev)
+__device__ unsigned long long g_dec_sub[2][256][4];
+__device__ __forceinline__ void dec_sub(bool w13, int i) {
+  if (threadIdx.x == 0 && blockIdx.x < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dec_sub[w13 ? 0 : 1][blockIdx.x][i] = t;
+  }
+}
+#define DEC_SUB(i) dec_sub(W13, i)
+#else
+#define DEC_SUB(i) do {} while (0)
+#define DEC_TR(ev) do {} while (0)
+#endif
+
 // Shared-memory budget per kernel (one 512-thread CTA per SM, <= 227 KB):
 //   codes ring [warp 16][stage S][m][16 rows][128 B]   (1024-aligned: 128-byte swizzle atoms)
 //   meta ring  [warp 16][stage S][m][gq <= 4][16 rows] words
@@ -109,19 +141,28 @@ __device__ __forceinline__ uint32_t elect_one() {
   asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n}" : "=r"(e));
   return e;
 }
+// The weight stream is read once per step: it is loaded with an L2 evict_first policy so that
+// the step's small, re-read data (the kernels' code, the expert table, the routing arrays, x, the
+// partials) are not flushed out of L2 by ~1 GB of streamed codes every step -- at kernel start
+// every miss on them is a DRAM round trip on the ramp's critical path (tools/dec_trace.py).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void tma2d_e(uint32_t e, uint32_t dst, const CUtensorMap* m, int x, int y,
-                                        uint32_t bar) {
+                                        uint32_t bar, uint64_t pol) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %5, 0;\n\t"
-      "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n}"
-      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar), "r"(e) : "memory");
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %6;\n}"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(bar), "r"(e), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void tma3d_e(uint32_t e, uint32_t dst, const CUtensorMap* m, int x, int y,
-                                        int z, uint32_t bar) {
+                                        int z, uint32_t bar, uint64_t pol) {
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %6, 0;\n\t"
-      "@p cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n}"
-      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(z), "r"(bar), "r"(e) : "memory");
+      "@p cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %7;\n}"
+      ::"r"(dst), "l"(m), "r"(x), "r"(y), "r"(z), "r"(bar), "r"(e), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx_e(uint32_t e, uint32_t a, uint32_t tx) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t"
@@ -166,11 +207,13 @@ __device__ __forceinline__ DQ dq_from_meta(uint32_t w) {
 // block (W13: W1 and W3 rows of the tile's 16 features; W2: the two 16-row halves of a 32-row
 // tile), plus the metadata boxes of the GQ groups those chunks span.
 template <bool W13, int BITS, int WPT>
-__device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts, int e, int k0,
+__device__ __noinline__ uint32_t run_tiles(const CUtensorMap* tm0, const CUtensorMap* tm1,
+                                           const CUtensorMap* tmm, int k0,
                                            int kl, int t0, int t1, int nt, void* out, int ostride,
                                            uint32_t xs, int row_gran, float* red,
                                            uint32_t codes_base, uint32_t meta_base,
-                                           uint32_t bar_base, int* sync, uint32_t seq) {
+                                           uint32_t bar_base, int* sync, uint32_t seq,
+                                           bool prime_only) {
   using Tr = WT<BITS>;
   using C = Cfg<W13>;
   constexpr int NM = C::NM;
@@ -203,21 +246,11 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
   sync += grp * 4;   // [arrivals buf0, arrivals buf1, generation buf0, generation buf1]
 
   // the producer (warp-collective issue, one elected lane): this expert's descriptors at this width
-  const CUtensorMap* tmc[NM];
-  const CUtensorMap* tmm = nullptr;
-  {   // every lane: the issue is warp-collective
-    const DevExpert& E = experts[e];
-#pragma unroll
-    for (int m = 0; m < NM; ++m) {
-      const int mi = W13 ? m : 2;   // W2: both operand blocks come from the W2 matrix
-      if constexpr (BITS == 16) {
-        tmc[m] = E.tm_w[mi];
-      } else {
-        tmc[m] = E.q[width_index(BITS)][mi].tm_codes;
-      }
-    }
-    if constexpr (BITS != 16) tmm = E.q[width_index(BITS)][W13 ? 0 : 2].tm_meta;
-  }
+  if (prime_only) DEC_SUB(0);
+  // the producer (warp-collective issue, one elected lane): this expert's descriptors at this
+  // width, loaded by the caller (W2: both operand blocks come from the W2 matrix)
+  const CUtensorMap* tmc[NM] = {tm0, tm1};
+  const uint64_t pol = evict_first_policy();
   const int kx0 = k0 * BITS / 8 + warp * (BOXES * 128);   // codes x coordinate (bytes), j = 0
   const int gy0 = k0 / DYMOE_GROUP + warp * GQ;      // meta group coordinate at j = 0
   // item (tile ti, j = jj) into ring position sq
@@ -237,14 +270,14 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
 #pragma unroll
       for (int bx = 0; bx < BOXES; ++bx)
         tma2d_e(el, cs + (m * BOXES + bx) * 2048, tmc[m], kx0 + jj * (WPT * BOXES * 128) + bx * 128,
-                ti * C::TILE_ROWS + (W13 ? 0 : m * 16), bar);
+                ti * C::TILE_ROWS + (W13 ? 0 : m * 16), bar, pol);
     if constexpr (BITS != 16) {
       const uint32_t ms = mring + slot * C::META;
       if constexpr (W13) {
-        tma3d_e(el, ms, tmm, ti * 16, gy0 + jj * (WPT * GQ), 0, bar);
+        tma3d_e(el, ms, tmm, ti * 16, gy0 + jj * (WPT * GQ), 0, bar, pol);
       } else {
-        tma2d_e(el, ms, tmm, ti * 32, gy0 + jj * (WPT * GQ), bar);
-        tma2d_e(el, ms + 256, tmm, ti * 32 + 16, gy0 + jj * (WPT * GQ), bar);   // 128-B aligned
+        tma2d_e(el, ms, tmm, ti * 32, gy0 + jj * (WPT * GQ), bar, pol);
+        tma2d_e(el, ms + 256, tmm, ti * 32 + 16, gy0 + jj * (WPT * GQ), bar, pol);   // 128-B aligned
       }
     }
   };
@@ -255,12 +288,19 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[m][i] = 0.f;
 
-  // producer cursor: the next item to issue is j_iss of tile tile_iss
+  // producer cursor: the next item to issue is j_iss of tile tile_iss.  The first S - 1 items are
+  // issued by a separate prime call (prime_only) made before the caller stages x / passes its
+  // barrier, so the first weights are in flight while the CTA stages its x slice; the run call
+  // only advances the cursor past them.
   int tile_iss = t0 + grp, j_iss = 0;
 #pragma unroll
   for (int p = 0; p < S - 1; ++p) {
-    if (p < n_items) issue(seq + p, tile_iss, j_iss);
+    if (prime_only && p < n_items) issue(seq + p, tile_iss, j_iss);
     if (++j_iss == cmax) { j_iss = 0; tile_iss += NSG; }
+  }
+  if (prime_only) {
+    DEC_SUB(1);
+    return seq;
   }
 
   // per-lane shared-memory offsets: x (token row g, quad position c, x_pos layout); codes of
@@ -406,6 +446,10 @@ __device__ __noinline__ uint32_t run_tiles(const DevExpert* __restrict__ experts
 // would get fewer than `min_items` items per tile -- short K slices (the fine-grained layer's
 // K = 2048 / 1408) then keep whole items per warp instead of a cross-warp reduction per item.
 constexpr int kDecodeMinItems = 6;   // DYMOE_DECODE_MIN_ITEMS overrides (measurement knob)
+__device__ __forceinline__ int items_per_tile(int bits, int kl) {
+  const int ck = 4 * (128 / bits);                         // WT<BITS>::CHUNK_K
+  return ((kl + ck - 1) / ck + 1) / 2;                     // 2 chunks per item
+}
 __device__ __forceinline__ int wpt_for(int bits, int kl, int min_items) {
   const int ck = 4 * (128 / bits);                         // WT<BITS>::CHUNK_K
   const int npr = ((kl + ck - 1) / ck + 1) / 2;            // items per tile (2 chunks each)
@@ -433,7 +477,7 @@ struct Smem {
   static constexpr size_t META = (size_t)2 * kWarps * Cfg<W13>::S * Cfg<W13>::META;
   static constexpr size_t RED = Cfg<W13>::RED;
   static constexpr size_t BARS = (size_t)2 * kWarps * Cfg<W13>::S * 8;
-  static constexpr int SYNC_INTS = 32;   // 4 words per tile subgroup, up to 8 subgroups
+  static constexpr int SYNC_INTS = 64;   // 4 words per tile subgroup, up to 8 subgroups; x2 parts
   static __host__ __device__ size_t x_off() { return CODES + META + RED; }
   static __host__ __device__ size_t tail_off(int sliceK) {
     return x_off() + (size_t)kMaxTok * x_row_gran(sliceK) * 16;
@@ -448,9 +492,12 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
   extern __shared__ __align__(1024) uint8_t smem[];
   using C = Cfg<W13>;
   using L = Smem<W13>;
-  constexpr int NM = C::NM;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   if (sbase & 1023) __trap();   // the swizzled TMA boxes need 1024-byte alignment
+#ifdef DYMOE_DEC_TRACE
+  int tr_n = 0;
+#endif
+  DEC_TR(0);
   const size_t tail = L::tail_off(sliceK);
   uint64_t* ring_bar = reinterpret_cast<uint64_t*>(smem + tail);
   int* tile_sync = reinterpret_cast<int*>(smem + tail + L::BARS);   // [group][4]
@@ -464,14 +511,15 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
   const int N = W13 ? a.F : a.Hd;
   const int NT = N / C::TILE_ROWS;
   const int row_gran = x_row_gran(sliceK);
-  // the codes ring is free until the first TMA: use it as the allocation scratch
-  if (threadIdx.x < 32) compute_alloc(a, gridDim.x / SK, W13, A, *reinterpret_cast<AllocScratch*>(smem));
   if ((threadIdx.x & 31) == 0) {   // each warp's ring mbarriers (one arrival + tx per phase)
     for (int i = 0; i < C::S; ++i) mbar_init(bar_base + ((threadIdx.x >> 5) * C::S + i) * 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
   }
+  // the codes ring is free until the first TMA: use it as the allocation scratch
+  if (threadIdx.x < 32) compute_alloc(a, gridDim.x / SK, W13, A, *reinterpret_cast<AllocScratch*>(smem));
   uint32_t seq = 0;   // this warp's ring position
   __syncthreads();
+  DEC_TR(1);
   if (A.n_act == 0) return;
   const int V = A.units_total * SK;
   for (int v = blockIdx.x; v < V; v += gridDim.x) {
@@ -484,18 +532,27 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
     const int t0 = (int)((long long)part * NT / u_e), t1 = (int)((long long)(part + 1) * NT / u_e);
     const int k0 = ks * sliceK;
     const int kl = min(sliceK, K - k0);
-    const int be = a.bits[e];
-    const int r_lo = a.expert_off[e], r_hi = a.expert_off[e + 1];
-    // residency check (device-side fault -> status word; outputs zeroed)
-    bool resident = true;
+    // one round of independent loads: the expert's row range and this width's descriptors (the
+    // width itself and the list came from the allocation's shared-memory table) -- every
+    // dependent global round trip here is ~1 us of ramp for the whole CTA (tools/dec_trace.py)
+    const int be = A.bits[i];
+    const int r_lo = __ldg(a.expert_off + e), r_hi = __ldg(a.expert_off + e + 1);
     const DevExpert& E = a.experts[e];
-#pragma unroll
-    for (int m = 0; m < NM; ++m) {
-      const int mi = W13 ? m : 2;
-      if (be == 16) resident &= E.w[mi] != nullptr;
-      else resident &= width_index(be) >= 0 && E.q[width_index(be)][mi].codes != nullptr;
+    const CUtensorMap *tm0, *tm1, *tmm = nullptr;
+    bool resident;   // residency check (device-side fault -> status word; outputs zeroed)
+    if (be == 16) {
+      tm0 = E.tm_w[W13 ? 0 : 2];
+      tm1 = E.tm_w[W13 ? 1 : 2];
+      resident = E.w[W13 ? 0 : 2] != nullptr && E.w[W13 ? 1 : 2] != nullptr;
+    } else {
+      const int wi = width_index(be);
+      const DevQMat* Q = E.q[wi < 0 ? 0 : wi];
+      tm0 = Q[W13 ? 0 : 2].tm_codes;
+      tm1 = Q[W13 ? 1 : 2].tm_codes;
+      tmm = Q[W13 ? 0 : 2].tm_meta;
+      resident = wi >= 0 && Q[W13 ? 0 : 2].codes != nullptr && Q[W13 ? 1 : 2].codes != nullptr &&
+                 tmm != nullptr;
     }
-    if (resident && be != 16) resident &= E.q[width_index(be)][W13 ? 0 : 2].tm_meta != nullptr;
     if (!resident) {
       if (threadIdx.x == 0 && a.status) atomicOr(a.status, (unsigned)DYMOE_STATUS_WIDTH_NOT_RESIDENT);
       for (int r = r_lo; r < r_hi; ++r)
@@ -515,55 +572,109 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
     }
     const int gran = kl / 8;                        // granules of real x
     const int npos = (kl + 255) / 256 * 32;         // staged positions (zero beyond gran)
+    // The unit's tiles run in (at most) two parts: the rem = ntl mod NSG tiles that would leave
+    // some tile subgroups a round short run FIRST on wider subgroups (up to all 16 warps on one
+    // tile, each warp a share of its K items), then the full rounds on the width's own subgroups.
+    // With whole tiles dealt round-robin a CTA whose unit has one tile more than a multiple of
+    // NSG took a whole extra tile time (~10 us at Int4) while its other subgroups idled -- the
+    // per-CTA end-time spread measured by tools/dec_trace.py.
+    const int wpt = wpt_for(be, kl, a.min_items);
+    const int nsg = 2 * kWarps / wpt;
+    const int rem = (t1 - t0) % nsg;
+    int wpt_a = wpt;
+    if (rem) {
+      const int npr = items_per_tile(be, kl);
+      wpt_a = 2 * kWarps;
+      while (wpt_a > wpt && (wpt_a * rem > 2 * kWarps || wpt_a > npr)) wpt_a >>= 1;
+    }
+    const int ta1 = wpt_a != wpt ? t0 + rem : t1;   // part A [t0, ta1) on wpt_a, part B [ta1, t1)
     for (int tok0 = r_lo; tok0 < r_hi; tok0 += kMaxTok) {
       const int nt = min(kMaxTok, r_hi - tok0);
-      // stage the x slice of this pass's tokens (zero rows beyond nt), x_pos layout
-      __syncthreads();  // the previous pass is done with xs / red / tile_sync
-      if (threadIdx.x < L::SYNC_INTS) tile_sync[threadIdx.x] = 0;
-      for (int idx = threadIdx.x; idx < kMaxTok * npos; idx += blockDim.x) {
-        const int t = idx / npos, pos = idx - t * npos;
-        const int gl = x_logical(pos, xu4);
-        uint4 v4 = make_uint4(0, 0, 0, 0);
-        if (t < nt) {
-          const int r = tok0 + t;
-          const uint16_t* src = (W13 ? a.x + (size_t)a.perm_token[r] * a.Hd : a.h + (size_t)r * a.F) + k0;
-          const uint4 z4 = make_uint4(0, 0, 0, 0);
-          if (be == 2) {   // granule pair (gb, gb + 1), element-interleaved (x_perm)
-            const int gb = gl & ~1;
-            const uint4 ga = gb < gran ? *reinterpret_cast<const uint4*>(src + gb * 8) : z4;
-            const uint4 gc = gb + 1 < gran ? *reinterpret_cast<const uint4*>(src + gb * 8 + 8) : z4;
-            v4 = x_perm<2>(ga, gc, gl & 1);
-          } else if (gl < gran) {
-            v4 = *reinterpret_cast<const uint4*>(src + gl * 8);
-            if (be == 4) v4 = x_perm<4>(v4, v4, 0);
-          }
-        }
-        xs[t * row_gran + pos] = v4;
-      }
-      __syncthreads();
       void* out = W13 ? (void*)(a.h + (size_t)tok0 * a.F)
                       : (void*)(a.y_part + ((size_t)ks * a.part_rows + tok0) * a.Hd);
       const int ostride = W13 ? a.F : a.Hd;
       const uint32_t xsa = (uint32_t)__cvta_generic_to_shared(xs);
-      const int wpt = wpt_for(be, kl, a.min_items);
-#define DYMOE_RUN(B, W) seq = run_tiles<W13, B, W>(a.experts, e, k0, kl, t0, t1, nt, out, ostride, \
+#define DYMOE_RUN(B, W) seq = run_tiles<W13, B, W>(tm0, tm1, tmm, k0, kl, ra, rb, nt, out, ostride, \
                                                    xsa, row_gran, red, codes_base, meta_base,    \
-                                                   bar_base, tile_sync, seq)
-      switch (be * 16 + wpt) {
-        case 2 * 16 + 4: DYMOE_RUN(2, 4); break;
-        case 2 * 16 + 2: DYMOE_RUN(2, 2); break;
-        case 4 * 16 + 4: DYMOE_RUN(4, 4); break;
-        case 4 * 16 + 2: DYMOE_RUN(4, 2); break;
-        case 8 * 16 + 8: DYMOE_RUN(8, 8); break;
-        case 8 * 16 + 4: DYMOE_RUN(8, 4); break;
-        case 8 * 16 + 2: DYMOE_RUN(8, 2); break;
-        case 16 * 16 + 8: DYMOE_RUN(16, 8); break;
-        case 16 * 16 + 4: DYMOE_RUN(16, 4); break;
-        default: DYMOE_RUN(16, 2); break;
-      }
+                                                   bar_base, tsync, seq, prime)
+      auto tiles = [&](int w, int ra, int rb, int* tsync, bool prime) {
+        switch (be * 32 + w) {
+          case 2 * 32 + 16: DYMOE_RUN(2, 16); break;
+          case 2 * 32 + 8: DYMOE_RUN(2, 8); break;
+          case 2 * 32 + 4: DYMOE_RUN(2, 4); break;
+          case 2 * 32 + 2: DYMOE_RUN(2, 2); break;
+          case 4 * 32 + 16: DYMOE_RUN(4, 16); break;
+          case 4 * 32 + 8: DYMOE_RUN(4, 8); break;
+          case 4 * 32 + 4: DYMOE_RUN(4, 4); break;
+          case 4 * 32 + 2: DYMOE_RUN(4, 2); break;
+          case 8 * 32 + 16: DYMOE_RUN(8, 16); break;
+          case 8 * 32 + 8: DYMOE_RUN(8, 8); break;
+          case 8 * 32 + 4: DYMOE_RUN(8, 4); break;
+          case 8 * 32 + 2: DYMOE_RUN(8, 2); break;
+          case 16 * 32 + 16: DYMOE_RUN(16, 16); break;
+          case 16 * 32 + 8: DYMOE_RUN(16, 8); break;
+          case 16 * 32 + 4: DYMOE_RUN(16, 4); break;
+          default: DYMOE_RUN(16, 2); break;
+        }
+      };
 #undef DYMOE_RUN
+      __syncthreads();  // the previous pass is done with xs / red / tile_sync
+      if (threadIdx.x < L::SYNC_INTS) tile_sync[threadIdx.x] = 0;
+      // each warp's first weight item goes out now (its own ring slot, no shared state), so the
+      // HBM latency overlaps the x staging below
+      tiles(wpt_a, t0, ta1, tile_sync, true);
+      DEC_TR(5);
+      // stage the x slice of this pass's tokens (zero rows beyond nt), x_pos layout: the row
+      // offsets first, then every load of a position for all 8 tokens before any store (16
+      // independent loads in flight per thread at Int2 instead of a dependent chain per element)
+      {
+        const uint16_t* xbase = W13 ? a.x : a.h;
+        const size_t xstride = W13 ? a.Hd : a.F;
+        const uint16_t* xk = xbase + k0;
+        int row[kMaxTok];
+#pragma unroll
+        for (int t = 0; t < kMaxTok; ++t) row[t] = t < nt ? (W13 ? __ldg(a.perm_token + tok0 + t) : tok0 + t) : 0;
+        const uint4 z4 = make_uint4(0, 0, 0, 0);
+        for (int pos = threadIdx.x; pos < npos; pos += blockDim.x) {
+          const int gl = x_logical(pos, xu4);
+          uint4 v[kMaxTok];
+          if (be == 2) {   // granule pair (gb, gb + 1), element-interleaved (x_perm)
+            const int gb = gl & ~1;
+            uint4 ga[kMaxTok], gc[kMaxTok];
+#pragma unroll
+            for (int t = 0; t < kMaxTok; ++t) {
+              const uint4* src = reinterpret_cast<const uint4*>(xk + (size_t)row[t] * xstride + gb * 8);
+              ga[t] = t < nt && gb < gran ? __ldg(src) : z4;
+              gc[t] = t < nt && gb + 1 < gran ? __ldg(src + 1) : z4;
+            }
+#pragma unroll
+            for (int t = 0; t < kMaxTok; ++t) v[t] = x_perm<2>(ga[t], gc[t], gl & 1);
+          } else {
+#pragma unroll
+            for (int t = 0; t < kMaxTok; ++t)
+              v[t] = t < nt && gl < gran ? __ldg(reinterpret_cast<const uint4*>(xk + (size_t)row[t] * xstride + gl * 8)) : z4;
+            if (be == 4) {
+#pragma unroll
+              for (int t = 0; t < kMaxTok; ++t) v[t] = x_perm<4>(v[t], v[t], 0);
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < kMaxTok; ++t) xs[t * row_gran + pos] = v[t];
+        }
+      }
+      DEC_TR(6);
+      __syncthreads();
+      DEC_TR(2 | (be << 8) | (i << 16));
+      tiles(wpt_a, t0, ta1, tile_sync, false);
+      if (ta1 < t1) {
+        tiles(wpt, ta1, t1, tile_sync + 32, true);
+        __syncthreads();   // part A's reduction buffers are free
+        tiles(wpt, ta1, t1, tile_sync + 32, false);
+      }
+      DEC_TR(3);
     }
   }
+  DEC_TR(4);
 }
 
 size_t smem_bytes(bool w13, int sliceK) {
@@ -636,6 +747,18 @@ cudaError_t launch_ffn_decode(const FfnArgs& args, cudaStream_t s, void* const* 
   record_ev(ev, 2, s);
   return cudaSuccess;
 }
+
+#ifdef DYMOE_DEC_TRACE
+extern "C" int dymoe_dec_trace_read(unsigned long long* host, int* counts) {
+  static int zero[2][256];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(counts, dec::g_dec_trn, sizeof(zero));
+  cudaMemcpyFromSymbol(host, dec::g_dec_tr, sizeof(dec::g_dec_tr));
+  cudaMemcpyToSymbol(dec::g_dec_trn, zero, sizeof(zero));
+  cudaMemcpyFromSymbol(host + sizeof(dec::g_dec_tr) / 8, dec::g_dec_sub, sizeof(dec::g_dec_sub));
+  return (int)cudaGetLastError();
+}
+#endif
 
 cudaError_t preload_ffn_decode() {
   return preload_kernels(dec::k_decode_gemv<true>, dec::k_decode_gemv<false>);

@@ -176,13 +176,15 @@ struct Alloc {   // compact: it shares the 227 KB shared-memory budget with the 
   int n_act;
   int units_total;                               // <= max(grid, M) < 2^16
   uint8_t expert[DYMOE_MAX_EXPERTS];             // M <= 256
+  uint8_t bits[DYMOE_MAX_EXPERTS];               // the expert's width, by list position
   uint16_t first_unit[DYMOE_MAX_EXPERTS + 1];
 };
 // scratch of compute_alloc (lives in shared memory the pipeline has not started using yet)
 struct AllocScratch {
   long long cost[DYMOE_MAX_EXPERTS];
-  long long rem[DYMOE_MAX_EXPERTS];
-  int u[DYMOE_MAX_EXPERTS];
+  int list[DYMOE_MAX_EXPERTS];
+  int rows[DYMOE_MAX_EXPERTS];
+  int bits[DYMOE_MAX_EXPERTS];
 };
 
 // Relative time to stream one expert matrix set at width b (per 8-token chunk), measured on B200
@@ -196,23 +198,37 @@ __device__ __forceinline__ int wcost(int b, bool w13) {
 // Cost-proportional allocation of `units_total` units to the active experts, every active
 // expert >= 1 unit: with C_i the exclusive prefix of the costs in list order and R = U - n,
 // first_unit[i] = i + floor(R * C_i / total) (so expert i gets 1 + floor(R C_{i+1} / total) -
-// floor(R C_i / total) units and the total is exactly U).  Warp 0, all 32 lanes: the list, row
-// counts and widths are loaded in parallel (one dependent round trip instead of a serial walk
-// over the experts -- the serial version held the whole CTA at its first barrier for tens of
-// microseconds with 20-60 active experts) and the prefix is a warp scan over contiguous blocks.
-// Every CTA computes the identical allocation; it only partitions tiles, never the arithmetic.
+// floor(R C_i / total) units and the total is exactly U).  Warp 0, all 32 lanes.  The active
+// list, every expert's row count and every width are loaded in ONE round of independent loads
+// (lanes stride over the M experts; the list length is loaded alongside) into shared scratch,
+// then each lane takes a contiguous block of the list and the prefix is a warp scan over the
+// blocks -- the kernel's whole ramp is this allocation plus the x staging, so dependent global
+// round trips here cost every CTA directly (tools/dec_trace.py: 2.0 us with three dependent
+// rounds).  Every CTA computes the identical allocation; it only partitions tiles, never the
+// arithmetic.
 __device__ void compute_alloc(const FfnArgs& a, int units_grid, bool w13, Alloc& A,
                               AllocScratch& X) {
   const int lane = threadIdx.x & 31;
-  const int n = a.active_list[0];
+  const int M = a.M;
+  const int n = __ldg(a.active_list);
+#pragma unroll 8
+  for (int i = lane; i < M; i += 32) {
+    const int l = __ldg(a.active_list + 1 + i);
+    const int o0 = __ldg(a.expert_off + i), o1 = __ldg(a.expert_off + i + 1);
+    const int b = __ldg(a.bits + i);
+    X.list[i] = l;
+    X.rows[i] = o1 - o0;
+    X.bits[i] = b;
+  }
+  __syncwarp();
   const int per = (n + 31) / 32;
   const int i0 = lane * per, i1 = min(n, i0 + per);
   long long local = 0;
   for (int i = i0; i < i1; ++i) {
-    const int e = a.active_list[1 + i];
-    const int rows = a.expert_off[e + 1] - a.expert_off[e];
-    const long long c = (long long)wcost(a.bits[e], w13) * ((rows + kMaxTok - 1) / kMaxTok);
+    const int e = X.list[i];
+    const long long c = (long long)wcost(X.bits[e], w13) * ((X.rows[e] + kMaxTok - 1) / kMaxTok);
     A.expert[i] = (uint8_t)e;
+    A.bits[i] = (uint8_t)X.bits[e];
     X.cost[i] = c;
     local += c;
   }
