@@ -191,8 +191,8 @@ struct AllocScratch {
 // with every expert forced to one width (tools/decode_width_sweep.py): the narrow widths are
 // bound by dequant issue slots rather than bytes, so they cost more than their bytes suggest.
 __device__ __forceinline__ int wcost(int b, bool w13) {
-  if (w13) return b == 16 ? 256 : b == 8 ? 167 : b == 4 ? 116 : 103;
-  return b == 16 ? 256 : b == 8 ? 180 : b == 4 ? 133 : 129;
+  if (w13) return b == 16 ? 259 : b == 8 ? 168 : b == 4 ? 115 : 103;
+  return b == 16 ? 256 : b == 8 ? 181 : b == 4 ? 130 : 129;
 }
 
 // Cost-proportional allocation of `units_total` units to the active experts, every active

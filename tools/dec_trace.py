@@ -49,6 +49,7 @@ def summarise(buf, cnt, g, ncta):
     sub0, sub1, sub2 = [], [], []
     units = []
     by_width = {}
+    unit_first, run_all = [], []
     for p in per:
         ev = {}
         for e, t in p:
@@ -62,6 +63,8 @@ def summarise(buf, cnt, g, ncta):
             run.append(sum(b - a for a, b in zip(ev[2], ev[3])) / 1e3)
             if len(ev[2]) == 1:
                 by_width.setdefault(units[-1][0], []).append(run[-1])
+            unit_first.append(units[-len(ev[2])] if units else None)
+            run_all.append(run[-1])
         ends.append((p[-1][1] - t0) / 1e3)
         sb = (2 * 256 * 2 * NEV) + (g * 256 + per.index(p)) * 4
         if 5 in ev:
@@ -79,7 +82,8 @@ def summarise(buf, cnt, g, ncta):
         v = sorted(v)
         return {"min": round(v[0], 2), "med": round(v[len(v) // 2], 2), "max": round(v[-1], 2),
                 "mean": round(sum(v) / len(v), 2)} if v else None
-    return {"ctas": len(per), "span_us": round(span, 2), "start_us": st(starts), "alloc_us": st(alloc),
+    raw = [[c, u[0] if u else -1, round(r, 2)] for c, (u, r) in enumerate(zip(unit_first, run_all))]
+    return {"raw": raw, "ctas": len(per), "span_us": round(span, 2), "start_us": st(starts), "alloc_us": st(alloc),
             "ramp_to_first_x_us": st(ramp), "staging_us_total": st(stage), "run_tiles_us": st(run),
             "end_us": st(ends), "run_by_width": {str(b): st(v) for b, v in sorted(by_width.items())}, "prime_us": st(prime), "stage_loop_us": st(stg), "stage_barrier_us": st(bar), "prime_call_us": st(sub0), "prime_body_us": st(sub1), "prime_ret_us": st(sub2), "busy_frac": round(sum(run) / (len(per) * span), 3)}
 
