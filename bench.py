@@ -753,7 +753,7 @@ def _broadcast(t):
 
 def load_traffic(kernel_key):
     """dram read+write bytes of the dominant kernel from the committed ncu --set full capture
-    (profiles/traffic.json, written from profiles/r01_ncu_*.md), with the algorithmic work of
+    (profiles/traffic.json, written from the committed ncu summaries, profiles/r02_final_ncu_*.md), with the algorithmic work of
     the same captured launch so the two can be compared."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
