@@ -49,6 +49,7 @@ constexpr int kRedTile = 8 * 16;
 constexpr int kTrEv = 32;
 __device__ unsigned long long g_dec_tr[2][256][2 * kTrEv];
 __device__ int g_dec_trn[2][256];
+__device__ unsigned long long g_dec_sub[2][256][8];
 __device__ __forceinline__ void dec_tr(bool w13, int& n, int ev) {
   if (threadIdx.x == 0 && n < kTrEv && blockIdx.x < 256) {
     unsigned long long t;
@@ -57,12 +58,13 @@ __device__ __forceinline__ void dec_tr(bool w13, int& n, int ev) {
     g_dec_tr[w13 ? 0 : 1][blockIdx.x][2 * n + 1] = t;
     ++n;
     g_dec_trn[w13 ? 0 : 1][blockIdx.x] = n;
+    if (ev == 0)
+      for (int i = 0; i < 8; ++i) g_dec_sub[w13 ? 0 : 1][blockIdx.x][i] = 0;
   }
 }
 #define DEC_TR(ev) dec_tr(W13, tr_n, ev)
-__device__ unsigned long long g_dec_sub[2][256][4];
-__device__ __forceinline__ void dec_sub(bool w13, int i) {
-  if (threadIdx.x == 0 && blockIdx.x < 256) {
+__device__ __forceinline__ void dec_sub(bool w13, int i) {   // first stamp per launch wins
+  if (threadIdx.x == 0 && blockIdx.x < 256 && g_dec_sub[w13 ? 0 : 1][blockIdx.x][i] == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_dec_sub[w13 ? 0 : 1][blockIdx.x][i] = t;
@@ -553,6 +555,12 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
       resident = wi >= 0 && Q[W13 ? 0 : 2].codes != nullptr && Q[W13 ? 1 : 2].codes != nullptr &&
                  tmm != nullptr;
     }
+    // the TMA unit fetches a descriptor on its first use; fetch them now, while the rest of the
+    // unit's setup runs, instead of on the first weight issue
+    if (resident && threadIdx.x < 3) {
+      const CUtensorMap* pm = threadIdx.x == 0 ? tm0 : threadIdx.x == 1 ? tm1 : tmm;
+      if (pm != nullptr) asm volatile("prefetch.tensormap [%0];" ::"l"(pm) : "memory");
+    }
     if (!resident) {
       if (threadIdx.x == 0 && a.status) atomicOr(a.status, (unsigned)DYMOE_STATUS_WIDTH_NOT_RESIDENT);
       for (int r = r_lo; r < r_hi; ++r)
@@ -563,6 +571,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
       continue;
     }
     if (t1 <= t0 || kl <= 0) continue;
+    DEC_SUB(2);
     int xu4;
     switch (be) {
       case 2: xu4 = WT<2>::XU4; break;
@@ -619,6 +628,7 @@ __global__ void __launch_bounds__(2 * kThreads, 1) k_decode_gemv(const FfnArgs a
       };
 #undef DYMOE_RUN
       __syncthreads();  // the previous pass is done with xs / red / tile_sync
+      DEC_SUB(3);
       if (threadIdx.x < L::SYNC_INTS) tile_sync[threadIdx.x] = 0;
       // each warp's first weight item goes out now (its own ring slot, no shared state), so the
       // HBM latency overlaps the x staging below

@@ -1,7 +1,7 @@
 """Per-CTA timeline of the decode GEMV kernels (measurement tool, not product code).
 
   python tools/dec_trace.py --build             # here: libdymoe with -DDYMOE_DEC_TRACE -> tools/trace/
-  python tools/dec_trace.py [mixed|16|8|4|2] [B]  # on the GPU: one layer step, timeline summary
+  python tools/dec_trace.py [mixed|16|8|4|2] [B] [config]  # on the GPU: one layer step, timeline summary
 
 Events per CTA (csrc/kernels/ffn_decode.cu DEC_TR, globaltimer ns): 0 start, 1 allocation done,
 2 x slice staged (per virtual CTA), 3 its tiles done, 4 end; 5 first items issued (before
@@ -66,11 +66,11 @@ def summarise(buf, cnt, g, ncta):
             unit_first.append(units[-len(ev[2])] if units else None)
             run_all.append(run[-1])
         ends.append((p[-1][1] - t0) / 1e3)
-        sb = (2 * 256 * 2 * NEV) + (g * 256 + per.index(p)) * 4
-        if 5 in ev:
-            sub0.append((buf[sb] - ev[1][0]) / 1e3)
-            sub1.append((buf[sb + 1] - buf[sb]) / 1e3)
-            sub2.append((ev[5][0] - buf[sb + 1]) / 1e3)
+        sb = (2 * 256 * 2 * NEV) + (g * 256 + per.index(p)) * 8
+        if 5 in ev and buf[sb + 2] and buf[sb + 3]:
+            sub0.append((buf[sb + 2] - ev[1][0]) / 1e3)     # allocation done -> unit decoded
+            sub1.append((buf[sb + 3] - buf[sb + 2]) / 1e3)  # -> past the pass-start barrier
+            sub2.append((buf[sb + 1] - buf[sb + 3]) / 1e3)  # -> first items issued (prime return)
         if 5 in ev and 6 in ev:
             prime.append((ev[5][0] - ev[1][0]) / 1e3)
             stg.append((ev[6][0] - ev[5][0]) / 1e3)
@@ -85,7 +85,7 @@ def summarise(buf, cnt, g, ncta):
     raw = [[c, u[0] if u else -1, round(r, 2)] for c, (u, r) in enumerate(zip(unit_first, run_all))]
     return {"raw": raw, "ctas": len(per), "span_us": round(span, 2), "start_us": st(starts), "alloc_us": st(alloc),
             "ramp_to_first_x_us": st(ramp), "staging_us_total": st(stage), "run_tiles_us": st(run),
-            "end_us": st(ends), "run_by_width": {str(b): st(v) for b, v in sorted(by_width.items())}, "prime_us": st(prime), "stage_loop_us": st(stg), "stage_barrier_us": st(bar), "prime_call_us": st(sub0), "prime_body_us": st(sub1), "prime_ret_us": st(sub2), "busy_frac": round(sum(run) / (len(per) * span), 3)}
+            "end_us": st(ends), "run_by_width": {str(b): st(v) for b, v in sorted(by_width.items())}, "prime_us": st(prime), "stage_loop_us": st(stg), "stage_barrier_us": st(bar), "unit_decode_us": st(sub0), "to_barrier_us": st(sub1), "to_first_issue_us": st(sub2), "busy_frac": round(sum(run) / (len(per) * span), 3)}
 
 
 def main():
@@ -99,15 +99,16 @@ def main():
     import synthetic
     mode = sys.argv[1] if len(sys.argv) > 1 else "mixed"
     B = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+    cname = sys.argv[3] if len(sys.argv) > 3 else "mixtral_decode"
     dev = torch.device("cuda", 0)
-    cfg = synthetic.CONFIGS["mixtral_decode"].with_tokens(B)
+    cfg = synthetic.CONFIGS[cname].with_tokens(B)
     (layer, _), = bench.build_layer_copies(d, cfg, 1, dev)
     inputs = bench.step_inputs(cfg, 4, dev)
     ws = layer.workspace(B, dev)
     lad = d.make_ladder(bench.LADDER_BITS, bench.LADDER_LAMBDAS)
     forced = None if mode == "mixed" else torch.full((cfg.M,), int(mode), dtype=torch.uint8, device=dev)
     L = d.lib()
-    buf = (ctypes.c_ulonglong * (2 * 256 * 2 * NEV + 2 * 256 * 4))()
+    buf = (ctypes.c_ulonglong * (2 * 256 * 2 * NEV + 2 * 256 * 8))()
     cnt = (ctypes.c_int * (2 * 256))()
     x, lg, a = inputs[0]
     for _ in range(3):
@@ -118,7 +119,7 @@ def main():
     torch.cuda.synchronize()
     L.dymoe_dec_trace_read(buf, cnt)
     ncta = torch.cuda.get_device_properties(0).multi_processor_count
-    out = {"mode": mode, "B": B, "w13": summarise(buf, cnt, 0, ncta), "w2": summarise(buf, cnt, 1, ncta)}
+    out = {"mode": mode, "B": B, "config": cname, "w13": summarise(buf, cnt, 0, ncta), "w2": summarise(buf, cnt, 1, ncta)}
     print(json.dumps(out))
 
 
