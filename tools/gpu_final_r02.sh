@@ -5,6 +5,7 @@ set -u
 O=gpurun_out/final
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" 2>&1 | tail -2
+python tools/attn_trace.py --build > /dev/null 2>&1; python tools/pf_trace.py --build > /dev/null 2>&1; python tools/dec_trace.py --build > /dev/null 2>&1
 timeout 1800 python -m pytest tests -m gpu -q -x --durations=15 > $O/pytest_gpu.txt 2>&1; tail -3 $O/pytest_gpu.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -2 $O/smoke.txt
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
