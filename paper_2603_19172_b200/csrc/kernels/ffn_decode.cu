@@ -44,7 +44,10 @@ constexpr int kRedTile = 8 * 16;
 
 // Optional per-CTA timeline (tools/dec_trace.py builds a separate library with -DDYMOE_DEC_TRACE;
 // the product build has no trace code): (event, globaltimer ns) pairs per CTA for the W13 (0) and
-// W2 (1) kernels -- 0 start, 1 allocation done, 2 x slice staged, 3 unit's tiles done, 4 end.
+// W2 (1) kernels -- 0 start, 1 allocation done, 5 first weight items issued, 6 staging loop done,
+// 2 x slice staged (payload: the unit's width and list position), 3 unit's tiles done, 4 end --
+// and first-per-launch stamps inside the first unit (0 prime entry, 1 prime return, 2 unit
+// decoded, 3 past the pass-start barrier).
 #ifdef DYMOE_DEC_TRACE
 constexpr int kTrEv = 32;
 __device__ unsigned long long g_dec_tr[2][256][2 * kTrEv];
@@ -247,7 +250,6 @@ __device__ __noinline__ uint32_t run_tiles(const CUtensorMap* tm0, const CUtenso
   red += grp * (C::NB * WPT * NM * kRedTile);
   sync += grp * 4;   // [arrivals buf0, arrivals buf1, generation buf0, generation buf1]
 
-  // the producer (warp-collective issue, one elected lane): this expert's descriptors at this width
   if (prime_only) DEC_SUB(0);
   // the producer (warp-collective issue, one elected lane): this expert's descriptors at this
   // width, loaded by the caller (W2: both operand blocks come from the W2 matrix)
