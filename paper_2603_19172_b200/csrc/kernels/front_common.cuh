@@ -32,32 +32,41 @@ __device__ __forceinline__ void route_token(const float* row, int M, int k, int 
     const int j = lane + 32 * i;
     v[i] = j < M ? row[j] : -FLT_MAX;
   }
+  // k rounds of a warp arg-max on an order-preserving unsigned key of the logit (monotonic in
+  // the float order, -0.0 and +0.0 mapped to one key, 0 = not a candidate): each lane scans its
+  // 8 candidates in index order (strict > keeps the lower index on ties), then two warp
+  // reductions (REDUX: max of the keys, min of the indices holding it) -- the same (value desc,
+  // index asc) order as `better` with two reduction instructions per round instead of five
+  // dependent shuffle-compare steps.
+  unsigned key[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = lane + 32 * i;
+    const unsigned u = v[i] == 0.f ? 0u : __float_as_uint(v[i]);
+    key[i] = j < M ? ((u & 0x80000000u) ? ~u : (u | 0x80000000u)) : 0u;
+  }
   float sel_v[8];
   int sel_i[8];
   for (int r = 0; r < k; ++r) {
+    unsigned bk = 0u;
+    int bj = 0x7fffffff;
     float bv = 0.f;
-    int bi = 0x7fffffff;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const int j = lane + 32 * i;
-      if (j < M && !(taken >> i & 1u) && (bi == 0x7fffffff || better(v[i], j, bv, bi))) {
+      const unsigned kk = (taken >> i & 1u) ? 0u : key[i];
+      if (kk > bk) {
+        bk = kk;
+        bj = lane + 32 * i;
         bv = v[i];
-        bi = j;
       }
     }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (oi != 0x7fffffff && (bi == 0x7fffffff || better(ov, oi, bv, bi))) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    sel_v[r] = bv;
+    const unsigned kmax = __reduce_max_sync(0xffffffffu, bk);
+    const int bi = (int)__reduce_min_sync(0xffffffffu, bk == kmax ? (unsigned)bj : 0x7fffffffu);
+    sel_v[r] = __shfl_sync(0xffffffffu, bv, bi & 31);
     sel_i[r] = bi;
     if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
   }
+
   const float vmax = sel_v[0];
   float e[8];
   float z = 0.f;
@@ -159,24 +168,23 @@ __device__ __forceinline__ void assign_bits(const float* importance, const uint8
     I[j] = importance[j];
     act[j] = p.m_active ? (active_mask != nullptr ? (active_mask[j] != 0) : 0) : 1;
   }
-  if (j == 0) *n_act = 0;
   __syncthreads();
   if (p.m_active && active_mask == nullptr) {
     for (int q = j; q < T * p.k_route; q += blockDim.x) act[topk_idx[q]] = 1;  // benign race
     __syncthreads();
   }
-  if (j < p.M && act[j]) atomicAdd(n_act, 1);
-  __syncthreads();
+  const int M_eff = __syncthreads_count(j < p.M && act[j]);   // the active count (a barrier)
+  if (j == 0) *n_act = M_eff;
   if (j < p.M) {
     if (active_out != nullptr) active_out[j] = (uint8_t)act[j];
-    const int M_eff = *n_act;
     if (!act[j]) {
       bits[j] = (uint8_t)p.bits[p.n_tiers - 1];
     } else {
       const float Ij = I[j];
-      int rank = 0;
+      int rank = 0;   // independent terms (no loop-carried branch): unrolled broadcast reads
+#pragma unroll 8
       for (int i = 0; i < p.M; ++i)
-        if (act[i] && (I[i] > Ij || (I[i] == Ij && i < j))) ++rank;
+        rank += (act[i] != 0) & ((I[i] > Ij) | ((I[i] == Ij) & (i < j)));
       int tier = p.n_tiers - 1;
       int prev = 0;
       for (int q = 0; q < p.n_tiers - 1; ++q) {

@@ -240,6 +240,26 @@ cudaError_t launch_assign(const float* importance, const uint8_t* active_mask,
 // ===========================================================================================
 constexpr int kFrontThreads = 256;
 
+// Optional phase timeline of the decode front (a build with -DDYMOE_FRONT_TRACE, tools/front_trace.py;
+// the product build has no trace code): globaltimer stamps of thread 0 after each phase.
+#ifdef DYMOE_FRONT_TRACE
+__device__ unsigned long long g_front_tr[16];
+#define FRONT_TR(i)                                                         \
+  do {                                                                      \
+    if (threadIdx.x == 0) {                                                 \
+      unsigned long long t_;                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                \
+      g_front_tr[i] = t_;                                                   \
+    }                                                                       \
+  } while (0)
+extern "C" int dymoe_front_trace_read(unsigned long long* host) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(host, g_front_tr, sizeof(g_front_tr));
+}
+#else
+#define FRONT_TR(i) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(kFrontThreads)
 k_front_decode(const float* logits, int T, int M, int k, AssignParams p,
                const uint8_t* forced_bits, int32_t* topk_idx, float* topk_w, float* probs,
@@ -258,6 +278,7 @@ k_front_decode(const float* logits, int T, int M, int k, AssignParams p,
   __shared__ float s_imp[DYMOE_MAX_EXPERTS];
   __shared__ uint8_t s_bits[DYMOE_MAX_EXPERTS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  FRONT_TR(0);
   // T <= NW (one token per warp): route's full-softmax rows go to shared memory, where the score
   // phase sums them -- they are exactly the rows decode_importance would recompute
   // (front::softmax_row), so the importance is unchanged; copied to `probs` below
@@ -268,6 +289,7 @@ k_front_decode(const float* logits, int T, int M, int k, AssignParams p,
                        topk_w + (size_t)t * k,
                        rows_in_smem ? sp + t * M : (probs != nullptr ? probs + (size_t)t * M : nullptr));
   __syncthreads();
+  FRONT_TR(1);
   const uint8_t* b = forced_bits;
   if (b == nullptr) {
     if (rows_in_smem) {
@@ -280,20 +302,25 @@ k_front_decode(const float* logits, int T, int M, int k, AssignParams p,
     } else {
       front::decode_importance(logits, T, M, sp, s_imp);
     }
+    FRONT_TR(2);
     front::assign_bits(s_imp, nullptr, s_idx, T, p, s_bits, active, I, act, &n_act);
     b = s_bits;
   }
+  FRONT_TR(3);
   if (rows_in_smem && probs != nullptr)
     for (int i = threadIdx.x; i < T * M; i += kFrontThreads) probs[i] = sp[i];
   __syncthreads();   // sp (= big) is reused by the permute's histograms
+  FRONT_TR(4);
   front::permute<kFrontThreads>(s_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row,
                                 active_list, running, big, keep);
+  FRONT_TR(5);
   for (int i = threadIdx.x; i < T * k; i += kFrontThreads) topk_idx[i] = s_idx[i];
   if (forced_bits == nullptr)
     for (int j = threadIdx.x; j < M; j += kFrontThreads) {
       importance[j] = s_imp[j];
       bits[j] = s_bits[j];
     }
+  FRONT_TR(6);
 }
 
 cudaError_t launch_front_decode(const float* logits, int T, int M, int k, const AssignParams& p,
