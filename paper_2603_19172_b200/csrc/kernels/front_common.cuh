@@ -291,5 +291,91 @@ __device__ __forceinline__ void permute(const int32_t* topk_idx, int T, int k, i
   }
 }
 
+// The same permutation by ONE warp for P = T*k <= 256 pairs (the decode front: 8 tokens x top-2
+// .. top-8): pairs are taken 32 at a time in token-major order (round r: pair 32 r + lane); per
+// round one __match_any_sync gives every pair its expert's count and its rank among the round's
+// earlier pairs, and the single leader of each expert group adds the count -- a pair's stable
+// position is its expert's offset + the same-expert pairs of earlier rounds + its in-round rank,
+// the stable counting sort of permute, with __syncwarp instead of permute's block barriers
+// (seven per chunk).  Bit-identical outputs: the stable counting sort is unique.
+// Shared: running [M] ints.  RMAX = the largest round count the instance handles (1: P <= 32).
+template <int RMAX>
+__device__ __forceinline__ void permute_small(const int32_t* topk_idx, int T, int k, int M,
+                                              const uint8_t* bits, int32_t* expert_off,
+                                              int32_t* perm_token, int32_t* perm_slot,
+                                              int32_t* inv_row, int32_t* active_list,
+                                              int* running) {
+  const int lane = threadIdx.x & 31;
+  const int P = T * k;
+  const int R = (P + 31) / 32;   // <= RMAX
+  for (int e = lane; e < M; e += 32) running[e] = 0;
+  __syncwarp();
+  int ex[RMAX];
+  unsigned peers[RMAX];
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    if (r >= R) break;
+    const int p = 32 * r + lane;
+    int e = -1;
+    if (p < P) {
+      e = topk_idx[p];
+      if (bits[e] == 0) {
+        inv_row[p] = -1;
+        e = -1;
+      }
+    }
+    ex[r] = e;
+    peers[r] = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && (peers[r] & ((1u << lane) - 1u)) == 0) running[e] += __popc(peers[r]);
+    __syncwarp();
+  }
+  {   // exclusive scan of the counts and the active list (permute's warp scan)
+    const int per = (M + 31) / 32;
+    const int e0 = lane * per, e1 = min(M, e0 + per);
+    int sum = 0, nz = 0;
+    for (int q = e0; q < e1; ++q) {
+      sum += running[q];
+      nz += running[q] > 0;
+    }
+    int is = sum, in = nz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int vs = __shfl_up_sync(0xffffffffu, is, o), vn = __shfl_up_sync(0xffffffffu, in, o);
+      if (lane >= o) { is += vs; in += vn; }
+    }
+    int acc = is - sum, na = in - nz;
+    for (int q = e0; q < e1; ++q) {
+      const int c = running[q];
+      expert_off[q] = acc;
+      running[q] = acc;
+      if (c > 0) active_list[1 + na++] = q;
+      acc += c;
+    }
+    if (lane == 31) {
+      expert_off[M] = acc;
+      active_list[0] = na;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < RMAX; ++r) {
+    if (r >= R) break;
+    const int e = ex[r];
+    const unsigned lower = peers[r] & ((1u << lane) - 1u);
+    int base = 0;
+    if (e >= 0) base = running[e];
+    __syncwarp();   // every lane has read its expert's running offset before the leaders advance it
+    if (e >= 0) {
+      const int p = 32 * r + lane;
+      const int pos = base + __popc(lower);
+      perm_token[pos] = p / k;
+      perm_slot[pos] = p - (p / k) * k;
+      inv_row[p] = pos;
+      if (lower == 0) running[e] = base + __popc(peers[r]);
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace front
 }  // namespace dymoe

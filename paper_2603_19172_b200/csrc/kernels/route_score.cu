@@ -311,8 +311,19 @@ k_front_decode(const float* logits, int T, int M, int k, AssignParams p,
     for (int i = threadIdx.x; i < T * M; i += kFrontThreads) probs[i] = sp[i];
   __syncthreads();   // sp (= big) is reused by the permute's histograms
   FRONT_TR(4);
-  front::permute<kFrontThreads>(s_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row,
-                                active_list, running, big, keep);
+  if (T * k <= 256) {   // one warp, no block barriers (front::permute_small)
+    if (threadIdx.x < 32) {
+      if (T * k <= 32)
+        front::permute_small<1>(s_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row,
+                                active_list, running);
+      else
+        front::permute_small<8>(s_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row,
+                                active_list, running);
+    }
+  } else {
+    front::permute<kFrontThreads>(s_idx, T, k, M, b, expert_off, perm_token, perm_slot, inv_row,
+                                  active_list, running, big, keep);
+  }
   FRONT_TR(5);
   for (int i = threadIdx.x; i < T * k; i += kFrontThreads) topk_idx[i] = s_idx[i];
   if (forced_bits == nullptr)

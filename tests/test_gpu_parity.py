@@ -385,14 +385,17 @@ def test_max_experts_and_multi_pass_decode(mode):
 
 
 # ------------------------------------------------------------------------------------ fused decode front
-@pytest.mark.parametrize("M,k,T,m_active,forced", [(8, 2, 1, False, False), (8, 2, 8, False, False),
-                                                   (64, 6, 33, False, False), (64, 6, 40, True, False),
-                                                   (256, 8, 256, False, False), (16, 4, 257, False, False),
-                                                   (8, 2, 5, False, True)])
+@pytest.mark.parametrize("M,k,T,m_active,forced", [(8, 2, 1, False, 0), (8, 2, 8, False, 0),
+                                                   (64, 6, 33, False, 0), (64, 6, 40, True, 0),
+                                                   (256, 8, 256, False, 0), (16, 4, 257, False, 0),
+                                                   (8, 2, 5, False, 1), (64, 4, 8, False, 0),
+                                                   (256, 8, 4, True, 0), (32, 6, 5, False, 2),
+                                                   (64, 6, 6, False, 2), (8, 2, 16, False, 0)])
 def test_fused_decode_front_equals_kernels(M, k, T, m_active, forced):
     """dymoe_moe_forward's decode front (one launch: route -> score -> assign -> permute, T <= 256)
     is bit-identical to the standalone dymoe_route / dymoe_score / dymoe_assign_bits /
-    dymoe_permute calls on the same inputs (T = 257 takes the four-launch path)."""
+    dymoe_permute calls on the same inputs (T = 257 takes the four-launch path).  T*k <= 32 takes
+    the front's one-warp permute (P = 2 .. 32, with skipped experts when forced = 2)."""
     d = D()
     cfg = synthetic.MoEConfig("front", M=M, k=k, hidden=128, ffn=128, T=T)
     ex = gpu_experts(cfg, 3, widths=(8, 4, 2))
@@ -400,7 +403,8 @@ def test_fused_decode_front_equals_kernels(M, k, T, m_active, forced):
     x, _, _ = synthetic.layer_inputs(cfg, 3)
     lg = synthetic.random_logits(T, M, seed=T + M, ties=(T % 2 == 1)).cuda()
     ladder = d.make_ladder((8, 4, 2), (0.25, 0.5), m_active=m_active)
-    fb = torch.from_numpy(np.array([(8, 4, 2)[e % 3] for e in range(M)], np.uint8)).cuda() if forced else None
+    cyc = (8, 4, 2) if forced == 1 else (8, 4, 2, 0)
+    fb = torch.from_numpy(np.array([cyc[e % len(cyc)] for e in range(M)], np.uint8)).cuda() if forced else None
     _, ws = layer.forward(x.cuda(), lg, ladder, 29, 32, phase=d.DYMOE_DECODE, forced_bits=fb)
     torch.cuda.synchronize()
     v = layer.views(T, ws)
