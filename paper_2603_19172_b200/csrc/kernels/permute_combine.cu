@@ -289,6 +289,33 @@ __global__ void __launch_bounds__(256) k_combine(const float* __restrict__ y_per
         acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], v[s].z));
         acc.w = __fadd_rn(acc.w, __fmul_rn(wt[s], v[s].w));
       }
+    } else if (k <= 2 && n_parts <= 4) {
+      // decode W2 partials (top-2, <= 4 K slices): all 8 loads in flight before the sums, which
+      // keep load_row's order (slices in order per slot, then slots in order)
+      float4 v[2][4];
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (s < k && rows[s] >= 0 && q < n_parts)
+            v[s][q] = *reinterpret_cast<const float4*>(y_perm + q * part_stride + (size_t)rows[s] * Hd + c);
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (s >= k || rows[s] < 0) continue;
+        float4 u = v[s][0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) {
+          if (q >= n_parts) break;
+          u.x = __fadd_rn(u.x, v[s][q].x);
+          u.y = __fadd_rn(u.y, v[s][q].y);
+          u.z = __fadd_rn(u.z, v[s][q].z);
+          u.w = __fadd_rn(u.w, v[s][q].w);
+        }
+        acc.x = __fadd_rn(acc.x, __fmul_rn(wt[s], u.x));
+        acc.y = __fadd_rn(acc.y, __fmul_rn(wt[s], u.y));
+        acc.z = __fadd_rn(acc.z, __fmul_rn(wt[s], u.z));
+        acc.w = __fadd_rn(acc.w, __fmul_rn(wt[s], u.w));
+      }
     } else {
       for (int s = 0; s < k; ++s) {
         if (rows[s] < 0) continue;
