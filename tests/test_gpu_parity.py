@@ -322,6 +322,37 @@ def test_moe_forward_layer(case):
     assert layer.check_status(T, ws)[0] == 0
 
 
+@pytest.mark.parametrize("phase,T", [("decode", 8), ("decode", 16), ("prefill", 40)])
+def test_moe_forward_256_experts(phase, T):
+    """The largest expert count the library supports (M = 256, top-8): the decode GEMV's one-round
+    allocation strides its loads over all 256 experts (8 per lane) and the decode front's one-warp
+    permutation takes up to 256 pairs; the whole layer equals the oracle."""
+    d = D()
+    cfg = synthetic.MoEConfig("wide256", M=256, k=8, hidden=256, ffn=256, T=T)
+    ex = gpu_experts(cfg, 5)
+    layer = d.MoELayer(ex, cfg.k, cfg.hidden, cfg.ffn)
+    x, lg, a = synthetic.layer_inputs(cfg, 5)
+    ph = d.DYMOE_PREFILL if phase == "prefill" else d.DYMOE_DECODE
+    bits_t, lams = (8, 4, 2), (0.25, 0.5)
+    y, ws = layer.forward(x.cuda(), lg.cuda(), d.make_ladder(bits_t, lams), 12, 32, phase=ph,
+                          attn_mass=a.cuda() if ph == d.DYMOE_PREFILL else None)
+    torch.cuda.synchronize()
+    v = layer.views(T, ws)
+    o_lad = o_sched.Ladder(bits=bits_t, lambdas=lams)
+    ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), np_experts(cfg, 5), 12, 32, o_lad, cfg.k,
+                            phase=phase, attn_mass=a.numpy())
+    assert np.array_equal(v["topk_idx"].cpu().numpy(), ref["topk_idx"])
+    bits = v["bits"].cpu().numpy()
+    tol = 0 if phase == "prefill" else decode_importance_tol(T)
+    if not check_bits(bits, ref["bits"], ref["importance"], tol):
+        ref = o_moe.moe_forward(x.float().numpy(), lg.numpy(), np_experts(cfg, 5), 12, 32, o_lad,
+                                cfg.k, phase=phase, attn_mass=a.numpy(), forced_bits=bits)
+    assert np.array_equal(v["expert_off"].cpu().numpy(), ref["expert_off"])
+    assert np.array_equal(v["inv_row"].cpu().numpy(), ref["inv_row"])
+    assert rel_err(y.cpu().numpy(), ref["y"]) <= FFN_TOL
+    assert layer.check_status(T, ws)[0] == 0
+
+
 def test_moe_forward_bf16_output_and_empty():
     d = D()
     cfg = synthetic.CONFIGS["tiny"]
