@@ -87,8 +87,37 @@ k_score_prefill(const float* __restrict__ attn, int H, const int32_t* __restrict
   __shared__ int sh_krem;
   const int tid = threadIdx.x;
 
-  // 1. token scores, sequential over heads (coalesced over tokens)
-  for (int i = tid; i < T; i += kScoreThreads) {
+  // 1. token scores, sequential over heads (coalesced over tokens).  One CTA pulls the whole
+  // [H][T] mass (256 KB at H = 32, T = 2048), so the loads are 16 bytes wide (4 tokens) with 8
+  // heads in flight; each token's sum keeps the head order.
+  const int T4 = (T % 4 == 0 && ((reinterpret_cast<uintptr_t>(attn) | reinterpret_cast<uintptr_t>(S)) & 15) == 0)
+                     ? T / 4 : 0;
+  for (int i4 = tid; i4 < T4; i4 += kScoreThreads) {
+    const float4* a4 = reinterpret_cast<const float4*>(attn);
+    float4 acc = a4[i4];
+    int h = 1;
+    for (; h + 8 <= H; h += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = a4[(size_t)(h + u) * T4 + i4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc.x = __fadd_rn(acc.x, v[u].x);
+        acc.y = __fadd_rn(acc.y, v[u].y);
+        acc.z = __fadd_rn(acc.z, v[u].z);
+        acc.w = __fadd_rn(acc.w, v[u].w);
+      }
+    }
+    for (; h < H; ++h) {
+      const float4 v = a4[(size_t)h * T4 + i4];
+      acc.x = __fadd_rn(acc.x, v.x);
+      acc.y = __fadd_rn(acc.y, v.y);
+      acc.z = __fadd_rn(acc.z, v.z);
+      acc.w = __fadd_rn(acc.w, v.w);
+    }
+    reinterpret_cast<float4*>(S)[i4] = acc;
+  }
+  for (int i = 4 * T4 + tid; i < T; i += kScoreThreads) {
     float acc = attn[i];
     int h = 1;
     for (; h + 8 <= H; h += 8) {   // 8 loads in flight, then the adds in head order
