@@ -116,6 +116,25 @@ __device__ __forceinline__ void a_frag(const uint4& w, const DQ& dq, int s, uint
     // q - z exact in fp32 (2^23 + q minus 2^23 + z), taken to bf16x2 exactly (|q - z| <= 255
     // has 8 significant bits), then one HMUL2 per pair gives RNE((q - z)·s) (D17)
     const uint32_t x = word(w, s);
+#ifndef DYMOE_I8_PRMT_PACK
+    // the two subtractions as one packed FADD2 and the exact bf16x2 pack as one F2FP, so that a
+    // pair costs 2 ALU instructions (the magic PRMTs) instead of 3: the Int8 loop is bound by the
+    // ALU pipe (ncu: PRMT at the top of the stall samples)
+    float2 z2 = make_float2(-dq.zf, -dq.zf);
+    float d0, d1, d2, d3;
+    {
+      uint64_t r, a, zz;
+      asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "r"(prmt(x, 0x4B000000u, 0x7440u)), "r"(prmt(x, 0x4B000000u, 0x7441u)));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(zz) : "f"(z2.x), "f"(z2.y));
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(zz));
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(r));
+      asm("mov.b64 %0, {%1, %2};" : "=l"(a) : "r"(prmt(x, 0x4B000000u, 0x7442u)), "r"(prmt(x, 0x4B000000u, 0x7443u)));
+      asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(zz));
+      asm("mov.b64 {%0, %1}, %2;" : "=f"(d2), "=f"(d3) : "l"(r));
+    }
+    lo = bf2_mul(pack_bf2(d0, d1), dq.ss);   // q - z has <= 8 significant bits: the pack is exact
+    hi = bf2_mul(pack_bf2(d2, d3), dq.ss);
+#else
     const float d0 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7440u)), dq.zf);
     const float d1 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7441u)), dq.zf);
     const float d2 = __fsub_rn(__uint_as_float(prmt(x, 0x4B000000u, 0x7442u)), dq.zf);
@@ -124,6 +143,7 @@ __device__ __forceinline__ void a_frag(const uint4& w, const DQ& dq, int s, uint
     // pair is just the two high halves (one PRMT instead of an F2FP conversion)
     lo = bf2_mul(prmt(__float_as_uint(d0), __float_as_uint(d1), 0x7632u), dq.ss);
     hi = bf2_mul(prmt(__float_as_uint(d2), __float_as_uint(d3), 0x7632u), dq.ss);
+#endif
   }
 }
 
@@ -191,8 +211,8 @@ struct AllocScratch {
 // with every expert forced to one width (tools/decode_width_sweep.py): the narrow widths are
 // bound by dequant issue slots rather than bytes, so they cost more than their bytes suggest.
 __device__ __forceinline__ int wcost(int b, bool w13) {
-  if (w13) return b == 16 ? 259 : b == 8 ? 168 : b == 4 ? 115 : 103;
-  return b == 16 ? 256 : b == 8 ? 181 : b == 4 ? 130 : 129;
+  if (w13) return b == 16 ? 259 : b == 8 ? 162 : b == 4 ? 115 : 103;
+  return b == 16 ? 256 : b == 8 ? 179 : b == 4 ? 130 : 129;
 }
 
 // Cost-proportional allocation of `units_total` units to the active experts, every active
