@@ -8,6 +8,7 @@ for r in 1 2 3; do
     (cd $dir && timeout 600 python bench.py --main-only --no-cpu-baseline "$@") > $O/${side}_$r.json 2> $O/${side}_$r.err
     python -c "
 import json; j=json.load(open('$O/${side}_$r.json')); r=j['roofline']
-print('$side', $r, round(j['value']), 'frac %.3f' % r['frac'], 'w13 %.1f w2 %.1f' % (r['w13_us_per_step'], r['w2_us_per_step']), j['clocks']['sm_mhz'], j['clocks']['reasons'])"
+k = ('w13 %.1f w2 %.1f us' % (r['w13_us_per_step'], r['w2_us_per_step'])) if 'w13_us_per_step' in r else ('w13 %.0f w2 %.0f TF' % (r['w13_tflops'], r['w2_tflops']))
+print('$side', $r, round(j['value']), 'frac %.3f' % r['frac'], k, j['clocks']['sm_mhz'], j['clocks']['reasons'])"
   done
 done
