@@ -324,10 +324,12 @@ bool encode_rows(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t 
   const uint32_t box[2] = {128, 16};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, base, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
-// group-major meta [n_mat][gpr][N] u32: boxes {16 rows, gq groups, n_mat}
-bool encode_meta(CUtensorMap* m, const void* base, uint64_t N, uint64_t gpr, int n_mat, uint32_t gq) {
+// group-major meta [n_mat][gpr][N] u32: boxes {rows, gq groups, n_mat} (W1 / W3: the 16 rows of a
+// decode tile of both matrices; W2: the 32 rows of a W2 tile in one box)
+bool encode_meta(CUtensorMap* m, const void* base, uint64_t N, uint64_t gpr, int n_mat, uint32_t gq,
+                 uint32_t rows) {
   const uint64_t dims[3] = {N, gpr, (uint64_t)n_mat}, str[2] = {N * 4, N * gpr * 4};
-  const uint32_t box[3] = {16, gq, (uint32_t)n_mat};
+  const uint32_t box[3] = {rows, gq, (uint32_t)n_mat};
   return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, base, n_mat > 1 ? 3 : 2, dims, str, box,
                 CU_TENSOR_MAP_SWIZZLE_NONE);
 }
@@ -425,7 +427,7 @@ int bind_expert(dymoe_layer* L, int e, const dymoe_expert_desc& x, cudaStream_t 
       // W3's own descriptor is not needed by the kernels
       const bool pair = m == 0 && y.q[wi][1].codes != nullptr;
       if (m == 2 || pair) {
-        maps_ok &= encode_meta(&hm[im], q.meta, N, K / DYMOE_GROUP, pair ? 2 : 1, gq);
+        maps_ok &= encode_meta(&hm[im], q.meta, N, K / DYMOE_GROUP, pair ? 2 : 1, gq, m == 2 ? 32 : 16);
         q.tm_meta = dm + im;
       }
     }

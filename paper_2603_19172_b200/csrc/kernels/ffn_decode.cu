@@ -229,8 +229,9 @@ __device__ __noinline__ uint32_t run_tiles(const CUtensorMap* tm0, const CUtenso
   constexpr int GQ = BITS == 16 ? 0 : NSUB * CK / DYMOE_GROUP;  // groups per item
   constexpr uint32_t TX = NM * BOXES * 2048 + NM * 64 * GQ;
   // meta words of operand block m start at m * MSTRIDE in the stage: W13's 3-D box packs the two
-  // blocks ([m][g][16]); W2's two boxes sit 256 B apart (TMA destinations are 128-B aligned)
-  constexpr int MSTRIDE = W13 ? GQ * 64 : 256;
+  // blocks ([m][g][16]); W2's one 32-row box is [g][32 rows], block m = rows 16 m .. 16 m + 15
+  constexpr int MSTRIDE = W13 ? GQ * 64 : 64;
+  constexpr int MGSTRIDE = W13 ? 16 : 32;   // words per group in the stage
   // WPT = warps sharing a tile (wpt_for below): K split over fewer warps when the slice is short
   constexpr int NSG = 2 * kWarps / WPT;              // subgroups per CTA, on interleaved tiles
   const int lane = threadIdx.x & 31;
@@ -280,8 +281,7 @@ __device__ __noinline__ uint32_t run_tiles(const CUtensorMap* tm0, const CUtenso
       if constexpr (W13) {
         tma3d_e(el, ms, tmm, ti * 16, gy0 + jj * (WPT * GQ), 0, bar, pol);
       } else {
-        tma2d_e(el, ms, tmm, ti * 32, gy0 + jj * (WPT * GQ), bar, pol);
-        tma2d_e(el, ms + 256, tmm, ti * 32 + 16, gy0 + jj * (WPT * GQ), bar, pol);   // 128-B aligned
+        tma2d_e(el, ms, tmm, ti * 32, gy0 + jj * (WPT * GQ), bar, pol);   // 32 rows x GQ groups
       }
     }
   };
@@ -317,7 +317,7 @@ __device__ __noinline__ uint32_t run_tiles(const CUtensorMap* tm0, const CUtenso
 #pragma unroll
   for (int sub = 0; sub < NSUB; ++sub) {
     const int gi = BITS == 16 ? 0 : (sub * CK + c * Tr::CODES) / DYMOE_GROUP;
-    mofs[sub] = (gi * 16 + g) * 4;
+    mofs[sub] = (gi * MGSTRIDE + g) * 4;
   }
   int tile_seq = 0;
   int tile = t0 + grp, j = 0;      // consumer cursor
